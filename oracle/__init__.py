@@ -1,0 +1,164 @@
+"""CPU oracle for BROS bidirectional paged decode attention -- TEST INFRASTRUCTURE.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` legs may import this package.  It wraps ``bkv_oracle.c``
+(plain C, fp64) through ctypes and shares nothing with the CUDA path.
+
+Function-level citations live in ``bkv_oracle.c``.  Parity pins: DESIGN.md
+"Oracle pins".  Nothing here is "parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "bkv_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (-O2 -fopenmp).  Returns the .so path."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fopenmp", "-fPIC", "-shared",
+                               "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        P = ctypes.c_void_p
+        i32, i64, dbl = ctypes.c_int, ctypes.c_int64, ctypes.c_double
+        L.bkvo_bf16_to_f64.argtypes = [ctypes.c_uint16]
+        L.bkvo_bf16_to_f64.restype = dbl
+        L.bkvo_slot_in_block.argtypes = [i32, i64, i32]
+        L.bkvo_slot_in_block.restype = i32
+        L.bkvo_validate.argtypes = [i32, P, i32, P, i32, i32, P, i32, i32, i32, P]
+        L.bkvo_validate.restype = i32
+        L.bkvo_append.argtypes = [P, P, i64, i64, i64, i32, i32, i32,
+                                  i32, P, i32, P, i32, i32, P, P, P, P, P]
+        L.bkvo_append.restype = None
+        L.bkvo_gather.argtypes = [P, P, i64, i64, i64, i32, i32, i32,
+                                  P, i32, P, i32, i32, i32, i64, P, P]
+        L.bkvo_gather.restype = None
+        L.bkvo_attention.argtypes = [P, P, i64, i64, i64, i32, i32, i32,
+                                     P, i32, P, i32, i32, P, i32, i32, P, i32, dbl, P]
+        L.bkvo_attention.restype = None
+        L.bkvo_num_threads.restype = i32
+        L.bkvo_set_num_threads.argtypes = [i32]
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    return a.ctypes.data_as(ctypes.c_void_p) if a is not None else None
+
+
+def _c(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+def _dirs(dirs):
+    d = _c(dirs, np.uint8)
+    if d.ndim == 1:          # one flag per request (reading Q5: col_stride 0)
+        return d, 1, 0
+    return d, d.shape[1], 1
+
+
+def _pool_geom(K):
+    assert K.dtype == np.uint16 and K.ndim == 4 and K.strides[3] == 2
+    sb, sh, ss = (s // 2 for s in K.strides[:3])
+    nblk, H, bs, d = K.shape
+    return sb, sh, ss, H, d, bs
+
+
+def bf16_to_f64(bits):
+    """Vectorised exact bf16 -> float64 (the bf16 pattern is the top half of a float32)."""
+    b = np.asarray(bits, dtype=np.uint16)
+    return (b.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
+def slot_in_block(direction: int, t: int, bs: int) -> int:
+    return lib().bkvo_slot_in_block(int(direction), int(t), int(bs))
+
+
+def validate(block_tables, dirs, lens, num_blocks: int, bs: int, require_nonempty=True):
+    """Return (code, info): 0 ok, 1 I4 range, 2 I1 slot collision, 3 I2 sharing."""
+    bt = _c(block_tables, np.int32)
+    d, rs, cs = _dirs(dirs)
+    ln = _c(lens, np.int32)
+    info = np.zeros(4, dtype=np.int64)
+    rc = lib().bkvo_validate(int(ln.shape[0]), _ptr(bt), int(bt.shape[1]), _ptr(d), rs, cs,
+                             _ptr(ln), int(num_blocks), int(bs), int(bool(require_nonempty)),
+                             _ptr(info))
+    return int(rc), tuple(int(x) for x in info)
+
+
+def new_pool(num_blocks: int, H: int, bs: int, d: int, fill: int = 0):
+    """Host KV pool pair, uint16 bf16 bits, layout [block][head][slot][d]."""
+    K = np.full((num_blocks, H, bs, d), fill, dtype=np.uint16)
+    return K, K.copy()
+
+
+def append(K, V, block_tables, dirs, before, cu_new, k_new, v_new):
+    """In-place append into host pools; returns int64 slot_mapping [total_new]."""
+    sb, sh, ss, H, d, bs = _pool_geom(K)
+    assert V.shape == K.shape and V.strides == K.strides
+    bt = _c(block_tables, np.int32)
+    dd, rs, cs = _dirs(dirs)
+    bf = _c(before, np.int32)
+    cu = _c(cu_new, np.int32)
+    kn = _c(k_new, np.uint16).reshape(-1, H, d)
+    vn = _c(v_new, np.uint16).reshape(-1, H, d)
+    assert kn.shape[0] == cu[-1]
+    sm = np.zeros(int(cu[-1]), dtype=np.int64)
+    lib().bkvo_append(_ptr(K), _ptr(V), sb, sh, ss, H, d, bs, int(bf.shape[0]), _ptr(bt),
+                      int(bt.shape[1]), _ptr(dd), rs, cs, _ptr(bf), _ptr(cu), _ptr(kn), _ptr(vn),
+                      _ptr(sm))
+    return sm
+
+
+def gather(K, V, block_tables, dirs, r: int, L: int):
+    """Dense logical-order (K_r, V_r), uint16 [L][H][d]."""
+    sb, sh, ss, H, d, bs = _pool_geom(K)
+    bt = _c(block_tables, np.int32)
+    dd, rs, cs = _dirs(dirs)
+    ko = np.zeros((L, H, d), dtype=np.uint16)
+    vo = np.zeros((L, H, d), dtype=np.uint16)
+    lib().bkvo_gather(_ptr(K), _ptr(V), sb, sh, ss, H, d, bs, _ptr(bt), int(bt.shape[1]),
+                      _ptr(dd), rs, cs, int(r), int(L), _ptr(ko), _ptr(vo))
+    return ko, vo
+
+
+def attention(K, V, block_tables, dirs, lens, q, scale: float, r_range=None):
+    """fp64 decode attention, out float64 [B][Hq][d] (rows outside r_range stay 0)."""
+    sb, sh, ss, H, d, bs = _pool_geom(K)
+    bt = _c(block_tables, np.int32)
+    dd, rs, cs = _dirs(dirs)
+    ln = _c(lens, np.int32)
+    qq = _c(q, np.uint16)
+    B, Hq, dq = qq.shape
+    assert dq == d and Hq % H == 0
+    out = np.zeros((B, Hq, d), dtype=np.float64)
+    r0, r1 = (0, B) if r_range is None else r_range
+    lib().bkvo_attention(_ptr(K), _ptr(V), sb, sh, ss, H, d, bs, _ptr(bt), int(bt.shape[1]),
+                         _ptr(dd), rs, cs, _ptr(ln), int(r0), int(r1), _ptr(qq), int(Hq),
+                         float(scale), _ptr(out))
+    return out
+
+
+def num_threads() -> int:
+    return int(lib().bkvo_num_threads())
+
+
+def set_num_threads(n: int) -> None:
+    lib().bkvo_set_num_threads(int(n))
