@@ -1,0 +1,195 @@
+/*
+ * bkv.h -- C ABI of libbkv: BROS bidirectional paged KV cache, B200 (sm_100a).
+ *
+ * BROS (arXiv 2504.09590) serves real-time (RT) and best-effort (BE) requests
+ * from ONE pool of KV blocks: "Each block can be used for KV cache storage of
+ * one RT request and one BE request ... the RT request occupies memory slots
+ * from the left to the right in the block while that of the BE request in the
+ * opposite direction" (§5.1).  The decode kernel is guided by
+ * "a binary direction table, which possesses an identical shape to the block
+ * tables" and inverts the slot order "whenever the flag of direction is
+ * evaluated to be true".  This library exports the two device calls of
+ * that hot path:
+ *
+ *   bkv_kv_append               -- write this step's new K/V rows into their slots
+ *   bkv_paged_decode_attention  -- per-request decode attention over the pool
+ *
+ * plus host helpers (workspace sizing, a host-side layout validator, status
+ * strings).
+ *
+ * Conventions (all entry points):
+ *   - Device pointers are caller-owned (allocated by PyTorch or cudaMalloc);
+ *     the library never allocates, frees or synchronises.  Every device call is
+ *     asynchronous on `stream` and CUDA-graph capturable.
+ *   - Argument errors are detected on the host BEFORE any launch and return a
+ *     non-zero bkv_status with no side effect; bkv_last_error() then returns a
+ *     thread-local one-line explanation.  Launch failures return BKV_ERR_CUDA.
+ *     Device-side faults (e.g. a block id out of range that the caller did not
+ *     validate) surface asynchronously, as for any CUDA kernel.
+ *   - No global mutable state besides a per-device cache of immutable device
+ *     properties: calls are thread-safe.
+ *   - Element type of K, V, Q, out, k_new, v_new is bf16 (IEEE bfloat16 bits);
+ *     all strides are in ELEMENTS.  Reading Q1: the paper never states the
+ *     precision; this library stores bf16 and accumulates in fp32.
+ */
+#ifndef BKV_H_
+#define BKV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define BKV_API __attribute__((visibility("default")))
+#else
+#define BKV_API
+#endif
+
+/* cudaStream_t without pulling in the CUDA headers (same underlying type). */
+typedef struct CUstream_st *bkv_stream_t;
+
+/* Direction flag values of the direction table (reading Q4). */
+#define BKV_DIR_FWD 0 /* RT: j-th token of a block at slot j             */
+#define BKV_DIR_REV 1 /* BE: j-th token of a block at slot block_size-1-j */
+
+typedef enum {
+  BKV_OK = 0,
+  BKV_ERR_INVALID_ARGUMENT = 1, /* null pointer, bad size/stride/alignment        */
+  BKV_ERR_UNSUPPORTED = 2,      /* head_dim/block_size/group outside the built set */
+  BKV_ERR_WORKSPACE_TOO_SMALL = 3,
+  BKV_ERR_LAYOUT = 4,           /* host validator found an I1-I4 violation         */
+  BKV_ERR_CUDA = 5              /* CUDA runtime / driver error                     */
+} bkv_status;
+
+/*
+ * One layer of one rank's head shard of the KV block pool.
+ * Element (block b, kv head h, slot s, dim i) of K lives at
+ *     k[b*stride_block + h*stride_head + s*stride_slot + i]      (same for V).
+ * Requirements: k, v 16-byte aligned; stride_* multiples of 8 elements;
+ * stride_slot >= head_dim; head_dim in {64, 128}; block_size in {16, 32}.
+ * Recommended (what the Python binding allocates): contiguous
+ * [num_blocks][num_kv_heads][block_size][head_dim], so one (block, head) tile
+ * is block_size*head_dim*2 contiguous bytes (4 KiB at bs16/d128).
+ */
+typedef struct {
+  void *k;
+  void *v;
+  int32_t num_blocks;
+  int32_t num_kv_heads;
+  int32_t block_size;
+  int32_t head_dim;
+  int64_t stride_block;
+  int64_t stride_head;
+  int64_t stride_slot;
+} bkv_kv_pool;
+
+/*
+ * Block map of a batch (SURVEY D2 + D3).
+ * Request r's logical token t lives in physical block
+ *     block_tables[r*bt_stride + t/block_size]
+ * at slot  t%block_size                  if dir == BKV_DIR_FWD
+ *          block_size-1-t%block_size     if dir == BKV_DIR_REV
+ * where dir = dirs[r*dir_row_stride + (t/block_size)*dir_col_stride].
+ * dir_col_stride = 0 gives one flag per request (reading Q5); a table of the
+ * block table's shape uses dir_col_stride = 1, dir_row_stride = bt_stride.
+ * Device pointers.  Only entries e < ceil(seq_len/block_size) are read.
+ */
+typedef struct {
+  const int32_t *block_tables;
+  int32_t bt_stride;
+  const uint8_t *dirs;
+  int32_t dir_row_stride;
+  int32_t dir_col_stride;
+  int32_t num_seqs;
+} bkv_block_map;
+
+/*
+ * kv_append -- SURVEY §8(a) row a2: write the K/V rows of this step's new
+ * tokens into the pool, each in its request's direction.  RT and BE
+ * requests sharing a block write opposite ends in the same launch.
+ *
+ *   seq_lens_before [num_seqs]   device int32: resident tokens before the append
+ *   cu_new_tokens   [num_seqs+1] device int32: new tokens of request r are rows
+ *                                cu_new_tokens[r] .. cu_new_tokens[r+1]-1 of
+ *                                k_new/v_new (decode step: cu[r] = r)
+ *   total_new_tokens             host int: cu_new_tokens[num_seqs]
+ *   k_new, v_new                 device bf16 [total_new][num_kv_heads][head_dim],
+ *                                contiguous, 16-byte aligned
+ *   slot_mapping_out             optional device int64 [total_new]: receives
+ *                                block*block_size + slot of every new token
+ * The new token t = seq_lens_before[r] + j must lie inside the block map
+ * (t < bt_stride*block_size) and its slot must not hold a live token of another
+ * request (invariant I5; lazy-checkpoint eviction is the caller's job).
+ * Bit-exact: each written row is a copy of the input row; no other byte of
+ * the pool changes.
+ */
+BKV_API bkv_status bkv_kv_append(const bkv_kv_pool *pool, const bkv_block_map *map,
+                         const int32_t *seq_lens_before, const int32_t *cu_new_tokens,
+                         int32_t total_new_tokens, const void *k_new, const void *v_new,
+                         int64_t *slot_mapping_out, bkv_stream_t stream);
+
+/*
+ * paged_decode_attention -- SURVEY §8(a) rows a3-a5.  For every request r and
+ * query head h (kv head h / (num_q_heads/num_kv_heads), reading Q9):
+ *     out[r][h] = softmax_t(softmax_scale * q[r][h] . K_r[t]) . V_r[t],  t < seq_lens[r]
+ * where K_r/V_r are read through the bidirectional block map.  Split-K across
+ * the context with an online-softmax merge; fp32 accumulation; output rounded
+ * to bf16 (round-to-nearest-even).  The result is permutation-invariant over
+ * a request's tokens, so blocks are consumed in physical slot order and the
+ * direction only decides which slots of a partly filled block are live.
+ *
+ *   seq_lens [num_seqs]  device int32, >= 0, includes the token appended this
+ *                        step (reading Q7); 0 yields a zero output row (Q8)
+ *   max_seq_len          host upper bound of seq_lens (<= bt_stride*block_size)
+ *   q                    device bf16, q[r*q_stride_seq + h*q_stride_head + i]
+ *   num_q_heads          multiple of pool->num_kv_heads, group <= 16
+ *   softmax_scale        e.g. 1/sqrt(head_dim) (reading Q2)
+ *   out                  device bf16, out[r*o_stride_seq + h*o_stride_head + i]
+ *                        (head-major [H_q][B][d] is o_stride_head = B*d,
+ *                        o_stride_seq = d: what the TP all-gather wants)
+ *   workspace            device buffer of >= bkv_decode_workspace_size(...) bytes,
+ *                        ZERO-FILLED before its first use; every call leaves
+ *                        it zero-filled again (self-resetting counters), so a
+ *                        workspace must not be shared by concurrent calls.
+ * Deterministic: split partials are merged in split order.
+ */
+BKV_API bkv_status bkv_paged_decode_attention(const bkv_kv_pool *pool, const bkv_block_map *map,
+                                      const int32_t *seq_lens, int32_t max_seq_len,
+                                      const void *q, int64_t q_stride_seq, int64_t q_stride_head,
+                                      int32_t num_q_heads, float softmax_scale,
+                                      void *out, int64_t o_stride_seq, int64_t o_stride_head,
+                                      void *workspace, size_t workspace_bytes,
+                                      bkv_stream_t stream);
+
+/* Workspace bytes for bkv_paged_decode_attention on the CURRENT device
+ * (depends on the SM count); 0 on error (see bkv_last_error). */
+BKV_API size_t bkv_decode_workspace_size(int32_t num_seqs, int32_t num_q_heads, int32_t num_kv_heads,
+                                 int32_t head_dim);
+
+/*
+ * Host-side layout validator on HOST copies of the map.
+ * Returns BKV_OK or BKV_ERR_LAYOUT (BKV_ERR_INVALID_ARGUMENT for null inputs).
+ * info[0] = invariant code (1 = I4 range/direction/length, 2 = I1 two live
+ * tokens on one slot -- the a3/B8 collision of P:731, 3 = I2 more than one
+ * forward or reversed entry on a block), info[1..4] = details
+ * (I1: r1, t1, r2, t2; I2: block, dir, r1, r2; I4: r, entry or -1, value).
+ */
+BKV_API bkv_status bkv_validate_layout_host(const int32_t *block_tables, int32_t bt_stride,
+                                    const uint8_t *dirs, int32_t dir_row_stride,
+                                    int32_t dir_col_stride, int32_t num_seqs,
+                                    const int32_t *seq_lens, int32_t num_blocks,
+                                    int32_t block_size, int32_t require_nonempty,
+                                    int64_t info[5]);
+
+BKV_API const char *bkv_status_string(bkv_status s);
+BKV_API const char *bkv_last_error(void); /* thread-local detail of the last failure */
+BKV_API int32_t bkv_version(void);        /* MAJOR*10000 + MINOR*100 + PATCH */
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* BKV_H_ */

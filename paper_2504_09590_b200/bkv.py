@@ -1,0 +1,233 @@
+"""ctypes binding of libbkv (include/bkv.h) over torch tensors.
+
+Argument marshalling only: every step of the hot path runs in the CUDA kernels
+of libbkv.so.  There is no CPU or PyTorch fallback -- if the library is missing
+or the device is not a CUDA device, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import threading
+from dataclasses import dataclass
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libbkv.so")
+
+BKV_DIR_FWD = 0   # RT: left -> right
+BKV_DIR_REV = 1   # BE: right -> left
+
+
+class BkvError(RuntimeError):
+    pass
+
+
+class _Pool(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_void_p), ("v", ctypes.c_void_p),
+                ("num_blocks", ctypes.c_int32), ("num_kv_heads", ctypes.c_int32),
+                ("block_size", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+                ("stride_block", ctypes.c_int64), ("stride_head", ctypes.c_int64),
+                ("stride_slot", ctypes.c_int64)]
+
+
+class _Map(ctypes.Structure):
+    _fields_ = [("block_tables", ctypes.c_void_p), ("bt_stride", ctypes.c_int32),
+                ("dirs", ctypes.c_void_p), ("dir_row_stride", ctypes.c_int32),
+                ("dir_col_stride", ctypes.c_int32), ("num_seqs", ctypes.c_int32)]
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+EXPORTS = ("bkv_kv_append", "bkv_paged_decode_attention", "bkv_decode_workspace_size",
+           "bkv_validate_layout_host", "bkv_status_string", "bkv_last_error", "bkv_version")
+
+
+def lib():
+    """Load libbkv.so (raises if it was not built -- no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        with _lib_lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise BkvError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+                L = ctypes.CDLL(LIB_PATH)
+                P, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+                L.bkv_kv_append.argtypes = [ctypes.POINTER(_Pool), ctypes.POINTER(_Map), P, P, i32, P, P, P, P]
+                L.bkv_kv_append.restype = ctypes.c_int
+                L.bkv_paged_decode_attention.argtypes = [
+                    ctypes.POINTER(_Pool), ctypes.POINTER(_Map), P, i32, P, i64, i64, i32, ctypes.c_float,
+                    P, i64, i64, P, ctypes.c_size_t, P]
+                L.bkv_paged_decode_attention.restype = ctypes.c_int
+                L.bkv_decode_workspace_size.argtypes = [i32, i32, i32, i32]
+                L.bkv_decode_workspace_size.restype = ctypes.c_size_t
+                L.bkv_validate_layout_host.argtypes = [P, i32, P, i32, i32, i32, P, i32, i32, i32, P]
+                L.bkv_validate_layout_host.restype = ctypes.c_int
+                L.bkv_status_string.argtypes = [ctypes.c_int]
+                L.bkv_status_string.restype = ctypes.c_char_p
+                L.bkv_last_error.restype = ctypes.c_char_p
+                L.bkv_version.restype = ctypes.c_int32
+                _lib = L
+    return _lib
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        L = lib()
+        raise BkvError(f"{what}: {L.bkv_status_string(rc).decode()} -- {L.bkv_last_error().decode()}")
+
+
+def _stream_ptr(stream):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dev(t: torch.Tensor, name: str, dtype=None):
+    if not t.is_cuda:
+        raise BkvError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if dtype is not None and t.dtype != dtype:
+        raise BkvError(f"{name} must be {dtype}, got {t.dtype}")
+    return t
+
+
+@dataclass
+class KVPool:
+    """One layer of one rank's KV block pool: K, V bf16 [num_blocks][H][bs][d] (D1)."""
+    k: torch.Tensor
+    v: torch.Tensor
+
+    @staticmethod
+    def empty(num_blocks, num_kv_heads, block_size, head_dim, device="cuda"):
+        shape = (num_blocks, num_kv_heads, block_size, head_dim)
+        return KVPool(torch.empty(shape, dtype=torch.bfloat16, device=device),
+                      torch.empty(shape, dtype=torch.bfloat16, device=device))
+
+    @property
+    def num_blocks(self): return self.k.shape[0]
+
+    @property
+    def num_kv_heads(self): return self.k.shape[1]
+
+    @property
+    def block_size(self): return self.k.shape[2]
+
+    @property
+    def head_dim(self): return self.k.shape[3]
+
+    def c(self) -> _Pool:
+        _dev(self.k, "pool.k", torch.bfloat16)
+        _dev(self.v, "pool.v", torch.bfloat16)
+        if self.k.shape != self.v.shape or self.k.stride() != self.v.stride() or self.k.stride(3) != 1:
+            raise BkvError("pool k/v must have equal shapes and strides with contiguous head_dim")
+        sb, sh, ss, _ = self.k.stride()
+        nb, H, bs, d = self.k.shape
+        return _Pool(self.k.data_ptr(), self.v.data_ptr(), nb, H, bs, d, sb, sh, ss)
+
+
+def block_map(block_tables: torch.Tensor, dirs: torch.Tensor) -> _Map:
+    """D2 + D3: int32 block tables [B][M]; uint8 dirs [B] (per request) or [B][M]."""
+    _dev(block_tables, "block_tables", torch.int32)
+    _dev(dirs, "dirs", torch.uint8)
+    if block_tables.dim() != 2 or block_tables.stride(1) != 1:
+        raise BkvError("block_tables must be [B][M] with unit column stride")
+    B = block_tables.shape[0]
+    if dirs.dim() == 1:
+        rs, cs = dirs.stride(0), 0
+    else:
+        rs, cs = dirs.stride(0), dirs.stride(1)
+    if dirs.shape[0] != B:
+        raise BkvError("dirs must have one row per request")
+    return _Map(block_tables.data_ptr(), block_tables.stride(0), dirs.data_ptr(), rs, cs, B)
+
+
+def kv_append(pool: KVPool, block_tables, dirs, seq_lens_before, cu_new_tokens, k_new, v_new,
+              slot_mapping=None, total_new_tokens=None, stream=None):
+    """bkv_kv_append: write new K/V rows [total_new][H][d] into their bidirectional slots."""
+    p, m = pool.c(), block_map(block_tables, dirs)
+    _dev(seq_lens_before, "seq_lens_before", torch.int32)
+    _dev(cu_new_tokens, "cu_new_tokens", torch.int32)
+    _dev(k_new, "k_new", torch.bfloat16)
+    _dev(v_new, "v_new", torch.bfloat16)
+    if not (k_new.is_contiguous() and v_new.is_contiguous()):
+        raise BkvError("k_new/v_new must be contiguous [total_new][H][d]")
+    n = k_new.shape[0] if total_new_tokens is None else int(total_new_tokens)
+    sm = 0
+    if slot_mapping is not None:
+        sm = _dev(slot_mapping, "slot_mapping", torch.int64).data_ptr()
+    rc = lib().bkv_kv_append(ctypes.byref(p), ctypes.byref(m), seq_lens_before.data_ptr(),
+                             cu_new_tokens.data_ptr(), n, k_new.data_ptr(), v_new.data_ptr(),
+                             ctypes.c_void_p(sm), _stream_ptr(stream))
+    _check(rc, "bkv_kv_append")
+
+
+def decode_workspace_size(num_seqs, num_q_heads, num_kv_heads, head_dim) -> int:
+    n = lib().bkv_decode_workspace_size(num_seqs, num_q_heads, num_kv_heads, head_dim)
+    if n == 0:
+        raise BkvError("bkv_decode_workspace_size: " + lib().bkv_last_error().decode())
+    return int(n)
+
+
+_ws_cache = {}
+_ws_lock = threading.Lock()
+
+
+def workspace(num_seqs, num_q_heads, num_kv_heads, head_dim, device=None, stream=None):
+    """Zero-initialised workspace cached per (device, stream); grows on demand."""
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    s = torch.cuda.current_stream(dev) if stream is None else stream
+    need = decode_workspace_size(num_seqs, num_q_heads, num_kv_heads, head_dim)
+    key = (dev.index, s.cuda_stream)
+    with _ws_lock:
+        ws = _ws_cache.get(key)
+        if ws is None or ws.numel() < need:
+            ws = torch.zeros(max(need, 1 << 20), dtype=torch.uint8, device=dev)
+            _ws_cache[key] = ws
+    return ws
+
+
+def paged_decode_attention(pool: KVPool, block_tables, dirs, seq_lens, q, softmax_scale=None,
+                           out=None, max_seq_len=None, ws=None, stream=None):
+    """bkv_paged_decode_attention.  q: bf16 [B][Hq][d] (any strides with unit last stride).
+    out: bf16 with the same indexing (allocated [B][Hq][d] if None).  Returns out."""
+    p, m = pool.c(), block_map(block_tables, dirs)
+    _dev(seq_lens, "seq_lens", torch.int32)
+    _dev(q, "q", torch.bfloat16)
+    B, Hq, d = q.shape
+    if q.stride(2) != 1:
+        raise BkvError("q must have a unit stride along head_dim")
+    if out is None:
+        out = torch.empty((B, Hq, d), dtype=torch.bfloat16, device=q.device)
+    _dev(out, "out", torch.bfloat16)
+    if out.stride(2) != 1:
+        raise BkvError("out must have a unit stride along head_dim")
+    if softmax_scale is None:
+        softmax_scale = 1.0 / math.sqrt(d)
+    if max_seq_len is None:
+        max_seq_len = block_tables.shape[1] * pool.block_size
+    if ws is None:
+        ws = workspace(B, Hq, pool.num_kv_heads, d, q.device, stream)
+    rc = lib().bkv_paged_decode_attention(
+        ctypes.byref(p), ctypes.byref(m), seq_lens.data_ptr(), int(max_seq_len), q.data_ptr(),
+        q.stride(0), q.stride(1), Hq, float(softmax_scale), out.data_ptr(), out.stride(0),
+        out.stride(1), ws.data_ptr(), ws.numel(), _stream_ptr(stream))
+    _check(rc, "bkv_paged_decode_attention")
+    return out
+
+
+def validate_layout_host(block_tables, dirs, seq_lens, num_blocks, block_size, require_nonempty=True):
+    """Host validator (I1-I4) on CPU tensors / numpy arrays.  Returns (ok, info[5])."""
+    import numpy as np
+    bt = np.ascontiguousarray(np.asarray(block_tables), dtype=np.int32)
+    dd = np.ascontiguousarray(np.asarray(dirs), dtype=np.uint8)
+    ln = np.ascontiguousarray(np.asarray(seq_lens), dtype=np.int32)
+    rs, cs = (1, 0) if dd.ndim == 1 else (dd.shape[1], 1)
+    info = np.zeros(5, dtype=np.int64)
+    rc = lib().bkv_validate_layout_host(bt.ctypes.data, bt.shape[1], dd.ctypes.data, rs, cs,
+                                        ln.shape[0], ln.ctypes.data, int(num_blocks), int(block_size),
+                                        int(bool(require_nonempty)), info.ctypes.data)
+    if rc not in (0, 4):
+        _check(rc, "bkv_validate_layout_host")
+    return rc == 0, [int(x) for x in info]

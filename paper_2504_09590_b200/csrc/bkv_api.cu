@@ -1,0 +1,332 @@
+// bkv_api.cu -- the C ABI of include/bkv.h: argument checks, TMA descriptor
+// encoding, workspace layout, launches, host-side layout validator.
+#include <cudaTypedefs.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+#include <vector>
+
+#include "../../include/bkv.h"
+#include "bkv_internal.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+bkv_status fail(bkv_status s, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+bkv_status fail(bkv_status s, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+bkv_status cuda_fail(cudaError_t e, const char *what) {
+  return fail(BKV_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+bkv_status check_pool(const bkv_kv_pool *pool) {
+  if (!pool) return fail(BKV_ERR_INVALID_ARGUMENT, "pool is NULL");
+  if (!pool->k || !pool->v) return fail(BKV_ERR_INVALID_ARGUMENT, "pool k/v pointer is NULL");
+  if (pool->head_dim != 64 && pool->head_dim != 128)
+    return fail(BKV_ERR_UNSUPPORTED, "head_dim %d not in {64, 128}", pool->head_dim);
+  if (pool->block_size != 16 && pool->block_size != 32)
+    return fail(BKV_ERR_UNSUPPORTED, "block_size %d not in {16, 32}", pool->block_size);
+  if (pool->num_blocks <= 0 || pool->num_kv_heads <= 0)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "num_blocks/num_kv_heads must be positive");
+  if (!aligned16(pool->k) || !aligned16(pool->v))
+    return fail(BKV_ERR_INVALID_ARGUMENT, "pool k/v must be 16-byte aligned");
+  if (pool->stride_block % 8 || pool->stride_head % 8 || pool->stride_slot % 8 ||
+      pool->stride_block <= 0 || pool->stride_head <= 0 || pool->stride_slot < pool->head_dim)
+    return fail(BKV_ERR_INVALID_ARGUMENT,
+                "pool strides must be positive multiples of 8 elements with stride_slot >= head_dim");
+  return BKV_OK;
+}
+
+bkv_status check_map(const bkv_block_map *map) {
+  if (!map) return fail(BKV_ERR_INVALID_ARGUMENT, "block map is NULL");
+  if (map->num_seqs < 0) return fail(BKV_ERR_INVALID_ARGUMENT, "num_seqs < 0");
+  if (map->num_seqs > 0 && (!map->block_tables || !map->dirs))
+    return fail(BKV_ERR_INVALID_ARGUMENT, "block_tables/dirs is NULL");
+  if (map->bt_stride <= 0) return fail(BKV_ERR_INVALID_ARGUMENT, "bt_stride must be positive");
+  if (map->dir_row_stride < 0 || map->dir_col_stride < 0)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "direction strides must be >= 0");
+  return BKV_OK;
+}
+
+// ----------------------------------------------------------- TMA descriptors
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 4-D view (d, slot, head, block) of one pool tensor; box = 64 d x 16 slots,
+// 128-byte swizzle so the decode kernel's ldmatrix/LDS reads are conflict-free.
+bkv_status encode_pool_map(CUtensorMap *m, void *base, const bkv_kv_pool *pool) {
+  auto fn = encode_fn();
+  if (!fn) return fail(BKV_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+  cuuint64_t dims[4] = {(cuuint64_t)pool->head_dim, (cuuint64_t)pool->block_size,
+                        (cuuint64_t)pool->num_kv_heads, (cuuint64_t)pool->num_blocks};
+  cuuint64_t strides[3] = {(cuuint64_t)pool->stride_slot * 2, (cuuint64_t)pool->stride_head * 2,
+                           (cuuint64_t)pool->stride_block * 2};
+  cuuint32_t box[4] = {64, 16, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(BKV_ERR_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)r);
+  return BKV_OK;
+}
+
+// ------------------------------------------------------------ workspace
+struct WsLayout {
+  size_t sched, counters, ml, o, total;
+  int units_max;
+};
+
+size_t up256(size_t x) { return (x + 255) & ~size_t(255); }
+
+bkv_status ws_layout(int B, int Hq, int H, int D, WsLayout *w, bkv::DecodeLaunch *cfg, int *slots,
+                     int *qb) {
+  const int g = Hq / H;
+  cudaError_t e = bkv::decode_config(D, g, B, cfg, slots, qb);
+  if (e != cudaSuccess) return cuda_fail(e, "querying the device");
+  const long long units = (long long)bkv::decode_target_units(*cfg) + (long long)B * H;
+  if (units > (1ll << 30)) return fail(BKV_ERR_INVALID_ARGUMENT, "problem too large");
+  w->units_max = (int)units;
+  w->sched = 0;
+  w->counters = 256;
+  w->ml = w->counters + up256((size_t)B * H * 4);
+  w->o = w->ml + up256((size_t)units * g * 2 * 4);
+  w->total = w->o + up256((size_t)units * g * D * 4);
+  return BKV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *bkv_status_string(bkv_status s) {
+  switch (s) {
+    case BKV_OK: return "BKV_OK";
+    case BKV_ERR_INVALID_ARGUMENT: return "BKV_ERR_INVALID_ARGUMENT";
+    case BKV_ERR_UNSUPPORTED: return "BKV_ERR_UNSUPPORTED";
+    case BKV_ERR_WORKSPACE_TOO_SMALL: return "BKV_ERR_WORKSPACE_TOO_SMALL";
+    case BKV_ERR_LAYOUT: return "BKV_ERR_LAYOUT";
+    case BKV_ERR_CUDA: return "BKV_ERR_CUDA";
+  }
+  return "BKV_ERR_UNKNOWN";
+}
+
+const char *bkv_last_error(void) { return g_err; }
+
+int32_t bkv_version(void) { return 100; }
+
+bkv_status bkv_kv_append(const bkv_kv_pool *pool, const bkv_block_map *map,
+                         const int32_t *seq_lens_before, const int32_t *cu_new_tokens,
+                         int32_t total_new_tokens, const void *k_new, const void *v_new,
+                         int64_t *slot_mapping_out, bkv_stream_t stream) {
+  bkv_status s = check_pool(pool);
+  if (s) return s;
+  if ((s = check_map(map))) return s;
+  if (map->num_seqs == 0 || total_new_tokens == 0) return BKV_OK;
+  if (total_new_tokens < 0) return fail(BKV_ERR_INVALID_ARGUMENT, "total_new_tokens < 0");
+  if (!seq_lens_before || !cu_new_tokens || !k_new || !v_new)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "seq_lens_before/cu_new_tokens/k_new/v_new is NULL");
+  if (!aligned16(k_new) || !aligned16(v_new))
+    return fail(BKV_ERR_INVALID_ARGUMENT, "k_new/v_new must be 16-byte aligned");
+  if (pool->stride_slot != pool->head_dim && pool->stride_slot % 8)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "stride_slot");
+  bkv::AppendParams p;
+  p.k = static_cast<uint16_t *>(pool->k);
+  p.v = static_cast<uint16_t *>(pool->v);
+  p.sb = pool->stride_block;
+  p.sh = pool->stride_head;
+  p.ss = pool->stride_slot;
+  p.H = pool->num_kv_heads;
+  p.bs = pool->block_size;
+  p.bt = map->block_tables;
+  p.bt_stride = map->bt_stride;
+  p.dirs = map->dirs;
+  p.dir_rs = map->dir_row_stride;
+  p.dir_cs = map->dir_col_stride;
+  p.before = seq_lens_before;
+  p.cu_new = cu_new_tokens;
+  p.k_new = static_cast<const uint16_t *>(k_new);
+  p.v_new = static_cast<const uint16_t *>(v_new);
+  p.slot_mapping = slot_mapping_out;
+  p.B = map->num_seqs;
+  cudaError_t e = bkv::launch_kv_append(p, pool->head_dim, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "kv_append launch");
+  return BKV_OK;
+}
+
+size_t bkv_decode_workspace_size(int32_t num_seqs, int32_t num_q_heads, int32_t num_kv_heads,
+                                 int32_t head_dim) {
+  if (num_seqs < 0 || num_kv_heads <= 0 || num_q_heads <= 0 || num_q_heads % num_kv_heads ||
+      (head_dim != 64 && head_dim != 128)) {
+    fail(BKV_ERR_INVALID_ARGUMENT, "bad workspace-size arguments");
+    return 0;
+  }
+  WsLayout w;
+  bkv::DecodeLaunch cfg;
+  int slots, qb;
+  if (ws_layout(num_seqs, num_q_heads, num_kv_heads, head_dim, &w, &cfg, &slots, &qb)) return 0;
+  return w.total;
+}
+
+bkv_status bkv_paged_decode_attention(const bkv_kv_pool *pool, const bkv_block_map *map,
+                                      const int32_t *seq_lens, int32_t max_seq_len,
+                                      const void *q, int64_t q_stride_seq, int64_t q_stride_head,
+                                      int32_t num_q_heads, float softmax_scale, void *out,
+                                      int64_t o_stride_seq, int64_t o_stride_head, void *workspace,
+                                      size_t workspace_bytes, bkv_stream_t stream) {
+  bkv_status s = check_pool(pool);
+  if (s) return s;
+  if ((s = check_map(map))) return s;
+  const int B = map->num_seqs, H = pool->num_kv_heads, D = pool->head_dim;
+  if (B == 0) return BKV_OK;
+  if (B > bkv::kMaxSeqs) return fail(BKV_ERR_UNSUPPORTED, "num_seqs %d > %d", B, bkv::kMaxSeqs);
+  if (!seq_lens || !q || !out || !workspace)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "seq_lens/q/out/workspace is NULL");
+  if (num_q_heads <= 0 || num_q_heads % H)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "num_q_heads %d is not a multiple of num_kv_heads %d",
+                num_q_heads, H);
+  const int g = num_q_heads / H;
+  if (g > bkv::kMaxGroup) return fail(BKV_ERR_UNSUPPORTED, "group %d > %d", g, bkv::kMaxGroup);
+  if (max_seq_len < 0 || (int64_t)max_seq_len > (int64_t)map->bt_stride * pool->block_size)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "max_seq_len %d exceeds bt_stride*block_size", max_seq_len);
+  if (!aligned16(q) || !aligned16(out) || q_stride_seq % 8 || q_stride_head % 8 ||
+      o_stride_seq % 8 || o_stride_head % 8)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "q/out must be 16-byte aligned with strides multiple of 8");
+  if (!(softmax_scale == softmax_scale) || isinf(softmax_scale))
+    return fail(BKV_ERR_INVALID_ARGUMENT, "softmax_scale must be finite");
+  if ((reinterpret_cast<uintptr_t>(workspace) & 255u) != 0)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+  WsLayout w;
+  bkv::DecodeLaunch cfg;
+  int slots, qb;
+  if ((s = ws_layout(B, num_q_heads, H, D, &w, &cfg, &slots, &qb))) return s;
+  if (workspace_bytes < w.total)
+    return fail(BKV_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < required %zu bytes", workspace_bytes,
+                w.total);
+  CUtensorMap tmK, tmV;
+  if ((s = encode_pool_map(&tmK, pool->k, pool))) return s;
+  if ((s = encode_pool_map(&tmV, pool->v, pool))) return s;
+  uint8_t *ws = static_cast<uint8_t *>(workspace);
+  bkv::DecodeParams p;
+  p.bt = map->block_tables;
+  p.bt_stride = map->bt_stride;
+  p.dirs = map->dirs;
+  p.dir_rs = map->dir_row_stride;
+  p.dir_cs = map->dir_col_stride;
+  p.seq_lens = seq_lens;
+  p.B = B;
+  p.H = H;
+  p.bs = pool->block_size;
+  p.g = g;
+  p.q = static_cast<const uint16_t *>(q);
+  p.q_ss = q_stride_seq;
+  p.q_sh = q_stride_head;
+  p.out = static_cast<uint16_t *>(out);
+  p.o_ss = o_stride_seq;
+  p.o_sh = o_stride_head;
+  p.scale_log2 = softmax_scale * 1.4426950408889634f;
+  p.sched = reinterpret_cast<int *>(ws + w.sched);
+  p.counters = reinterpret_cast<int *>(ws + w.counters);
+  p.part_ml = reinterpret_cast<float *>(ws + w.ml);
+  p.part_o = reinterpret_cast<float *>(ws + w.o);
+  p.target_units = bkv::decode_target_units(cfg);
+  p.min_split = bkv::decode_min_split(g);
+  p.units_max = w.units_max;
+  p.slots = slots;
+  p.q_bytes = qb;
+  p.total_warps = cfg.grid * cfg.warps;
+  cudaError_t e = bkv::launch_decode(tmK, tmV, p, D, cfg, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "decode attention launch");
+  return BKV_OK;
+}
+
+bkv_status bkv_validate_layout_host(const int32_t *block_tables, int32_t bt_stride,
+                                    const uint8_t *dirs, int32_t dir_row_stride,
+                                    int32_t dir_col_stride, int32_t num_seqs,
+                                    const int32_t *seq_lens, int32_t num_blocks,
+                                    int32_t block_size, int32_t require_nonempty,
+                                    int64_t info[5]) {
+  if (!info) return fail(BKV_ERR_INVALID_ARGUMENT, "info is NULL");
+  for (int i = 0; i < 5; ++i) info[i] = 0;
+  if (num_seqs < 0 || block_size <= 0 || num_blocks < 0 || bt_stride <= 0)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "bad sizes");
+  if (num_seqs > 0 && (!block_tables || !dirs || !seq_lens))
+    return fail(BKV_ERR_INVALID_ARGUMENT, "NULL input");
+  auto entry = [&](int r, int e) { return block_tables[(int64_t)r * bt_stride + e]; };
+  auto dir = [&](int r, int e) {
+    return dirs[(int64_t)r * dir_row_stride + (int64_t)e * dir_col_stride];
+  };
+  // I4: ranges
+  for (int r = 0; r < num_seqs; ++r) {
+    const int64_t L = seq_lens[r];
+    if (L < 0 || L > (int64_t)bt_stride * block_size || (require_nonempty && L == 0)) {
+      info[0] = 1; info[1] = r; info[2] = -1; info[3] = L;
+      return fail(BKV_ERR_LAYOUT, "I4: seq_len %lld of request %d out of range", (long long)L, r);
+    }
+    const int nb = (int)((L + block_size - 1) / block_size);
+    for (int e = 0; e < nb; ++e) {
+      if (entry(r, e) < 0 || entry(r, e) >= num_blocks || dir(r, e) > 1) {
+        info[0] = 1; info[1] = r; info[2] = e; info[3] = entry(r, e);
+        return fail(BKV_ERR_LAYOUT, "I4: entry %d of request %d invalid", e, r);
+      }
+    }
+  }
+  // I2: at most one forward and one reversed entry per physical block
+  std::vector<int32_t> fwd(num_blocks, -1), rev(num_blocks, -1);
+  for (int r = 0; r < num_seqs; ++r) {
+    const int nb = (int)((seq_lens[r] + block_size - 1) / block_size);
+    for (int e = 0; e < nb; ++e) {
+      std::vector<int32_t> &own = dir(r, e) ? rev : fwd;
+      const int32_t b = entry(r, e);
+      if (own[b] >= 0) {
+        info[0] = 3; info[1] = b; info[2] = dir(r, e); info[3] = own[b]; info[4] = r;
+        return fail(BKV_ERR_LAYOUT, "I2: block %d has two %s entries", b, dir(r, e) ? "reversed" : "forward");
+      }
+      own[b] = r;
+    }
+  }
+  // I1: live slots disjoint.  A forward entry with n live tokens covers slots
+  // [0, n), a reversed one [bs-n, bs); check occupancy per slot.
+  std::vector<int32_t> occ_r((size_t)num_blocks * block_size, -1);
+  std::vector<int64_t> occ_t((size_t)num_blocks * block_size, 0);
+  for (int r = 0; r < num_seqs; ++r) {
+    const int64_t L = seq_lens[r];
+    for (int64_t t = 0; t < L; ++t) {
+      const int e = (int)(t / block_size), j = (int)(t % block_size);
+      const int slot = dir(r, e) ? block_size - 1 - j : j;
+      const size_t k = (size_t)entry(r, e) * block_size + slot;
+      if (occ_r[k] >= 0) {
+        info[0] = 2; info[1] = occ_r[k]; info[2] = occ_t[k]; info[3] = r; info[4] = t;
+        return fail(BKV_ERR_LAYOUT, "I1: token %lld of request %d and token %lld of request %d share a slot",
+                    (long long)occ_t[k], occ_r[k], (long long)t, r);
+      }
+      occ_r[k] = r;
+      occ_t[k] = t;
+    }
+  }
+  return BKV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,68 @@
+// bkv_internal.h -- declarations shared by the bkv translation units (not part
+// of the public ABI; include/bkv.h is).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace bkv {
+
+// ---------------------------------------------------------------- kv_append
+struct AppendParams {
+  uint16_t *k, *v;  // pool (bf16 bits)
+  int64_t sb, sh, ss;
+  int H, bs;
+  const int32_t *bt;
+  int bt_stride;
+  const uint8_t *dirs;
+  int dir_rs, dir_cs;
+  const int32_t *before;
+  const int32_t *cu_new;
+  const uint16_t *k_new, *v_new;
+  int64_t *slot_mapping;  // optional
+  int B;
+};
+cudaError_t launch_kv_append(const AppendParams &p, int head_dim, cudaStream_t s);
+
+// ------------------------------------------------------- decode attention
+struct DecodeParams {
+  const int32_t *bt;
+  int bt_stride;
+  const uint8_t *dirs;
+  int dir_rs, dir_cs;
+  const int32_t *seq_lens;
+  int B, H, bs, g;
+  const uint16_t *q;
+  int64_t q_ss, q_sh;
+  uint16_t *out;
+  int64_t o_ss, o_sh;
+  float scale_log2;      // softmax_scale * log2(e)
+  int *sched;            // [0] next unit, [1] finished warps (self-resetting)
+  int *counters;         // [B*H] split arrival counters (self-resetting)
+  float *part_ml;        // [units_max][g][2]  (m in log2 domain, l)
+  float *part_o;         // [units_max][g][D]  un-normalised partial outputs
+  int target_units;      // split plan: aim for about this many units
+  int min_split;         // split plan: at least this many blocks per unit
+  int units_max;         // workspace capacity in units
+  int slots;             // ring depth per warp (S)
+  int q_bytes;           // smem bytes per q-ring entry
+  int total_warps;       // grid * warps per CTA
+};
+
+struct DecodeLaunch {
+  int grid, warps, smem_bytes;
+};
+
+// Grid / ring configuration for (head_dim, group) on the current device.
+cudaError_t decode_config(int head_dim, int group, int num_seqs, DecodeLaunch *cfg,
+                          int *slots, int *q_bytes);
+int decode_target_units(const DecodeLaunch &cfg);
+int decode_min_split(int group);
+cudaError_t launch_decode(const CUtensorMap &tmK, const CUtensorMap &tmV, const DecodeParams &p,
+                          int head_dim, const DecodeLaunch &cfg, cudaStream_t s);
+
+constexpr int kMaxSeqs = 2048;  // plan arrays live in shared memory
+constexpr int kMaxGroup = 16;   // GQA rows per MMA tile
+
+}  // namespace bkv

@@ -1,0 +1,62 @@
+// kv_append.cu -- direction-aware KV-cache write.
+//
+// in a shared block "KV cache of the RT request occupies memory
+// slots from the left to the right ... that of the BE request in the opposite
+// direction".  New token t of request r goes to block-table entry e = t / bs;
+// slot t % bs for a forward (RT) entry, bs-1 - t % bs for a reversed (BE) one
+// (direction table, readings Q3/Q4).  The copy is bit-exact.
+//
+// One CTA per request; each (token, head, K|V) row of head_dim bf16 is moved
+// by head_dim/8 threads with one 16-byte load and one 16-byte store each, so a
+// warp touches whole 128-byte lines on both sides.  The step is launch-latency
+// bound (a decode step moves 4*B*H*d bytes); NEXT f2 fuses it into attention.
+#include "bkv_internal.h"
+
+namespace bkv {
+
+template <int D>
+__global__ void __launch_bounds__(256) kv_append_kernel(AppendParams p) {
+  constexpr int TPR = D / 8;  // threads per row, 16 B each
+  const int r = blockIdx.x;
+  const int32_t first = p.cu_new[r];
+  const int n = p.cu_new[r + 1] - first;
+  if (n <= 0) return;
+  const int before = p.before[r];
+  const int sub = threadIdx.x % TPR;
+  const int rows = n * p.H * 2;
+  const int64_t bt_row = static_cast<int64_t>(r) * p.bt_stride;
+  const int64_t dir_row = static_cast<int64_t>(r) * p.dir_rs;
+  for (int row = threadIdx.x / TPR; row < rows; row += blockDim.x / TPR) {
+    const int j = row / (2 * p.H);
+    const int rem = row - j * 2 * p.H;
+    const int which = rem / p.H;  // 0 = K, 1 = V
+    const int h = rem - which * p.H;
+    const int t = before + j;
+    const int e = t / p.bs;
+    const int within = t - e * p.bs;
+    const int32_t blk = __ldg(p.bt + bt_row + e);
+    const uint8_t dir = __ldg(p.dirs + dir_row + static_cast<int64_t>(e) * p.dir_cs);
+    const int slot = dir ? (p.bs - 1 - within) : within;
+    const int64_t src = (static_cast<int64_t>(first + j) * p.H + h) * D + sub * 8;
+    const int64_t dst = static_cast<int64_t>(blk) * p.sb + static_cast<int64_t>(h) * p.sh +
+                        static_cast<int64_t>(slot) * p.ss + sub * 8;
+    const uint16_t *s = which ? p.v_new : p.k_new;
+    uint16_t *d = which ? p.v : p.k;
+    const uint4 val = __ldg(reinterpret_cast<const uint4 *>(s + src));
+    *reinterpret_cast<uint4 *>(d + dst) = val;
+    if (p.slot_mapping && which == 0 && h == 0 && sub == 0)
+      p.slot_mapping[first + j] = static_cast<int64_t>(blk) * p.bs + slot;
+  }
+}
+
+cudaError_t launch_kv_append(const AppendParams &p, int head_dim, cudaStream_t s) {
+  if (p.B <= 0) return cudaSuccess;
+  dim3 grid(p.B), block(256);
+  if (head_dim == 128)
+    kv_append_kernel<128><<<grid, block, 0, s>>>(p);
+  else
+    kv_append_kernel<64><<<grid, block, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace bkv
