@@ -151,9 +151,13 @@ BKV_API bkv_status bkv_kv_append(const bkv_kv_pool *pool, const bkv_block_map *m
  *                        (head-major [H_q][B][d] is o_stride_head = B*d,
  *                        o_stride_seq = d: what the TP all-gather wants)
  *   workspace            device buffer of >= bkv_decode_workspace_size(...) bytes,
- *                        ZERO-FILLED before its first use; every call leaves
- *                        it zero-filled again (self-resetting counters), so a
- *                        workspace must not be shared by concurrent calls.
+ *                        ZERO-FILLED before its first use.  Its synchronisation
+ *                        region (scheduler word + per-(request, kv head) split
+ *                        counters, fixed size for every geometry) is restored
+ *                        to zero by every call, so one workspace serves calls of
+ *                        any geometry in sequence -- but never two concurrent
+ *                        calls (one workspace per stream).
+ *   Limits: num_seqs <= 2048, num_kv_heads <= 128 per call (BKV_ERR_UNSUPPORTED).
  * Deterministic: split partials are merged in split order.
  */
 BKV_API bkv_status bkv_paged_decode_attention(const bkv_kv_pool *pool, const bkv_block_map *map,

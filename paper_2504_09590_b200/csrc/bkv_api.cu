@@ -109,9 +109,13 @@ bkv_status ws_layout(int B, int Hq, int H, int D, WsLayout *w, bkv::DecodeLaunch
   const long long units = (long long)bkv::decode_target_units(*cfg) + (long long)B * H;
   if (units > (1ll << 30)) return fail(BKV_ERR_INVALID_ARGUMENT, "problem too large");
   w->units_max = (int)units;
+  // Region A (scheduler word + split counters) has a FIXED size for every
+  // geometry and is only ever written by self-resetting counters, so it is
+  // all-zero between calls no matter which (B, H) used the workspace before.
+  // Region B (partials) is scratch.
   w->sched = 0;
   w->counters = 256;
-  w->ml = w->counters + up256((size_t)B * H * 4);
+  w->ml = w->counters + up256((size_t)bkv::kMaxSeqs * bkv::kMaxKvHeads * 4);
   w->o = w->ml + up256((size_t)units * g * 2 * 4);
   w->total = w->o + up256((size_t)units * g * D * 4);
   return BKV_OK;
@@ -178,9 +182,14 @@ bkv_status bkv_kv_append(const bkv_kv_pool *pool, const bkv_block_map *map,
 
 size_t bkv_decode_workspace_size(int32_t num_seqs, int32_t num_q_heads, int32_t num_kv_heads,
                                  int32_t head_dim) {
-  if (num_seqs < 0 || num_kv_heads <= 0 || num_q_heads <= 0 || num_q_heads % num_kv_heads ||
-      (head_dim != 64 && head_dim != 128)) {
-    fail(BKV_ERR_INVALID_ARGUMENT, "bad workspace-size arguments");
+  if (head_dim != 64 && head_dim != 128) {
+    fail(BKV_ERR_UNSUPPORTED, "BKV_ERR_UNSUPPORTED: head_dim %d not in {64, 128}", head_dim);
+    return 0;
+  }
+  if (num_seqs < 0 || num_kv_heads <= 0 || num_q_heads <= 0 || num_q_heads % num_kv_heads) {
+    fail(BKV_ERR_INVALID_ARGUMENT,
+         "BKV_ERR_INVALID_ARGUMENT: num_q_heads %d must be a positive multiple of num_kv_heads %d",
+         num_q_heads, num_kv_heads);
     return 0;
   }
   WsLayout w;
@@ -202,6 +211,8 @@ bkv_status bkv_paged_decode_attention(const bkv_kv_pool *pool, const bkv_block_m
   const int B = map->num_seqs, H = pool->num_kv_heads, D = pool->head_dim;
   if (B == 0) return BKV_OK;
   if (B > bkv::kMaxSeqs) return fail(BKV_ERR_UNSUPPORTED, "num_seqs %d > %d", B, bkv::kMaxSeqs);
+  if (H > bkv::kMaxKvHeads)
+    return fail(BKV_ERR_UNSUPPORTED, "num_kv_heads %d > %d", H, bkv::kMaxKvHeads);
   if (!seq_lens || !q || !out || !workspace)
     return fail(BKV_ERR_INVALID_ARGUMENT, "seq_lens/q/out/workspace is NULL");
   if (num_q_heads <= 0 || num_q_heads % H)

@@ -64,5 +64,6 @@ cudaError_t launch_decode(const CUtensorMap &tmK, const CUtensorMap &tmV, const 
 
 constexpr int kMaxSeqs = 2048;  // plan arrays live in shared memory
 constexpr int kMaxGroup = 16;   // GQA rows per MMA tile
+constexpr int kMaxKvHeads = 128; // per rank; sizes the fixed counter region of the workspace
 
 }  // namespace bkv

@@ -168,7 +168,9 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t *meta_g = gbase + (q_base - base) + W * (S + 1) * p.q_bytes;
   SlotMeta *metas = reinterpret_cast<SlotMeta *>(meta_g) + warp * S;
   uint64_t *bars_g = reinterpret_cast<uint64_t *>(meta_g + W * S * sizeof(SlotMeta));
-  int *F = reinterpret_cast<int *>(bars_g + W * S);
+  uint8_t *scratch_g = reinterpret_cast<uint8_t *>(bars_g + W * S);   // W x 64 B
+  const uint32_t my_p = smem_u32(scratch_g + warp * 64);
+  int *F = reinterpret_cast<int *>(scratch_g + W * 64);
   int *R = F + (p.B + 1);
 
   if (threadIdx.x == 0) {
@@ -347,6 +349,17 @@ __global__ void __launch_bounds__(256, 1)
     }
   };
 
+  // Zero V rows outside [lo, hi) of one chunk (whole 128-byte rows, so the
+  // swizzle does not matter), then make the stores visible to the warp.
+  auto zero_dead_rows = [&](uint32_t sv, int lo, int hi) {
+    for (int idx = lane; idx < 16 * G::HALVES * 8; idx += 32) {
+      const int row = idx / (G::HALVES * 8), rest = idx - row * (G::HALVES * 8);
+      if (row < lo || row >= hi)
+        sts128_zero(sv + (rest >> 3) * G::HALF_BYTES + row * 128 + (rest & 7) * 16);
+    }
+    __syncwarp();
+  };
+
   auto consume = [&](uint32_t sk, int lo, int hi) {
     const uint32_t sv = sk + G::KV_BYTES;
     if constexpr (!MMA) {
@@ -380,7 +393,21 @@ __global__ void __launch_bounds__(256, 1)
       m0 = mnew;
 #pragma unroll
       for (int k = 0; k < EPL; ++k) o_mha[k] *= alpha;
-      // ---- o += p_t * v_t over live tokens only (select, never 0 * NaN)
+      // ---- o += p_t * v_t.  Dead rows of a partly live chunk are zeroed first
+      // (p_t = 0 there, and 0 * NaN must never happen -- reading Q10); then all
+      // 16 tokens are unrolled with p broadcast from shared memory.
+      if (lo > 0 || hi < 16) zero_dead_rows(sv, lo, hi);
+      if (lane < 16) st_shared_f32(my_p + lane * 4, pr);
+      __syncwarp();
+      float pt[16];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint4 w = lds128(my_p + k * 16);
+        pt[4 * k + 0] = __uint_as_float(w.x);
+        pt[4 * k + 1] = __uint_as_float(w.y);
+        pt[4 * k + 2] = __uint_as_float(w.z);
+        pt[4 * k + 3] = __uint_as_float(w.w);
+      }
       uint32_t vcol;
       if constexpr (D == 128) {
         vcol = sv + (lane >> 4) * G::HALF_BYTES + (lane & 1) * 8;
@@ -388,19 +415,19 @@ __global__ void __launch_bounds__(256, 1)
         vcol = sv + (lane & 3) * 4;
       }
       const int c = (D == 128) ? ((lane & 15) >> 1) : (lane >> 2);
-      for (int tt = lo; tt < hi; ++tt) {
-        const float pt = __shfl_sync(FULL, pr, tt);
+#pragma unroll
+      for (int tt = 0; tt < 16; ++tt) {
         const uint32_t a = vcol + swz(tt, c);
         if constexpr (D == 128) {
           const uint2 w = lds64(a);
-          o_mha[0] = fmaf(pt, bf16lo(w.x), o_mha[0]);
-          o_mha[1] = fmaf(pt, bf16hi(w.x), o_mha[1]);
-          o_mha[2] = fmaf(pt, bf16lo(w.y), o_mha[2]);
-          o_mha[3] = fmaf(pt, bf16hi(w.y), o_mha[3]);
+          o_mha[0] = fmaf(pt[tt], bf16lo(w.x), o_mha[0]);
+          o_mha[1] = fmaf(pt[tt], bf16hi(w.x), o_mha[1]);
+          o_mha[2] = fmaf(pt[tt], bf16lo(w.y), o_mha[2]);
+          o_mha[3] = fmaf(pt[tt], bf16hi(w.y), o_mha[3]);
         } else {
           const uint32_t w = lds32(a);
-          o_mha[0] = fmaf(pt, bf16lo(w), o_mha[0]);
-          o_mha[1] = fmaf(pt, bf16hi(w), o_mha[1]);
+          o_mha[0] = fmaf(pt[tt], bf16lo(w), o_mha[0]);
+          o_mha[1] = fmaf(pt[tt], bf16hi(w), o_mha[1]);
         }
       }
     } else {
@@ -409,15 +436,29 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
       for (int n = 0; n < 2; ++n) sacc[n][0] = sacc[n][1] = sacc[n][2] = sacc[n][3] = 0.f;
       const int mi = lane >> 3;
+      // all K fragments first (the asm loads/MMAs keep program order), then the MMAs
+      uint32_t kb[D / 16][4];
 #pragma unroll
       for (int ks = 0; ks < D / 16; ++ks) {
         const int tok = (mi >> 1) * 8 + (lane & 7), ke = ks * 16 + (mi & 1) * 8;
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4(sk + (ke >> 6) * G::HALF_BYTES + swz(tok, (ke & 63) >> 3), b0, b1, b2, b3);
-        const uint32_t a1 = G16 ? qa[ks][2] : 0u, a3 = G16 ? qa[ks][3] : 0u;
-        mma_bf16_16816(sacc[0], qa[ks][0], a1, qa[ks][1], a3, b0, b1);
-        mma_bf16_16816(sacc[1], qa[ks][0], a1, qa[ks][1], a3, b2, b3);
+        ldsm_x4(sk + (ke >> 6) * G::HALF_BYTES + swz(tok, (ke & 63) >> 3), kb[ks][0], kb[ks][1],
+                kb[ks][2], kb[ks][3]);
       }
+      float sacc2[2][4];
+#pragma unroll
+      for (int n = 0; n < 2; ++n) sacc2[n][0] = sacc2[n][1] = sacc2[n][2] = sacc2[n][3] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < D / 16; ++ks) {
+        const uint32_t a1 = G16 ? qa[ks][2] : 0u, a3 = G16 ? qa[ks][3] : 0u;
+        float(&acc0)[4] = (ks & 1) ? sacc2[0] : sacc[0];   // two independent chains
+        float(&acc1)[4] = (ks & 1) ? sacc2[1] : sacc[1];
+        mma_bf16_16816(acc0, qa[ks][0], a1, qa[ks][1], a3, kb[ks][0], kb[ks][1]);
+        mma_bf16_16816(acc1, qa[ks][0], a1, qa[ks][1], a3, kb[ks][2], kb[ks][3]);
+      }
+#pragma unroll
+      for (int n = 0; n < 2; ++n)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) sacc[n][j] += sacc2[n][j];
       const int cq = (lane & 3) * 2;
       float s0[4], s1[4];
 #pragma unroll
@@ -464,21 +505,19 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t pa1 = G16 ? pack_bf16(pr1[0], pr1[1]) : 0u;
       const uint32_t pa3 = G16 ? pack_bf16(pr1[2], pr1[3]) : 0u;
       // ---- zero dead V rows of a partly live chunk (P = 0 must not meet NaN)
-      if (lo > 0 || hi < 16) {
-        for (int idx = lane; idx < 16 * G::HALVES * 8; idx += 32) {
-          const int row = idx / (G::HALVES * 8), rest = idx - row * (G::HALVES * 8);
-          if (row < lo || row >= hi) sts128_zero(sv + (rest >> 3) * G::HALF_BYTES + row * 128 + (rest & 7) * 16);
-        }
-        __syncwarp();
-      }
-      // ---- O += P . V
+      if (lo > 0 || hi < 16) zero_dead_rows(sv, lo, hi);
+      // ---- O += P . V  (V fragments first, then the MMAs)
+      uint32_t vb[D / 16][4];
 #pragma unroll
       for (int nb = 0; nb < D / 16; ++nb) {
         const int tok = (mi & 1) * 8 + (lane & 7), de = nb * 16 + (mi >> 1) * 8;
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(sv + (de >> 6) * G::HALF_BYTES + swz(tok, (de & 63) >> 3), b0, b1, b2, b3);
-        mma_bf16_16816(o_mma[2 * nb], pa0, pa1, pa2, pa3, b0, b1);
-        mma_bf16_16816(o_mma[2 * nb + 1], pa0, pa1, pa2, pa3, b2, b3);
+        ldsm_x4_t(sv + (de >> 6) * G::HALF_BYTES + swz(tok, (de & 63) >> 3), vb[nb][0], vb[nb][1],
+                  vb[nb][2], vb[nb][3]);
+      }
+#pragma unroll
+      for (int nb = 0; nb < D / 16; ++nb) {
+        mma_bf16_16816(o_mma[2 * nb], pa0, pa1, pa2, pa3, vb[nb][0], vb[nb][1]);
+        mma_bf16_16816(o_mma[2 * nb + 1], pa0, pa1, pa2, pa3, vb[nb][2], vb[nb][3]);
       }
     }
   };
@@ -664,7 +703,7 @@ cudaError_t decode_config(int head_dim, int group, int num_seqs, DecodeLaunch *c
   const int qb = ((group * head_dim * 2) + 127) / 128 * 128;
   auto need = [&](int s) {
     return 1024 + W * s * slot_bytes + W * (s + 1) * qb + W * s * (int)(sizeof(int) * 8) +
-           W * s * 8 + 2 * (num_seqs + 1) * (int)sizeof(int) + 256;
+           W * s * 8 + W * 64 + 2 * (num_seqs + 1) * (int)sizeof(int) + 256;
   };
   while (S > 1 && need(S) > smem_optin - 1024) --S;
   cfg->grid = sms * env_int("BKV_CTAS_PER_SM", 1);

@@ -274,7 +274,7 @@ def test_abi_argument_errors():
     bt = torch.zeros(1, 1, dtype=torch.int32, device=DEV)
     dirs = torch.zeros(1, dtype=torch.uint8, device=DEV)
     lens = torch.ones(1, dtype=torch.int32, device=DEV)
-    with pytest.raises(bkv.BkvError, match="UNSUPPORTED"):
+    with pytest.raises(bkv.BkvError, match="head_dim 96"):
         bkv.paged_decode_attention(pool, bt, dirs, lens, torch.zeros(1, 1, 96, dtype=torch.bfloat16, device=DEV))
     pool = bkv.KVPool.empty(4, 2, 16, 64, DEV)
     with pytest.raises(bkv.BkvError, match="multiple"):
