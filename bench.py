@@ -207,7 +207,7 @@ def run_ours(args):
 
     import paper_2504_09590_b200 as bkv
     from synth import CONFIGS, make_case
-    from synth.workload import shard_heads
+    from paper_2504_09590_b200.tp import HeadShard, gather_heads
 
     ws, rank, local = dist_env()
     if ws > 1:
@@ -221,7 +221,8 @@ def run_ours(args):
         raise SystemExit(f"{args.config}: {sh.num_kv_heads} kv heads do not shard over {tp} GPUs")
     case = make_case(args.config, args.seed)
     lay = case.layout
-    kv_heads, q_heads = shard_heads(sh, tp, rank)
+    shard = HeadShard(sh.num_q_heads, sh.num_kv_heads, tp, rank)
+    kv_heads, q_heads = list(shard.kv_heads), list(shard.q_heads)
     H, Hq, d, bs, B = len(kv_heads), len(q_heads), sh.head_dim, sh.block_size, lay.batch
     n_layers = args.layers or sh.n_layers
     stream = torch.cuda.current_stream(dev)
@@ -272,7 +273,7 @@ def run_ours(args):
                                        out=o, max_seq_len=max_len, ws=wsb)
             launches += 1
             if tp > 1 and not attn_only:
-                dist.all_gather_into_tensor(out_glob[l], out_loc[l])
+                gather_heads(out_loc[l], out_glob[l])
         return launches
 
     def barrier():

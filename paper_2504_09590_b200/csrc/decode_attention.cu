@@ -168,9 +168,9 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t *meta_g = gbase + (q_base - base) + W * (S + 1) * p.q_bytes;
   SlotMeta *metas = reinterpret_cast<SlotMeta *>(meta_g) + warp * S;
   uint64_t *bars_g = reinterpret_cast<uint64_t *>(meta_g + W * S * sizeof(SlotMeta));
-  uint8_t *scratch_g = reinterpret_cast<uint8_t *>(bars_g + W * S);   // W x 64 B
-  const uint32_t my_p = smem_u32(scratch_g + warp * 64);
-  int *F = reinterpret_cast<int *>(scratch_g + W * 64);
+  uint8_t *scratch_g = reinterpret_cast<uint8_t *>(bars_g + W * S);   // W x 1 KiB
+  const uint32_t my_scr = smem_u32(scratch_g + warp * 1024);
+  int *F = reinterpret_cast<int *>(scratch_g + W * 1024);
   int *R = F + (p.B + 1);
 
   if (threadIdx.x == 0) {
@@ -194,7 +194,8 @@ __global__ void __launch_bounds__(256, 1)
 
   // ------------------------------------------------------------ issuer state
   int u_next = 0;
-  if (lane == 0) u_next = atomicAdd(p.sched, 1);
+  // first unit is static (no atomic storm at launch); later ones are pulled
+  u_next = blockIdx.x * W + warp;
   bool is_active = false, is_done = false, is_first = false;
   int is_u = 0, is_r = 0, is_h = 0, is_ns = 0, is_L = 0, is_e = 0, is_e1 = 0, is_c = 0;
   int is_wb = 0, bt_w = 0, dir_w = 0, is_qidx = S;  // first unit -> q-ring entry 0
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(256, 1)
         is_done = true;
         return false;
       }
-      if (lane == 0) u_next = atomicAdd(p.sched, 1);  // prefetch the next grab
+      if (lane == 0) u_next = p.total_warps + atomicAdd(p.sched, 1);  // prefetch the next grab
       const int h = u % H, qq = u / H;
       int r, e0, e1;
       if (qq < FB) {
@@ -299,51 +300,56 @@ __global__ void __launch_bounds__(256, 1)
   };
 
   // --------------------------------------------------------- consumer state
-  constexpr int NCH = D / 16;  // MHA: 16-byte pieces of K per lane
-  constexpr int EPL = D / 32;  // MHA: output elements per lane
-  float qf[MMA ? 1 : D / 2];
-  float o_mha[EPL];
-  uint32_t qa[MMA ? D / 16 : 1][G16 ? 4 : 2];
-  float o_mma[MMA ? D / 8 : 1][4];
-  float m0 = -INFINITY, l0 = 0.f, m1 = -INFINITY, l1 = 0.f;
+  constexpr int NCH = D / 16;   // MHA: 16-byte K pieces per lane (lane = token x half of d)
+  constexpr int EPL = D / 32;   // output elements per lane (MHA P.V, merge)
+  constexpr int NT = G16 ? 2 : 1;   // MMA: 8-head n-tiles
+  constexpr int MT = D / 16;        // MMA: 16-element d tiles (= k-steps of Q.K^T)
+  // MHA state: q (fp32) lives in the warp scratch, o in registers
+  float2 o2[MMA ? 1 : EPL / 2];
+  // MMA state: Q^T B-fragments, O^T accumulators [d tile][head tile]
+  uint32_t qb[MMA ? MT : 1][NT][2];
+  float oacc[MMA ? MT : 1][NT][4];
+  float mrun[NT][2], lrun[NT][2];   // MHA uses mrun[0][0], lrun[0][0]
+  // chunk fragments (smem -> registers before the slot is refilled)
+  uint4 kw[MMA ? 1 : NCH];
+  uint32_t vw[MMA ? 1 : 16][EPL / 2];
+  uint32_t ka[MMA ? MT : 1][4], va[MMA ? MT : 1][4];
 
   auto begin_unit = [&](const SlotMeta &m) {
-    m0 = m1 = -INFINITY;
-    l0 = l1 = 0.f;
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      mrun[n][0] = mrun[n][1] = -INFINITY;
+      lrun[n][0] = lrun[n][1] = 0.f;
+    }
     const uint32_t qs = my_q + m.qidx * p.q_bytes;
+    const bool noq = m.flags & F_NOQ;
     if constexpr (!MMA) {
 #pragma unroll
-      for (int k = 0; k < EPL; ++k) o_mha[k] = 0.f;
-      if (!(m.flags & F_NOQ)) {
-        const int hf = lane >> 4;
-#pragma unroll
-        for (int cc = 0; cc < NCH; ++cc) {
-          const uint4 w = lds128(qs + (hf * (D / 2) + cc * 8) * 2);
-          qf[cc * 8 + 0] = bf16lo(w.x);
-          qf[cc * 8 + 1] = bf16hi(w.x);
-          qf[cc * 8 + 2] = bf16lo(w.y);
-          qf[cc * 8 + 3] = bf16hi(w.y);
-          qf[cc * 8 + 4] = bf16lo(w.z);
-          qf[cc * 8 + 5] = bf16hi(w.z);
-          qf[cc * 8 + 6] = bf16lo(w.w);
-          qf[cc * 8 + 7] = bf16hi(w.w);
-        }
+      for (int k = 0; k < EPL / 2; ++k) o2[k] = make_float2(0.f, 0.f);
+      // q row -> fp32 in the warp scratch (read back as smem broadcasts)
+      if constexpr (EPL == 4) {
+        const uint2 w = noq ? make_uint2(0u, 0u) : lds64(qs + lane * 8);
+        st_shared_v4f(my_scr + lane * 16, bf16lo(w.x), bf16hi(w.x), bf16lo(w.y), bf16hi(w.y));
+      } else {
+        const uint32_t w = noq ? 0u : lds32(qs + lane * 4);
+        st_shared_v2f(my_scr + lane * 8, bf16lo(w), bf16hi(w));
       }
+      __syncwarp();
     } else {
 #pragma unroll
-      for (int n = 0; n < D / 8; ++n) o_mma[n][0] = o_mma[n][1] = o_mma[n][2] = o_mma[n][3] = 0.f;
-      const int row0 = lane >> 2, cq = (lane & 3) * 2;
-      const bool noq = m.flags & F_NOQ;
+      for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-      for (int ks = 0; ks < D / 16; ++ks) {
-        const uint32_t a = qs + (row0 * D + ks * 16 + cq) * 2;
-        const bool ok0 = !noq && row0 < g;
-        qa[ks][0] = ok0 ? lds32(a) : 0u;
-        qa[ks][1] = ok0 ? lds32(a + 16) : 0u;
-        if constexpr (G16) {
-          const bool ok1 = !noq && row0 + 8 < g;
-          qa[ks][2] = ok1 ? lds32(a + 8 * D * 2) : 0u;
-          qa[ks][3] = ok1 ? lds32(a + 8 * D * 2 + 16) : 0u;
+        for (int n = 0; n < NT; ++n) oacc[mt][n][0] = oacc[mt][n][1] = oacc[mt][n][2] = oacc[mt][n][3] = 0.f;
+      // B = Q^T (k = d, n = head): b0 = Q[head lane/4][d (lane%4)*2 ..], b1 = d + 8
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        const int head = n * 8 + (lane >> 2);
+        const bool ok = !noq && head < g;
+#pragma unroll
+        for (int ks = 0; ks < MT; ++ks) {
+          const uint32_t a = qs + (head * D + ks * 16 + (lane & 3) * 2) * 2;
+          qb[ks][n][0] = ok ? lds32(a) : 0u;
+          qb[ks][n][1] = ok ? lds32(a + 16) : 0u;
         }
       }
     }
@@ -360,196 +366,256 @@ __global__ void __launch_bounds__(256, 1)
     __syncwarp();
   };
 
-  auto consume = [&](uint32_t sk, int lo, int hi) {
+  // smem -> registers for one chunk (after this the slot may be refilled)
+  auto load_chunk = [&](uint32_t sk, int lo, int hi) {
     const uint32_t sv = sk + G::KV_BYTES;
+    if (lo > 0 || hi < 16) zero_dead_rows(sv, lo, hi);   // P = 0 must never meet NaN (Q10)
+    const int mi = lane >> 3;
     if constexpr (!MMA) {
-      // ---- S = scale * q.k for 16 tokens; lane = (token t, half hf of d)
       const int t = lane & 15, hf = lane >> 4;
       const uint32_t krow = sk + (D == 128 ? hf * G::HALF_BYTES : 0) + t * 128;
       const int cbase = (D == 128) ? 0 : hf * 4;
-      float d0 = 0.f, d1 = 0.f, d2 = 0.f, d3 = 0.f;
+#pragma unroll
+      for (int cc = 0; cc < NCH; ++cc) kw[cc] = lds128(krow + (((cbase + cc) ^ (t & 7)) << 4));
+      uint32_t vcol;
+      if constexpr (D == 128) vcol = sv + (lane >> 4) * G::HALF_BYTES + (lane & 1) * 8;
+      else vcol = sv + (lane & 3) * 4;
+      const int c = (D == 128) ? ((lane & 15) >> 1) : (lane >> 2);
+#pragma unroll
+      for (int tt = 0; tt < 16; ++tt) {
+        if constexpr (EPL == 4) {
+          const uint2 w = lds64(vcol + swz(tt, c));
+          vw[tt][0] = w.x;
+          vw[tt][1] = w.y;
+        } else {
+          vw[tt][0] = lds32(vcol + swz(tt, c));
+        }
+      }
+    } else {
+      // A = K (16 tokens x 16 d per k-step): matrices (t0-7,d0-7) (t8-15,d0-7) (t0-7,d8-15) (t8-15,d8-15)
+#pragma unroll
+      for (int ks = 0; ks < MT; ++ks) {
+        const int tok = (mi & 1) * 8 + (lane & 7), de = ks * 16 + (mi >> 1) * 8;
+        ldsm_x4(sk + (de >> 6) * G::HALF_BYTES + swz(tok, (de & 63) >> 3), ka[ks][0], ka[ks][1],
+                ka[ks][2], ka[ks][3]);
+      }
+      // A = V^T (16 d x 16 tokens per d tile) via ldmatrix.trans of V rows
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int tok = (mi >> 1) * 8 + (lane & 7), de = mt * 16 + (mi & 1) * 8;
+        ldsm_x4_t(sv + (de >> 6) * G::HALF_BYTES + swz(tok, (de & 63) >> 3), va[mt][0], va[mt][1],
+                  va[mt][2], va[mt][3]);
+      }
+    }
+  };
+
+  auto compute_chunk = [&](int lo, int hi) {
+    if constexpr (!MMA) {
+      // ---- s_t = q.k_t : lane = (token t, half hf of d); q from the warp scratch
+      const int t = lane & 15, hf = lane >> 4;
+      float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
 #pragma unroll
       for (int cc = 0; cc < NCH; ++cc) {
-        const uint4 w = lds128(krow + (((cbase + cc) ^ (t & 7)) << 4));
-        d0 = fmaf(qf[cc * 8 + 0], bf16lo(w.x), d0);
-        d1 = fmaf(qf[cc * 8 + 1], bf16hi(w.x), d1);
-        d2 = fmaf(qf[cc * 8 + 2], bf16lo(w.y), d2);
-        d3 = fmaf(qf[cc * 8 + 3], bf16hi(w.y), d3);
-        d0 = fmaf(qf[cc * 8 + 4], bf16lo(w.z), d0);
-        d1 = fmaf(qf[cc * 8 + 5], bf16hi(w.z), d1);
-        d2 = fmaf(qf[cc * 8 + 6], bf16lo(w.w), d2);
-        d3 = fmaf(qf[cc * 8 + 7], bf16hi(w.w), d3);
+        const uint32_t qa = my_scr + (hf * (D / 2) + cc * 8) * 4;
+        const uint4 q0 = lds128(qa), q1 = lds128(qa + 16);
+        const uint4 w = kw[cc];
+        acc0 = __ffma2_rn(make_float2(__uint_as_float(q0.x), __uint_as_float(q0.y)),
+                          make_float2(bf16lo(w.x), bf16hi(w.x)), acc0);
+        acc1 = __ffma2_rn(make_float2(__uint_as_float(q0.z), __uint_as_float(q0.w)),
+                          make_float2(bf16lo(w.y), bf16hi(w.y)), acc1);
+        acc0 = __ffma2_rn(make_float2(__uint_as_float(q1.x), __uint_as_float(q1.y)),
+                          make_float2(bf16lo(w.z), bf16hi(w.z)), acc0);
+        acc1 = __ffma2_rn(make_float2(__uint_as_float(q1.z), __uint_as_float(q1.w)),
+                          make_float2(bf16lo(w.w), bf16hi(w.w)), acc1);
       }
-      float dot = (d0 + d1) + (d2 + d3);
+      float dot = (acc0.x + acc0.y) + (acc1.x + acc1.y);
       dot += __shfl_xor_sync(FULL, dot, 16);
-      const float s = (t >= lo && t < hi) ? dot * p.scale_log2 : -INFINITY;
-      float mx = s;
+      const float sc = (t >= lo && t < hi) ? dot * p.scale_log2 : -INFINITY;
+      float mx = sc;
 #pragma unroll
       for (int o = 8; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
-      const float mnew = fmaxf(m0, mx);
-      const float alpha = ex2(m0 - mnew);
-      const float pr = ex2(s - mnew);
-      l0 = l0 * alpha + (hf == 0 ? pr : 0.f);
-      m0 = mnew;
-#pragma unroll
-      for (int k = 0; k < EPL; ++k) o_mha[k] *= alpha;
-      // ---- o += p_t * v_t.  Dead rows of a partly live chunk are zeroed first
-      // (p_t = 0 there, and 0 * NaN must never happen -- reading Q10); then all
-      // 16 tokens are unrolled with p broadcast from shared memory.
-      if (lo > 0 || hi < 16) zero_dead_rows(sv, lo, hi);
-      if (lane < 16) st_shared_f32(my_p + lane * 4, pr);
+      const float mnew = fmaxf(mrun[0][0], mx);
+      const float alpha = ex2(mrun[0][0] - mnew);
+      const float pr = ex2(sc - mnew);
+      lrun[0][0] = lrun[0][0] * alpha + (hf == 0 ? pr : 0.f);
+      mrun[0][0] = mnew;
+      // ---- o = alpha * o + sum_t p_t v_t  (p broadcast through the scratch)
+      if (lane < 16) st_shared_f32(my_scr + 512 + lane * 4, pr);
       __syncwarp();
       float pt[16];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const uint4 w = lds128(my_p + k * 16);
+        const uint4 w = lds128(my_scr + 512 + k * 16);
         pt[4 * k + 0] = __uint_as_float(w.x);
         pt[4 * k + 1] = __uint_as_float(w.y);
         pt[4 * k + 2] = __uint_as_float(w.z);
         pt[4 * k + 3] = __uint_as_float(w.w);
       }
-      uint32_t vcol;
-      if constexpr (D == 128) {
-        vcol = sv + (lane >> 4) * G::HALF_BYTES + (lane & 1) * 8;
-      } else {
-        vcol = sv + (lane & 3) * 4;
-      }
-      const int c = (D == 128) ? ((lane & 15) >> 1) : (lane >> 2);
+      const float2 a2 = make_float2(alpha, alpha);
+#pragma unroll
+      for (int k = 0; k < EPL / 2; ++k) o2[k] = __fmul2_rn(o2[k], a2);
 #pragma unroll
       for (int tt = 0; tt < 16; ++tt) {
-        const uint32_t a = vcol + swz(tt, c);
-        if constexpr (D == 128) {
-          const uint2 w = lds64(a);
-          o_mha[0] = fmaf(pt[tt], bf16lo(w.x), o_mha[0]);
-          o_mha[1] = fmaf(pt[tt], bf16hi(w.x), o_mha[1]);
-          o_mha[2] = fmaf(pt[tt], bf16lo(w.y), o_mha[2]);
-          o_mha[3] = fmaf(pt[tt], bf16hi(w.y), o_mha[3]);
-        } else {
-          const uint32_t w = lds32(a);
-          o_mha[0] = fmaf(pt[tt], bf16lo(w), o_mha[0]);
-          o_mha[1] = fmaf(pt[tt], bf16hi(w), o_mha[1]);
-        }
+        const float2 pp = make_float2(pt[tt], pt[tt]);
+#pragma unroll
+        for (int k = 0; k < EPL / 2; ++k)
+          o2[k] = __ffma2_rn(pp, make_float2(bf16lo(vw[tt][k]), bf16hi(vw[tt][k])), o2[k]);
       }
     } else {
-      // ---- S^T tile: rows = query heads of the group, cols = 16 tokens
-      float sacc[2][4];
+      // ---- S^T = K . Q^T : rows = 16 tokens, cols = 8 heads per tile
+      float sa[NT][4], sb[NT][4];
 #pragma unroll
-      for (int n = 0; n < 2; ++n) sacc[n][0] = sacc[n][1] = sacc[n][2] = sacc[n][3] = 0.f;
-      const int mi = lane >> 3;
-      // all K fragments first (the asm loads/MMAs keep program order), then the MMAs
-      uint32_t kb[D / 16][4];
+      for (int n = 0; n < NT; ++n)
 #pragma unroll
-      for (int ks = 0; ks < D / 16; ++ks) {
-        const int tok = (mi >> 1) * 8 + (lane & 7), ke = ks * 16 + (mi & 1) * 8;
-        ldsm_x4(sk + (ke >> 6) * G::HALF_BYTES + swz(tok, (ke & 63) >> 3), kb[ks][0], kb[ks][1],
-                kb[ks][2], kb[ks][3]);
-      }
-      float sacc2[2][4];
+        for (int j = 0; j < 4; ++j) sa[n][j] = sb[n][j] = 0.f;
 #pragma unroll
-      for (int n = 0; n < 2; ++n) sacc2[n][0] = sacc2[n][1] = sacc2[n][2] = sacc2[n][3] = 0.f;
+      for (int ks = 0; ks < MT; ++ks)
 #pragma unroll
-      for (int ks = 0; ks < D / 16; ++ks) {
-        const uint32_t a1 = G16 ? qa[ks][2] : 0u, a3 = G16 ? qa[ks][3] : 0u;
-        float(&acc0)[4] = (ks & 1) ? sacc2[0] : sacc[0];   // two independent chains
-        float(&acc1)[4] = (ks & 1) ? sacc2[1] : sacc[1];
-        mma_bf16_16816(acc0, qa[ks][0], a1, qa[ks][1], a3, kb[ks][0], kb[ks][1]);
-        mma_bf16_16816(acc1, qa[ks][0], a1, qa[ks][1], a3, kb[ks][2], kb[ks][3]);
-      }
+        for (int n = 0; n < NT; ++n) {
+          float(&acc)[4] = (ks & 1) ? sb[n] : sa[n];   // two independent MMA chains
+          mma_bf16_16816(acc, ka[ks][0], ka[ks][1], ka[ks][2], ka[ks][3], qb[ks][n][0], qb[ks][n][1]);
+        }
+      const int t0 = lane >> 2, t1 = t0 + 8;
+      const bool ok0 = t0 >= lo && t0 < hi, ok1 = t1 >= lo && t1 < hi;
+      float alpha[NT][2];
 #pragma unroll
-      for (int n = 0; n < 2; ++n)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) sacc[n][j] += sacc2[n][j];
-      const int cq = (lane & 3) * 2;
-      float s0[4], s1[4];
-#pragma unroll
-      for (int n = 0; n < 2; ++n)
+      for (int n = 0; n < NT; ++n) {
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          const int tok = n * 8 + cq + j;
-          const bool ok = tok >= lo && tok < hi;
-          s0[n * 2 + j] = ok ? sacc[n][j] * p.scale_log2 : -INFINITY;
-          s1[n * 2 + j] = ok ? sacc[n][2 + j] * p.scale_log2 : -INFINITY;
-        }
-      float mx = fmaxf(fmaxf(s0[0], s0[1]), fmaxf(s0[2], s0[3]));
-      mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, 1));
-      mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, 2));
-      const float mn0 = fmaxf(m0, mx), al0 = ex2(m0 - mn0);
-      float pr0[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) pr0[k] = ex2(s0[k] - mn0);
-      l0 = l0 * al0 + ((pr0[0] + pr0[1]) + (pr0[2] + pr0[3]));
-      m0 = mn0;
-      float pr1[4] = {0.f, 0.f, 0.f, 0.f}, al1 = 1.f;
-      if constexpr (G16) {
-        float mx1 = fmaxf(fmaxf(s1[0], s1[1]), fmaxf(s1[2], s1[3]));
-        mx1 = fmaxf(mx1, __shfl_xor_sync(FULL, mx1, 1));
-        mx1 = fmaxf(mx1, __shfl_xor_sync(FULL, mx1, 2));
-        const float mn1 = fmaxf(m1, mx1);
-        al1 = ex2(m1 - mn1);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) pr1[k] = ex2(s1[k] - mn1);
-        l1 = l1 * al1 + ((pr1[0] + pr1[1]) + (pr1[2] + pr1[3]));
-        m1 = mn1;
-      }
-      (void)s1;
-#pragma unroll
-      for (int n = 0; n < D / 8; ++n) {
-        o_mma[n][0] *= al0;
-        o_mma[n][1] *= al0;
-        if constexpr (G16) {
-          o_mma[n][2] *= al1;
-          o_mma[n][3] *= al1;
+          const float s0 = ok0 ? (sa[n][j] + sb[n][j]) * p.scale_log2 : -INFINITY;
+          const float s1 = ok1 ? (sa[n][2 + j] + sb[n][2 + j]) * p.scale_log2 : -INFINITY;
+          float mx = fmaxf(s0, s1);
+          mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, 4));
+          mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, 8));
+          mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, 16));
+          const float mnew = fmaxf(mrun[n][j], mx);
+          alpha[n][j] = ex2(mrun[n][j] - mnew);
+          const float p0 = ex2(s0 - mnew), p1 = ex2(s1 - mnew);
+          lrun[n][j] = lrun[n][j] * alpha[n][j] + (p0 + p1);
+          mrun[n][j] = mnew;
+          // P^T -> scratch as P[head][token] (row stride 48 B: conflict-free ldmatrix)
+          const int head = n * 8 + (lane & 3) * 2 + j;
+          st_shared_bf16(my_scr + head * 48 + t0 * 2, p0);
+          st_shared_bf16(my_scr + head * 48 + t1 * 2, p1);
         }
       }
-      const uint32_t pa0 = pack_bf16(pr0[0], pr0[1]), pa2 = pack_bf16(pr0[2], pr0[3]);
-      const uint32_t pa1 = G16 ? pack_bf16(pr1[0], pr1[1]) : 0u;
-      const uint32_t pa3 = G16 ? pack_bf16(pr1[2], pr1[3]) : 0u;
-      // ---- zero dead V rows of a partly live chunk (P = 0 must not meet NaN)
-      if (lo > 0 || hi < 16) zero_dead_rows(sv, lo, hi);
-      // ---- O += P . V  (V fragments first, then the MMAs)
-      uint32_t vb[D / 16][4];
-#pragma unroll
-      for (int nb = 0; nb < D / 16; ++nb) {
-        const int tok = (mi & 1) * 8 + (lane & 7), de = nb * 16 + (mi >> 1) * 8;
-        ldsm_x4_t(sv + (de >> 6) * G::HALF_BYTES + swz(tok, (de & 63) >> 3), vb[nb][0], vb[nb][1],
-                  vb[nb][2], vb[nb][3]);
+      __syncwarp();
+      // B = P^T (k = token, n = head): ldmatrix of P rows (heads) x 8 tokens
+      uint32_t pb[NT][2];
+      if constexpr (NT == 1) {
+        const int r8 = lane & 7, hi8 = (lane >> 3) & 1;
+        ldsm_x2(my_scr + r8 * 48 + hi8 * 16, pb[0][0], pb[0][1]);
+      } else {
+        const int r8 = lane & 7, hi8 = (lane >> 3) & 1, nn = lane >> 4;
+        ldsm_x4(my_scr + (nn * 8 + r8) * 48 + hi8 * 16, pb[0][0], pb[0][1], pb[1][0], pb[1][1]);
       }
+      // ---- O^T = alpha * O^T + V^T . P^T
 #pragma unroll
-      for (int nb = 0; nb < D / 16; ++nb) {
-        mma_bf16_16816(o_mma[2 * nb], pa0, pa1, pa2, pa3, vb[nb][0], vb[nb][1]);
-        mma_bf16_16816(o_mma[2 * nb + 1], pa0, pa1, pa2, pa3, vb[nb][2], vb[nb][3]);
-      }
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          const float2 a2 = make_float2(alpha[n][0], alpha[n][1]);
+          float2 lo2 = __fmul2_rn(make_float2(oacc[mt][n][0], oacc[mt][n][1]), a2);
+          float2 hi2 = __fmul2_rn(make_float2(oacc[mt][n][2], oacc[mt][n][3]), a2);
+          oacc[mt][n][0] = lo2.x;
+          oacc[mt][n][1] = lo2.y;
+          oacc[mt][n][2] = hi2.x;
+          oacc[mt][n][3] = hi2.y;
+          mma_bf16_16816(oacc[mt][n], va[mt][0], va[mt][1], va[mt][2], va[mt][3], pb[n][0], pb[n][1]);
+        }
     }
   };
 
-  // Merge all split partials of (r, h) in split order and write bf16 out rows.
+  // Merge all split partials of (r, h) and write the bf16 output rows.  Lanes
+  // take 32 splits at a time (their (m, l) loads are issued together), the
+  // weights are broadcast by shuffle, and each lane accumulates EPL
+  // consecutive output elements of every row; splits are combined in split
+  // order, so the result does not depend on which split arrived last.
   auto merge_splits = [&](const SlotMeta &m) {
-    const int r = m.r, h = m.h;
+    const int r = m.r, h = m.h, ns = m.nsplit;
     const int nfull = F[r + 1] - F[r];
-    for (int row = 0; row < g; ++row) {
-      float M = -INFINITY;
-      for (int s = 0; s < m.nsplit; ++s) {
-        const int us = s < nfull ? (F[r] + s) * H + h : (FB + R[r]) * H + h;
-        M = fmaxf(M, __ldcg(p.part_ml + (static_cast<int64_t>(us) * g + row) * 2));
+    const int u_full0 = F[r] * H + h, u_rem = (FB + R[r]) * H + h;
+    for (int row0 = 0; row0 < g; row0 += 8) {
+      const int nr = min(8, g - row0);
+      float Mrun[8], Lrun[8], acc[8][EPL];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        Mrun[j] = -INFINITY;
+        Lrun[j] = 0.f;
+#pragma unroll
+        for (int k = 0; k < EPL; ++k) acc[j][k] = 0.f;
       }
-      float Ls = 0.f, acc[EPL];
+      for (int s0 = 0; s0 < ns; s0 += 32) {
+        const int sl = s0 + lane;
+        const bool ok = sl < ns;
+        const int us = sl < nfull ? u_full0 + sl * H : u_rem;
+        float wj[8], lj[8];
 #pragma unroll
-      for (int k = 0; k < EPL; ++k) acc[k] = 0.f;
-      for (int s = 0; s < m.nsplit; ++s) {
-        const int us = s < nfull ? (F[r] + s) * H + h : (FB + R[r]) * H + h;
-        const int64_t pr = static_cast<int64_t>(us) * g + row;
-        const float ms = __ldcg(p.part_ml + pr * 2), ls = __ldcg(p.part_ml + pr * 2 + 1);
-        const float w = ex2(ms - M);
-        Ls = fmaf(ls, w, Ls);
+        for (int j = 0; j < 8; ++j) {
+          wj[j] = -INFINITY;
+          lj[j] = 0.f;
+          if (ok && j < nr) {
+            const float2 v = __ldcg(reinterpret_cast<const float2 *>(
+                p.part_ml + (static_cast<int64_t>(us) * g + row0 + j) * 2));
+            wj[j] = v.x;
+            lj[j] = v.y;
+          }
+        }
 #pragma unroll
-        for (int k = 0; k < EPL; ++k) acc[k] = fmaf(w, __ldcg(p.part_o + pr * D + lane + 32 * k), acc[k]);
+        for (int j = 0; j < 8; ++j) {
+          if (j >= nr) break;
+          float mg = wj[j];
+#pragma unroll
+          for (int o = 16; o; o >>= 1) mg = fmaxf(mg, __shfl_xor_sync(FULL, mg, o));
+          const float Mn = fmaxf(Mrun[j], mg);
+          const float a = ex2(Mrun[j] - Mn);
+          const float w = ok ? ex2(wj[j] - Mn) : 0.f;
+          float ls = lj[j] * w;
+#pragma unroll
+          for (int o = 16; o; o >>= 1) ls += __shfl_xor_sync(FULL, ls, o);
+          Lrun[j] = Lrun[j] * a + ls;
+#pragma unroll
+          for (int k = 0; k < EPL; ++k) acc[j][k] *= a;
+          Mrun[j] = Mn;
+          wj[j] = w;
+        }
+        const int cnt = min(32, ns - s0);
+#pragma unroll 2
+        for (int t = 0; t < cnt; ++t) {
+          const int ut = __shfl_sync(FULL, us, t);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (j >= nr) break;
+            const float wt = __shfl_sync(FULL, wj[j], t);
+            const float *po = p.part_o + (static_cast<int64_t>(ut) * g + row0 + j) * D + lane * EPL;
+            if constexpr (EPL == 4) {
+              const float4 v = __ldcg(reinterpret_cast<const float4 *>(po));
+              acc[j][0] = fmaf(wt, v.x, acc[j][0]);
+              acc[j][1] = fmaf(wt, v.y, acc[j][1]);
+              acc[j][2] = fmaf(wt, v.z, acc[j][2]);
+              acc[j][3] = fmaf(wt, v.w, acc[j][3]);
+            } else {
+              const float2 v = __ldcg(reinterpret_cast<const float2 *>(po));
+              acc[j][0] = fmaf(wt, v.x, acc[j][0]);
+              acc[j][1] = fmaf(wt, v.y, acc[j][1]);
+            }
+          }
+        }
       }
-      const float inv = Ls > 0.f ? 1.f / Ls : 0.f;
-      uint16_t *o = p.out + static_cast<int64_t>(r) * p.o_ss + static_cast<int64_t>(h * g + row) * p.o_sh;
 #pragma unroll
-      for (int k = 0; k < EPL; ++k) {
-        const __nv_bfloat16 b = __float2bfloat16_rn(acc[k] * inv);
-        o[lane + 32 * k] = *reinterpret_cast<const uint16_t *>(&b);
+      for (int j = 0; j < 8; ++j) {
+        if (j >= nr) break;
+        const float inv = Lrun[j] > 0.f ? 1.f / Lrun[j] : 0.f;
+        uint16_t *o = p.out + static_cast<int64_t>(r) * p.o_ss +
+                      static_cast<int64_t>(h * g + row0 + j) * p.o_sh + lane * EPL;
+        if constexpr (EPL == 4) {
+          uint2 w;
+          w.x = pack_bf16(acc[j][0] * inv, acc[j][1] * inv);
+          w.y = pack_bf16(acc[j][2] * inv, acc[j][3] * inv);
+          *reinterpret_cast<uint2 *>(o) = w;
+        } else {
+          *reinterpret_cast<uint32_t *>(o) = pack_bf16(acc[j][0] * inv, acc[j][1] * inv);
+        }
       }
     }
     if (lane == 0) p.counters[r * H + h] = 0;  // self-reset for the next call
@@ -558,6 +624,7 @@ __global__ void __launch_bounds__(256, 1)
   auto end_unit = [&](const SlotMeta &m) {
     const int r = m.r, h = m.h, u = m.u;
     if constexpr (!MMA) {
+      float l0 = lrun[0][0];
 #pragma unroll
       for (int o = 16; o; o >>= 1) l0 += __shfl_xor_sync(FULL, l0, o);
       const int e0 = lane * EPL;
@@ -566,74 +633,77 @@ __global__ void __launch_bounds__(256, 1)
         uint16_t *o = p.out + static_cast<int64_t>(r) * p.o_ss + static_cast<int64_t>(h) * p.o_sh + e0;
         if constexpr (EPL == 4) {
           uint2 w;
-          w.x = pack_bf16(o_mha[0] * inv, o_mha[1] * inv);
-          w.y = pack_bf16(o_mha[2] * inv, o_mha[3] * inv);
+          w.x = pack_bf16(o2[0].x * inv, o2[0].y * inv);
+          w.y = pack_bf16(o2[1].x * inv, o2[1].y * inv);
           *reinterpret_cast<uint2 *>(o) = w;
         } else {
-          *reinterpret_cast<uint32_t *>(o) = pack_bf16(o_mha[0] * inv, o_mha[1] * inv);
+          *reinterpret_cast<uint32_t *>(o) = pack_bf16(o2[0].x * inv, o2[0].y * inv);
         }
         return;
       }
       float *po = p.part_o + static_cast<int64_t>(u) * D + e0;   // g == 1
       if constexpr (EPL == 4)
-        *reinterpret_cast<float4 *>(po) = make_float4(o_mha[0], o_mha[1], o_mha[2], o_mha[3]);
+        *reinterpret_cast<float4 *>(po) = make_float4(o2[0].x, o2[0].y, o2[1].x, o2[1].y);
       else
-        *reinterpret_cast<float2 *>(po) = make_float2(o_mha[0], o_mha[1]);
-      if (lane == 0) *reinterpret_cast<float2 *>(p.part_ml + static_cast<int64_t>(u) * 2) = make_float2(m0, l0);
+        *reinterpret_cast<float2 *>(po) = o2[0];
+      if (lane == 0)
+        *reinterpret_cast<float2 *>(p.part_ml + static_cast<int64_t>(u) * 2) = make_float2(mrun[0][0], l0);
     } else {
-      l0 += __shfl_xor_sync(FULL, l0, 1);
-      l0 += __shfl_xor_sync(FULL, l0, 2);
-      if constexpr (G16) {
-        l1 += __shfl_xor_sync(FULL, l1, 1);
-        l1 += __shfl_xor_sync(FULL, l1, 2);
-      }
-      const int row0 = lane >> 2, cq = (lane & 3) * 2;
-      if (m.nsplit == 1) {
-        const float inv0 = l0 > 0.f ? 1.f / l0 : 0.f;
-        if (row0 < g) {
-          uint16_t *o = p.out + static_cast<int64_t>(r) * p.o_ss + static_cast<int64_t>(h * g + row0) * p.o_sh + cq;
+      float lsum[NT][2];
 #pragma unroll
-          for (int n = 0; n < D / 8; ++n)
-            *reinterpret_cast<uint32_t *>(o + n * 8) = pack_bf16(o_mma[n][0] * inv0, o_mma[n][1] * inv0);
+      for (int n = 0; n < NT; ++n)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          float l = lrun[n][j];
+          l += __shfl_xor_sync(FULL, l, 4);
+          l += __shfl_xor_sync(FULL, l, 8);
+          l += __shfl_xor_sync(FULL, l, 16);
+          lsum[n][j] = l;
         }
-        if constexpr (G16) {
-          const float inv1 = l1 > 0.f ? 1.f / l1 : 0.f;
-          if (row0 + 8 < g) {
-            uint16_t *o = p.out + static_cast<int64_t>(r) * p.o_ss + static_cast<int64_t>(h * g + row0 + 8) * p.o_sh + cq;
+      const int d0 = lane >> 2;
+      const bool direct = m.nsplit == 1;
 #pragma unroll
-            for (int n = 0; n < D / 8; ++n)
-              *reinterpret_cast<uint32_t *>(o + n * 8) = pack_bf16(o_mma[n][2] * inv1, o_mma[n][3] * inv1);
+      for (int n = 0; n < NT; ++n)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int head = n * 8 + (lane & 3) * 2 + j;
+          if (head >= g) continue;
+          if (direct) {
+            const float inv = lsum[n][j] > 0.f ? 1.f / lsum[n][j] : 0.f;
+            uint16_t *o = p.out + static_cast<int64_t>(r) * p.o_ss + static_cast<int64_t>(h * g + head) * p.o_sh;
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+              const __nv_bfloat16 b0 = __float2bfloat16_rn(oacc[mt][n][j] * inv);
+              const __nv_bfloat16 b1 = __float2bfloat16_rn(oacc[mt][n][2 + j] * inv);
+              o[mt * 16 + d0] = *reinterpret_cast<const uint16_t *>(&b0);
+              o[mt * 16 + d0 + 8] = *reinterpret_cast<const uint16_t *>(&b1);
+            }
+          } else {
+            float *po = p.part_o + (static_cast<int64_t>(u) * g + head) * D;
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+              po[mt * 16 + d0] = oacc[mt][n][j];
+              po[mt * 16 + d0 + 8] = oacc[mt][n][2 + j];
+            }
+            if (d0 == 0)
+              *reinterpret_cast<float2 *>(p.part_ml + (static_cast<int64_t>(u) * g + head) * 2) =
+                  make_float2(mrun[n][j], lsum[n][j]);
           }
         }
-        return;
-      }
-      if (row0 < g) {
-        float *po = p.part_o + (static_cast<int64_t>(u) * g + row0) * D + cq;
-#pragma unroll
-        for (int n = 0; n < D / 8; ++n) *reinterpret_cast<float2 *>(po + n * 8) = make_float2(o_mma[n][0], o_mma[n][1]);
-        if ((lane & 3) == 0)
-          *reinterpret_cast<float2 *>(p.part_ml + (static_cast<int64_t>(u) * g + row0) * 2) = make_float2(m0, l0);
-      }
-      if constexpr (G16) {
-        if (row0 + 8 < g) {
-          float *po = p.part_o + (static_cast<int64_t>(u) * g + row0 + 8) * D + cq;
-#pragma unroll
-          for (int n = 0; n < D / 8; ++n) *reinterpret_cast<float2 *>(po + n * 8) = make_float2(o_mma[n][2], o_mma[n][3]);
-          if ((lane & 3) == 0)
-            *reinterpret_cast<float2 *>(p.part_ml + (static_cast<int64_t>(u) * g + row0 + 8) * 2) = make_float2(m1, l1);
-        }
-      }
+      if (direct) return;
     }
-    // split partial written: count arrivals; the last split merges (deterministic order)
-    __threadfence();
+    // split partial written: count arrivals; the last split merges.  The warp
+    // barrier orders every lane's partial stores before lane 0's fence+atomic
+    // (release); lane 0's second fence + the barrier give the acquire side.
     __syncwarp();
     int prev = 0;
-    if (lane == 0) prev = atomicAdd(p.counters + r * H + h, 1);
-    prev = __shfl_sync(FULL, prev, 0);
-    if (prev == m.nsplit - 1) {
+    if (lane == 0) {
       __threadfence();
-      merge_splits(m);
+      prev = atomicAdd(p.counters + r * H + h, 1);
+      if (prev == m.nsplit - 1) __threadfence();
     }
+    prev = __shfl_sync(FULL, prev, 0);
+    if (prev == m.nsplit - 1) merge_splits(m);
   };
 
   // ------------------------------------------------------------- main loop
@@ -651,7 +721,8 @@ __global__ void __launch_bounds__(256, 1)
     const SlotMeta m = metas[slot];
     mbar_wait(my_bars + 8 * slot, phase);
     if (m.flags & F_FIRST) begin_unit(m);
-    if (!(m.flags & F_NOKV)) consume(my_slots + slot * G::SLOT_BYTES, m.lo, m.hi);
+    const bool has_kv = !(m.flags & F_NOKV);
+    if (has_kv) load_chunk(my_slots + slot * G::SLOT_BYTES, m.lo, m.hi);
     __syncwarp();
     fence_proxy_async_smem();  // our smem reads/writes of this slot precede the TMA refill
     {
@@ -662,6 +733,7 @@ __global__ void __launch_bounds__(256, 1)
         ++issued;
       }
     }
+    if (has_kv) compute_chunk(m.lo, m.hi);
     if (m.flags & F_LAST) end_unit(m);
     if (++slot == S) {
       slot = 0;
@@ -670,11 +742,12 @@ __global__ void __launch_bounds__(256, 1)
   }
 
   // ------------------------------------------------- scheduler self-reset
-  __syncwarp();
-  if (lane == 0) {
+  // (one atomic per CTA; the last CTA to finish restores the counters to 0)
+  __syncthreads();
+  if (threadIdx.x == 0) {
     __threadfence();
     const int d = atomicAdd(p.sched + 1, 1);
-    if (d == p.total_warps - 1) {
+    if (d == static_cast<int>(gridDim.x) - 1) {
       p.sched[0] = 0;
       p.sched[1] = 0;
       __threadfence();
@@ -697,13 +770,13 @@ cudaError_t decode_config(int head_dim, int group, int num_seqs, DecodeLaunch *c
   if (e != cudaSuccess) return e;
   e = cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (e != cudaSuccess) return e;
-  const int W = env_int("BKV_WARPS", 4);
-  int S = env_int("BKV_SLOTS", 4);
+  const int W = env_int("BKV_WARPS", 8);
+  int S = env_int("BKV_SLOTS", 2);
   const int slot_bytes = 2 * (head_dim / 64) * 2048;
   const int qb = ((group * head_dim * 2) + 127) / 128 * 128;
   auto need = [&](int s) {
     return 1024 + W * s * slot_bytes + W * (s + 1) * qb + W * s * (int)(sizeof(int) * 8) +
-           W * s * 8 + W * 64 + 2 * (num_seqs + 1) * (int)sizeof(int) + 256;
+           W * s * 8 + W * 1024 + 2 * (num_seqs + 1) * (int)sizeof(int) + 256;
   };
   while (S > 1 && need(S) > smem_optin - 1024) --S;
   cfg->grid = sms * env_int("BKV_CTAS_PER_SM", 1);

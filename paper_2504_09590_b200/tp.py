@@ -1,0 +1,92 @@
+"""Head-sharded tensor parallelism for the decode step.
+
+The paper runs OPT-13B on 2, OPT-30B on 4 and Llama-70B on 8 GPUs with tensor
+parallelism and moves tensors with NCCL.  For the
+attention hot path that means: rank r owns kv heads [r*H/tp, (r+1)*H/tp) and
+their query-head groups, keeps only those heads in its KV pool, runs
+kv_append + decode attention on them, and -- only where the full output is
+needed -- reassembles it with one all-gather.  Outputs are head-major
+[H_q_local][B][d], so the rank-major concatenation produced by the all-gather
+IS the global head-major [H_q][B][d]: no permute kernel.  Block tables,
+direction tables and lengths are replicated (one host scheduler decision).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+from .bkv import kv_append, paged_decode_attention
+
+
+@dataclass(frozen=True)
+class HeadShard:
+    num_q_heads: int
+    num_kv_heads: int
+    tp: int
+    rank: int
+
+    def __post_init__(self):
+        if self.num_kv_heads % self.tp:
+            raise ValueError(f"{self.num_kv_heads} kv heads do not shard over tp={self.tp}")
+        if self.num_q_heads % self.num_kv_heads:
+            raise ValueError("num_q_heads must be a multiple of num_kv_heads")
+        if not 0 <= self.rank < self.tp:
+            raise ValueError("rank out of range")
+
+    @property
+    def group(self) -> int:
+        return self.num_q_heads // self.num_kv_heads
+
+    @property
+    def kv_heads(self) -> range:   # global kv-head ids owned by this rank
+        h = self.num_kv_heads // self.tp
+        return range(self.rank * h, (self.rank + 1) * h)
+
+    @property
+    def q_heads(self) -> range:    # their query heads (groups stay intact, reading Q9)
+        h = self.num_q_heads // self.tp
+        return range(self.rank * h, (self.rank + 1) * h)
+
+    def local_q(self, q_global: torch.Tensor) -> torch.Tensor:
+        """[B][H_q][d] -> this rank's [B][H_q_local][d] view (no copy)."""
+        return q_global[:, self.q_heads.start:self.q_heads.stop]
+
+    def alloc_out(self, batch: int, head_dim: int, device, dtype=torch.bfloat16):
+        """Head-major local output [H_q_local][B][d] (contiguous)."""
+        return torch.empty((len(self.q_heads), batch, head_dim), dtype=dtype, device=device)
+
+
+def gather_heads(out_local_hm: torch.Tensor, out_global_hm: torch.Tensor | None = None, group=None):
+    """All-gather head-major shards into the global head-major [H_q][B][d]."""
+    tp = dist.get_world_size(group)
+    if out_global_hm is None:
+        out_global_hm = torch.empty((out_local_hm.shape[0] * tp, *out_local_hm.shape[1:]),
+                                    dtype=out_local_hm.dtype, device=out_local_hm.device)
+    if tp == 1:
+        out_global_hm.copy_(out_local_hm)
+    elif dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out_global_hm, out_local_hm.contiguous(), group=group)
+    else:   # gloo (CPU tests): list all-gather, rank-major
+        parts = list(out_global_hm.chunk(tp, dim=0))
+        dist.all_gather(parts, out_local_hm.contiguous(), group=group)
+        out_global_hm.copy_(torch.cat(parts, dim=0))
+    return out_global_hm
+
+
+def decode_step(shard: HeadShard, pool, block_tables, dirs, seq_lens_before, cu_new_tokens,
+                k_new, v_new, seq_lens, q_local, out_local_hm, softmax_scale=None,
+                out_global_hm=None, max_seq_len=None, ws=None, gather=True, group=None,
+                append_fn=kv_append, attn_fn=paged_decode_attention):
+    """One layer of one rank: append this step's tokens, attend, optionally all-gather.
+
+    ``append_fn``/``attn_fn`` default to the CUDA kernels; tests substitute the
+    CPU oracle to check the sharding and reassembly logic without a GPU.
+    """
+    append_fn(pool, block_tables, dirs, seq_lens_before, cu_new_tokens, k_new, v_new)
+    attn_fn(pool, block_tables, dirs, seq_lens, q_local, softmax_scale,
+            out=out_local_hm.permute(1, 0, 2), max_seq_len=max_seq_len, ws=ws)
+    if gather and shard.tp > 1:
+        return gather_heads(out_local_hm, out_global_hm, group)
+    return out_local_hm
