@@ -75,18 +75,21 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 4-D view (d, slot, head, block) of one pool tensor; box = 64 d x 16 slots,
-// 128-byte swizzle so the decode kernel's ldmatrix/LDS reads are conflict-free.
+// 5-D view (64 d, slot, d-half, head, block) of one pool tensor.  The d-half
+// dimension (stride 128 B) lets ONE box {64, 16, d/64, 1, 1} fetch a whole
+// 16-slot x d tile, landing as [half][slot][128 B] with the 128-byte swizzle
+// the decode kernel's ldmatrix / LDS reads are conflict-free against.
 bkv_status encode_pool_map(CUtensorMap *m, void *base, const bkv_kv_pool *pool) {
   auto fn = encode_fn();
   if (!fn) return fail(BKV_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
-  cuuint64_t dims[4] = {(cuuint64_t)pool->head_dim, (cuuint64_t)pool->block_size,
+  const int halves = pool->head_dim / 64;
+  cuuint64_t dims[5] = {64, (cuuint64_t)pool->block_size, (cuuint64_t)halves,
                         (cuuint64_t)pool->num_kv_heads, (cuuint64_t)pool->num_blocks};
-  cuuint64_t strides[3] = {(cuuint64_t)pool->stride_slot * 2, (cuuint64_t)pool->stride_head * 2,
-                           (cuuint64_t)pool->stride_block * 2};
-  cuuint32_t box[4] = {64, 16, 1, 1};
-  cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, estr,
+  cuuint64_t strides[4] = {(cuuint64_t)pool->stride_slot * 2, 128,
+                           (cuuint64_t)pool->stride_head * 2, (cuuint64_t)pool->stride_block * 2};
+  cuuint32_t box[5] = {64, 16, (cuuint32_t)halves, 1, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, base, dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(BKV_ERR_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)r);
@@ -95,7 +98,8 @@ bkv_status encode_pool_map(CUtensorMap *m, void *base, const bkv_kv_pool *pool) 
 
 // ------------------------------------------------------------ workspace
 struct WsLayout {
-  size_t sched, counters, ml, o, total;
+  size_t sched, counters, ml, o, trace, total;
+  int trace_cap;
   int units_max;
 };
 
@@ -117,7 +121,10 @@ bkv_status ws_layout(int B, int Hq, int H, int D, WsLayout *w, bkv::DecodeLaunch
   w->counters = 256;
   w->ml = w->counters + up256((size_t)bkv::kMaxSeqs * bkv::kMaxKvHeads * 4);
   w->o = w->ml + up256((size_t)units * g * 2 * 4);
-  w->total = w->o + up256((size_t)units * g * D * 4);
+  w->trace = w->o + up256((size_t)units * g * D * 4);
+  const char *tr = getenv("BKV_TRACE");   // dev only: per-warp event log after the partials
+  w->trace_cap = (tr && *tr) ? atoi(tr) : 0;
+  w->total = w->trace + up256((size_t)cfg->grid * cfg->warps * w->trace_cap * 16);
   return BKV_OK;
 }
 
@@ -268,6 +275,11 @@ bkv_status bkv_paged_decode_attention(const bkv_kv_pool *pool, const bkv_block_m
   p.slots = slots;
   p.q_bytes = qb;
   p.total_warps = cfg.grid * cfg.warps;
+  p.debug_flags = getenv("BKV_DEBUG") ? atoi(getenv("BKV_DEBUG")) : 0;
+  p.team_force = getenv("BKV_TEAM") ? atoi(getenv("BKV_TEAM")) : 0;
+  p.team_max = g <= 8 ? cfg.warps : 1;
+  p.trace_cap = w.trace_cap;
+  p.trace = w.trace_cap ? reinterpret_cast<unsigned long long *>(ws + w.trace) : nullptr;
   cudaError_t e = bkv::launch_decode(tmK, tmV, p, D, cfg, reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "decode attention launch");
   return BKV_OK;

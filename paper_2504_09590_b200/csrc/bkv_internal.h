@@ -48,6 +48,11 @@ struct DecodeParams {
   int slots;             // ring depth per warp (S)
   int q_bytes;           // smem bytes per q-ring entry
   int total_warps;       // grid * warps per CTA
+  int team_force;        // 0 = choose the team size in-kernel, else force it (dev)
+  int team_max;          // largest allowed team (1 when the state area is not allocated)
+  int debug_flags;       // dev only: 1 = skip the math (data-movement skeleton)
+  unsigned long long *trace;  // dev only (BKV_TRACE): per-warp event log, else nullptr
+  int trace_cap;         // events per warp
 };
 
 struct DecodeLaunch {

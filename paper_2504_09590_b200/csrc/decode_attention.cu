@@ -45,11 +45,13 @@ struct SlotMeta {
   int lo, hi, flags, qidx;
 };
 
+constexpr int kBuckets = 4;
+
 struct Plan {
-  int P;   // blocks per full split
-  int FB;  // full splits over all requests
-  int RB;  // remainder splits over all requests
-  int U;   // units = (FB + RB) * H
+  int team;               // warps cooperating on one unit (1, 2, 4 or 8)
+  int P;                  // target blocks per split
+  int base[kBuckets + 1]; // split-slot offset of each size bucket (largest first)
+  int U;                  // units = base[kBuckets] * H
 };
 
 template <int D>
@@ -80,68 +82,116 @@ __device__ __forceinline__ int search_le(const int *a, int n, int x) {
   return lo;
 }
 
-// Split plan, computed identically by every CTA from seq_lens.
-__device__ void compute_plan(const DecodeParams &p, int *F, int *R, Plan *plan) {
+// Split plan, computed identically by every CTA from
+// seq_lens (no host round trip).  P = max(min_split, ceil(sum_r nb_r * H /
+// target)) blocks; request r is cut into n_r = ceil(nb_r / P) near-equal
+// splits of s_r <= P blocks.  Requests are grouped into 4 buckets by split
+// size (largest first) and units are enumerated bucket by bucket, so the
+// dynamically scheduled work list runs roughly longest-first and the tail is
+// made of small units.  Pre[k][r] = exclusive prefix of n_r over bucket k.
+__device__ __forceinline__ int bucket_of(int s, int P) {
+  // s in (3P/4, P] -> 0, (P/2, 3P/4] -> 1, (P/4, P/2] -> 2, [0, P/4] -> 3
+  return 4 * s > 3 * P ? 0 : (2 * s > P ? 1 : (4 * s > P ? 2 : 3));
+}
+
+__device__ void compute_plan(const DecodeParams &p, int *Pre, int *Lsm, Plan *plan) {
   __shared__ long long red_ll[32];
-  __shared__ int2 red2[32];
+  __shared__ int4 red4[32];
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5,
             nw = nt >> 5;
+  const int B = p.B;
   long long local = 0;
-  for (int r = tid; r < p.B; r += nt) local += nblocks_of(__ldg(p.seq_lens + r), p.bs);
+  for (int r = tid; r < B; r += nt) {
+    const int L = __ldg(p.seq_lens + r);
+    Lsm[r] = L;
+    local += nblocks_of(L, p.bs);
+  }
 #pragma unroll
   for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
   if (lane == 0) red_ll[warp] = local;
   __syncthreads();
   long long T = 0;
   for (int w = 0; w < nw; ++w) T += red_ll[w];
-  const long long work = T * p.H;
-  long long Pll = (work + p.target_units - 1) / p.target_units;
+  // Team size: small problems (few 16-slot chunks per warp) let several warps
+  // share one unit, since one warp's TMA ring sustains only a few copies per us.
+  int team = p.team_force;
+  if (team <= 0) {
+    const long long per_warp = T * p.H * (p.bs / 16) / p.total_warps;
+    team = per_warp >= 48 ? 1 : (per_warp >= 24 ? 2 : (per_warp >= 12 ? 4 : 8));
+  }
+  while (team > 1 && (team > p.team_max || nw % team)) team >>= 1;
+  const long long target = max(1, p.target_units / team);
+  long long Pll = (T * p.H + target - 1) / target;
   if (Pll < p.min_split) Pll = p.min_split;
   const int P = static_cast<int>(Pll);
-  // exclusive scans of full_r = nb/P and rem_r = (nb % P != 0 || nb == 0)
-  const int per = (p.B + nt - 1) / nt;
-  const int r0 = min(p.B, tid * per), r1 = min(p.B, r0 + per);
-  int fs = 0, rs = 0;
+  // per-thread contiguous ranges -> 4-bucket exclusive scans of n_r
+  const int per = (B + nt - 1) / nt;
+  const int r0 = min(B, tid * per), r1 = min(B, r0 + per);
+  int4 cnt = make_int4(0, 0, 0, 0);
   for (int r = r0; r < r1; ++r) {
-    const int nb = nblocks_of(__ldg(p.seq_lens + r), p.bs);
-    fs += nb / P;
-    rs += (nb % P != 0 || nb == 0) ? 1 : 0;
+    const int nb = nblocks_of(Lsm[r], p.bs);
+    const int n = nb > 0 ? (nb + P - 1) / P : 1;
+    const int bk = bucket_of((nb + n - 1) / n, P);
+    cnt.x += bk == 0 ? n : 0;
+    cnt.y += bk == 1 ? n : 0;
+    cnt.z += bk == 2 ? n : 0;
+    cnt.w += bk == 3 ? n : 0;
   }
-  int fi = fs, ri = rs;  // inclusive warp scan
+  int4 inc = cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const int fu = __shfl_up_sync(0xffffffffu, fi, o), ru = __shfl_up_sync(0xffffffffu, ri, o);
+    const int x = __shfl_up_sync(0xffffffffu, inc.x, o), y = __shfl_up_sync(0xffffffffu, inc.y, o);
+    const int z = __shfl_up_sync(0xffffffffu, inc.z, o), w = __shfl_up_sync(0xffffffffu, inc.w, o);
     if (lane >= o) {
-      fi += fu;
-      ri += ru;
+      inc.x += x;
+      inc.y += y;
+      inc.z += z;
+      inc.w += w;
     }
   }
-  if (lane == 31) red2[warp] = make_int2(fi, ri);
+  if (lane == 31) red4[warp] = inc;
   __syncthreads();
-  int fo = fi - fs, ro = ri - rs;
+  int4 e = make_int4(inc.x - cnt.x, inc.y - cnt.y, inc.z - cnt.z, inc.w - cnt.w);
   for (int w = 0; w < warp; ++w) {
-    fo += red2[w].x;
-    ro += red2[w].y;
+    e.x += red4[w].x;
+    e.y += red4[w].y;
+    e.z += red4[w].z;
+    e.w += red4[w].w;
   }
   for (int r = r0; r < r1; ++r) {
-    F[r] = fo;
-    R[r] = ro;
-    const int nb = nblocks_of(__ldg(p.seq_lens + r), p.bs);
-    fo += nb / P;
-    ro += (nb % P != 0 || nb == 0) ? 1 : 0;
+    Pre[0 * (B + 1) + r] = e.x;
+    Pre[1 * (B + 1) + r] = e.y;
+    Pre[2 * (B + 1) + r] = e.z;
+    Pre[3 * (B + 1) + r] = e.w;
+    const int nb = nblocks_of(Lsm[r], p.bs);
+    const int n = nb > 0 ? (nb + P - 1) / P : 1;
+    const int bk = bucket_of((nb + n - 1) / n, P);
+    e.x += bk == 0 ? n : 0;
+    e.y += bk == 1 ? n : 0;
+    e.z += bk == 2 ? n : 0;
+    e.w += bk == 3 ? n : 0;
   }
   if (tid == nt - 1) {
-    int ft = 0, rt = 0;
+    int4 tot = make_int4(0, 0, 0, 0);
     for (int w = 0; w < nw; ++w) {
-      ft += red2[w].x;
-      rt += red2[w].y;
+      tot.x += red4[w].x;
+      tot.y += red4[w].y;
+      tot.z += red4[w].z;
+      tot.w += red4[w].w;
     }
-    F[p.B] = ft;
-    R[p.B] = rt;
+    Pre[0 * (B + 1) + B] = tot.x;
+    Pre[1 * (B + 1) + B] = tot.y;
+    Pre[2 * (B + 1) + B] = tot.z;
+    Pre[3 * (B + 1) + B] = tot.w;
+    plan->base[0] = 0;
+    plan->base[1] = tot.x;
+    plan->base[2] = tot.x + tot.y;
+    plan->base[3] = tot.x + tot.y + tot.z;
+    const int acc = tot.x + tot.y + tot.z + tot.w;
+    plan->base[kBuckets] = acc;
+    plan->team = team;
     plan->P = P;
-    plan->FB = ft;
-    plan->RB = rt;
-    plan->U = (ft + rt) * p.H;
+    plan->U = acc * p.H;
   }
   __syncthreads();
 }
@@ -170,15 +220,36 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t *bars_g = reinterpret_cast<uint64_t *>(meta_g + W * S * sizeof(SlotMeta));
   uint8_t *scratch_g = reinterpret_cast<uint8_t *>(bars_g + W * S);   // W x 1 KiB
   const uint32_t my_scr = smem_u32(scratch_g + warp * 1024);
-  int *F = reinterpret_cast<int *>(scratch_g + W * 1024);
-  int *R = F + (p.B + 1);
+  int *Pre = reinterpret_cast<int *>(scratch_g + W * 1024);   // [kBuckets][B + 1]
+  // team states: per warp g rows x (D o-values + m + l) floats (only if team_max > 1)
+  int *Lsm = Pre + kBuckets * (p.B + 1);                      // seq_lens cache [B]
+  float *tstate = reinterpret_cast<float *>(Lsm + ((p.B + 3) & ~3));
 
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmK);
     prefetch_tmap(&tmV);
   }
-  compute_plan(p, F, R, &plan);
-  const int P = plan.P, FB = plan.FB, U = plan.U;
+  // dev-only event trace: (globaltimer ns << 8 | kind), unit id in a second word
+  int trace_n = 0;
+  auto trace = [&](int kind, int u) {
+    if (p.trace && lane == 0 && trace_n < p.trace_cap) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      unsigned long long *e = p.trace + (static_cast<int64_t>(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * p.trace_cap + trace_n) * 2;
+      e[0] = (t << 8) | kind;
+      e[1] = static_cast<unsigned long long>(u);
+      ++trace_n;
+    }
+  };
+  trace(0, -1);
+  compute_plan(p, Pre, Lsm, &plan);
+  trace(1, -1);
+  const int P = plan.P, U = plan.U, T = plan.team;
+  const int tm = warp / T, wt = warp - tm * T;                    // team, rank in team
+  const int n_teams = static_cast<int>(gridDim.x) * (W / T);
+  const int gt = static_cast<int>(blockIdx.x) * (W / T) + tm;
+  const int SF = p.g * (D + 2);                                   // floats per team state
+  float *my_state = tstate + warp * SF;
 
   const uint32_t my_slots = slots_base + warp * S * G::SLOT_BYTES;
   const uint32_t my_q = q_base + warp * (S + 1) * p.q_bytes;
@@ -193,82 +264,110 @@ __global__ void __launch_bounds__(256, 1)
   const int chunks_per_block = bs >> 4;
 
   // ------------------------------------------------------------ issuer state
-  int u_next = 0;
-  // first unit is static (no atomic storm at launch); later ones are pulled
-  u_next = blockIdx.x * W + warp;
+  // team == 1: first unit static (no atomic storm at launch), then pulled from
+  // a global counter; team > 1: units gt, gt + n_teams, ... (every warp of the
+  // team derives the same sequence, no communication needed).  The issuer
+  // decodes the NEXT unit and starts its block-table loads when it enters the
+  // current one, so unit boundaries do not stall on global memory.
+  int u_pref = blockIdx.x * W + warp, team_k = 0;
+  auto pull_unit = [&]() -> int {
+    if (T == 1) {
+      const int u = __shfl_sync(FULL, u_pref, 0);
+      if (u < U && lane == 0) u_pref = p.total_warps + atomicAdd(p.sched, 1);  // used one unit later
+      return u;
+    }
+    return gt + (team_k++) * n_teams;
+  };
+  struct UnitInfo {
+    int u, r, h, L, n, e0, e1;
+  };
+  auto decode_unit = [&](int u) -> UnitInfo {
+    UnitInfo x;
+    x.u = u;
+    if (u >= U) return x;
+    x.h = u % H;
+    const int qq = u / H;
+    int k = 0;
+    while (k < kBuckets - 1 && qq >= plan.base[k + 1]) ++k;
+    const int j = qq - plan.base[k];
+    const int *pk = Pre + k * (p.B + 1);
+    x.r = search_le(pk, p.B, j);
+    x.L = Lsm[x.r];
+    const int nb = nblocks_of(x.L, bs);
+    x.n = nb > 0 ? (nb + P - 1) / P : 1;
+    const int sidx = j - pk[x.r];
+    x.e0 = static_cast<int>(static_cast<long long>(sidx) * nb / x.n);
+    x.e1 = static_cast<int>(static_cast<long long>(sidx + 1) * nb / x.n);
+    return x;
+  };
+  // window of 32 block-table/direction entries starting at block wb (lane i: entry wb + i)
+  auto load_window = [&](const UnitInfo &x, int wb, int &btv, int &dirv) {
+    const int ew = wb + lane;
+    btv = 0;
+    dirv = 0;
+    if (x.u < U && ew < x.e1) {
+      btv = __ldg(p.bt + static_cast<int64_t>(x.r) * p.bt_stride + ew);
+      dirv = __ldg(p.dirs + static_cast<int64_t>(x.r) * p.dir_rs + static_cast<int64_t>(ew) * p.dir_cs);
+    }
+  };
+  UnitInfo cur{}, nxt = decode_unit(pull_unit());
+  int nx_bt = 0, nx_dir = 0;
+  load_window(nxt, nxt.e0, nx_bt, nx_dir);
   bool is_active = false, is_done = false, is_first = false;
-  int is_u = 0, is_r = 0, is_h = 0, is_ns = 0, is_L = 0, is_e = 0, is_e1 = 0, is_c = 0;
-  int is_wb = 0, bt_w = 0, dir_w = 0, is_qidx = S;  // first unit -> q-ring entry 0
+  int is_ci = 0, is_nc = 0, is_wb = 0, bt_w = 0, dir_w = 0, is_qidx = S;  // first unit -> q entry 0
 
   // Produce the next chunk of this warp's work stream (warp-collective).
+  // Chunk ci of a unit = 16 slots (sub-chunk ci % cpb) of block e0 + ci / cpb;
+  // a warp of a team takes chunks wt, wt + T, ...
   auto next_chunk = [&](SlotMeta &m, int &blk, int &csub) -> bool {
     if (!is_active) {
       if (is_done) return false;
-      const int u = __shfl_sync(FULL, u_next, 0);
-      if (u >= U) {
+      if (nxt.u >= U) {
         is_done = true;
         return false;
       }
-      if (lane == 0) u_next = p.total_warps + atomicAdd(p.sched, 1);  // prefetch the next grab
-      const int h = u % H, qq = u / H;
-      int r, e0, e1;
-      if (qq < FB) {
-        r = search_le(F, p.B, qq);
-        e0 = (qq - F[r]) * P;
-        e1 = e0 + P;
-      } else {
-        r = search_le(R, p.B, qq - FB);
-        e0 = (F[r + 1] - F[r]) * P;
-        e1 = nblocks_of(__ldg(p.seq_lens + r), bs);
-      }
-      is_u = u;
-      is_r = r;
-      is_h = h;
-      is_L = __ldg(p.seq_lens + r);
-      is_ns = (F[r + 1] - F[r]) + (R[r + 1] - R[r]);
+      cur = nxt;
+      bt_w = nx_bt;
+      dir_w = nx_dir;
+      is_wb = cur.e0;
+      nxt = decode_unit(pull_unit());             // look one unit ahead ...
+      load_window(nxt, nxt.e0, nx_bt, nx_dir);    // ... its loads overlap this unit
       is_qidx = (is_qidx == S) ? 0 : is_qidx + 1;
-      is_e = e0;
-      is_e1 = e1;
-      is_c = 0;
-      is_wb = -(1 << 30);
+      is_ci = wt;
+      is_nc = (cur.e1 - cur.e0) * chunks_per_block;
       is_first = true;
-      if (e0 >= e1) {  // empty context (L = 0, reading Q8): one flag-only chunk
-        m = SlotMeta{u, r, h, is_ns, 0, 0, F_FIRST | F_LAST | F_NOKV | F_NOQ, is_qidx};
+      trace(2, cur.u);
+      if (is_ci >= is_nc) {  // no chunk for this warp (or empty context, Q8): flag-only slot
+        m = SlotMeta{cur.u, cur.r, cur.h, cur.n, 0, 0, F_FIRST | F_LAST | F_NOKV | F_NOQ, is_qidx};
         blk = 0;
         csub = 0;
         return true;
       }
       is_active = true;
     }
-    if (is_e - is_wb >= 32) {  // refill the block-table window (32 entries, one per lane)
-      is_wb = is_e;
-      const int e = is_wb + lane;
-      if (e < is_e1) {
-        bt_w = __ldg(p.bt + static_cast<int64_t>(is_r) * p.bt_stride + e);
-        dir_w = __ldg(p.dirs + static_cast<int64_t>(is_r) * p.dir_rs +
-                      static_cast<int64_t>(e) * p.dir_cs);
-      }
+    const int e = cur.e0 + (chunks_per_block == 1 ? is_ci : (is_ci >> 1));
+    const int c = chunks_per_block == 1 ? 0 : (is_ci & 1);
+    if (e - is_wb >= 32) {  // long unit: refill the window (rare)
+      is_wb = e;
+      load_window(cur, e, bt_w, dir_w);
     }
-    const int idx = is_e - is_wb;
+    const int idx = e - is_wb;
     const int b = __shfl_sync(FULL, bt_w, idx);
     const int dr = __shfl_sync(FULL, dir_w, idx);
-    const int ne = min(bs, is_L - is_e * bs);       // live tokens in this block
+    const int ne = min(bs, cur.L - e * bs);          // live tokens in this block
     const int lo_s = dr ? bs - ne : 0;               // RT from the left,
     const int hi_s = dr ? bs : ne;                   //        BE from the right
-    const int lo = max(lo_s - is_c * 16, 0), hi = min(hi_s - is_c * 16, 16);
+    const int lo = max(lo_s - c * 16, 0), hi = min(hi_s - c * 16, 16);
     int flags = (is_first ? F_FIRST : 0) | (lo >= hi ? F_NOKV : 0);
     is_first = false;
-    csub = is_c;
+    csub = c;
     blk = b;
-    if (++is_c == chunks_per_block) {
-      is_c = 0;
-      ++is_e;
-    }
-    if (is_e == is_e1) {
+    is_ci += T;
+    if (is_ci >= is_nc) {
       flags |= F_LAST;
       is_active = false;
     }
-    m = SlotMeta{is_u, is_r, is_h, is_ns, lo, hi, flags, is_qidx};
+    m = SlotMeta{cur.u, cur.r, cur.h, cur.n, lo, hi, flags, is_qidx};
     return true;
   };
 
@@ -282,11 +381,9 @@ __global__ void __launch_bounds__(256, 1)
       mbar_arrive_expect_tx(bar, bytes);
       if (kv) {
         const uint32_t dk = my_slots + i * G::SLOT_BYTES, dv = dk + G::KV_BYTES;
-#pragma unroll
-        for (int hr = 0; hr < G::HALVES; ++hr) {
-          tma_load_4d(dk + hr * G::HALF_BYTES, &tmK, hr * 64, csub * 16, m.h, blk, bar, pol);
-          tma_load_4d(dv + hr * G::HALF_BYTES, &tmV, hr * 64, csub * 16, m.h, blk, bar, pol);
-        }
+        // one 5-D box = the whole 16-slot x d tile, laid out [half][slot][128 B] swizzled
+        tma_load_5d(dk, &tmK, 0, csub * 16, 0, m.h, blk, bar, pol);
+        tma_load_5d(dv, &tmV, 0, csub * 16, 0, m.h, blk, bar, pol);
       }
       if (qq) {
         const uint32_t dq = my_q + m.qidx * p.q_bytes;
@@ -533,8 +630,11 @@ __global__ void __launch_bounds__(256, 1)
   // order, so the result does not depend on which split arrived last.
   auto merge_splits = [&](const SlotMeta &m) {
     const int r = m.r, h = m.h, ns = m.nsplit;
-    const int nfull = F[r + 1] - F[r];
-    const int u_full0 = F[r] * H + h, u_rem = (FB + R[r]) * H + h;
+    // all splits of (r, h) are consecutive split slots of r's bucket: u = (slot0 + s) * H + h
+    const int qq = m.u / H;
+    int k = 0;
+    while (k < kBuckets - 1 && qq >= plan.base[k + 1]) ++k;
+    const int u0 = (plan.base[k] + Pre[k * (p.B + 1) + r]) * H + h;
     for (int row0 = 0; row0 < g; row0 += 8) {
       const int nr = min(8, g - row0);
       float Mrun[8], Lrun[8], acc[8][EPL];
@@ -548,7 +648,7 @@ __global__ void __launch_bounds__(256, 1)
       for (int s0 = 0; s0 < ns; s0 += 32) {
         const int sl = s0 + lane;
         const bool ok = sl < ns;
-        const int us = sl < nfull ? u_full0 + sl * H : u_rem;
+        const int us = u0 + sl * H;
         float wj[8], lj[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -621,7 +721,93 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) p.counters[r * H + h] = 0;  // self-reset for the next call
   };
 
+  // Team end of unit: every warp of the team deposits its (m, l, o) state in
+  // shared memory; after a named barrier the team combines them (online-
+  // softmax merge, fixed warp order) and writes the output rows or the unit's
+  // split partial; a second barrier frees the state area.
+  auto team_end_unit = [&](const SlotMeta &m) {
+    const int r = m.r, h = m.h, u = m.u;
+    if constexpr (!MMA) {
+      float l0 = lrun[0][0];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) l0 += __shfl_xor_sync(FULL, l0, o);
+#pragma unroll
+      for (int k = 0; k < EPL / 2; ++k) {
+        my_state[lane * EPL + 2 * k] = o2[k].x;
+        my_state[lane * EPL + 2 * k + 1] = o2[k].y;
+      }
+      if (lane == 0) {
+        my_state[D] = mrun[0][0];
+        my_state[D + 1] = l0;
+      }
+    } else {
+      const int d0 = lane >> 2;
+#pragma unroll
+      for (int n = 0; n < NT; ++n)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          float l = lrun[n][j];
+          l += __shfl_xor_sync(FULL, l, 4);
+          l += __shfl_xor_sync(FULL, l, 8);
+          l += __shfl_xor_sync(FULL, l, 16);
+          const int head = n * 8 + (lane & 3) * 2 + j;
+          if (head < g) {
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+              my_state[head * D + mt * 16 + d0] = oacc[mt][n][j];
+              my_state[head * D + mt * 16 + d0 + 8] = oacc[mt][n][2 + j];
+            }
+            if (d0 == 0) {
+              my_state[g * D + 2 * head] = mrun[n][j];
+              my_state[g * D + 2 * head + 1] = l;
+            }
+          }
+        }
+    }
+    named_bar_sync(1 + tm, T * 32);
+    const float *ts = tstate + tm * T * SF;
+    for (int idx = wt * 32 + lane; idx < g * D; idx += T * 32) {
+      const int row = idx / D, e = idx - row * D;
+      float M = -INFINITY;
+      for (int k = 0; k < T; ++k) M = fmaxf(M, ts[k * SF + g * D + 2 * row]);
+      float Ls = 0.f, O = 0.f;
+      if (M != -INFINITY) {
+        for (int k = 0; k < T; ++k) {
+          const float w = ex2(ts[k * SF + g * D + 2 * row] - M);
+          Ls = fmaf(ts[k * SF + g * D + 2 * row + 1], w, Ls);
+          O = fmaf(ts[k * SF + row * D + e], w, O);
+        }
+      }
+      if (m.nsplit == 1) {
+        const __nv_bfloat16 b = __float2bfloat16_rn(Ls > 0.f ? O / Ls : 0.f);
+        p.out[static_cast<int64_t>(r) * p.o_ss + static_cast<int64_t>(h * g + row) * p.o_sh + e] =
+            *reinterpret_cast<const uint16_t *>(&b);
+      } else {
+        p.part_o[(static_cast<int64_t>(u) * g + row) * D + e] = O;
+        if (e == 0)
+          *reinterpret_cast<float2 *>(p.part_ml + (static_cast<int64_t>(u) * g + row) * 2) = make_float2(M, Ls);
+      }
+    }
+    named_bar_sync(1 + tm, T * 32);
+    if (m.nsplit > 1 && wt == 0) {
+      int prev = 0;
+      if (lane == 0) {
+        prev = atom_add_release_gpu(p.counters + r * H + h, 1);
+        if (prev == m.nsplit - 1) fence_acq_rel_gpu();
+      }
+      prev = __shfl_sync(FULL, prev, 0);
+      if (prev == m.nsplit - 1) {
+        trace(5, m.u);
+        merge_splits(m);
+      }
+    }
+  };
+
   auto end_unit = [&](const SlotMeta &m) {
+    if (T > 1) {
+      team_end_unit(m);
+      return;
+    }
     const int r = m.r, h = m.h, u = m.u;
     if constexpr (!MMA) {
       float l0 = lrun[0][0];
@@ -698,12 +884,14 @@ __global__ void __launch_bounds__(256, 1)
     __syncwarp();
     int prev = 0;
     if (lane == 0) {
-      __threadfence();
-      prev = atomicAdd(p.counters + r * H + h, 1);
-      if (prev == m.nsplit - 1) __threadfence();
+      prev = atom_add_release_gpu(p.counters + r * H + h, 1);
+      if (prev == m.nsplit - 1) fence_acq_rel_gpu();
     }
     prev = __shfl_sync(FULL, prev, 0);
-    if (prev == m.nsplit - 1) merge_splits(m);
+    if (prev == m.nsplit - 1) {
+      trace(5, m.u);
+      merge_splits(m);
+    }
   };
 
   // ------------------------------------------------------------- main loop
@@ -716,31 +904,61 @@ __global__ void __launch_bounds__(256, 1)
   }
   int slot = 0;
   uint32_t phase = 0;
+  long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // dev (BKV_TRACE): cycle breakdown, chunks
+  const bool profiling = p.trace != nullptr;
   for (int seq = 0; seq < issued; ++seq) {
     __syncwarp();
     const SlotMeta m = metas[slot];
+    long long c0 = profiling ? clock64() : 0;
     mbar_wait(my_bars + 8 * slot, phase);
-    if (m.flags & F_FIRST) begin_unit(m);
+    long long c1 = profiling ? clock64() : 0;
+    if (m.flags & F_FIRST) {
+      trace(3, m.u);
+      begin_unit(m);
+    }
     const bool has_kv = !(m.flags & F_NOKV);
     if (has_kv) load_chunk(my_slots + slot * G::SLOT_BYTES, m.lo, m.hi);
+    long long c1b = profiling ? clock64() : 0;
     __syncwarp();
-    fence_proxy_async_smem();  // our smem reads/writes of this slot precede the TMA refill
+    if (!(p.debug_flags & 2)) fence_proxy_async_smem();  // our smem accesses precede the TMA refill
+    long long c2 = profiling ? clock64() : 0;
+    long long c2b = c2;
     {
       SlotMeta mn;
       int blk, cs;
       if (next_chunk(mn, blk, cs)) {
+        c2b = profiling ? clock64() : 0;
         issue(slot, mn, blk, cs);
         ++issued;
       }
     }
-    if (has_kv) compute_chunk(m.lo, m.hi);
-    if (m.flags & F_LAST) end_unit(m);
+    long long c3 = profiling ? clock64() : 0;
+    if (has_kv && !(p.debug_flags & 1)) compute_chunk(m.lo, m.hi);
+    long long c4 = profiling ? clock64() : 0;
+    if (m.flags & F_LAST) {
+      end_unit(m);
+      trace(4, m.u);
+    }
+    if (profiling) {
+      const long long c5 = clock64();
+      prof[0] += c1 - c0;
+      prof[1] += c1b - c1;
+      prof[2] += c3 - c2;
+      prof[3] += c4 - c3;
+      prof[4] += c5 - c4;
+      prof[5] += 1;
+      prof[6] += c2 - c1b;
+      prof[7] += c3 - c2b;
+    }
     if (++slot == S) {
       slot = 0;
       phase ^= 1u;
     }
   }
+  if (profiling)
+    for (int k = 0; k < 8; ++k) trace(8 + k, static_cast<int>(min(prof[k], (long long)0x7fffffff)));
 
+  trace(6, -1);
   // ------------------------------------------------- scheduler self-reset
   // (one atomic per CTA; the last CTA to finish restores the counters to 0)
   __syncthreads();
@@ -774,9 +992,10 @@ cudaError_t decode_config(int head_dim, int group, int num_seqs, DecodeLaunch *c
   int S = env_int("BKV_SLOTS", 2);
   const int slot_bytes = 2 * (head_dim / 64) * 2048;
   const int qb = ((group * head_dim * 2) + 127) / 128 * 128;
+  const int team_state = group <= 8 ? W * group * (head_dim + 2) * 4 : 0;
   auto need = [&](int s) {
     return 1024 + W * s * slot_bytes + W * (s + 1) * qb + W * s * (int)(sizeof(int) * 8) +
-           W * s * 8 + W * 1024 + 2 * (num_seqs + 1) * (int)sizeof(int) + 256;
+           W * s * 8 + W * 1024 + 4 * (num_seqs + 1) * (int)sizeof(int) + ((num_seqs + 3) & ~3) * 4 + team_state + 256;
   };
   while (S > 1 && need(S) > smem_optin - 1024) --S;
   cfg->grid = sms * env_int("BKV_CTAS_PER_SM", 1);
