@@ -48,7 +48,6 @@ struct SlotMeta {
 constexpr int kBuckets = 4;
 
 struct Plan {
-  int team;               // warps cooperating on one unit (1, 2, 4 or 8)
   int P;                  // target blocks per split
   int base[kBuckets + 1]; // split-slot offset of each size bucket (largest first)
   int U;                  // units = base[kBuckets] * H
@@ -112,15 +111,7 @@ __device__ void compute_plan(const DecodeParams &p, int *Pre, int *Lsm, Plan *pl
   __syncthreads();
   long long T = 0;
   for (int w = 0; w < nw; ++w) T += red_ll[w];
-  // Team size: small problems (few 16-slot chunks per warp) let several warps
-  // share one unit, since one warp's TMA ring sustains only a few copies per us.
-  int team = p.team_force;
-  if (team <= 0) {
-    const long long per_warp = T * p.H * (p.bs / 16) / p.total_warps;
-    team = per_warp >= 48 ? 1 : (per_warp >= 24 ? 2 : (per_warp >= 12 ? 4 : 8));
-  }
-  while (team > 1 && (team > p.team_max || nw % team)) team >>= 1;
-  const long long target = max(1, p.target_units / team);
+  const long long target = max(1, p.target_units);
   long long Pll = (T * p.H + target - 1) / target;
   if (Pll < p.min_split) Pll = p.min_split;
   const int P = static_cast<int>(Pll);
@@ -189,7 +180,6 @@ __device__ void compute_plan(const DecodeParams &p, int *Pre, int *Lsm, Plan *pl
     plan->base[3] = tot.x + tot.y + tot.z;
     const int acc = tot.x + tot.y + tot.z + tot.w;
     plan->base[kBuckets] = acc;
-    plan->team = team;
     plan->P = P;
     plan->U = acc * p.H;
   }
@@ -198,7 +188,7 @@ __device__ void compute_plan(const DecodeParams &p, int *Pre, int *Lsm, Plan *pl
 
 // KIND 0: MHA on CUDA cores; 1: MMA with g <= 8; 2: MMA with 8 < g <= 16.
 template <int D, int KIND>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     decode_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                   const DecodeParams p) {
   using G = Geo<D>;
@@ -214,16 +204,13 @@ __global__ void __launch_bounds__(256, 1)
   const int W = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = p.slots;
   const uint32_t slots_base = base;
-  const uint32_t q_base = slots_base + W * S * G::SLOT_BYTES;
-  uint8_t *meta_g = gbase + (q_base - base) + W * (S + 1) * p.q_bytes;
+  uint8_t *meta_g = gbase + W * S * G::SLOT_BYTES;
   SlotMeta *metas = reinterpret_cast<SlotMeta *>(meta_g) + warp * S;
   uint64_t *bars_g = reinterpret_cast<uint64_t *>(meta_g + W * S * sizeof(SlotMeta));
   uint8_t *scratch_g = reinterpret_cast<uint8_t *>(bars_g + W * S);   // W x 1 KiB
   const uint32_t my_scr = smem_u32(scratch_g + warp * 1024);
   int *Pre = reinterpret_cast<int *>(scratch_g + W * 1024);   // [kBuckets][B + 1]
-  // team states: per warp g rows x (D o-values + m + l) floats (only if team_max > 1)
   int *Lsm = Pre + kBuckets * (p.B + 1);                      // seq_lens cache [B]
-  float *tstate = reinterpret_cast<float *>(Lsm + ((p.B + 3) & ~3));
 
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmK);
@@ -244,15 +231,9 @@ __global__ void __launch_bounds__(256, 1)
   trace(0, -1);
   compute_plan(p, Pre, Lsm, &plan);
   trace(1, -1);
-  const int P = plan.P, U = plan.U, T = plan.team;
-  const int tm = warp / T, wt = warp - tm * T;                    // team, rank in team
-  const int n_teams = static_cast<int>(gridDim.x) * (W / T);
-  const int gt = static_cast<int>(blockIdx.x) * (W / T) + tm;
-  const int SF = p.g * (D + 2);                                   // floats per team state
-  float *my_state = tstate + warp * SF;
+  const int P = plan.P, U = plan.U;
 
   const uint32_t my_slots = slots_base + warp * S * G::SLOT_BYTES;
-  const uint32_t my_q = q_base + warp * (S + 1) * p.q_bytes;
   const uint32_t my_bars = smem_u32(bars_g + warp * S);
   if (lane == 0) {
     for (int i = 0; i < S; ++i) mbar_init(my_bars + 8 * i, 1);
@@ -264,19 +245,17 @@ __global__ void __launch_bounds__(256, 1)
   const int chunks_per_block = bs >> 4;
 
   // ------------------------------------------------------------ issuer state
-  // team == 1: first unit static (no atomic storm at launch), then pulled from
-  // a global counter; team > 1: units gt, gt + n_teams, ... (every warp of the
-  // team derives the same sequence, no communication needed).  The issuer
+  // First unit static (no atomic storm at launch), later ones pulled from a
+  // global counter.  The issuer
   // decodes the NEXT unit and starts its block-table loads when it enters the
   // current one, so unit boundaries do not stall on global memory.
-  int u_pref = blockIdx.x * W + warp, team_k = 0;
+  // first units interleave across SMs (warp-major), so small problems spread over the whole chip
+  int u_pref = (p.debug_flags & 4) ? static_cast<int>(blockIdx.x) * W + warp
+                                    : warp * static_cast<int>(gridDim.x) + static_cast<int>(blockIdx.x);
   auto pull_unit = [&]() -> int {
-    if (T == 1) {
-      const int u = __shfl_sync(FULL, u_pref, 0);
-      if (u < U && lane == 0) u_pref = p.total_warps + atomicAdd(p.sched, 1);  // used one unit later
-      return u;
-    }
-    return gt + (team_k++) * n_teams;
+    const int u = __shfl_sync(FULL, u_pref, 0);
+    if (u < U && lane == 0) u_pref = p.total_warps + atomicAdd(p.sched, 1);  // used one unit later
+    return u;
   };
   struct UnitInfo {
     int u, r, h, L, n, e0, e1;
@@ -314,11 +293,10 @@ __global__ void __launch_bounds__(256, 1)
   int nx_bt = 0, nx_dir = 0;
   load_window(nxt, nxt.e0, nx_bt, nx_dir);
   bool is_active = false, is_done = false, is_first = false;
-  int is_ci = 0, is_nc = 0, is_wb = 0, bt_w = 0, dir_w = 0, is_qidx = S;  // first unit -> q entry 0
+  int is_ci = 0, is_nc = 0, is_wb = 0, bt_w = 0, dir_w = 0, is_qidx = 0;
 
   // Produce the next chunk of this warp's work stream (warp-collective).
   // Chunk ci of a unit = 16 slots (sub-chunk ci % cpb) of block e0 + ci / cpb;
-  // a warp of a team takes chunks wt, wt + T, ...
   auto next_chunk = [&](SlotMeta &m, int &blk, int &csub) -> bool {
     if (!is_active) {
       if (is_done) return false;
@@ -332,8 +310,13 @@ __global__ void __launch_bounds__(256, 1)
       is_wb = cur.e0;
       nxt = decode_unit(pull_unit());             // look one unit ahead ...
       load_window(nxt, nxt.e0, nx_bt, nx_dir);    // ... its loads overlap this unit
-      is_qidx = (is_qidx == S) ? 0 : is_qidx + 1;
-      is_ci = wt;
+      if (lane < g) {   // the unit's q rows: pull into L2 now, the consumer loads them later
+        const uint16_t *qrow = p.q + static_cast<int64_t>(cur.r) * p.q_ss +
+                               static_cast<int64_t>(cur.h * g + lane) * p.q_sh;
+        asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(qrow));
+        if (D == 128) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(qrow + 64));
+      }
+      is_ci = 0;
       is_nc = (cur.e1 - cur.e0) * chunks_per_block;
       is_first = true;
       trace(2, cur.u);
@@ -362,7 +345,7 @@ __global__ void __launch_bounds__(256, 1)
     is_first = false;
     csub = c;
     blk = b;
-    is_ci += T;
+    is_ci += 1;
     if (is_ci >= is_nc) {
       flags |= F_LAST;
       is_active = false;
@@ -373,62 +356,49 @@ __global__ void __launch_bounds__(256, 1)
 
   auto issue = [&](int i, const SlotMeta &m, int blk, int csub) {
     if (lane == 0) {
-      metas[i] = m;
+      reinterpret_cast<int4 *>(metas + i)[0] = make_int4(m.u, m.r, m.h, m.nsplit);
+      reinterpret_cast<int4 *>(metas + i)[1] = make_int4(m.lo, m.hi, m.flags, m.qidx);
       const uint32_t bar = my_bars + 8 * i;
       const bool kv = !(m.flags & F_NOKV);
-      const bool qq = (m.flags & F_FIRST) && !(m.flags & F_NOQ);
-      const uint32_t bytes = (kv ? G::SLOT_BYTES : 0) + (qq ? g * D * 2 : 0);
+      const uint32_t bytes = kv ? G::SLOT_BYTES : 0;
       mbar_arrive_expect_tx(bar, bytes);
       if (kv) {
-        const uint32_t dk = my_slots + i * G::SLOT_BYTES, dv = dk + G::KV_BYTES;
         // one 5-D box = the whole 16-slot x d tile, laid out [half][slot][128 B] swizzled
+        const uint32_t dk = my_slots + i * G::SLOT_BYTES, dv = dk + G::KV_BYTES;
         tma_load_5d(dk, &tmK, 0, csub * 16, 0, m.h, blk, bar, pol);
         tma_load_5d(dv, &tmV, 0, csub * 16, 0, m.h, blk, bar, pol);
-      }
-      if (qq) {
-        const uint32_t dq = my_q + m.qidx * p.q_bytes;
-        for (int j = 0; j < g; ++j)
-          bulk_load(dq + j * D * 2,
-                    p.q + static_cast<int64_t>(m.r) * p.q_ss +
-                        static_cast<int64_t>(m.h * g + j) * p.q_sh,
-                    D * 2, bar);
       }
     }
   };
 
   // --------------------------------------------------------- consumer state
-  constexpr int NCH = D / 16;   // MHA: 16-byte K pieces per lane (lane = token x half of d)
-  constexpr int EPL = D / 32;   // output elements per lane (MHA P.V, merge)
+  constexpr int NCH = D / 16;       // MHA: 16-byte K pieces per lane (lane = token x half of d)
+  constexpr int EPL = D / 32;       // output elements per lane (MHA P.V, merge)
   constexpr int NT = G16 ? 2 : 1;   // MMA: 8-head n-tiles
   constexpr int MT = D / 16;        // MMA: 16-element d tiles (= k-steps of Q.K^T)
-  // MHA state: q (fp32) lives in the warp scratch, o in registers
-  float2 o2[MMA ? 1 : EPL / 2];
-  // MMA state: Q^T B-fragments, O^T accumulators [d tile][head tile]
-  uint32_t qb[MMA ? MT : 1][NT][2];
-  float oacc[MMA ? MT : 1][NT][4];
-  float mrun[NT][2], lrun[NT][2];   // MHA uses mrun[0][0], lrun[0][0]
-  // chunk fragments (smem -> registers before the slot is refilled)
-  uint4 kw[MMA ? 1 : NCH];
-  uint32_t vw[MMA ? 1 : 16][EPL / 2];
-  uint32_t ka[MMA ? MT : 1][4], va[MMA ? MT : 1][4];
+  float2 o2[MMA ? 1 : EPL / 2];                  // MHA output accumulator (q lives in scratch)
+  uint32_t qb[MMA ? MT : 1][NT][2];              // MMA: Q^T B-fragments
+  float oacc[MMA ? MT : 1][NT][4];               // MMA: O^T accumulators [d tile][head tile]
+  float mrun[NT][2], lrun[NT][2];                // MHA uses [0][0]
 
+  // q of the unit: global loads (the issuer pulled the rows into L2 when it
+  // started the unit, several chunks ago)
   auto begin_unit = [&](const SlotMeta &m) {
 #pragma unroll
     for (int n = 0; n < NT; ++n) {
       mrun[n][0] = mrun[n][1] = -INFINITY;
       lrun[n][0] = lrun[n][1] = 0.f;
     }
-    const uint32_t qs = my_q + m.qidx * p.q_bytes;
     const bool noq = m.flags & F_NOQ;
+    const uint16_t *qg = p.q + static_cast<int64_t>(m.r) * p.q_ss + static_cast<int64_t>(m.h * g) * p.q_sh;
     if constexpr (!MMA) {
 #pragma unroll
       for (int k = 0; k < EPL / 2; ++k) o2[k] = make_float2(0.f, 0.f);
-      // q row -> fp32 in the warp scratch (read back as smem broadcasts)
-      if constexpr (EPL == 4) {
-        const uint2 w = noq ? make_uint2(0u, 0u) : lds64(qs + lane * 8);
+      if constexpr (EPL == 4) {   // q row -> fp32 in the warp scratch (read back as broadcasts)
+        const uint2 w = noq ? make_uint2(0u, 0u) : __ldg(reinterpret_cast<const uint2 *>(qg) + lane);
         st_shared_v4f(my_scr + lane * 16, bf16lo(w.x), bf16hi(w.x), bf16lo(w.y), bf16hi(w.y));
       } else {
-        const uint32_t w = noq ? 0u : lds32(qs + lane * 4);
+        const uint32_t w = noq ? 0u : __ldg(reinterpret_cast<const uint32_t *>(qg) + lane);
         st_shared_v2f(my_scr + lane * 8, bf16lo(w), bf16hi(w));
       }
       __syncwarp();
@@ -442,11 +412,11 @@ __global__ void __launch_bounds__(256, 1)
       for (int n = 0; n < NT; ++n) {
         const int head = n * 8 + (lane >> 2);
         const bool ok = !noq && head < g;
+        const uint32_t *qh = reinterpret_cast<const uint32_t *>(qg + static_cast<int64_t>(ok ? head : 0) * p.q_sh) + (lane & 3);
 #pragma unroll
         for (int ks = 0; ks < MT; ++ks) {
-          const uint32_t a = qs + (head * D + ks * 16 + (lane & 3) * 2) * 2;
-          qb[ks][n][0] = ok ? lds32(a) : 0u;
-          qb[ks][n][1] = ok ? lds32(a + 16) : 0u;
+          qb[ks][n][0] = ok ? __ldg(qh + ks * 8) : 0u;
+          qb[ks][n][1] = ok ? __ldg(qh + ks * 8 + 4) : 0u;
         }
       }
     }
@@ -463,21 +433,24 @@ __global__ void __launch_bounds__(256, 1)
     __syncwarp();
   };
 
-  // smem -> registers for one chunk (after this the slot may be refilled)
-  auto load_chunk = [&](uint32_t sk, int lo, int hi) {
+  // One chunk: loads are placed right before their use, and the slot is handed
+  // back to the issuer (`release`) as soon as both tiles sit in registers.
+  auto consume = [&](uint32_t sk, int lo, int hi, auto &&release) {
     const uint32_t sv = sk + G::KV_BYTES;
     if (lo > 0 || hi < 16) zero_dead_rows(sv, lo, hi);   // P = 0 must never meet NaN (Q10)
-    const int mi = lane >> 3;
     if constexpr (!MMA) {
+      // ---- s_t = q.k_t : lane = (token t, half hf of d); q from the warp scratch
       const int t = lane & 15, hf = lane >> 4;
       const uint32_t krow = sk + (D == 128 ? hf * G::HALF_BYTES : 0) + t * 128;
       const int cbase = (D == 128) ? 0 : hf * 4;
+      uint4 kw[NCH];
 #pragma unroll
       for (int cc = 0; cc < NCH; ++cc) kw[cc] = lds128(krow + (((cbase + cc) ^ (t & 7)) << 4));
       uint32_t vcol;
       if constexpr (D == 128) vcol = sv + (lane >> 4) * G::HALF_BYTES + (lane & 1) * 8;
       else vcol = sv + (lane & 3) * 4;
       const int c = (D == 128) ? ((lane & 15) >> 1) : (lane >> 2);
+      uint32_t vw[16][EPL / 2];
 #pragma unroll
       for (int tt = 0; tt < 16; ++tt) {
         if constexpr (EPL == 4) {
@@ -488,28 +461,7 @@ __global__ void __launch_bounds__(256, 1)
           vw[tt][0] = lds32(vcol + swz(tt, c));
         }
       }
-    } else {
-      // A = K (16 tokens x 16 d per k-step): matrices (t0-7,d0-7) (t8-15,d0-7) (t0-7,d8-15) (t8-15,d8-15)
-#pragma unroll
-      for (int ks = 0; ks < MT; ++ks) {
-        const int tok = (mi & 1) * 8 + (lane & 7), de = ks * 16 + (mi >> 1) * 8;
-        ldsm_x4(sk + (de >> 6) * G::HALF_BYTES + swz(tok, (de & 63) >> 3), ka[ks][0], ka[ks][1],
-                ka[ks][2], ka[ks][3]);
-      }
-      // A = V^T (16 d x 16 tokens per d tile) via ldmatrix.trans of V rows
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        const int tok = (mi >> 1) * 8 + (lane & 7), de = mt * 16 + (mi & 1) * 8;
-        ldsm_x4_t(sv + (de >> 6) * G::HALF_BYTES + swz(tok, (de & 63) >> 3), va[mt][0], va[mt][1],
-                  va[mt][2], va[mt][3]);
-      }
-    }
-  };
-
-  auto compute_chunk = [&](int lo, int hi) {
-    if constexpr (!MMA) {
-      // ---- s_t = q.k_t : lane = (token t, half hf of d); q from the warp scratch
-      const int t = lane & 15, hf = lane >> 4;
+      release();
       float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
 #pragma unroll
       for (int cc = 0; cc < NCH; ++cc) {
@@ -539,26 +491,24 @@ __global__ void __launch_bounds__(256, 1)
       // ---- o = alpha * o + sum_t p_t v_t  (p broadcast through the scratch)
       if (lane < 16) st_shared_f32(my_scr + 512 + lane * 4, pr);
       __syncwarp();
-      float pt[16];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint4 w = lds128(my_scr + 512 + k * 16);
-        pt[4 * k + 0] = __uint_as_float(w.x);
-        pt[4 * k + 1] = __uint_as_float(w.y);
-        pt[4 * k + 2] = __uint_as_float(w.z);
-        pt[4 * k + 3] = __uint_as_float(w.w);
-      }
       const float2 a2 = make_float2(alpha, alpha);
 #pragma unroll
       for (int k = 0; k < EPL / 2; ++k) o2[k] = __fmul2_rn(o2[k], a2);
 #pragma unroll
-      for (int tt = 0; tt < 16; ++tt) {
-        const float2 pp = make_float2(pt[tt], pt[tt]);
+      for (int t4 = 0; t4 < 4; ++t4) {
+        const uint4 pw4 = lds128(my_scr + 512 + t4 * 16);
+        const float pt[4] = {__uint_as_float(pw4.x), __uint_as_float(pw4.y), __uint_as_float(pw4.z),
+                             __uint_as_float(pw4.w)};
 #pragma unroll
-        for (int k = 0; k < EPL / 2; ++k)
-          o2[k] = __ffma2_rn(pp, make_float2(bf16lo(vw[tt][k]), bf16hi(vw[tt][k])), o2[k]);
+        for (int i = 0; i < 4; ++i) {
+          const float2 pp = make_float2(pt[i], pt[i]);
+#pragma unroll
+          for (int k = 0; k < EPL / 2; ++k)
+            o2[k] = __ffma2_rn(pp, make_float2(bf16lo(vw[t4 * 4 + i][k]), bf16hi(vw[t4 * 4 + i][k])), o2[k]);
+        }
       }
     } else {
+      const int mi = lane >> 3;
       // ---- S^T = K . Q^T : rows = 16 tokens, cols = 8 heads per tile
       float sa[NT][4], sb[NT][4];
 #pragma unroll
@@ -566,12 +516,26 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
         for (int j = 0; j < 4; ++j) sa[n][j] = sb[n][j] = 0.f;
 #pragma unroll
-      for (int ks = 0; ks < MT; ++ks)
+      for (int ks = 0; ks < MT; ++ks) {
+        // A = K (16 tokens x 16 d): matrices (t0-7,d0-7) (t8-15,d0-7) (t0-7,d8-15) (t8-15,d8-15)
+        const int tok = (mi & 1) * 8 + (lane & 7), de = ks * 16 + (mi >> 1) * 8;
+        uint32_t a0, a1, a2, a3;
+        ldsm_x4(sk + (de >> 6) * G::HALF_BYTES + swz(tok, (de & 63) >> 3), a0, a1, a2, a3);
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
           float(&acc)[4] = (ks & 1) ? sb[n] : sa[n];   // two independent MMA chains
-          mma_bf16_16816(acc, ka[ks][0], ka[ks][1], ka[ks][2], ka[ks][3], qb[ks][n][0], qb[ks][n][1]);
+          mma_bf16_16816(acc, a0, a1, a2, a3, qb[ks][n][0], qb[ks][n][1]);
         }
+      }
+      // A = V^T (16 d x 16 tokens per d tile) via ldmatrix.trans of V rows, then free the slot
+      uint32_t va[MT][4];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int tok = (mi >> 1) * 8 + (lane & 7), de = mt * 16 + (mi & 1) * 8;
+        ldsm_x4_t(sv + (de >> 6) * G::HALF_BYTES + swz(tok, (de & 63) >> 3), va[mt][0], va[mt][1],
+                  va[mt][2], va[mt][3]);
+      }
+      release();
       const int t0 = lane >> 2, t1 = t0 + 8;
       const bool ok0 = t0 >= lo && t0 < hi, ok1 = t1 >= lo && t1 < hi;
       float alpha[NT][2];
@@ -612,8 +576,8 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
           const float2 a2 = make_float2(alpha[n][0], alpha[n][1]);
-          float2 lo2 = __fmul2_rn(make_float2(oacc[mt][n][0], oacc[mt][n][1]), a2);
-          float2 hi2 = __fmul2_rn(make_float2(oacc[mt][n][2], oacc[mt][n][3]), a2);
+          const float2 lo2 = __fmul2_rn(make_float2(oacc[mt][n][0], oacc[mt][n][1]), a2);
+          const float2 hi2 = __fmul2_rn(make_float2(oacc[mt][n][2], oacc[mt][n][3]), a2);
           oacc[mt][n][0] = lo2.x;
           oacc[mt][n][1] = lo2.y;
           oacc[mt][n][2] = hi2.x;
@@ -721,93 +685,7 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) p.counters[r * H + h] = 0;  // self-reset for the next call
   };
 
-  // Team end of unit: every warp of the team deposits its (m, l, o) state in
-  // shared memory; after a named barrier the team combines them (online-
-  // softmax merge, fixed warp order) and writes the output rows or the unit's
-  // split partial; a second barrier frees the state area.
-  auto team_end_unit = [&](const SlotMeta &m) {
-    const int r = m.r, h = m.h, u = m.u;
-    if constexpr (!MMA) {
-      float l0 = lrun[0][0];
-#pragma unroll
-      for (int o = 16; o; o >>= 1) l0 += __shfl_xor_sync(FULL, l0, o);
-#pragma unroll
-      for (int k = 0; k < EPL / 2; ++k) {
-        my_state[lane * EPL + 2 * k] = o2[k].x;
-        my_state[lane * EPL + 2 * k + 1] = o2[k].y;
-      }
-      if (lane == 0) {
-        my_state[D] = mrun[0][0];
-        my_state[D + 1] = l0;
-      }
-    } else {
-      const int d0 = lane >> 2;
-#pragma unroll
-      for (int n = 0; n < NT; ++n)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          float l = lrun[n][j];
-          l += __shfl_xor_sync(FULL, l, 4);
-          l += __shfl_xor_sync(FULL, l, 8);
-          l += __shfl_xor_sync(FULL, l, 16);
-          const int head = n * 8 + (lane & 3) * 2 + j;
-          if (head < g) {
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt) {
-              my_state[head * D + mt * 16 + d0] = oacc[mt][n][j];
-              my_state[head * D + mt * 16 + d0 + 8] = oacc[mt][n][2 + j];
-            }
-            if (d0 == 0) {
-              my_state[g * D + 2 * head] = mrun[n][j];
-              my_state[g * D + 2 * head + 1] = l;
-            }
-          }
-        }
-    }
-    named_bar_sync(1 + tm, T * 32);
-    const float *ts = tstate + tm * T * SF;
-    for (int idx = wt * 32 + lane; idx < g * D; idx += T * 32) {
-      const int row = idx / D, e = idx - row * D;
-      float M = -INFINITY;
-      for (int k = 0; k < T; ++k) M = fmaxf(M, ts[k * SF + g * D + 2 * row]);
-      float Ls = 0.f, O = 0.f;
-      if (M != -INFINITY) {
-        for (int k = 0; k < T; ++k) {
-          const float w = ex2(ts[k * SF + g * D + 2 * row] - M);
-          Ls = fmaf(ts[k * SF + g * D + 2 * row + 1], w, Ls);
-          O = fmaf(ts[k * SF + row * D + e], w, O);
-        }
-      }
-      if (m.nsplit == 1) {
-        const __nv_bfloat16 b = __float2bfloat16_rn(Ls > 0.f ? O / Ls : 0.f);
-        p.out[static_cast<int64_t>(r) * p.o_ss + static_cast<int64_t>(h * g + row) * p.o_sh + e] =
-            *reinterpret_cast<const uint16_t *>(&b);
-      } else {
-        p.part_o[(static_cast<int64_t>(u) * g + row) * D + e] = O;
-        if (e == 0)
-          *reinterpret_cast<float2 *>(p.part_ml + (static_cast<int64_t>(u) * g + row) * 2) = make_float2(M, Ls);
-      }
-    }
-    named_bar_sync(1 + tm, T * 32);
-    if (m.nsplit > 1 && wt == 0) {
-      int prev = 0;
-      if (lane == 0) {
-        prev = atom_add_release_gpu(p.counters + r * H + h, 1);
-        if (prev == m.nsplit - 1) fence_acq_rel_gpu();
-      }
-      prev = __shfl_sync(FULL, prev, 0);
-      if (prev == m.nsplit - 1) {
-        trace(5, m.u);
-        merge_splits(m);
-      }
-    }
-  };
-
   auto end_unit = [&](const SlotMeta &m) {
-    if (T > 1) {
-      team_end_unit(m);
-      return;
-    }
     const int r = m.r, h = m.h, u = m.u;
     if constexpr (!MMA) {
       float l0 = lrun[0][0];
@@ -902,53 +780,55 @@ __global__ void __launch_bounds__(256, 1)
     if (!next_chunk(m, blk, cs)) break;
     issue(issued, m, blk, cs);
   }
+  long long prof[6] = {0, 0, 0, 0, 0, 0};   // dev (BKV_TRACE): cycles wait/begin/consume/issue/end, chunks
+  const bool profiling = p.trace != nullptr;
   int slot = 0;
   uint32_t phase = 0;
-  long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // dev (BKV_TRACE): cycle breakdown, chunks
-  const bool profiling = p.trace != nullptr;
   for (int seq = 0; seq < issued; ++seq) {
     __syncwarp();
-    const SlotMeta m = metas[slot];
-    long long c0 = profiling ? clock64() : 0;
+    const int4 mw0 = reinterpret_cast<const int4 *>(metas + slot)[0];
+    const int4 mw1 = reinterpret_cast<const int4 *>(metas + slot)[1];
+    const SlotMeta m{mw0.x, mw0.y, mw0.z, mw0.w, mw1.x, mw1.y, mw1.z, mw1.w};
+    const long long c0 = profiling ? clock64() : 0;
     mbar_wait(my_bars + 8 * slot, phase);
-    long long c1 = profiling ? clock64() : 0;
+    const long long c1 = profiling ? clock64() : 0;
     if (m.flags & F_FIRST) {
       trace(3, m.u);
       begin_unit(m);
     }
-    const bool has_kv = !(m.flags & F_NOKV);
-    if (has_kv) load_chunk(my_slots + slot * G::SLOT_BYTES, m.lo, m.hi);
-    long long c1b = profiling ? clock64() : 0;
-    __syncwarp();
-    if (!(p.debug_flags & 2)) fence_proxy_async_smem();  // our smem accesses precede the TMA refill
-    long long c2 = profiling ? clock64() : 0;
-    long long c2b = c2;
-    {
+    const long long c2 = profiling ? clock64() : 0;
+    long long ci0 = 0, ci1 = 0;
+    // refill this slot with the warp's next chunk (after our reads of it)
+    auto release = [&]() {
+      if (profiling) ci0 = clock64();
+      __syncwarp();
+      if (m.lo > 0 || m.hi < 16) fence_proxy_async_smem();   // zeroed rows precede the TMA write
       SlotMeta mn;
       int blk, cs;
       if (next_chunk(mn, blk, cs)) {
-        c2b = profiling ? clock64() : 0;
         issue(slot, mn, blk, cs);
         ++issued;
       }
+      if (profiling) ci1 = clock64();
+    };
+    if (!(m.flags & F_NOKV) && !(p.debug_flags & 1)) {
+      consume(my_slots + slot * G::SLOT_BYTES, m.lo, m.hi, release);
+    } else {
+      release();
     }
-    long long c3 = profiling ? clock64() : 0;
-    if (has_kv && !(p.debug_flags & 1)) compute_chunk(m.lo, m.hi);
-    long long c4 = profiling ? clock64() : 0;
+    const long long c3 = profiling ? clock64() : 0;
     if (m.flags & F_LAST) {
       end_unit(m);
       trace(4, m.u);
     }
     if (profiling) {
-      const long long c5 = clock64();
+      const long long c4 = clock64();
       prof[0] += c1 - c0;
-      prof[1] += c1b - c1;
-      prof[2] += c3 - c2;
-      prof[3] += c4 - c3;
-      prof[4] += c5 - c4;
+      prof[1] += c2 - c1;
+      prof[2] += (c3 - c2) - (ci1 - ci0);
+      prof[3] += ci1 - ci0;
+      prof[4] += c4 - c3;
       prof[5] += 1;
-      prof[6] += c2 - c1b;
-      prof[7] += c3 - c2b;
     }
     if (++slot == S) {
       slot = 0;
@@ -956,7 +836,7 @@ __global__ void __launch_bounds__(256, 1)
     }
   }
   if (profiling)
-    for (int k = 0; k < 8; ++k) trace(8 + k, static_cast<int>(min(prof[k], (long long)0x7fffffff)));
+    for (int k = 0; k < 6; ++k) trace(8 + k, static_cast<int>(min(prof[k], (long long)0x7fffffff)));
 
   trace(6, -1);
   // ------------------------------------------------- scheduler self-reset
@@ -988,26 +868,26 @@ cudaError_t decode_config(int head_dim, int group, int num_seqs, DecodeLaunch *c
   if (e != cudaSuccess) return e;
   e = cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (e != cudaSuccess) return e;
-  const int W = env_int("BKV_WARPS", 8);
   int S = env_int("BKV_SLOTS", 2);
   const int slot_bytes = 2 * (head_dim / 64) * 2048;
-  const int qb = ((group * head_dim * 2) + 127) / 128 * 128;
-  const int team_state = group <= 8 ? W * group * (head_dim + 2) * 4 : 0;
-  auto need = [&](int s) {
-    return 1024 + W * s * slot_bytes + W * (s + 1) * qb + W * s * (int)(sizeof(int) * 8) +
-           W * s * 8 + W * 1024 + 4 * (num_seqs + 1) * (int)sizeof(int) + ((num_seqs + 3) & ~3) * 4 + team_state + 256;
+  const int qb = 0;   // q is read from global (L2-prefetched), no shared-memory ring
+  auto need = [&](int w, int s) {
+    return 1024 + w * s * slot_bytes + w * s * (int)(sizeof(int) * 8) + w * s * 8 + w * 1024 +
+           4 * (num_seqs + 1) * (int)sizeof(int) + ((num_seqs + 3) & ~3) * 4 + 256;
   };
-  while (S > 1 && need(S) > smem_optin - 1024) --S;
+  int W = env_int("BKV_WARPS", 12);
+  while (W > 4 && need(W, S) > smem_optin - 1024) W -= 4;
+  while (S > 1 && need(W, S) > smem_optin - 1024) --S;
   cfg->grid = sms * env_int("BKV_CTAS_PER_SM", 1);
   cfg->warps = W;
-  cfg->smem_bytes = need(S);
+  cfg->smem_bytes = need(W, S);
   *slots = S;
   *q_bytes = qb;
   return cudaSuccess;
 }
 
 int decode_target_units(const DecodeLaunch &cfg) {
-  return env_int("BKV_UNITS_PER_WARP", 4) * cfg.grid * cfg.warps;
+  return env_int("BKV_UNITS_PER_WARP", 3) * cfg.grid * cfg.warps;
 }
 
 int decode_min_split(int group) { return env_int("BKV_MIN_SPLIT", group > 1 ? 16 : 4); }

@@ -15,7 +15,7 @@ bt = torch.from_numpy(lay.block_tables).cuda(); dirs = torch.from_numpy(lay.dirs
 lens = torch.from_numpy(lay.lens).cuda(); q = torch.randn(lay.batch, Hq, d, device="cuda").to(torch.bfloat16)
 ws = bkv.workspace(lay.batch, Hq, H, d)
 cap = int(os.environ["BKV_TRACE"])
-nw = 148 * int(os.environ.get("BKV_WARPS", "8"))
+nw = 148 * int(os.environ.get("BKV_WARPS", "12"))
 need = nw * cap * 16
 total = bkv.decode_workspace_size(lay.batch, Hq, H, d)   # trace region = last up256(need) bytes
 start = total - ((need + 255) // 256 * 256)
@@ -51,14 +51,13 @@ busy = (exit_ - plan_done)
 print(f"  units per warp: {np.bincount((col(4) >= 0).sum(1))[:8]}")
 
 # per-warp cycle breakdown (kinds 8..13: wait, smem->reg, issue, math, end-of-unit, chunks)
-vals = np.zeros((nw, 8))
-for kk in range(8):
+vals = np.zeros((nw, 6))
+for kk in range(6):
     sel = (k == 8 + kk) & valid
     vals[:, kk] = np.where(sel, tr[:, :, 1], 0).sum(1)
 act = vals[:, 5] > 0
 v = vals[act]
-names = ["wait", "smem->reg", "issue(all)", "math", "end-unit"]
+names = ["wait", "begin-unit", "consume", "issue", "end-unit"]
 tot = v[:, :5].sum(1)
 print("  per-warp cycles (active warps, median): " + ", ".join(f"{n} {np.median(v[:, i]):.0f}" for i, n in enumerate(names)) +
       f"; chunks {np.median(v[:, 5]):.0f}; per chunk: " + ", ".join(f"{n} {np.median(v[:, i] / np.maximum(v[:, 5], 1)):.0f}" for i, n in enumerate(names)))
-print(f"  per chunk: syncwarp+fence {np.median(v[:, 6] / np.maximum(v[:, 5], 1)):.0f}, TMA-issue part {np.median(v[:, 7] / np.maximum(v[:, 5], 1)):.0f}")
