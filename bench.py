@@ -83,7 +83,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
@@ -321,8 +321,8 @@ def run_ours(args):
     # ---- device-resident timed region (W warm-up steps done above)
     clocks = ClockSampler(local)
     clocks.start()
+    time.sleep(0.2)                          # let nvidia-smi attach before the timed region
     ms_total = timed(run_step, args.steps)
-    clk = clocks.stop()
     ms_step = ms_total / args.steps
     launches = launches_per_step * args.steps
     # ---- the dominant kernel alone: same pools, attention launches only, same stream
@@ -345,6 +345,7 @@ def run_ours(args):
     for _ in range(2):
         e2e_step()
     ms_e2e = timed(e2e_step, args.steps) / args.steps
+    clk = clocks.stop()                      # clocks sampled over all three timed regions
     h2d = sum(v.numel() * v.element_size() for v in meta_h.values()) + \
         (q_h.numel() + kn_h.numel() + vn_h.numel()) * 2
     d2h = out_h.numel() * 2
@@ -404,7 +405,7 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="opt13b", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

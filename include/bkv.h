@@ -168,6 +168,31 @@ BKV_API bkv_status bkv_paged_decode_attention(const bkv_kv_pool *pool, const bkv
                                       void *workspace, size_t workspace_bytes,
                                       bkv_stream_t stream);
 
+/*
+ * Lazy checkpointing.  "Only the KV tensors of a
+ * specific request that are about to be overwritten by its peer need to be
+ * checkpointed in CPU memory" and are "swapped back into GPU memory when the
+ * request is scheduled"; BROS uses "CUDA kernels to
+ * efficiently fetch and store KV caches in non-continuous GPU memory".
+ *
+ *   bkv_kv_checkpoint  gathers the K and V rows (every kv head of the pool) of
+ *                      n physical slots -- slot id = block*block_size + slot,
+ *                      the value bkv_kv_append reports in slot_mapping_out --
+ *                      into k_out / v_out, bf16 [n][num_kv_heads][head_dim]
+ *                      contiguous, 16-byte aligned.  The destination may be
+ *                      device memory or the device alias of mapped pinned host
+ *                      memory (a direct device-to-host checkpoint).
+ *   bkv_kv_restore     scatters such rows back into their slots (swap-in).
+ * Both are bit-exact copies and change nothing else.  Issue the checkpoint
+ * BEFORE the bkv_kv_append that overwrites those slots, on the same stream
+ * (stream order is the synchronisation).  Slot ids must be < num_blocks *
+ * block_size; n = 0 is a no-op.
+ */
+BKV_API bkv_status bkv_kv_checkpoint(const bkv_kv_pool *pool, const int64_t *slot_ids, int32_t n,
+                                     void *k_out, void *v_out, bkv_stream_t stream);
+BKV_API bkv_status bkv_kv_restore(const bkv_kv_pool *pool, const int64_t *slot_ids, int32_t n,
+                                  const void *k_in, const void *v_in, bkv_stream_t stream);
+
 /* Workspace bytes for bkv_paged_decode_attention on the CURRENT device
  * (depends on the SM count); 0 on error (see bkv_last_error). */
 BKV_API size_t bkv_decode_workspace_size(int32_t num_seqs, int32_t num_q_heads, int32_t num_kv_heads,

@@ -53,6 +53,12 @@ def lib():
         L.bkvo_attention.argtypes = [P, P, i64, i64, i64, i32, i32, i32,
                                      P, i32, P, i32, i32, P, i32, i32, P, i32, dbl, P]
         L.bkvo_attention.restype = None
+        L.bkvo_checkpoint.argtypes = [P, P, i64, i64, i64, i32, i32, i32, P, i32, P, P]
+        L.bkvo_checkpoint.restype = None
+        L.bkvo_restore.argtypes = [P, P, i64, i64, i64, i32, i32, i32, P, i32, P, P]
+        L.bkvo_restore.restype = None
+        L.bkvo_overwritten_peers.argtypes = [i32, P, i32, P, i32, i32, P, P, P, i32, i32, P, P, P, i32]
+        L.bkvo_overwritten_peers.restype = i32
         L.bkvo_num_threads.restype = i32
         L.bkvo_set_num_threads.argtypes = [i32]
         _lib = L
@@ -154,6 +160,38 @@ def attention(K, V, block_tables, dirs, lens, q, scale: float, r_range=None):
                          _ptr(dd), rs, cs, _ptr(ln), int(r0), int(r1), _ptr(qq), int(Hq),
                          float(scale), _ptr(out))
     return out
+
+
+def checkpoint(K, V, slot_ids):
+    """Rows of the given physical slots -> (k, v) uint16 [n][H][d] (lazy checkpoint)."""
+    sb, sh, ss, H, d, bs = _pool_geom(K)
+    sl = _c(slot_ids, np.int64)
+    ko = np.zeros((sl.shape[0], H, d), np.uint16)
+    vo = np.zeros((sl.shape[0], H, d), np.uint16)
+    lib().bkvo_checkpoint(_ptr(K), _ptr(V), sb, sh, ss, H, d, bs, _ptr(sl), int(sl.shape[0]), _ptr(ko), _ptr(vo))
+    return ko, vo
+
+
+def restore(K, V, slot_ids, k_in, v_in):
+    """In-place scatter of checkpointed rows back into their slots (swap-in)."""
+    sb, sh, ss, H, d, bs = _pool_geom(K)
+    sl = _c(slot_ids, np.int64)
+    lib().bkvo_restore(_ptr(K), _ptr(V), sb, sh, ss, H, d, bs, _ptr(sl), int(sl.shape[0]),
+                       _ptr(_c(k_in, np.uint16)), _ptr(_c(v_in, np.uint16)))
+
+
+def overwritten_peers(block_tables, dirs, live_lens, before, n_new, num_blocks, bs, cap=1 << 16):
+    """Live peer tokens an append would overwrite: list of (request, token, slot id)."""
+    bt = _c(block_tables, np.int32)
+    d, rs, cs = _dirs(dirs)
+    ll, bf, nn = _c(live_lens, np.int32), _c(before, np.int32), _c(n_new, np.int32)
+    vr = np.zeros(cap, np.int32)
+    vt = np.zeros(cap, np.int64)
+    vs = np.zeros(cap, np.int64)
+    k = lib().bkvo_overwritten_peers(int(ll.shape[0]), _ptr(bt), int(bt.shape[1]), _ptr(d), rs, cs, _ptr(ll),
+                                     _ptr(bf), _ptr(nn), int(num_blocks), int(bs), _ptr(vr), _ptr(vt), _ptr(vs), cap)
+    k = min(k, cap)
+    return [(int(vr[i]), int(vt[i]), int(vs[i])) for i in range(k)]
 
 
 def num_threads() -> int:

@@ -230,6 +230,79 @@ void bkvo_attention(const uint16_t *K, const uint16_t *V, int64_t sb, int64_t sh
     }
 }
 
+/*
+ * Lazy checkpointing: copy the K/V rows (every head) of the given
+ * physical slots (slot id = block*bs + slot) out of the pool, or back into it
+ * on swap-in.  Buffers are [n][H][d].  Pure copies.
+ */
+void bkvo_checkpoint(const uint16_t *K, const uint16_t *V, int64_t sb, int64_t sh, int64_t ss,
+                     int H, int d, int bs, const int64_t *slot_ids, int n,
+                     uint16_t *k_out, uint16_t *v_out) {
+    for (int i = 0; i < n; ++i) {
+        int64_t blk = slot_ids[i] / bs, slot = slot_ids[i] % bs;
+        for (int h = 0; h < H; ++h) {
+            int64_t src = blk * sb + (int64_t)h * sh + slot * ss;
+            memcpy(k_out + ((int64_t)i * H + h) * d, K + src, sizeof(uint16_t) * (size_t)d);
+            memcpy(v_out + ((int64_t)i * H + h) * d, V + src, sizeof(uint16_t) * (size_t)d);
+        }
+    }
+}
+
+void bkvo_restore(uint16_t *K, uint16_t *V, int64_t sb, int64_t sh, int64_t ss,
+                  int H, int d, int bs, const int64_t *slot_ids, int n,
+                  const uint16_t *k_in, const uint16_t *v_in) {
+    for (int i = 0; i < n; ++i) {
+        int64_t blk = slot_ids[i] / bs, slot = slot_ids[i] % bs;
+        for (int h = 0; h < H; ++h) {
+            int64_t dst = blk * sb + (int64_t)h * sh + slot * ss;
+            memcpy(K + dst, k_in + ((int64_t)i * H + h) * d, sizeof(uint16_t) * (size_t)d);
+            memcpy(V + dst, v_in + ((int64_t)i * H + h) * d, sizeof(uint16_t) * (size_t)d);
+        }
+    }
+}
+
+/*
+ * Peer slots an append would overwrite (the lazy-checkpoint trigger of
+ * P:726-728): for every new token of every request, if its target slot holds
+ * a live token of ANOTHER request (per the current lengths `live_lens`),
+ * report that victim (request, token, slot id).  Returns the number found
+ * (at most cap are written).  O(sum of lengths) with a per-slot owner table.
+ */
+int bkvo_overwritten_peers(int B, const int32_t *bt, int bt_stride, const uint8_t *dirs, int rs, int cs,
+                           const int32_t *live_lens, const int32_t *before, const int32_t *n_new,
+                           int num_blocks, int bs, int32_t *victim_r, int64_t *victim_t,
+                           int64_t *victim_slot, int cap) {
+    int64_t nslots = (int64_t)num_blocks * bs;
+    int32_t *own_r = malloc(sizeof(int32_t) * (size_t)nslots);
+    int64_t *own_t = malloc(sizeof(int64_t) * (size_t)nslots);
+    for (int64_t s = 0; s < nslots; ++s) own_r[s] = -1;
+    for (int r = 0; r < B; ++r)
+        for (int64_t t = 0; t < live_lens[r]; ++t) {
+            int32_t blk; int slot;
+            locate(bt, bt_stride, dirs, rs, cs, bs, r, t, &blk, &slot);
+            own_r[(int64_t)blk * bs + slot] = r;
+            own_t[(int64_t)blk * bs + slot] = t;
+        }
+    int found = 0;
+    for (int r = 0; r < B; ++r)
+        for (int32_t j = 0; j < n_new[r]; ++j) {
+            int64_t t = (int64_t)before[r] + j;
+            int32_t blk; int slot;
+            locate(bt, bt_stride, dirs, rs, cs, bs, r, t, &blk, &slot);
+            int64_t sid = (int64_t)blk * bs + slot;
+            if (own_r[sid] >= 0 && own_r[sid] != r) {
+                if (found < cap) {
+                    victim_r[found] = own_r[sid];
+                    victim_t[found] = own_t[sid];
+                    victim_slot[found] = sid;
+                }
+                ++found;
+            }
+        }
+    free(own_r); free(own_t);
+    return found;
+}
+
 int bkvo_num_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

@@ -43,7 +43,8 @@ _lib = None
 _lib_lock = threading.Lock()
 
 EXPORTS = ("bkv_kv_append", "bkv_paged_decode_attention", "bkv_decode_workspace_size",
-           "bkv_validate_layout_host", "bkv_status_string", "bkv_last_error", "bkv_version")
+           "bkv_validate_layout_host", "bkv_status_string", "bkv_last_error", "bkv_version",
+           "bkv_kv_checkpoint", "bkv_kv_restore")
 
 
 def lib():
@@ -66,6 +67,10 @@ def lib():
                 L.bkv_decode_workspace_size.restype = ctypes.c_size_t
                 L.bkv_validate_layout_host.argtypes = [P, i32, P, i32, i32, i32, P, i32, i32, i32, P]
                 L.bkv_validate_layout_host.restype = ctypes.c_int
+                L.bkv_kv_checkpoint.argtypes = [ctypes.POINTER(_Pool), P, i32, P, P, P]
+                L.bkv_kv_checkpoint.restype = ctypes.c_int
+                L.bkv_kv_restore.argtypes = [ctypes.POINTER(_Pool), P, i32, P, P, P]
+                L.bkv_kv_restore.restype = ctypes.c_int
                 L.bkv_status_string.argtypes = [ctypes.c_int]
                 L.bkv_status_string.restype = ctypes.c_char_p
                 L.bkv_last_error.restype = ctypes.c_char_p
@@ -161,6 +166,32 @@ def kv_append(pool: KVPool, block_tables, dirs, seq_lens_before, cu_new_tokens, 
                              cu_new_tokens.data_ptr(), n, k_new.data_ptr(), v_new.data_ptr(),
                              ctypes.c_void_p(sm), _stream_ptr(stream))
     _check(rc, "bkv_kv_append")
+
+
+def kv_checkpoint(pool: KVPool, slot_ids, k_out=None, v_out=None, stream=None):
+    """bkv_kv_checkpoint: rows of physical slots (int64 ids block*bs+slot) -> [n][H][d] buffers
+    (device tensors, or device views of pinned host memory).  Returns (k_out, v_out)."""
+    p = pool.c()
+    _dev(slot_ids, "slot_ids", torch.int64)
+    n = slot_ids.numel()
+    shape = (n, pool.num_kv_heads, pool.head_dim)
+    if k_out is None:
+        k_out = torch.empty(shape, dtype=torch.bfloat16, device=pool.k.device)
+    if v_out is None:
+        v_out = torch.empty(shape, dtype=torch.bfloat16, device=pool.k.device)
+    rc = lib().bkv_kv_checkpoint(ctypes.byref(p), slot_ids.data_ptr(), n, k_out.data_ptr(), v_out.data_ptr(),
+                                 _stream_ptr(stream))
+    _check(rc, "bkv_kv_checkpoint")
+    return k_out, v_out
+
+
+def kv_restore(pool: KVPool, slot_ids, k_in, v_in, stream=None):
+    """bkv_kv_restore: scatter checkpointed rows back into their slots (swap-in)."""
+    p = pool.c()
+    _dev(slot_ids, "slot_ids", torch.int64)
+    rc = lib().bkv_kv_restore(ctypes.byref(p), slot_ids.data_ptr(), slot_ids.numel(), k_in.data_ptr(),
+                              v_in.data_ptr(), _stream_ptr(stream))
+    _check(rc, "bkv_kv_restore")
 
 
 def decode_workspace_size(num_seqs, num_q_heads, num_kv_heads, head_dim) -> int:

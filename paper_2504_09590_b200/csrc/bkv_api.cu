@@ -187,6 +187,42 @@ bkv_status bkv_kv_append(const bkv_kv_pool *pool, const bkv_block_map *map,
   return BKV_OK;
 }
 
+static bkv_status slot_copy(const bkv_kv_pool *pool, const int64_t *slot_ids, int32_t n, void *kb,
+                            void *vb, int restore, bkv_stream_t stream) {
+  bkv_status s = check_pool(pool);
+  if (s) return s;
+  if (n < 0) return fail(BKV_ERR_INVALID_ARGUMENT, "n < 0");
+  if (n == 0) return BKV_OK;
+  if (!slot_ids || !kb || !vb) return fail(BKV_ERR_INVALID_ARGUMENT, "slot_ids/buffers is NULL");
+  if (!aligned16(kb) || !aligned16(vb)) return fail(BKV_ERR_INVALID_ARGUMENT, "buffers must be 16-byte aligned");
+  bkv::SlotCopyParams p;
+  p.k = static_cast<uint16_t *>(pool->k);
+  p.v = static_cast<uint16_t *>(pool->v);
+  p.sb = pool->stride_block;
+  p.sh = pool->stride_head;
+  p.ss = pool->stride_slot;
+  p.H = pool->num_kv_heads;
+  p.bs = pool->block_size;
+  p.slots = slot_ids;
+  p.n = n;
+  p.buf_k = static_cast<uint16_t *>(kb);
+  p.buf_v = static_cast<uint16_t *>(vb);
+  p.restore = restore;
+  cudaError_t e = bkv::launch_slot_copy(p, pool->head_dim, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, restore ? "kv_restore launch" : "kv_checkpoint launch");
+  return BKV_OK;
+}
+
+bkv_status bkv_kv_checkpoint(const bkv_kv_pool *pool, const int64_t *slot_ids, int32_t n, void *k_out,
+                             void *v_out, bkv_stream_t stream) {
+  return slot_copy(pool, slot_ids, n, k_out, v_out, 0, stream);
+}
+
+bkv_status bkv_kv_restore(const bkv_kv_pool *pool, const int64_t *slot_ids, int32_t n, const void *k_in,
+                          const void *v_in, bkv_stream_t stream) {
+  return slot_copy(pool, slot_ids, n, const_cast<void *>(k_in), const_cast<void *>(v_in), 1, stream);
+}
+
 size_t bkv_decode_workspace_size(int32_t num_seqs, int32_t num_q_heads, int32_t num_kv_heads,
                                  int32_t head_dim) {
   if (head_dim != 64 && head_dim != 128) {

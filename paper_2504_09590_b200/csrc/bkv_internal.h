@@ -25,6 +25,18 @@ struct AppendParams {
 };
 cudaError_t launch_kv_append(const AppendParams &p, int head_dim, cudaStream_t s);
 
+// lazy-checkpoint gather / restore scatter of whole slots (all heads, K and V)
+struct SlotCopyParams {
+  uint16_t *k, *v;  // pool
+  int64_t sb, sh, ss;
+  int H, bs;
+  const int64_t *slots;
+  int n;
+  uint16_t *buf_k, *buf_v;  // [n][H][d] contiguous
+  int restore;              // 0: pool -> buf (checkpoint), 1: buf -> pool (restore)
+};
+cudaError_t launch_slot_copy(const SlotCopyParams &p, int head_dim, cudaStream_t s);
+
 // ------------------------------------------------------- decode attention
 struct DecodeParams {
   const int32_t *bt;

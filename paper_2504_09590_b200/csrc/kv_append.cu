@@ -59,4 +59,44 @@ cudaError_t launch_kv_append(const AppendParams &p, int head_dim, cudaStream_t s
   return cudaGetLastError();
 }
 
+// Lazy checkpoint / restore: move the K and
+// V rows of n arbitrary physical slots between the pool and a contiguous
+// [n][H][d] buffer.  Grid-stride over (slot, head, K|V) rows, D/8 threads per
+// row, one 16-byte load + store each.
+template <int D>
+__global__ void __launch_bounds__(256) slot_copy_kernel(SlotCopyParams p) {
+  constexpr int TPR = D / 8;
+  const int sub = threadIdx.x % TPR;
+  const long long rows = static_cast<long long>(p.n) * p.H * 2;
+  const long long stride = static_cast<long long>(gridDim.x) * (blockDim.x / TPR);
+  for (long long row = blockIdx.x * (blockDim.x / TPR) + threadIdx.x / TPR; row < rows; row += stride) {
+    const int i = static_cast<int>(row / (2 * p.H));
+    const int rem = static_cast<int>(row - static_cast<long long>(i) * 2 * p.H);
+    const int which = rem / p.H, h = rem - which * p.H;
+    const int64_t sid = __ldg(p.slots + i);
+    const int64_t blk = sid / p.bs, slot = sid - blk * p.bs;
+    uint16_t *pool = which ? p.v : p.k;
+    uint16_t *buf = which ? p.buf_v : p.buf_k;
+    uint4 *pp = reinterpret_cast<uint4 *>(pool + blk * p.sb + h * p.sh + slot * p.ss + sub * 8);
+    uint4 *bp = reinterpret_cast<uint4 *>(buf + (static_cast<int64_t>(i) * p.H + h) * D + sub * 8);
+    if (p.restore)
+      *pp = *bp;
+    else
+      *bp = *pp;
+  }
+}
+
+cudaError_t launch_slot_copy(const SlotCopyParams &p, int head_dim, cudaStream_t s) {
+  if (p.n <= 0) return cudaSuccess;
+  const long long rows = static_cast<long long>(p.n) * p.H * 2;
+  const int rows_per_cta = 256 / (head_dim / 8);
+  const long long want = (rows + rows_per_cta - 1) / rows_per_cta;
+  const int grid = static_cast<int>(want < 148 * 8 ? want : 148 * 8);
+  if (head_dim == 128)
+    slot_copy_kernel<128><<<grid, 256, 0, s>>>(p);
+  else
+    slot_copy_kernel<64><<<grid, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
 }  // namespace bkv

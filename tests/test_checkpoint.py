@@ -1,0 +1,122 @@
+"""Lazy checkpointing.
+
+CPU: the oracle's checkpoint/restore and overwritten-peer detection are pinned
+to the paper's a3/B8 example and to a flat-array replay.
+GPU: bkv_kv_checkpoint / bkv_kv_restore match the oracle bit for bit.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from synth import build_layout
+from synth.values import BF16_NAN
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _a3b8(bs):
+    """RT request B (forward) and BE request a (reversed) sharing B's last block."""
+    c = [c for c in json.load(open(os.path.join(GOLD, "a3_b8_collision.json")))["cases"]
+         if c["bs"] == bs and c["expect_code"] == 2][0]
+    M = max(len(c["B_bt"]), len(c["a_bt"]))
+    bt = np.full((2, M), -1, np.int32)
+    bt[0, :len(c["B_bt"])] = c["B_bt"]
+    bt[1, :len(c["a_bt"])] = c["a_bt"]
+    return c, bt, np.array([0, 1], np.uint8)
+
+
+@pytest.mark.parametrize("bs", [12, 4])
+def test_a3_b8_lazy_checkpoint_oracle(bs):
+    """B holds 8 tokens, a holds 4; appending B8 must checkpoint exactly a3,
+    overwrite it, and a later restore brings a3 back bitwise."""
+    c, bt, dirs = _a3b8(bs)
+    H, d = 2, 8
+    K, V = oracle.new_pool(c["num_blocks"], H, bs, d, fill=0)
+    rng = np.random.default_rng(0)
+    dense_B = rng.integers(1, 60000, (9, H, d)).astype(np.uint16)
+    dense_a = rng.integers(1, 60000, (4, H, d)).astype(np.uint16)
+    # resident state before the step: B tokens 0..7, a tokens 0..3 (fills 8 + 4 = 12 / bs slots used)
+    oracle.append(K, V, bt[:1], dirs[:1], np.zeros(1, np.int32), np.array([0, 8], np.int32), dense_B[:8], dense_B[:8])
+    oracle.append(K, V, bt[1:], dirs[1:], np.zeros(1, np.int32), np.array([0, 4], np.int32), dense_a, dense_a)
+    # the step appends B8: which live peer token does it overwrite?
+    victims = oracle.overwritten_peers(bt, dirs, live_lens=[8, 4], before=[8, 4], n_new=[1, 0],
+                                       num_blocks=c["num_blocks"], bs=bs)
+    assert [(r, t) for r, t, _ in victims] == [(1, 3)]            # exactly a3
+    sid = victims[0][2]
+    assert sid == c["B_bt"][-1] * bs + c["collision_slot"]
+    ck, cv = oracle.checkpoint(K, V, [sid])
+    assert np.array_equal(ck[0], dense_a[3]) and np.array_equal(cv[0], dense_a[3])
+    sm = oracle.append(K, V, bt[:1], dirs[:1], np.array([8], np.int32), np.array([0, 1], np.int32),
+                       dense_B[8:9], dense_B[8:9])
+    assert sm.tolist() == [sid]
+    kB, _ = oracle.gather(K, V, bt[:1], dirs[:1], 0, 9)
+    assert np.array_equal(kB, dense_B)
+    # B finishes and releases; a is scheduled again: swap a3 back in
+    oracle.restore(K, V, [sid], ck, cv)
+    ka, va = oracle.gather(K, V, bt[1:], dirs[1:], 0, 4)
+    assert np.array_equal(ka, dense_a) and np.array_equal(va, dense_a)
+
+
+def test_overwritten_peers_flat_array_replay():
+    """Random shared-tail layouts, RT tails grown past their share: every reported
+    victim is exactly a live BE token on the RT token's slot (flat slot-owner replay)."""
+    rng = np.random.default_rng(3)
+    bs = 16
+    lens = rng.integers(1, 120, 16)
+    is_be = np.arange(16) % 2 == 1
+    lay = build_layout(lens, is_be, bs, rng, spare_blocks=2)
+    # grow every RT request by up to 6 tokens inside its last block (overlap allowed now)
+    grow = np.where(~is_be, np.minimum(6, (-lens) % bs), 0).astype(np.int32)
+    victims = oracle.overwritten_peers(lay.block_tables, lay.dirs, lay.lens, lay.lens, grow,
+                                       lay.num_blocks, bs)
+    owner = {}
+    for r in range(16):
+        for t in range(lens[r]):
+            e, j = divmod(t, bs)
+            slot = bs - 1 - j if is_be[r] else j
+            owner[int(lay.block_tables[r, e]) * bs + slot] = (r, t)
+    expect = []
+    for r in range(16):
+        for j in range(grow[r]):
+            t = lens[r] + j
+            e, jj = divmod(t, bs)
+            sid = int(lay.block_tables[r, e]) * bs + jj
+            if sid in owner and owner[sid][0] != r:
+                expect.append((owner[sid][0], owner[sid][1], sid))
+    assert victims == expect
+
+
+@pytest.mark.gpu
+def test_gpu_checkpoint_restore_bitwise():
+    import paper_2504_09590_b200 as bkv
+    rng = np.random.default_rng(5)
+    for H, d, bs in ((2, 128, 16), (4, 64, 32)):
+        nblk = 64
+        K = rng.integers(0, 65535, (nblk, H, bs, d)).astype(np.uint16)
+        V = rng.integers(0, 65535, (nblk, H, bs, d)).astype(np.uint16)
+
+        def g(a):
+            return torch.from_numpy(a.view(np.int16).copy()).cuda().view(torch.bfloat16)
+
+        def u(t):
+            return t.view(torch.int16).cpu().numpy().view(np.uint16)
+
+        pool = bkv.KVPool(g(K), g(V))
+        sids = rng.choice(nblk * bs, 300, replace=False).astype(np.int64)
+        ck, cv = oracle.checkpoint(K, V, sids)
+        gk, gv = bkv.kv_checkpoint(pool, torch.from_numpy(sids).cuda())
+        torch.cuda.synchronize()
+        assert np.array_equal(u(gk), ck) and np.array_equal(u(gv), cv)
+        # overwrite, then restore: the pool is back to its original bytes
+        pool.k[:] = 0
+        pool.v.view(torch.int16).fill_(np.int16(np.uint16(BF16_NAN).view(np.int16)))
+        bkv.kv_restore(pool, torch.from_numpy(sids).cuda(), gk, gv)
+        torch.cuda.synchronize()
+        Ko = np.zeros_like(K)
+        Vo = np.full_like(V, BF16_NAN)
+        oracle.restore(Ko, Vo, sids, ck, cv)
+        assert np.array_equal(u(pool.k), Ko) and np.array_equal(u(pool.v), Vo)
