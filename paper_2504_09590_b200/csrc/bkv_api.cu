@@ -113,10 +113,9 @@ bkv_status ws_layout(int B, int Hq, int H, int D, WsLayout *w, bkv::DecodeLaunch
   const long long units = (long long)bkv::decode_target_units(*cfg) + (long long)B * H;
   if (units > (1ll << 30)) return fail(BKV_ERR_INVALID_ARGUMENT, "problem too large");
   w->units_max = (int)units;
-  // Region A (scheduler word + split counters) has a FIXED size for every
-  // geometry and is only ever written by self-resetting counters, so it is
-  // all-zero between calls no matter which (B, H) used the workspace before.
-  // Region B (partials) is scratch.
+  // Region A: scheduler word (re-armed to 0 by every call's merge kernel) and
+  // the published split plan; fixed size for every geometry.  Region B
+  // (partials) is scratch.
   w->sched = 0;
   w->counters = 256;
   w->ml = w->counters + up256((size_t)bkv::kMaxSeqs * bkv::kMaxKvHeads * 4);
@@ -302,7 +301,7 @@ bkv_status bkv_paged_decode_attention(const bkv_kv_pool *pool, const bkv_block_m
   p.o_sh = o_stride_head;
   p.scale_log2 = softmax_scale * 1.4426950408889634f;
   p.sched = reinterpret_cast<int *>(ws + w.sched);
-  p.counters = reinterpret_cast<int *>(ws + w.counters);
+  p.plan_out = reinterpret_cast<int *>(ws + w.counters);
   p.part_ml = reinterpret_cast<float *>(ws + w.ml);
   p.part_o = reinterpret_cast<float *>(ws + w.o);
   p.target_units = bkv::decode_target_units(cfg);

@@ -50,8 +50,8 @@ struct DecodeParams {
   uint16_t *out;
   int64_t o_ss, o_sh;
   float scale_log2;      // softmax_scale * log2(e)
-  int *sched;            // [0] next unit, [1] finished warps (self-resetting)
-  int *counters;         // [B*H] split arrival counters (self-resetting)
+  int *sched;            // [0] next unit (re-armed to 0 by the merge kernel)
+  int *plan_out;         // split plan published by CTA 0 for the merge kernel
   float *part_ml;        // [units_max][g][2]  (m in log2 domain, l)
   float *part_o;         // [units_max][g][D]  un-normalised partial outputs
   int target_units;      // split plan: aim for about this many units

@@ -230,6 +230,14 @@ __global__ void __launch_bounds__(384, 1)
   };
   trace(0, -1);
   compute_plan(p, Pre, Lsm, &plan);
+  if (blockIdx.x == 0) {   // publish the split plan for the merge kernel
+    if (threadIdx.x == 0) {
+      p.plan_out[0] = plan.P;
+      for (int k = 0; k <= kBuckets; ++k) p.plan_out[1 + k] = plan.base[k];
+      p.plan_out[6] = plan.U;
+    }
+    for (int i = threadIdx.x; i < kBuckets * (p.B + 1); i += blockDim.x) p.plan_out[16 + i] = Pre[i];
+  }
   trace(1, -1);
   const int P = plan.P, U = plan.U;
 
@@ -587,104 +595,6 @@ __global__ void __launch_bounds__(384, 1)
     }
   };
 
-  // Merge all split partials of (r, h) and write the bf16 output rows.  Lanes
-  // take 32 splits at a time (their (m, l) loads are issued together), the
-  // weights are broadcast by shuffle, and each lane accumulates EPL
-  // consecutive output elements of every row; splits are combined in split
-  // order, so the result does not depend on which split arrived last.
-  auto merge_splits = [&](const SlotMeta &m) {
-    const int r = m.r, h = m.h, ns = m.nsplit;
-    // all splits of (r, h) are consecutive split slots of r's bucket: u = (slot0 + s) * H + h
-    const int qq = m.u / H;
-    int k = 0;
-    while (k < kBuckets - 1 && qq >= plan.base[k + 1]) ++k;
-    const int u0 = (plan.base[k] + Pre[k * (p.B + 1) + r]) * H + h;
-    for (int row0 = 0; row0 < g; row0 += 8) {
-      const int nr = min(8, g - row0);
-      float Mrun[8], Lrun[8], acc[8][EPL];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        Mrun[j] = -INFINITY;
-        Lrun[j] = 0.f;
-#pragma unroll
-        for (int k = 0; k < EPL; ++k) acc[j][k] = 0.f;
-      }
-      for (int s0 = 0; s0 < ns; s0 += 32) {
-        const int sl = s0 + lane;
-        const bool ok = sl < ns;
-        const int us = u0 + sl * H;
-        float wj[8], lj[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          wj[j] = -INFINITY;
-          lj[j] = 0.f;
-          if (ok && j < nr) {
-            const float2 v = __ldcg(reinterpret_cast<const float2 *>(
-                p.part_ml + (static_cast<int64_t>(us) * g + row0 + j) * 2));
-            wj[j] = v.x;
-            lj[j] = v.y;
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (j >= nr) break;
-          float mg = wj[j];
-#pragma unroll
-          for (int o = 16; o; o >>= 1) mg = fmaxf(mg, __shfl_xor_sync(FULL, mg, o));
-          const float Mn = fmaxf(Mrun[j], mg);
-          const float a = ex2(Mrun[j] - Mn);
-          const float w = ok ? ex2(wj[j] - Mn) : 0.f;
-          float ls = lj[j] * w;
-#pragma unroll
-          for (int o = 16; o; o >>= 1) ls += __shfl_xor_sync(FULL, ls, o);
-          Lrun[j] = Lrun[j] * a + ls;
-#pragma unroll
-          for (int k = 0; k < EPL; ++k) acc[j][k] *= a;
-          Mrun[j] = Mn;
-          wj[j] = w;
-        }
-        const int cnt = min(32, ns - s0);
-#pragma unroll 2
-        for (int t = 0; t < cnt; ++t) {
-          const int ut = __shfl_sync(FULL, us, t);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            if (j >= nr) break;
-            const float wt = __shfl_sync(FULL, wj[j], t);
-            const float *po = p.part_o + (static_cast<int64_t>(ut) * g + row0 + j) * D + lane * EPL;
-            if constexpr (EPL == 4) {
-              const float4 v = __ldcg(reinterpret_cast<const float4 *>(po));
-              acc[j][0] = fmaf(wt, v.x, acc[j][0]);
-              acc[j][1] = fmaf(wt, v.y, acc[j][1]);
-              acc[j][2] = fmaf(wt, v.z, acc[j][2]);
-              acc[j][3] = fmaf(wt, v.w, acc[j][3]);
-            } else {
-              const float2 v = __ldcg(reinterpret_cast<const float2 *>(po));
-              acc[j][0] = fmaf(wt, v.x, acc[j][0]);
-              acc[j][1] = fmaf(wt, v.y, acc[j][1]);
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if (j >= nr) break;
-        const float inv = Lrun[j] > 0.f ? 1.f / Lrun[j] : 0.f;
-        uint16_t *o = p.out + static_cast<int64_t>(r) * p.o_ss +
-                      static_cast<int64_t>(h * g + row0 + j) * p.o_sh + lane * EPL;
-        if constexpr (EPL == 4) {
-          uint2 w;
-          w.x = pack_bf16(acc[j][0] * inv, acc[j][1] * inv);
-          w.y = pack_bf16(acc[j][2] * inv, acc[j][3] * inv);
-          *reinterpret_cast<uint2 *>(o) = w;
-        } else {
-          *reinterpret_cast<uint32_t *>(o) = pack_bf16(acc[j][0] * inv, acc[j][1] * inv);
-        }
-      }
-    }
-    if (lane == 0) p.counters[r * H + h] = 0;  // self-reset for the next call
-  };
-
   auto end_unit = [&](const SlotMeta &m) {
     const int r = m.r, h = m.h, u = m.u;
     if constexpr (!MMA) {
@@ -756,20 +666,7 @@ __global__ void __launch_bounds__(384, 1)
         }
       if (direct) return;
     }
-    // split partial written: count arrivals; the last split merges.  The warp
-    // barrier orders every lane's partial stores before lane 0's fence+atomic
-    // (release); lane 0's second fence + the barrier give the acquire side.
-    __syncwarp();
-    int prev = 0;
-    if (lane == 0) {
-      prev = atom_add_release_gpu(p.counters + r * H + h, 1);
-      if (prev == m.nsplit - 1) fence_acq_rel_gpu();
-    }
-    prev = __shfl_sync(FULL, prev, 0);
-    if (prev == m.nsplit - 1) {
-      trace(5, m.u);
-      merge_splits(m);
-    }
+    // split partial written; bkv merge_kernel (next on the stream) combines the splits
   };
 
   // ------------------------------------------------------------- main loop
@@ -839,16 +736,115 @@ __global__ void __launch_bounds__(384, 1)
     for (int k = 0; k < 6; ++k) trace(8 + k, static_cast<int>(min(prof[k], (long long)0x7fffffff)));
 
   trace(6, -1);
-  // ------------------------------------------------- scheduler self-reset
-  // (one atomic per CTA; the last CTA to finish restores the counters to 0)
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const int d = atomicAdd(p.sched + 1, 1);
-    if (d == static_cast<int>(gridDim.x) - 1) {
-      p.sched[0] = 0;
-      p.sched[1] = 0;
-      __threadfence();
+}
+
+// Split merge, a second, stream-ordered kernel: one warp
+// per (request, kv head).  Requests with one split were written by the decode
+// kernel directly; for the others the fp32 (m, l, o) partials of all splits
+// are combined in split order -- M = max m_s, L = sum l_s 2^(m_s - M),
+// O = sum o_s 2^(m_s - M) / L -- so the result is deterministic.  Lanes take 32
+// splits at a time (their (m, l) loads issue together), weights are broadcast
+// by shuffle and each lane accumulates EPL consecutive output elements.  Being
+// stream-ordered after the decode kernel, it needs no atomics or fences; it
+// also re-arms the decode kernel's unit counter for the next call.
+template <int D>
+__global__ void __launch_bounds__(256) merge_kernel(const DecodeParams p) {
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int EPL = D / 32;
+  if (blockIdx.x == 0 && threadIdx.x == 0) p.sched[0] = 0;
+  const int lane = threadIdx.x & 31;
+  const int wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int H = p.H, g = p.g;
+  if (wid >= p.B * H * g) return;   // one warp per (request, kv head, q head of the group)
+  const int rh = wid / g, row1 = wid - rh * g;
+  const int r = rh / H, h = rh - r * H;
+  const int P = p.plan_out[0];
+  const int L = __ldg(p.seq_lens + r);
+  const int nb = nblocks_of(L, p.bs);
+  const int ns = nb > 0 ? (nb + P - 1) / P : 1;
+  if (ns <= 1) return;
+  const int k = bucket_of((nb + ns - 1) / ns, P);
+  // all splits of (r, h) are consecutive split slots of r's bucket: u = (slot0 + s) * H + h
+  const int u0 = (p.plan_out[1 + k] + p.plan_out[16 + k * (p.B + 1) + r]) * H + h;
+  {
+    const int row0 = row1, nr = 1;
+    float Mrun[8], Lrun[8], acc[8][EPL];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      Mrun[j] = -INFINITY;
+      Lrun[j] = 0.f;
+#pragma unroll
+      for (int q = 0; q < EPL; ++q) acc[j][q] = 0.f;
+    }
+    for (int s0 = 0; s0 < ns; s0 += 32) {
+      const int sl = s0 + lane;
+      const bool ok = sl < ns;
+      const int us = u0 + sl * H;
+      float wj[8], lj[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        wj[j] = -INFINITY;
+        lj[j] = 0.f;
+        if (ok && j < nr) {
+          const float2 v = __ldg(reinterpret_cast<const float2 *>(p.part_ml + (static_cast<int64_t>(us) * g + row0 + j) * 2));
+          wj[j] = v.x;
+          lj[j] = v.y;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (j >= nr) break;
+        float mg = wj[j];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) mg = fmaxf(mg, __shfl_xor_sync(FULL, mg, o));
+        const float Mn = fmaxf(Mrun[j], mg);
+        const float a = ex2(Mrun[j] - Mn);
+        const float w = ok ? ex2(wj[j] - Mn) : 0.f;
+        float ls = lj[j] * w;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) ls += __shfl_xor_sync(FULL, ls, o);
+        Lrun[j] = Lrun[j] * a + ls;
+#pragma unroll
+        for (int q = 0; q < EPL; ++q) acc[j][q] *= a;
+        Mrun[j] = Mn;
+        wj[j] = w;
+      }
+      const int cnt = min(32, ns - s0);
+#pragma unroll 4
+      for (int t = 0; t < cnt; ++t) {
+        const int ut = __shfl_sync(FULL, us, t);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (j >= nr) break;
+          const float wt = __shfl_sync(FULL, wj[j], t);
+          const float *po = p.part_o + (static_cast<int64_t>(ut) * g + row0 + j) * D + lane * EPL;
+          if constexpr (EPL == 4) {
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(po));
+            acc[j][0] = fmaf(wt, v.x, acc[j][0]);
+            acc[j][1] = fmaf(wt, v.y, acc[j][1]);
+            acc[j][2] = fmaf(wt, v.z, acc[j][2]);
+            acc[j][3] = fmaf(wt, v.w, acc[j][3]);
+          } else {
+            const float2 v = __ldg(reinterpret_cast<const float2 *>(po));
+            acc[j][0] = fmaf(wt, v.x, acc[j][0]);
+            acc[j][1] = fmaf(wt, v.y, acc[j][1]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j >= nr) break;
+      const float inv = Lrun[j] > 0.f ? 1.f / Lrun[j] : 0.f;
+      uint16_t *o = p.out + static_cast<int64_t>(r) * p.o_ss + static_cast<int64_t>(h * g + row0 + j) * p.o_sh + lane * EPL;
+      if constexpr (EPL == 4) {
+        uint2 w;
+        w.x = pack_bf16(acc[j][0] * inv, acc[j][1] * inv);
+        w.y = pack_bf16(acc[j][2] * inv, acc[j][3] * inv);
+        *reinterpret_cast<uint2 *>(o) = w;
+      } else {
+        *reinterpret_cast<uint32_t *>(o) = pack_bf16(acc[j][0] * inv, acc[j][1] * inv);
+      }
     }
   }
 }
@@ -903,6 +899,10 @@ static cudaError_t launch_t(const CUtensorMap &tmK, const CUtensorMap &tmV, cons
     configured = cfg.smem_bytes;
   }
   decode_kernel<D, KIND><<<cfg.grid, cfg.warps * 32, cfg.smem_bytes, s>>>(tmK, tmV, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int warps = p.B * p.H * p.g;
+  merge_kernel<D><<<(warps + 7) / 8, 256, 0, s>>>(p);
   return cudaGetLastError();
 }
 
