@@ -210,9 +210,16 @@ def run_ours(args):
     from paper_2504_09590_b200.tp import HeadShard, gather_heads
 
     ws, rank, local = dist_env()
+    # dev-only: BKV_DIST_BACKEND=gloo runs several ranks on one GPU (smoke test of the N>1 path)
+    backend = os.environ.get("BKV_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())
     if ws > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     sh = CONFIGS[args.config]
@@ -270,7 +277,7 @@ def run_ours(args):
                 launches += 1
             o = out_loc[l].permute(1, 0, 2)                                   # [B][Hq][d] view
             bkv.paged_decode_attention(pools[l], md["bt"], md["dirs"], md["lens"], qd[l], scale,
-                                       out=o, max_seq_len=max_len, ws=wsb)
+                                       out=o, max_seq_len=max_len, ws=wsb, pdl=args.pdl)
             launches += 1
             if tp > 1 and not attn_only:
                 gather_heads(out_loc[l], out_glob[l])
@@ -415,6 +422,8 @@ def main():
     ap.add_argument("--warmup-ref", type=int, default=1)
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-pdl", dest="pdl", action="store_false",
+                    help="launch attention without programmatic dependent launch")
     ap.add_argument("--no-graphs", dest="graphs", action="store_false",
                     help="launch eagerly instead of replaying CUDA graphs")
     args = ap.parse_args()

@@ -193,6 +193,27 @@ BKV_API bkv_status bkv_kv_checkpoint(const bkv_kv_pool *pool, const int64_t *slo
 BKV_API bkv_status bkv_kv_restore(const bkv_kv_pool *pool, const int64_t *slot_ids, int32_t n,
                                   const void *k_in, const void *v_in, bkv_stream_t stream);
 
+/*
+ * bkv_paged_decode_attention_ex -- the same call with launch flags.
+ *   BKV_FLAG_PDL  launch the attention and merge kernels with programmatic
+ *                 dependent launch: the split-plan prologue (which reads only
+ *                 seq_lens) overlaps the tail of the preceding kernel on the
+ *                 stream, e.g. bkv_kv_append.  Contract: seq_lens must NOT be
+ *                 written by the kernel that immediately precedes this call on
+ *                 the stream (host copies and earlier kernels are fine); every
+ *                 other input is read only after that kernel has completed.
+ * Unknown flag bits return BKV_ERR_INVALID_ARGUMENT.
+ */
+#define BKV_FLAG_PDL 1u
+BKV_API bkv_status bkv_paged_decode_attention_ex(const bkv_kv_pool *pool, const bkv_block_map *map,
+                                                 const int32_t *seq_lens, int32_t max_seq_len,
+                                                 const void *q, int64_t q_stride_seq,
+                                                 int64_t q_stride_head, int32_t num_q_heads,
+                                                 float softmax_scale, void *out, int64_t o_stride_seq,
+                                                 int64_t o_stride_head, void *workspace,
+                                                 size_t workspace_bytes, uint32_t flags,
+                                                 bkv_stream_t stream);
+
 /* Workspace bytes for bkv_paged_decode_attention on the CURRENT device
  * (depends on the SM count); 0 on error (see bkv_last_error). */
 BKV_API size_t bkv_decode_workspace_size(int32_t num_seqs, int32_t num_q_heads, int32_t num_kv_heads,

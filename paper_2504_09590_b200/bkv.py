@@ -44,7 +44,8 @@ _lib_lock = threading.Lock()
 
 EXPORTS = ("bkv_kv_append", "bkv_paged_decode_attention", "bkv_decode_workspace_size",
            "bkv_validate_layout_host", "bkv_status_string", "bkv_last_error", "bkv_version",
-           "bkv_kv_checkpoint", "bkv_kv_restore")
+           "bkv_kv_checkpoint", "bkv_kv_restore", "bkv_paged_decode_attention_ex")
+BKV_FLAG_PDL = 1   # include/bkv.h: programmatic dependent launch (seq_lens not written by the previous kernel)
 
 
 def lib():
@@ -63,6 +64,10 @@ def lib():
                     ctypes.POINTER(_Pool), ctypes.POINTER(_Map), P, i32, P, i64, i64, i32, ctypes.c_float,
                     P, i64, i64, P, ctypes.c_size_t, P]
                 L.bkv_paged_decode_attention.restype = ctypes.c_int
+                L.bkv_paged_decode_attention_ex.argtypes = [
+                    ctypes.POINTER(_Pool), ctypes.POINTER(_Map), P, i32, P, i64, i64, i32, ctypes.c_float,
+                    P, i64, i64, P, ctypes.c_size_t, ctypes.c_uint32, P]
+                L.bkv_paged_decode_attention_ex.restype = ctypes.c_int
                 L.bkv_decode_workspace_size.argtypes = [i32, i32, i32, i32]
                 L.bkv_decode_workspace_size.restype = ctypes.c_size_t
                 L.bkv_validate_layout_host.argtypes = [P, i32, P, i32, i32, i32, P, i32, i32, i32, P]
@@ -220,7 +225,7 @@ def workspace(num_seqs, num_q_heads, num_kv_heads, head_dim, device=None, stream
 
 
 def paged_decode_attention(pool: KVPool, block_tables, dirs, seq_lens, q, softmax_scale=None,
-                           out=None, max_seq_len=None, ws=None, stream=None):
+                           out=None, max_seq_len=None, ws=None, stream=None, pdl=False):
     """bkv_paged_decode_attention.  q: bf16 [B][Hq][d] (any strides with unit last stride).
     out: bf16 with the same indexing (allocated [B][Hq][d] if None).  Returns out."""
     p, m = pool.c(), block_map(block_tables, dirs)
@@ -240,10 +245,10 @@ def paged_decode_attention(pool: KVPool, block_tables, dirs, seq_lens, q, softma
         max_seq_len = block_tables.shape[1] * pool.block_size
     if ws is None:
         ws = workspace(B, Hq, pool.num_kv_heads, d, q.device, stream)
-    rc = lib().bkv_paged_decode_attention(
+    rc = lib().bkv_paged_decode_attention_ex(
         ctypes.byref(p), ctypes.byref(m), seq_lens.data_ptr(), int(max_seq_len), q.data_ptr(),
         q.stride(0), q.stride(1), Hq, float(softmax_scale), out.data_ptr(), out.stride(0),
-        out.stride(1), ws.data_ptr(), ws.numel(), _stream_ptr(stream))
+        out.stride(1), ws.data_ptr(), ws.numel(), BKV_FLAG_PDL if pdl else 0, _stream_ptr(stream))
     _check(rc, "bkv_paged_decode_attention")
     return out
 

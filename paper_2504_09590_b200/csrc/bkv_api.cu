@@ -247,6 +247,19 @@ bkv_status bkv_paged_decode_attention(const bkv_kv_pool *pool, const bkv_block_m
                                       int32_t num_q_heads, float softmax_scale, void *out,
                                       int64_t o_stride_seq, int64_t o_stride_head, void *workspace,
                                       size_t workspace_bytes, bkv_stream_t stream) {
+  return bkv_paged_decode_attention_ex(pool, map, seq_lens, max_seq_len, q, q_stride_seq,
+                                       q_stride_head, num_q_heads, softmax_scale, out, o_stride_seq,
+                                       o_stride_head, workspace, workspace_bytes, 0u, stream);
+}
+
+bkv_status bkv_paged_decode_attention_ex(const bkv_kv_pool *pool, const bkv_block_map *map,
+                                         const int32_t *seq_lens, int32_t max_seq_len,
+                                         const void *q, int64_t q_stride_seq, int64_t q_stride_head,
+                                         int32_t num_q_heads, float softmax_scale, void *out,
+                                         int64_t o_stride_seq, int64_t o_stride_head,
+                                         void *workspace, size_t workspace_bytes, uint32_t flags,
+                                         bkv_stream_t stream) {
+  if (flags & ~BKV_FLAG_PDL) return fail(BKV_ERR_INVALID_ARGUMENT, "unknown flags 0x%x", flags);
   bkv_status s = check_pool(pool);
   if (s) return s;
   if ((s = check_map(map))) return s;
@@ -310,6 +323,7 @@ bkv_status bkv_paged_decode_attention(const bkv_kv_pool *pool, const bkv_block_m
   p.slots = slots;
   p.q_bytes = qb;
   p.total_warps = cfg.grid * cfg.warps;
+  p.pdl = (flags & BKV_FLAG_PDL) ? 1 : 0;
   p.debug_flags = getenv("BKV_DEBUG") ? atoi(getenv("BKV_DEBUG")) : 0;
   p.team_force = getenv("BKV_TEAM") ? atoi(getenv("BKV_TEAM")) : 0;
   p.team_max = g <= 8 ? cfg.warps : 1;

@@ -60,6 +60,7 @@ struct DecodeParams {
   int slots;             // ring depth per warp (S)
   int q_bytes;           // smem bytes per q-ring entry
   int total_warps;       // grid * warps per CTA
+  int pdl;               // launched with programmatic dependent launch (BKV_FLAG_PDL)
   int team_force;        // 0 = choose the team size in-kernel, else force it (dev)
   int team_max;          // largest allowed team (1 when the state area is not allocated)
   int debug_flags;       // dev only: 1 = skip the math (data-movement skeleton)

@@ -230,6 +230,9 @@ __global__ void __launch_bounds__(384, 1)
   };
   trace(0, -1);
   compute_plan(p, Pre, Lsm, &plan);
+  // PDL: everything above read only seq_lens; wait for the preceding kernel
+  // (it may have written the pool / q) before touching anything else.
+  if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
   if (blockIdx.x == 0) {   // publish the split plan for the merge kernel
     if (threadIdx.x == 0) {
       p.plan_out[0] = plan.P;
@@ -751,6 +754,7 @@ template <int D>
 __global__ void __launch_bounds__(256) merge_kernel(const DecodeParams p) {
   constexpr unsigned FULL = 0xffffffffu;
   constexpr int EPL = D / 32;
+  if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");   // decode results complete
   if (blockIdx.x == 0 && threadIdx.x == 0) p.sched[0] = 0;
   const int lane = threadIdx.x & 31;
   const int wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -898,11 +902,31 @@ static cudaError_t launch_t(const CUtensorMap &tmK, const CUtensorMap &tmV, cons
     if (e != cudaSuccess) return e;
     configured = cfg.smem_bytes;
   }
-  decode_kernel<D, KIND><<<cfg.grid, cfg.warps * 32, cfg.smem_bytes, s>>>(tmK, tmV, p);
-  cudaError_t e = cudaGetLastError();
+  cudaLaunchConfig_t lc = {};
+  cudaLaunchAttribute attr[1];
+  lc.gridDim = dim3(cfg.grid);
+  lc.blockDim = dim3(cfg.warps * 32);
+  lc.dynamicSmemBytes = cfg.smem_bytes;
+  lc.stream = s;
+  if (p.pdl) {   // programmatic dependent launch: the prologue overlaps the previous kernel
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+  }
+  cudaError_t e = cudaLaunchKernelEx(&lc, decode_kernel<D, KIND>, tmK, tmV, p);
   if (e != cudaSuccess) return e;
   const int warps = p.B * p.H * p.g;
-  merge_kernel<D><<<(warps + 7) / 8, 256, 0, s>>>(p);
+  cudaLaunchConfig_t lm = {};
+  lm.gridDim = dim3((warps + 7) / 8);
+  lm.blockDim = dim3(256);
+  lm.stream = s;
+  if (p.pdl) {
+    lm.attrs = attr;
+    lm.numAttrs = 1;
+  }
+  e = cudaLaunchKernelEx(&lm, merge_kernel<D>, p);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -17,6 +17,8 @@ namespace bkv {
 template <int D>
 __global__ void __launch_bounds__(256) kv_append_kernel(AppendParams p) {
   constexpr int TPR = D / 8;  // threads per row, 16 B each
+  // let a PDL-launched decode kernel start its seq_lens-only prologue now
+  asm volatile("griddepcontrol.launch_dependents;");
   const int r = blockIdx.x;
   const int32_t first = p.cu_new[r];
   const int n = p.cu_new[r + 1] - first;

@@ -68,9 +68,10 @@ def gather_heads(out_local_hm: torch.Tensor, out_global_hm: torch.Tensor | None 
         out_global_hm.copy_(out_local_hm)
     elif dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out_global_hm, out_local_hm.contiguous(), group=group)
-    else:   # gloo (CPU tests): list all-gather, rank-major
-        parts = list(out_global_hm.chunk(tp, dim=0))
-        dist.all_gather(parts, out_local_hm.contiguous(), group=group)
+    else:   # gloo (CPU tests, single-GPU smoke runs): list all-gather on host copies, rank-major
+        src = out_local_hm.detach().contiguous().cpu()
+        parts = [torch.empty_like(src) for _ in range(tp)]
+        dist.all_gather(parts, src, group=group)
         out_global_hm.copy_(torch.cat(parts, dim=0))
     return out_global_hm
 

@@ -20,7 +20,7 @@ os.makedirs(DST, exist_ok=True)
 
 
 def short(name):
-    for k in ("decode_kernel", "kv_append_kernel", "slot_copy_kernel"):
+    for k in ("decode_kernel", "merge_kernel", "kv_append_kernel", "slot_copy_kernel"):
         if k in name:
             return "bkv::" + k + name[name.index(k) + len(k):].split("(")[0]
     return name.split("(")[0][:60]

@@ -282,3 +282,32 @@ def test_abi_argument_errors():
     small = torch.zeros(1024, dtype=torch.uint8, device=DEV)
     with pytest.raises(bkv.BkvError, match="WORKSPACE"):
         bkv.paged_decode_attention(pool, bt, dirs, lens, torch.zeros(1, 2, 64, dtype=torch.bfloat16, device=DEV), ws=small)
+
+
+def test_pdl_launch_after_append_matches():
+    """BKV_FLAG_PDL: attention launched right behind the kv_append that wrote the
+    pool (programmatic dependent launch) gives bitwise the same output."""
+    sh = Shape("pdl", 16, 2, 128, 16, 24, 0.5, "uniform", 600, 1, 1, uniform_max=600)
+    case = make_case(sh, 31)
+    lay = case.layout
+    ks, vs, q = dense_case(case)
+    before = (lay.lens - 1).astype(np.int32)
+    B = lay.batch
+    outs = []
+    for pdl in (False, True):
+        Kp, Vp = oracle.new_pool(lay.num_blocks, 2, 16, 128, BF16_NAN)
+        kn, vn, cu = ragged(ks, vs, before, np.zeros(B, np.int32))
+        oracle.append(Kp, Vp, lay.block_tables, lay.dirs, np.zeros(B, np.int32), cu, kn, vn)
+        pool = bkv.KVPool(t_u16(Kp), t_u16(Vp))
+        bt, dirs, lens = gpu_map(lay)
+        kd, vd, cud = ragged(ks, vs, lay.lens, before)
+        for _ in range(3):   # append then attention, back to back on one stream
+            bkv.kv_append(pool, bt, dirs, torch.from_numpy(before).to(DEV), torch.from_numpy(cud).to(DEV),
+                          t_u16(kd), t_u16(vd))
+            o = bkv.paged_decode_attention(pool, bt, dirs, lens, t_u16(q), pdl=pdl)
+        torch.cuda.synchronize()
+        outs.append(o)
+    assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16))
+    K, V, _ = oracle_pool(case, ks, vs, 2)
+    ref = oracle.attention(K, V, lay.block_tables, lay.dirs, lay.lens, q, default_scale(128))
+    check_close(outs[1], ref, "pdl")
