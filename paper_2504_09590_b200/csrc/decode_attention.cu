@@ -581,20 +581,30 @@ __global__ void __launch_bounds__(384, 1)
         const int r8 = lane & 7, hi8 = (lane >> 3) & 1, nn = lane >> 4;
         ldsm_x4(my_scr + (nn * 8 + r8) * 48 + hi8 * 16, pb[0][0], pb[0][1], pb[1][0], pb[1][1]);
       }
-      // ---- O^T = alpha * O^T + V^T . P^T
+      // ---- O^T = alpha * O^T + V^T . P^T  (the rescale is skipped, warp-uniformly,
+      // once no running max moved -- the common case after the first chunks)
+      bool moved = false;
+#pragma unroll
+      for (int n = 0; n < NT; ++n) moved |= (alpha[n][0] != 1.f) | (alpha[n][1] != 1.f);
+      if (__any_sync(FULL, moved)) {
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int n = 0; n < NT; ++n) {
+            const float2 a2 = make_float2(alpha[n][0], alpha[n][1]);
+            const float2 lo2 = __fmul2_rn(make_float2(oacc[mt][n][0], oacc[mt][n][1]), a2);
+            const float2 hi2 = __fmul2_rn(make_float2(oacc[mt][n][2], oacc[mt][n][3]), a2);
+            oacc[mt][n][0] = lo2.x;
+            oacc[mt][n][1] = lo2.y;
+            oacc[mt][n][2] = hi2.x;
+            oacc[mt][n][3] = hi2.y;
+          }
+      }
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int n = 0; n < NT; ++n) {
-          const float2 a2 = make_float2(alpha[n][0], alpha[n][1]);
-          const float2 lo2 = __fmul2_rn(make_float2(oacc[mt][n][0], oacc[mt][n][1]), a2);
-          const float2 hi2 = __fmul2_rn(make_float2(oacc[mt][n][2], oacc[mt][n][3]), a2);
-          oacc[mt][n][0] = lo2.x;
-          oacc[mt][n][1] = lo2.y;
-          oacc[mt][n][2] = hi2.x;
-          oacc[mt][n][3] = hi2.y;
+        for (int n = 0; n < NT; ++n)
           mma_bf16_16816(oacc[mt][n], va[mt][0], va[mt][1], va[mt][2], va[mt][3], pb[n][0], pb[n][1]);
-        }
     }
   };
 
@@ -875,7 +885,7 @@ cudaError_t decode_config(int head_dim, int group, int num_seqs, DecodeLaunch *c
     return 1024 + w * s * slot_bytes + w * s * (int)(sizeof(int) * 8) + w * s * 8 + w * 1024 +
            4 * (num_seqs + 1) * (int)sizeof(int) + ((num_seqs + 3) & ~3) * 4 + 256;
   };
-  int W = env_int("BKV_WARPS", 12);
+  int W = env_int("BKV_WARPS", group > 1 ? 8 : 12);   // measured best: GQA 8, MHA 12
   while (W > 4 && need(W, S) > smem_optin - 1024) W -= 4;
   while (S > 1 && need(W, S) > smem_optin - 1024) --S;
   cfg->grid = sms * env_int("BKV_CTAS_PER_SM", 1);
