@@ -10,27 +10,27 @@
 // (forward entry: slots [0, n), reversed entry: slots [bs-n, bs)).  That is
 // why the paper's PTX value-vector reversal has no counterpart here.
 //
-// Design (B200):
-//  * Persistent grid, one CTA per SM, W independent warps per CTA.  Each warp
-//    is its own producer: lane 0 streams 16-slot "chunks" (K and V tile of one
-//    (block, kv head), 2*d*32 bytes) through a private S-deep ring of
-//    128B-swizzled shared-memory slots with 4-D TMA tensor loads and mbarrier
-//    completion, so S*8 KiB per warp are in flight while it computes.
+// Design (B200, DESIGN.md §6 "decode attention"):
+//  * Persistent grid, one CTA per SM, W independent warps per CTA (12 MHA, 8
+//    GQA).  Each warp is its own producer: lane 0 streams 16-slot "chunks" (K
+//    and V tile of one (block, kv head), 2*d*32 bytes) through a private 2-deep
+//    ring of 128B-swizzled shared-memory slots with ONE 5-D TMA tensor load per
+//    tile and mbarrier completion; the consumer moves the tile to registers
+//    and refills the slot before doing the math.
 //  * Work units = (request, kv head, split of <= P blocks), pulled from a
-//    global atomic counter; full-size splits are enumerated before the
-//    remainders (largest first).  P is chosen in-kernel from sum(ceil(L/bs))
-//    so the whole grid gets work (split-K only as needed).
-//  * MHA (g = 1): CUDA-core fp32 dot products, lanes = (token, half of d).
-//  * GQA (g >= 2): the g query heads of a kv head form the M rows of a bf16
-//    mma.sync m16n8k16 tile: S = Q.K^T (K via ldmatrix), online softmax on the
-//    accumulator fragments, O += P.V with P re-used from registers as the A
-//    operand and V via ldmatrix.trans.
+//    global atomic counter (first unit static), enumerated longest-first by a
+//    4-bucket split plan computed in-kernel from seq_lens; the issuer decodes
+//    the next unit one unit ahead (block-table window loads, q L2 prefetch).
+//  * MHA (g = 1): CUDA-core fp32 (FFMA2), lanes = (token, half of d), q in smem.
+//  * GQA (g >= 2): tokens on the MMA M dimension: S^T = K.Q^T and
+//    O^T += V^T.P^T with bf16 mma.sync m16n8k16 (K via ldmatrix, V via
+//    ldmatrix.trans, P^T re-laid through 256 B of smem).
 //  * A unit's output is written directly when the request has one split;
-//    otherwise fp32 (m, l, o) partials go to the workspace and the last split
-//    to arrive merges all of them in split order (deterministic).
+//    otherwise fp32 (m, l, o) partials go to the workspace and merge_kernel,
+//    stream-ordered after this kernel, combines them in split order.
 //  * NaN hygiene (reading Q10): dead slots are never combined arithmetically:
-//    their scores are selected to -inf and (MMA path) their V rows are zeroed
-//    in shared memory before P.V.
+//    their scores are selected to -inf and their V rows are zeroed in shared
+//    memory before P.V.
 #include <math.h>
 
 #include "bkv_internal.h"
