@@ -130,7 +130,7 @@ def algorithmic_bytes(lay, H, Hq, d, bs):
 
 
 def append_bytes(B, H, d):
-    return 4.0 * B * H * d   # read k_new, v_new + write the two rows (bf16): 2 * 2 * B*H*d bytes
+    return 8.0 * B * H * d   # read k_new, v_new + write the two rows: 4 x B*H*d bf16 values
 
 
 # --------------------------------------------------------- reference (oracle) arm
@@ -271,14 +271,18 @@ def run_ours(args):
         """One decode step over all layers (append + attention [+ all-gather])."""
         launches = 0
         for l in range(n_layers):
-            if not attn_only:
-                bkv.kv_append(pools[l], md["bt"], md["dirs"], md["before"], md["cu"], knd[l], vnd[l],
-                              total_new_tokens=B)
-                launches += 1
             o = out_loc[l].permute(1, 0, 2)                                   # [B][Hq][d] view
-            bkv.paged_decode_attention(pools[l], md["bt"], md["dirs"], md["lens"], qd[l], scale,
-                                       out=o, max_seq_len=max_len, ws=wsb, pdl=args.pdl)
-            launches += 1
+            if args.fused:   # f2: append fused into the attention kernel (bkv_decode_step)
+                bkv.decode_step(pools[l], md["bt"], md["dirs"], md["lens"], knd[l], vnd[l], qd[l],
+                                scale, out=o, max_seq_len=max_len, ws=wsb, pdl=args.pdl)
+            else:
+                if not attn_only:
+                    bkv.kv_append(pools[l], md["bt"], md["dirs"], md["before"], md["cu"], knd[l],
+                                  vnd[l], total_new_tokens=B)
+                    launches += 1
+                bkv.paged_decode_attention(pools[l], md["bt"], md["dirs"], md["lens"], qd[l], scale,
+                                           out=o, max_seq_len=max_len, ws=wsb, pdl=args.pdl)
+            launches += 2                                                     # decode + merge kernels
             if tp > 1 and not attn_only:
                 gather_heads(out_loc[l], out_glob[l])
         return launches
@@ -297,9 +301,8 @@ def run_ours(args):
 
     # ---- eager warm-up, then capture the step (and an attention-only step) in CUDA graphs
     for _ in range(args.warmup):
-        step(meta_d, q_d, kn_d, vn_d)
+        launches_per_step = step(meta_d, q_d, kn_d, vn_d)
     barrier()
-    launches_per_step = n_layers * 2
     g_step, g_attn = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
     if args.graphs:
         with torch.cuda.graph(g_step):
@@ -361,6 +364,8 @@ def run_ours(args):
         dist.destroy_process_group()
         return
     alg_bytes, kv_bytes = algorithmic_bytes(lay, H, Hq, d, bs)
+    if args.fused:   # the fused kernel also reads the new rows and writes them into the pool
+        alg_bytes += append_bytes(B, H, d)
     peak, peak_src = load_peaks()
     achieved = alg_bytes / (att_avg_us * 1e-6) / 1e9
     tok_s = B / (ms_step * 1e-3)
@@ -389,11 +394,12 @@ def run_ours(args):
             "attn_us_per_layer": att_avg_us,
             "attn_share_of_step": att_avg_us * n_layers / (ms_step * 1e3),
             "cuda_graphs": bool(args.graphs),
+            "fused_append": bool(args.fused),
             "attn_layer_tokens_per_s": B / (att_avg_us * 1e-6),
             "seed": args.seed,
         },
         "roofline": {
-            "bound": "hbm", "kernel": "bkv::decode_kernel", "achieved": achieved, "peak": peak,
+            "bound": "hbm", "kernel": "bkv::decode_kernel" + (" (fused append)" if args.fused else ""), "achieved": achieved, "peak": peak,
             "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
             "algorithmic_bytes_per_launch": alg_bytes,
             "traffic": ncu_traffic(f"{args.config}_tp{tp}"),
@@ -424,6 +430,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-pdl", dest="pdl", action="store_false",
                     help="launch attention without programmatic dependent launch")
+    ap.add_argument("--no-fused", dest="fused", action="store_false",
+                    help="separate kv_append + attention launches instead of bkv_decode_step")
     ap.add_argument("--no-graphs", dest="graphs", action="store_false",
                     help="launch eagerly instead of replaying CUDA graphs")
     args = ap.parse_args()

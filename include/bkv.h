@@ -214,6 +214,39 @@ BKV_API bkv_status bkv_paged_decode_attention_ex(const bkv_kv_pool *pool, const 
                                                  size_t workspace_bytes, uint32_t flags,
                                                  bkv_stream_t stream);
 
+/*
+ * bkv_decode_step -- one decode iteration of a layer in ONE launch pair
+ * (SURVEY §8(f) f2): append each request's newest token and attend over the
+ * context that includes it.
+ *
+ * Defined as exactly
+ *     bkv_kv_append(pool, map, seq_lens_before = seq_lens - 1,
+ *                   cu_new_tokens = {0, 1, ..., num_seqs}, k_new, v_new, NULL)
+ *     bkv_paged_decode_attention_ex(pool, map, seq_lens, ...)
+ * i.e. token t = seq_lens[r] - 1 of request r goes to slot
+ * (dir ? bs-1-t%bs : t%bs) of block block_tables[r][t / bs] (§5.1,
+ * RT fills a block from the left, BE from the right) and the attention
+ * then reads it.  Results (pool bytes and out) are bit-identical to the two
+ * separate calls.  The warp that owns the chunk holding slot(t) writes the
+ * row and fences it into the TMA (async) proxy before loading that chunk, so
+ * no separate append kernel and no extra pool read is needed.
+ *   k_new, v_new  device bf16 [num_seqs][num_kv_heads][head_dim], contiguous,
+ *                 16-byte aligned; read only.
+ *   seq_lens      device int32 [num_seqs], lengths AFTER the append (>= 1 for
+ *                 a request to receive a token; a request with seq_lens 0 is
+ *                 left untouched and its output is 0).
+ *   the rest      as bkv_paged_decode_attention_ex (same workspace, flags).
+ * The map must be valid for lengths seq_lens (I1-I4): the new slot must be
+ * free of other requests' live tokens.
+ */
+BKV_API bkv_status bkv_decode_step(const bkv_kv_pool *pool, const bkv_block_map *map,
+                                   const int32_t *seq_lens, int32_t max_seq_len,
+                                   const void *k_new, const void *v_new, const void *q,
+                                   int64_t q_stride_seq, int64_t q_stride_head,
+                                   int32_t num_q_heads, float softmax_scale, void *out,
+                                   int64_t o_stride_seq, int64_t o_stride_head, void *workspace,
+                                   size_t workspace_bytes, uint32_t flags, bkv_stream_t stream);
+
 /* Workspace bytes for bkv_paged_decode_attention on the CURRENT device
  * (depends on the SM count); 0 on error (see bkv_last_error). */
 BKV_API size_t bkv_decode_workspace_size(int32_t num_seqs, int32_t num_q_heads, int32_t num_kv_heads,

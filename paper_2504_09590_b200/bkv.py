@@ -44,7 +44,8 @@ _lib_lock = threading.Lock()
 
 EXPORTS = ("bkv_kv_append", "bkv_paged_decode_attention", "bkv_decode_workspace_size",
            "bkv_validate_layout_host", "bkv_status_string", "bkv_last_error", "bkv_version",
-           "bkv_kv_checkpoint", "bkv_kv_restore", "bkv_paged_decode_attention_ex")
+           "bkv_kv_checkpoint", "bkv_kv_restore", "bkv_paged_decode_attention_ex",
+           "bkv_decode_step")
 BKV_FLAG_PDL = 1   # include/bkv.h: programmatic dependent launch (seq_lens not written by the previous kernel)
 
 
@@ -68,6 +69,10 @@ def lib():
                     ctypes.POINTER(_Pool), ctypes.POINTER(_Map), P, i32, P, i64, i64, i32, ctypes.c_float,
                     P, i64, i64, P, ctypes.c_size_t, ctypes.c_uint32, P]
                 L.bkv_paged_decode_attention_ex.restype = ctypes.c_int
+                L.bkv_decode_step.argtypes = [
+                    ctypes.POINTER(_Pool), ctypes.POINTER(_Map), P, i32, P, P, P, i64, i64, i32,
+                    ctypes.c_float, P, i64, i64, P, ctypes.c_size_t, ctypes.c_uint32, P]
+                L.bkv_decode_step.restype = ctypes.c_int
                 L.bkv_decode_workspace_size.argtypes = [i32, i32, i32, i32]
                 L.bkv_decode_workspace_size.restype = ctypes.c_size_t
                 L.bkv_validate_layout_host.argtypes = [P, i32, P, i32, i32, i32, P, i32, i32, i32, P]
@@ -224,10 +229,7 @@ def workspace(num_seqs, num_q_heads, num_kv_heads, head_dim, device=None, stream
     return ws
 
 
-def paged_decode_attention(pool: KVPool, block_tables, dirs, seq_lens, q, softmax_scale=None,
-                           out=None, max_seq_len=None, ws=None, stream=None, pdl=False):
-    """bkv_paged_decode_attention.  q: bf16 [B][Hq][d] (any strides with unit last stride).
-    out: bf16 with the same indexing (allocated [B][Hq][d] if None).  Returns out."""
+def _attn_args(pool, block_tables, dirs, seq_lens, q, softmax_scale, out, max_seq_len, ws, stream):
     p, m = pool.c(), block_map(block_tables, dirs)
     _dev(seq_lens, "seq_lens", torch.int32)
     _dev(q, "q", torch.bfloat16)
@@ -245,11 +247,43 @@ def paged_decode_attention(pool: KVPool, block_tables, dirs, seq_lens, q, softma
         max_seq_len = block_tables.shape[1] * pool.block_size
     if ws is None:
         ws = workspace(B, Hq, pool.num_kv_heads, d, q.device, stream)
+    return p, m, out, softmax_scale, max_seq_len, ws
+
+
+def paged_decode_attention(pool: KVPool, block_tables, dirs, seq_lens, q, softmax_scale=None,
+                           out=None, max_seq_len=None, ws=None, stream=None, pdl=False):
+    """bkv_paged_decode_attention.  q: bf16 [B][Hq][d] (any strides with unit last stride).
+    out: bf16 with the same indexing (allocated [B][Hq][d] if None).  Returns out."""
+    p, m, out, scale, msl, ws = _attn_args(pool, block_tables, dirs, seq_lens, q, softmax_scale,
+                                           out, max_seq_len, ws, stream)
     rc = lib().bkv_paged_decode_attention_ex(
-        ctypes.byref(p), ctypes.byref(m), seq_lens.data_ptr(), int(max_seq_len), q.data_ptr(),
-        q.stride(0), q.stride(1), Hq, float(softmax_scale), out.data_ptr(), out.stride(0),
+        ctypes.byref(p), ctypes.byref(m), seq_lens.data_ptr(), int(msl), q.data_ptr(),
+        q.stride(0), q.stride(1), q.shape[1], float(scale), out.data_ptr(), out.stride(0),
         out.stride(1), ws.data_ptr(), ws.numel(), BKV_FLAG_PDL if pdl else 0, _stream_ptr(stream))
     _check(rc, "bkv_paged_decode_attention")
+    return out
+
+
+def decode_step(pool: KVPool, block_tables, dirs, seq_lens, k_new, v_new, q, softmax_scale=None,
+                out=None, max_seq_len=None, ws=None, stream=None, pdl=False):
+    """bkv_decode_step: append token seq_lens[r]-1 of every request (k_new/v_new contiguous
+    bf16 [B][H_kv][d]) and attend over the context including it, in one launch pair.
+    Equal to kv_append(before=seq_lens-1, cu=arange(B+1)) + paged_decode_attention."""
+    p, m, out, scale, msl, ws = _attn_args(pool, block_tables, dirs, seq_lens, q, softmax_scale,
+                                           out, max_seq_len, ws, stream)
+    _dev(k_new, "k_new", torch.bfloat16)
+    _dev(v_new, "v_new", torch.bfloat16)
+    shape = (q.shape[0], pool.num_kv_heads, pool.head_dim)
+    if tuple(k_new.shape) != shape or tuple(v_new.shape) != shape:
+        raise BkvError(f"k_new/v_new must be [B][H_kv][d] = {list(shape)}")
+    if not (k_new.is_contiguous() and v_new.is_contiguous()):
+        raise BkvError("k_new/v_new must be contiguous")
+    rc = lib().bkv_decode_step(
+        ctypes.byref(p), ctypes.byref(m), seq_lens.data_ptr(), int(msl), k_new.data_ptr(),
+        v_new.data_ptr(), q.data_ptr(), q.stride(0), q.stride(1), q.shape[1], float(scale),
+        out.data_ptr(), out.stride(0), out.stride(1), ws.data_ptr(), ws.numel(),
+        BKV_FLAG_PDL if pdl else 0, _stream_ptr(stream))
+    _check(rc, "bkv_decode_step")
     return out
 
 

@@ -252,13 +252,15 @@ bkv_status bkv_paged_decode_attention(const bkv_kv_pool *pool, const bkv_block_m
                                        o_stride_head, workspace, workspace_bytes, 0u, stream);
 }
 
-bkv_status bkv_paged_decode_attention_ex(const bkv_kv_pool *pool, const bkv_block_map *map,
-                                         const int32_t *seq_lens, int32_t max_seq_len,
-                                         const void *q, int64_t q_stride_seq, int64_t q_stride_head,
-                                         int32_t num_q_heads, float softmax_scale, void *out,
-                                         int64_t o_stride_seq, int64_t o_stride_head,
-                                         void *workspace, size_t workspace_bytes, uint32_t flags,
-                                         bkv_stream_t stream) {
+// Shared by bkv_paged_decode_attention_ex (k_new == v_new == NULL) and
+// bkv_decode_step (the fused append of each request's token L-1).
+static bkv_status decode_impl(const bkv_kv_pool *pool, const bkv_block_map *map,
+                              const int32_t *seq_lens, int32_t max_seq_len, const void *k_new,
+                              const void *v_new, const void *q, int64_t q_stride_seq,
+                              int64_t q_stride_head, int32_t num_q_heads, float softmax_scale,
+                              void *out, int64_t o_stride_seq, int64_t o_stride_head,
+                              void *workspace, size_t workspace_bytes, uint32_t flags,
+                              bkv_stream_t stream) {
   if (flags & ~BKV_FLAG_PDL) return fail(BKV_ERR_INVALID_ARGUMENT, "unknown flags 0x%x", flags);
   bkv_status s = check_pool(pool);
   if (s) return s;
@@ -324,14 +326,48 @@ bkv_status bkv_paged_decode_attention_ex(const bkv_kv_pool *pool, const bkv_bloc
   p.q_bytes = qb;
   p.total_warps = cfg.grid * cfg.warps;
   p.pdl = (flags & BKV_FLAG_PDL) ? 1 : 0;
+  p.k_new = static_cast<const uint16_t *>(k_new);
+  p.v_new = static_cast<const uint16_t *>(v_new);
+  p.k_pool = static_cast<uint16_t *>(pool->k);
+  p.v_pool = static_cast<uint16_t *>(pool->v);
+  p.pool_sb = pool->stride_block;
+  p.pool_sh = pool->stride_head;
+  p.pool_ss = pool->stride_slot;
   p.debug_flags = getenv("BKV_DEBUG") ? atoi(getenv("BKV_DEBUG")) : 0;
-  p.team_force = getenv("BKV_TEAM") ? atoi(getenv("BKV_TEAM")) : 0;
-  p.team_max = g <= 8 ? cfg.warps : 1;
   p.trace_cap = w.trace_cap;
   p.trace = w.trace_cap ? reinterpret_cast<unsigned long long *>(ws + w.trace) : nullptr;
   cudaError_t e = bkv::launch_decode(tmK, tmV, p, D, cfg, reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "decode attention launch");
   return BKV_OK;
+}
+
+bkv_status bkv_paged_decode_attention_ex(const bkv_kv_pool *pool, const bkv_block_map *map,
+                                         const int32_t *seq_lens, int32_t max_seq_len,
+                                         const void *q, int64_t q_stride_seq, int64_t q_stride_head,
+                                         int32_t num_q_heads, float softmax_scale, void *out,
+                                         int64_t o_stride_seq, int64_t o_stride_head,
+                                         void *workspace, size_t workspace_bytes, uint32_t flags,
+                                         bkv_stream_t stream) {
+  return decode_impl(pool, map, seq_lens, max_seq_len, nullptr, nullptr, q, q_stride_seq,
+                     q_stride_head, num_q_heads, softmax_scale, out, o_stride_seq, o_stride_head,
+                     workspace, workspace_bytes, flags, stream);
+}
+
+bkv_status bkv_decode_step(const bkv_kv_pool *pool, const bkv_block_map *map,
+                           const int32_t *seq_lens, int32_t max_seq_len, const void *k_new,
+                           const void *v_new, const void *q, int64_t q_stride_seq,
+                           int64_t q_stride_head, int32_t num_q_heads, float softmax_scale,
+                           void *out, int64_t o_stride_seq, int64_t o_stride_head,
+                           void *workspace, size_t workspace_bytes, uint32_t flags,
+                           bkv_stream_t stream) {
+  if (map && map->num_seqs > 0) {
+    if (!k_new || !v_new) return fail(BKV_ERR_INVALID_ARGUMENT, "k_new/v_new is NULL");
+    if (!aligned16(k_new) || !aligned16(v_new))
+      return fail(BKV_ERR_INVALID_ARGUMENT, "k_new/v_new must be 16-byte aligned");
+  }
+  return decode_impl(pool, map, seq_lens, max_seq_len, k_new, v_new, q, q_stride_seq,
+                     q_stride_head, num_q_heads, softmax_scale, out, o_stride_seq, o_stride_head,
+                     workspace, workspace_bytes, flags, stream);
 }
 
 bkv_status bkv_validate_layout_host(const int32_t *block_tables, int32_t bt_stride,

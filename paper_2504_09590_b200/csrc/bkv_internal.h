@@ -61,8 +61,10 @@ struct DecodeParams {
   int q_bytes;           // smem bytes per q-ring entry
   int total_warps;       // grid * warps per CTA
   int pdl;               // launched with programmatic dependent launch (BKV_FLAG_PDL)
-  int team_force;        // 0 = choose the team size in-kernel, else force it (dev)
-  int team_max;          // largest allowed team (1 when the state area is not allocated)
+  // fused decode step (bkv_decode_step): new token rows [B][H][D] + pool for the write; k_new == nullptr otherwise
+  const uint16_t *k_new, *v_new;
+  uint16_t *k_pool, *v_pool;
+  int64_t pool_sb, pool_sh, pool_ss;
   int debug_flags;       // dev only: 1 = skip the math (data-movement skeleton)
   unsigned long long *trace;  // dev only (BKV_TRACE): per-warp event log, else nullptr
   int trace_cap;         // events per warp

@@ -187,8 +187,10 @@ __device__ void compute_plan(const DecodeParams &p, int *Pre, int *Lsm, Plan *pl
 }
 
 // KIND 0: MHA on CUDA cores; 1: MMA with g <= 8; 2: MMA with 8 < g <= 16.
+// GQA runs 8 warps (measured best) and gets the 255-register budget of a
+// 256-thread CTA -- at 384 threads the MMA kernels spill (ptxas -v).
 template <int D, int KIND>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
     decode_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                   const DecodeParams p) {
   using G = Geo<D>;
@@ -352,6 +354,28 @@ __global__ void __launch_bounds__(384, 1)
     const int lo_s = dr ? bs - ne : 0;               // RT from the left,
     const int hi_s = dr ? bs : ne;                   //        BE from the right
     const int lo = max(lo_s - c * 16, 0), hi = min(hi_s - c * 16, 16);
+    if (p.k_new != nullptr && e == (cur.L - 1) / bs) {
+      // fused decode step: this step's token t = L-1 of
+      // (r, h) lands in this block -- in its direction's slot -- and this
+      // warp is the only one that owns it.  Write its K and V rows first (lanes
+      // 0-15 K, 16-31 V, 16 B each), then make the generic stores visible to the
+      // TMA (async proxy) read of this very tile issued next.
+      const int j = (cur.L - 1) - e * bs;
+      const int slot_new = dr ? bs - 1 - j : j;
+      if ((slot_new >> 4) == c) {
+        constexpr int TPR = D / 8;
+        const int which = lane / 16, sub = lane & 15;
+        if (sub < TPR) {
+          const uint16_t *src = (which ? p.v_new : p.k_new) +
+                                (static_cast<int64_t>(cur.r) * H + cur.h) * D + sub * 8;
+          uint16_t *dst = (which ? p.v_pool : p.k_pool) + static_cast<int64_t>(b) * p.pool_sb +
+                          static_cast<int64_t>(cur.h) * p.pool_sh + static_cast<int64_t>(slot_new) * p.pool_ss + sub * 8;
+          *reinterpret_cast<uint4 *>(dst) = __ldg(reinterpret_cast<const uint4 *>(src));
+        }
+        __syncwarp();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
+    }
     int flags = (is_first ? F_FIRST : 0) | (lo >= hi ? F_NOKV : 0);
     is_first = false;
     csub = c;
@@ -886,6 +910,7 @@ cudaError_t decode_config(int head_dim, int group, int num_seqs, DecodeLaunch *c
            4 * (num_seqs + 1) * (int)sizeof(int) + ((num_seqs + 3) & ~3) * 4 + 256;
   };
   int W = env_int("BKV_WARPS", group > 1 ? 8 : 12);   // measured best: GQA 8, MHA 12
+  W = std::min(W, group > 1 ? 8 : 12);                 // = the kernels' __launch_bounds__
   while (W > 4 && need(W, S) > smem_optin - 1024) W -= 4;
   while (S > 1 && need(W, S) > smem_optin - 1024) --S;
   cfg->grid = sms * env_int("BKV_CTAS_PER_SM", 1);
