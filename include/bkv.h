@@ -227,9 +227,10 @@ BKV_API bkv_status bkv_paged_decode_attention_ex(const bkv_kv_pool *pool, const 
  * (dir ? bs-1-t%bs : t%bs) of block block_tables[r][t / bs] (§5.1,
  * RT fills a block from the left, BE from the right) and the attention
  * then reads it.  Results (pool bytes and out) are bit-identical to the two
- * separate calls.  The warp that owns the chunk holding slot(t) writes the
- * row and fences it into the TMA (async) proxy before loading that chunk, so
- * no separate append kernel and no extra pool read is needed.
+ * separate calls.  The warp that owns the 16-slot chunk holding slot(t)
+ * bulk-loads the new K/V rows together with that chunk's tile, patches them
+ * into the tile in shared memory and bulk-stores them into the pool: no
+ * separate append kernel, no extra pool read, no ordering stall.
  *   k_new, v_new  device bf16 [num_seqs][num_kv_heads][head_dim], contiguous,
  *                 16-byte aligned; read only.
  *   seq_lens      device int32 [num_seqs], lengths AFTER the append (>= 1 for

@@ -28,6 +28,12 @@
 //  * A unit's output is written directly when the request has one split;
 //    otherwise fp32 (m, l, o) partials go to the workspace and merge_kernel,
 //    stream-ordered after this kernel, combines them in split order.
+//  * Fused decode step (bkv_decode_step): the chunk that
+//    holds a unit's new token t = L-1 also bulk-loads the token's K/V rows
+//    (from k_new/v_new) into a per-slot patch area on the same mbarrier; the
+//    consumer writes them into the tile's slot row (128B swizzle) and bulk-
+//    stores them into the pool -- the append costs no extra launch and no
+//    ordering stall.
 //  * NaN hygiene (reading Q10): dead slots are never combined arithmetically:
 //    their scores are selected to -inf and their V rows are zeroed in shared
 //    memory before P.V.
@@ -38,11 +44,13 @@
 
 namespace bkv {
 
-enum : int { F_FIRST = 1, F_LAST = 2, F_NOKV = 4, F_NOQ = 8 };
+// F_NEW (fused decode step): the chunk holds this step's new token; its slot
+// in the block sits in flags bits 8..15 and the physical block in SlotMeta::aux.
+enum : int { F_FIRST = 1, F_LAST = 2, F_NOKV = 4, F_NOQ = 8, F_NEW = 16 };
 
 struct SlotMeta {
   int u, r, h, nsplit;
-  int lo, hi, flags, qidx;
+  int lo, hi, flags, aux;
 };
 
 constexpr int kBuckets = 4;
@@ -211,7 +219,9 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
   uint64_t *bars_g = reinterpret_cast<uint64_t *>(meta_g + W * S * sizeof(SlotMeta));
   uint8_t *scratch_g = reinterpret_cast<uint8_t *>(bars_g + W * S);   // W x 1 KiB
   const uint32_t my_scr = smem_u32(scratch_g + warp * 1024);
-  int *Pre = reinterpret_cast<int *>(scratch_g + W * 1024);   // [kBuckets][B + 1]
+  uint8_t *patch_g = scratch_g + W * 1024;                    // W x S x 512 B: new K|V rows
+  const uint32_t my_patch = smem_u32(patch_g + warp * S * 512);
+  int *Pre = reinterpret_cast<int *>(patch_g + W * S * 512);  // [kBuckets][B + 1]
   int *Lsm = Pre + kBuckets * (p.B + 1);                      // seq_lens cache [B]
 
   if (threadIdx.x == 0) {
@@ -306,7 +316,7 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
   int nx_bt = 0, nx_dir = 0;
   load_window(nxt, nxt.e0, nx_bt, nx_dir);
   bool is_active = false, is_done = false, is_first = false;
-  int is_ci = 0, is_nc = 0, is_wb = 0, bt_w = 0, dir_w = 0, is_qidx = 0;
+  int is_ci = 0, is_nc = 0, is_wb = 0, bt_w = 0, dir_w = 0;
 
   // Produce the next chunk of this warp's work stream (warp-collective).
   // Chunk ci of a unit = 16 slots (sub-chunk ci % cpb) of block e0 + ci / cpb;
@@ -334,7 +344,7 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
       is_first = true;
       trace(2, cur.u);
       if (is_ci >= is_nc) {  // no chunk for this warp (or empty context, Q8): flag-only slot
-        m = SlotMeta{cur.u, cur.r, cur.h, cur.n, 0, 0, F_FIRST | F_LAST | F_NOKV | F_NOQ, is_qidx};
+        m = SlotMeta{cur.u, cur.r, cur.h, cur.n, 0, 0, F_FIRST | F_LAST | F_NOKV | F_NOQ, 0};
         blk = 0;
         csub = 0;
         return true;
@@ -354,29 +364,14 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
     const int lo_s = dr ? bs - ne : 0;               // RT from the left,
     const int hi_s = dr ? bs : ne;                   //        BE from the right
     const int lo = max(lo_s - c * 16, 0), hi = min(hi_s - c * 16, 16);
+    int flags = (is_first ? F_FIRST : 0) | (lo >= hi ? F_NOKV : 0);
     if (p.k_new != nullptr && e == (cur.L - 1) / bs) {
-      // fused decode step: this step's token t = L-1 of
-      // (r, h) lands in this block -- in its direction's slot -- and this
-      // warp is the only one that owns it.  Write its K and V rows first (lanes
-      // 0-15 K, 16-31 V, 16 B each), then make the generic stores visible to the
-      // TMA (async proxy) read of this very tile issued next.
+      // fused decode step: token t = L-1 of (r, h) lands in
+      // this block, in its direction's slot; this warp alone owns it.
       const int j = (cur.L - 1) - e * bs;
       const int slot_new = dr ? bs - 1 - j : j;
-      if ((slot_new >> 4) == c) {
-        constexpr int TPR = D / 8;
-        const int which = lane / 16, sub = lane & 15;
-        if (sub < TPR) {
-          const uint16_t *src = (which ? p.v_new : p.k_new) +
-                                (static_cast<int64_t>(cur.r) * H + cur.h) * D + sub * 8;
-          uint16_t *dst = (which ? p.v_pool : p.k_pool) + static_cast<int64_t>(b) * p.pool_sb +
-                          static_cast<int64_t>(cur.h) * p.pool_sh + static_cast<int64_t>(slot_new) * p.pool_ss + sub * 8;
-          *reinterpret_cast<uint4 *>(dst) = __ldg(reinterpret_cast<const uint4 *>(src));
-        }
-        __syncwarp();
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-      }
+      if ((slot_new >> 4) == c) flags |= F_NEW | (slot_new << 8);
     }
-    int flags = (is_first ? F_FIRST : 0) | (lo >= hi ? F_NOKV : 0);
     is_first = false;
     csub = c;
     blk = b;
@@ -385,18 +380,25 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
       flags |= F_LAST;
       is_active = false;
     }
-    m = SlotMeta{cur.u, cur.r, cur.h, cur.n, lo, hi, flags, is_qidx};
+    m = SlotMeta{cur.u, cur.r, cur.h, cur.n, lo, hi, flags, b};
     return true;
   };
 
   auto issue = [&](int i, const SlotMeta &m, int blk, int csub) {
     if (lane == 0) {
       reinterpret_cast<int4 *>(metas + i)[0] = make_int4(m.u, m.r, m.h, m.nsplit);
-      reinterpret_cast<int4 *>(metas + i)[1] = make_int4(m.lo, m.hi, m.flags, m.qidx);
+      reinterpret_cast<int4 *>(metas + i)[1] = make_int4(m.lo, m.hi, m.flags, m.aux);
       const uint32_t bar = my_bars + 8 * i;
       const bool kv = !(m.flags & F_NOKV);
-      const uint32_t bytes = kv ? G::SLOT_BYTES : 0;
+      const bool nw = m.flags & F_NEW;
+      const uint32_t bytes = (kv ? G::SLOT_BYTES : 0) + (nw ? 4 * D : 0);
       mbar_arrive_expect_tx(bar, bytes);
+      if (nw) {   // the new K and V rows ride on the same barrier into the slot's patch area
+        bulk_wait_read_all();   // (the previous bulk store out of this area has read it)
+        const int64_t row = (static_cast<int64_t>(m.r) * H + m.h) * D;
+        bulk_load(my_patch + i * 512, p.k_new + row, 2 * D, bar);
+        bulk_load(my_patch + i * 512 + 2 * D, p.v_new + row, 2 * D, bar);
+      }
       if (kv) {
         // one 5-D box = the whole 16-slot x d tile, laid out [half][slot][128 B] swizzled
         const uint32_t dk = my_slots + i * G::SLOT_BYTES, dv = dk + G::KV_BYTES;
@@ -730,13 +732,33 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
       trace(3, m.u);
       begin_unit(m);
     }
+    if (m.flags & F_NEW) {
+      // The tile was loaded before the token existed: patch its row (swizzled)
+      // from the patch area, and store the row into the pool (the append).
+      constexpr int TPR = D / 8;   // 16-byte pieces per row
+      const int which = lane >> 4, pc = lane & 15, slot_new = (m.flags >> 8) & 0xff;
+      if (pc < TPR) {
+        const uint4 v = lds128(my_patch + slot * 512 + which * 2 * D + pc * 16);
+        const uint32_t tile = my_slots + slot * G::SLOT_BYTES + which * G::KV_BYTES;
+        st_shared_v4(tile + (pc >> 3) * G::HALF_BYTES + swz(slot_new & 15, pc & 7), v);
+      }
+      if (lane == 0) {   // pool rows: async bulk stores straight from the patch area
+        const int64_t off = static_cast<int64_t>(m.aux) * p.pool_sb + static_cast<int64_t>(m.h) * p.pool_sh +
+                            static_cast<int64_t>(slot_new) * p.pool_ss;
+        bulk_store(p.k_pool + off, my_patch + slot * 512, 2 * D);
+        bulk_store(p.v_pool + off, my_patch + slot * 512 + 2 * D, 2 * D);
+        bulk_commit();
+      }
+      __syncwarp();
+    }
     const long long c2 = profiling ? clock64() : 0;
     long long ci0 = 0, ci1 = 0;
     // refill this slot with the warp's next chunk (after our reads of it)
     auto release = [&]() {
       if (profiling) ci0 = clock64();
       __syncwarp();
-      if (m.lo > 0 || m.hi < 16) fence_proxy_async_smem();   // zeroed rows precede the TMA write
+      if (m.lo > 0 || m.hi < 16 || (m.flags & F_NEW))   // our generic smem writes precede
+        fence_proxy_async_smem();                       // the next async (TMA) writes
       SlotMeta mn;
       int blk, cs;
       if (next_chunk(mn, blk, cs)) {
@@ -769,6 +791,7 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
       phase ^= 1u;
     }
   }
+  if (p.k_new != nullptr && lane == 0) bulk_wait_all();   // pool rows written before exit
   if (profiling)
     for (int k = 0; k < 6; ++k) trace(8 + k, static_cast<int>(min(prof[k], (long long)0x7fffffff)));
 
@@ -906,7 +929,7 @@ cudaError_t decode_config(int head_dim, int group, int num_seqs, DecodeLaunch *c
   const int slot_bytes = 2 * (head_dim / 64) * 2048;
   const int qb = 0;   // q is read from global (L2-prefetched), no shared-memory ring
   auto need = [&](int w, int s) {
-    return 1024 + w * s * slot_bytes + w * s * (int)(sizeof(int) * 8) + w * s * 8 + w * 1024 +
+    return 1024 + w * s * slot_bytes + w * s * (int)(sizeof(int) * 8) + w * s * 8 + w * 1024 + w * s * 512 +
            4 * (num_seqs + 1) * (int)sizeof(int) + ((num_seqs + 3) & ~3) * 4 + 256;
   };
   int W = env_int("BKV_WARPS", group > 1 ? 8 : 12);   // measured best: GQA 8, MHA 12

@@ -6,7 +6,7 @@ import paper_2504_09590_b200 as bkv
 from synth import CONFIGS, make_case
 from synth.workload import shard_heads
 
-def run(cfg, tp=1, layers=8, iters=20):
+def run(cfg, tp=1, layers=8, iters=20, mode="attn"):
     sh = CONFIGS[cfg]; case = make_case(cfg, 0); lay = case.layout
     kvh, qh = shard_heads(sh, tp, 0); H = len(kvh); Hq = len(qh); d = sh.head_dim
     dev = "cuda"
@@ -19,8 +19,14 @@ def run(cfg, tp=1, layers=8, iters=20):
     q = torch.randn(lay.batch, Hq, d, device=dev).to(torch.bfloat16)
     out = torch.empty_like(q)
     ws = bkv.workspace(lay.batch, Hq, H, d)
+    kn = torch.randn(lay.batch, H, d, device=dev).to(torch.bfloat16)
+    vn = torch.randn(lay.batch, H, d, device=dev).to(torch.bfloat16)
     def body():
-        for p in pools: bkv.paged_decode_attention(p, bt, dirs, lens, q, out=out, ws=ws)
+        for p in pools:
+            if mode == "fused":
+                bkv.decode_step(p, bt, dirs, lens, kn, vn, q, out=out, ws=ws, pdl=True)
+            else:
+                bkv.paged_decode_attention(p, bt, dirs, lens, q, out=out, ws=ws, pdl=True)
     body(); torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
@@ -35,11 +41,11 @@ def run(cfg, tp=1, layers=8, iters=20):
     kv_bytes = float((lay.lens.astype(np.int64)).sum()) * 2 * H * d * 2
     byts = kv_bytes + 2 * lay.batch * Hq * d * 2
     med = np.median(ts)
-    print(f"{cfg} tp{tp}: B={lay.batch} H={H} Hq={Hq} KV={kv_bytes/1e6:.1f}MB x{layers}  median {med:.1f}us/layer  "
+    print(f"{cfg} tp{tp} {mode} dbg={os.environ.get('BKV_DEBUG', '0')}: B={lay.batch} H={H} Hq={Hq} KV={kv_bytes/1e6:.1f}MB x{layers}  median {med:.1f}us/layer  "
           f"p10 {np.percentile(ts,10):.1f} p90 {np.percentile(ts,90):.1f}  -> {byts/med/1e3:.0f} GB/s "
           f"({byts/med/1e3/6525.9*100:.1f}% of 6526)", flush=True)
     del pools; torch.cuda.empty_cache()
 
 if __name__ == "__main__":
     for spec in sys.argv[1:] or ["opt13b:1", "opt13b:2", "opt30b:4", "llama70b:1", "llama70b:8"]:
-        c, t = spec.split(":"); run(c, int(t))
+        c, t, *m = spec.split(":"); run(c, int(t), mode=m[0] if m else "attn")

@@ -121,7 +121,8 @@ def test_fused_steps_in_sequence_grow_context():
     after each step the pool is the oracle's append of every token so far."""
     sh = Shape("seq", 16, 2, 128, 16, 12, 0.5, "uniform", 300, 1, 1, uniform_max=300)
     n_steps = 5
-    case = make_case(sh, 17)
+    lens = np.random.default_rng(17).integers(n_steps + 1, 300, size=12)
+    case = make_case(sh, 17, lens=lens)
     lay = case.layout
     B, H, d = lay.batch, sh.num_kv_heads, sh.head_dim
     # the layout is built for the FINAL lengths; run steps L-n+1 .. L
