@@ -916,6 +916,12 @@ static int env_int(const char *name, int dflt) {
   return (s && *s) ? atoi(s) : dflt;
 }
 
+// g = 1 runs on the tensor-core kernel too (one useful n column of 8, but half
+// the instructions per chunk of the CUDA-core kernel: no bf16 unpacking; measured
+// opt13b TP1 88.8% -> 92.7% of HBM peak).  BKV_MHA_CUDA_CORES=1 (dev) keeps the
+// CUDA-core kernel selectable.
+static bool mha_on_mma() { return env_int("BKV_MHA_CUDA_CORES", 0) == 0; }
+
 cudaError_t decode_config(int head_dim, int group, int num_seqs, DecodeLaunch *cfg, int *slots,
                           int *q_bytes) {
   int dev = 0, sms = 0, smem_optin = 0;
@@ -932,8 +938,9 @@ cudaError_t decode_config(int head_dim, int group, int num_seqs, DecodeLaunch *c
     return 1024 + w * s * slot_bytes + w * s * (int)(sizeof(int) * 8) + w * s * 8 + w * 1024 + w * s * 512 +
            4 * (num_seqs + 1) * (int)sizeof(int) + ((num_seqs + 3) & ~3) * 4 + 256;
   };
-  int W = env_int("BKV_WARPS", group > 1 ? 8 : 12);   // measured best: GQA 8, MHA 12
-  W = std::min(W, group > 1 ? 8 : 12);                 // = the kernels' __launch_bounds__
+  const bool mma = group > 1 || mha_on_mma();
+  int W = env_int("BKV_WARPS", mma ? 8 : 12);   // measured best: MMA kernels 8, CUDA-core MHA 12
+  W = std::min(W, mma ? 8 : 12);                 // = the kernels' __launch_bounds__
   while (W > 4 && need(W, S) > smem_optin - 1024) W -= 4;
   while (S > 1 && need(W, S) > smem_optin - 1024) --S;
   cfg->grid = sms * env_int("BKV_CTAS_PER_SM", 1);
@@ -948,7 +955,9 @@ int decode_target_units(const DecodeLaunch &cfg) {
   return env_int("BKV_UNITS_PER_WARP", 3) * cfg.grid * cfg.warps;
 }
 
-int decode_min_split(int group) { return env_int("BKV_MIN_SPLIT", group > 1 ? 16 : 4); }
+int decode_min_split(int group) {
+  return env_int("BKV_MIN_SPLIT", group > 1 || mha_on_mma() ? 16 : 4);
+}
 
 template <int D, int KIND>
 static cudaError_t launch_t(const CUtensorMap &tmK, const CUtensorMap &tmV, const DecodeParams &p,
@@ -990,7 +999,7 @@ static cudaError_t launch_t(const CUtensorMap &tmK, const CUtensorMap &tmV, cons
 
 cudaError_t launch_decode(const CUtensorMap &tmK, const CUtensorMap &tmV, const DecodeParams &p,
                           int head_dim, const DecodeLaunch &cfg, cudaStream_t s) {
-  const int kind = p.g == 1 ? 0 : (p.g <= 8 ? 1 : 2);
+  const int kind = p.g == 1 && !mha_on_mma() ? 0 : (p.g <= 8 ? 1 : 2);
   if (head_dim == 128) {
     if (kind == 0) return launch_t<128, 0>(tmK, tmV, p, cfg, s);
     if (kind == 1) return launch_t<128, 1>(tmK, tmV, p, cfg, s);

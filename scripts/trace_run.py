@@ -15,7 +15,7 @@ bt = torch.from_numpy(lay.block_tables).cuda(); dirs = torch.from_numpy(lay.dirs
 lens = torch.from_numpy(lay.lens).cuda(); q = torch.randn(lay.batch, Hq, d, device="cuda").to(torch.bfloat16)
 ws = bkv.workspace(lay.batch, Hq, H, d)
 cap = int(os.environ["BKV_TRACE"])
-nw = 148 * int(os.environ.get("BKV_WARPS", "12"))
+nw = 148 * int(os.environ.get("BKV_WARPS", "8" if Hq > H else "12"))
 need = nw * cap * 16
 total = bkv.decode_workspace_size(lay.batch, Hq, H, d)   # trace region = last up256(need) bytes
 start = total - ((need + 255) // 256 * 256)

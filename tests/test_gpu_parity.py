@@ -311,3 +311,25 @@ def test_pdl_launch_after_append_matches():
     K, V, _ = oracle_pool(case, ks, vs, 2)
     ref = oracle.attention(K, V, lay.block_tables, lay.dirs, lay.lens, q, default_scale(128))
     check_close(outs[1], ref, "pdl")
+
+
+def test_mha_cuda_core_kernel_parity(monkeypatch):
+    """g = 1 runs on the tensor-core kernel by default; the CUDA-core (FFMA2)
+    kernel stays selectable (BKV_MHA_CUDA_CORES=1) and must agree with the oracle
+    and, within 2x tolerance, with the tensor-core kernel."""
+    monkeypatch.setenv("BKV_MHA_CUDA_CORES", "1")
+    for cfg, seed in (("tiny", 40), ("tiny", 41)):
+        case = make_case(cfg, seed)
+        o_cc, ref, (ks, vs, q, pool) = _run_case(case)
+        check_close(o_cc, ref, f"cuda-core {cfg}")
+        lay = case.layout
+        bt, dirs, lens = gpu_map(lay)
+        monkeypatch.delenv("BKV_MHA_CUDA_CORES")
+        o_tc = bkv.paged_decode_attention(pool, bt, dirs, lens, t_u16(q))
+        torch.cuda.synchronize()
+        check_close(o_tc, ref, f"tensor-core {cfg}")
+        assert (o_cc.float() - o_tc.float()).abs().max().item() <= 2 * MAX_ABS
+        monkeypatch.setenv("BKV_MHA_CUDA_CORES", "1")
+    sh = Shape("cc", 5, 5, 128, 32, 20, 0.5, "uniform", 900, 1, 1, uniform_max=900)
+    o, ref, _ = _run_case(make_case(sh, 42))
+    check_close(o, ref, "cuda-core d128 bs32")
