@@ -88,14 +88,32 @@ typedef struct {
 
 /*
  * Block map of a batch (SURVEY D2 + D3).
- * Request r's logical token t lives in physical block
+ *
+ * Dense map (fills == NULL, the vLLM-style table the paper's kernel reads):
+ * request r's logical token t lives in physical block
  *     block_tables[r*bt_stride + t/block_size]
  * at slot  t%block_size                  if dir == BKV_DIR_FWD
  *          block_size-1-t%block_size     if dir == BKV_DIR_REV
  * where dir = dirs[r*dir_row_stride + (t/block_size)*dir_col_stride].
  * dir_col_stride = 0 gives one flag per request (reading Q5); a table of the
  * block table's shape uses dir_col_stride = 1, dir_row_stride = bt_stride.
- * Device pointers.  Only entries e < ceil(seq_len/block_size) are read.
+ * Only entries e < ceil(seq_len/block_size) are read.
+ *
+ * General map (fills != NULL, reading Q6 option B):
+ * FindBlock places a BE prefill "according to the maximum number of empty
+ * slots" and FindPreemptBlock lets an RT request write a BE block
+ * "from the opposite end", so ANY entry may be partly filled.
+ * Entry e < num_entries[r] of request r holds
+ *     n_e = fills[r*fill_row_stride + e]   (1 <= n_e <= block_size)
+ * of the request's tokens: tokens are numbered in entry order (entry e holds
+ * tokens [n_0+...+n_{e-1}, n_0+...+n_e)) and the j-th token of an entry sits
+ * at slot j (forward) or block_size-1-j (reversed) -- the in-block rule of
+ * P:711.  The request's resident length is n_0 + ... + n_{num_entries[r]-1};
+ * every call that takes seq_lens requires them to be equal (caller
+ * precondition, checked by bkv_validate_block_map_host).  A dense map is the
+ * general map with every non-last entry full.
+ *
+ * All pointers are device pointers (host pointers for the host validator).
  */
 typedef struct {
   const int32_t *block_tables;
@@ -104,6 +122,10 @@ typedef struct {
   int32_t dir_row_stride;
   int32_t dir_col_stride;
   int32_t num_seqs;
+  /* general map only (NULL/0 for a dense map) */
+  const uint8_t *fills;        /* [num_seqs][fill_row_stride], entries 1..block_size */
+  int32_t fill_row_stride;     /* >= num_entries[r] for every r                      */
+  const int32_t *num_entries;  /* [num_seqs], 0..bt_stride; required iff fills       */
 } bkv_block_map;
 
 /*
@@ -121,8 +143,10 @@ typedef struct {
  *   slot_mapping_out             optional device int64 [total_new]: receives
  *                                block*block_size + slot of every new token
  * The new token t = seq_lens_before[r] + j must lie inside the block map
- * (t < bt_stride*block_size) and its slot must not hold a live token of another
- * request (invariant I5; lazy-checkpoint eviction is the caller's job).
+ * (dense: t < bt_stride*block_size; general: t < the sum of the request's
+ * fills -- the map describes the state AFTER the append) and its slot must not
+ * hold a live token of another request (invariant I5; lazy-checkpoint
+ * eviction is the caller's job).  General maps: num_entries[r] <= 16384.
  * Bit-exact: each written row is a copy of the input row; no other byte of
  * the pool changes.
  */
@@ -192,6 +216,31 @@ BKV_API bkv_status bkv_kv_checkpoint(const bkv_kv_pool *pool, const int64_t *slo
                                      void *k_out, void *v_out, bkv_stream_t stream);
 BKV_API bkv_status bkv_kv_restore(const bkv_kv_pool *pool, const int64_t *slot_ids, int32_t n,
                                   const void *k_in, const void *v_in, bkv_stream_t stream);
+
+/*
+ * bkv_kv_append_checkpoint -- kv_append with the lazy checkpoint fused in
+ * ("only the KV tensors of a specific request
+ * that are about to be overwritten by its peer need to be checkpointed in CPU
+ * memory", the a3/B8 example of P:731).  Identical to bkv_kv_append, except:
+ *   evict_rows [total_new]  device int32: -1, or the row of ckpt_k/ckpt_v that
+ *                           receives the OLD K and V rows (every kv head) of
+ *                           new token i's slot before the new rows replace them
+ *   ckpt_k, ckpt_v          bf16 [rows][num_kv_heads][head_dim], contiguous,
+ *                           16-byte aligned: device memory or the device alias
+ *                           of mapped pinned host memory (a direct D2H
+ *                           checkpoint)
+ * Equal, bit for bit, to bkv_kv_checkpoint of those slots followed by
+ * bkv_kv_append; the old row is read and the new one written by the same
+ * thread, so no ordering is needed.  Which slots hold live peer tokens is
+ * the host scheduler's knowledge (its preemption table).  Rows of
+ * ckpt_* not named by evict_rows are not written.
+ */
+BKV_API bkv_status bkv_kv_append_checkpoint(const bkv_kv_pool *pool, const bkv_block_map *map,
+                                            const int32_t *seq_lens_before,
+                                            const int32_t *cu_new_tokens, int32_t total_new_tokens,
+                                            const void *k_new, const void *v_new,
+                                            int64_t *slot_mapping_out, const int32_t *evict_rows,
+                                            void *ckpt_k, void *ckpt_v, bkv_stream_t stream);
 
 /*
  * bkv_paged_decode_attention_ex -- the same call with launch flags.
@@ -268,9 +317,21 @@ BKV_API bkv_status bkv_validate_layout_host(const int32_t *block_tables, int32_t
                                     int32_t block_size, int32_t require_nonempty,
                                     int64_t info[5]);
 
+/*
+ * The same validator for a dense OR general map, given as a
+ * bkv_block_map whose pointers are HOST pointers.  For a general map, I4 also
+ * covers num_entries[r] outside [0, bt_stride] (info = 1, r, -1, value), a
+ * fill outside [1, block_size] (info = 1, r, e, fill) and seq_lens[r] != the
+ * sum of its fills (info = 1, r, -2, seq_len); I1 and I2 are checked over the
+ * num_entries[r] entries with the general token -> slot rule.
+ */
+BKV_API bkv_status bkv_validate_block_map_host(const bkv_block_map *map, const int32_t *seq_lens,
+                                               int32_t num_blocks, int32_t block_size,
+                                               int32_t require_nonempty, int64_t info[5]);
+
 BKV_API const char *bkv_status_string(bkv_status s);
 BKV_API const char *bkv_last_error(void); /* thread-local detail of the last failure */
-BKV_API int32_t bkv_version(void);        /* MAJOR*10000 + MINOR*100 + PATCH */
+BKV_API int32_t bkv_version(void);        /* MAJOR*10000 + MINOR*100 + PATCH (0.2.0: general maps) */
 
 #ifdef __cplusplus
 } /* extern "C" */

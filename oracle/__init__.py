@@ -59,6 +59,17 @@ def lib():
         L.bkvo_restore.restype = None
         L.bkvo_overwritten_peers.argtypes = [i32, P, i32, P, i32, i32, P, P, P, i32, i32, P, P, P, i32]
         L.bkvo_overwritten_peers.restype = i32
+        L.bkvo_validate_f.argtypes = [i32, P, i32, P, i32, i32, P, i32, P, P, i32, i32, i32, P]
+        L.bkvo_validate_f.restype = i32
+        L.bkvo_append_f.argtypes = [P, P, i64, i64, i64, i32, i32, i32,
+                                    i32, P, i32, P, i32, i32, P, i32, P, P, P, P, P]
+        L.bkvo_append_f.restype = None
+        L.bkvo_gather_f.argtypes = [P, P, i64, i64, i64, i32, i32, i32,
+                                    P, i32, P, i32, i32, P, i32, i32, i64, P, P]
+        L.bkvo_gather_f.restype = None
+        L.bkvo_attention_f.argtypes = [P, P, i64, i64, i64, i32, i32, i32,
+                                       P, i32, P, i32, i32, P, i32, P, i32, i32, P, i32, dbl, P]
+        L.bkvo_attention_f.restype = None
         L.bkvo_num_threads.restype = i32
         L.bkvo_set_num_threads.argtypes = [i32]
         _lib = L
@@ -97,12 +108,28 @@ def slot_in_block(direction: int, t: int, bs: int) -> int:
     return lib().bkvo_slot_in_block(int(direction), int(t), int(bs))
 
 
-def validate(block_tables, dirs, lens, num_blocks: int, bs: int, require_nonempty=True):
-    """Return (code, info): 0 ok, 1 I4 range, 2 I1 slot collision, 3 I2 sharing."""
+def _fills(fills, num_entries, B):
+    """General map: uint8 fills [B][M] + int32 num_entries [B]."""
+    f = _c(fills, np.uint8)
+    ne = _c(num_entries, np.int32)
+    assert f.ndim == 2 and f.shape[0] == B and ne.shape == (B,)
+    return f, f.shape[1], ne
+
+
+def validate(block_tables, dirs, lens, num_blocks: int, bs: int, require_nonempty=True,
+             fills=None, num_entries=None):
+    """Return (code, info): 0 ok, 1 I4 range, 2 I1 slot collision, 3 I2 sharing.
+    With ``fills``/``num_entries`` the map is a general one (bkvo_validate_f)."""
     bt = _c(block_tables, np.int32)
     d, rs, cs = _dirs(dirs)
     ln = _c(lens, np.int32)
     info = np.zeros(4, dtype=np.int64)
+    if fills is not None:
+        f, frs, ne = _fills(fills, num_entries, int(ln.shape[0]))
+        rc = lib().bkvo_validate_f(int(ln.shape[0]), _ptr(bt), int(bt.shape[1]), _ptr(d), rs, cs,
+                                   _ptr(f), frs, _ptr(ne), _ptr(ln), int(num_blocks), int(bs),
+                                   int(bool(require_nonempty)), _ptr(info))
+        return int(rc), tuple(int(x) for x in info)
     rc = lib().bkvo_validate(int(ln.shape[0]), _ptr(bt), int(bt.shape[1]), _ptr(d), rs, cs,
                              _ptr(ln), int(num_blocks), int(bs), int(bool(require_nonempty)),
                              _ptr(info))
@@ -115,7 +142,7 @@ def new_pool(num_blocks: int, H: int, bs: int, d: int, fill: int = 0):
     return K, K.copy()
 
 
-def append(K, V, block_tables, dirs, before, cu_new, k_new, v_new):
+def append(K, V, block_tables, dirs, before, cu_new, k_new, v_new, fills=None, num_entries=None):
     """In-place append into host pools; returns int64 slot_mapping [total_new]."""
     sb, sh, ss, H, d, bs = _pool_geom(K)
     assert V.shape == K.shape and V.strides == K.strides
@@ -127,25 +154,37 @@ def append(K, V, block_tables, dirs, before, cu_new, k_new, v_new):
     vn = _c(v_new, np.uint16).reshape(-1, H, d)
     assert kn.shape[0] == cu[-1]
     sm = np.zeros(int(cu[-1]), dtype=np.int64)
+    if fills is not None:
+        f, frs, _ = _fills(fills, num_entries, int(bf.shape[0]))
+        lib().bkvo_append_f(_ptr(K), _ptr(V), sb, sh, ss, H, d, bs, int(bf.shape[0]), _ptr(bt),
+                            int(bt.shape[1]), _ptr(dd), rs, cs, _ptr(f), frs, _ptr(bf), _ptr(cu),
+                            _ptr(kn), _ptr(vn), _ptr(sm))
+        return sm
     lib().bkvo_append(_ptr(K), _ptr(V), sb, sh, ss, H, d, bs, int(bf.shape[0]), _ptr(bt),
                       int(bt.shape[1]), _ptr(dd), rs, cs, _ptr(bf), _ptr(cu), _ptr(kn), _ptr(vn),
                       _ptr(sm))
     return sm
 
 
-def gather(K, V, block_tables, dirs, r: int, L: int):
+def gather(K, V, block_tables, dirs, r: int, L: int, fills=None, num_entries=None):
     """Dense logical-order (K_r, V_r), uint16 [L][H][d]."""
     sb, sh, ss, H, d, bs = _pool_geom(K)
     bt = _c(block_tables, np.int32)
     dd, rs, cs = _dirs(dirs)
     ko = np.zeros((L, H, d), dtype=np.uint16)
     vo = np.zeros((L, H, d), dtype=np.uint16)
+    if fills is not None:
+        f, frs, _ = _fills(fills, num_entries, int(bt.shape[0]))
+        lib().bkvo_gather_f(_ptr(K), _ptr(V), sb, sh, ss, H, d, bs, _ptr(bt), int(bt.shape[1]),
+                            _ptr(dd), rs, cs, _ptr(f), frs, int(r), int(L), _ptr(ko), _ptr(vo))
+        return ko, vo
     lib().bkvo_gather(_ptr(K), _ptr(V), sb, sh, ss, H, d, bs, _ptr(bt), int(bt.shape[1]),
                       _ptr(dd), rs, cs, int(r), int(L), _ptr(ko), _ptr(vo))
     return ko, vo
 
 
-def attention(K, V, block_tables, dirs, lens, q, scale: float, r_range=None):
+def attention(K, V, block_tables, dirs, lens, q, scale: float, r_range=None, fills=None,
+              num_entries=None):
     """fp64 decode attention, out float64 [B][Hq][d] (rows outside r_range stay 0)."""
     sb, sh, ss, H, d, bs = _pool_geom(K)
     bt = _c(block_tables, np.int32)
@@ -156,6 +195,12 @@ def attention(K, V, block_tables, dirs, lens, q, scale: float, r_range=None):
     assert dq == d and Hq % H == 0
     out = np.zeros((B, Hq, d), dtype=np.float64)
     r0, r1 = (0, B) if r_range is None else r_range
+    if fills is not None:
+        f, frs, _ = _fills(fills, num_entries, B)
+        lib().bkvo_attention_f(_ptr(K), _ptr(V), sb, sh, ss, H, d, bs, _ptr(bt), int(bt.shape[1]),
+                               _ptr(dd), rs, cs, _ptr(f), frs, _ptr(ln), int(r0), int(r1), _ptr(qq),
+                               int(Hq), float(scale), _ptr(out))
+        return out
     lib().bkvo_attention(_ptr(K), _ptr(V), sb, sh, ss, H, d, bs, _ptr(bt), int(bt.shape[1]),
                          _ptr(dd), rs, cs, _ptr(ln), int(r0), int(r1), _ptr(qq), int(Hq),
                          float(scale), _ptr(out))

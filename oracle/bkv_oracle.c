@@ -303,6 +303,184 @@ int bkvo_overwritten_peers(int B, const int32_t *bt, int bt_stride, const uint8_
     return found;
 }
 
+/*
+ * ---------------------------------------------------------------------------
+ * General block map (reading Q6 option B).
+ *
+ * FindBlock places a BE prefill "according to the maximum number of empty
+ * slots" and FindPreemptBlock lets an RT request "write its KV cache
+ * from the opposite end" of a BE block, so any block -- not just a
+ * request's last -- may hold fewer than bs of the request's tokens.  The
+ * general map therefore carries, per block-table entry, the number of the
+ * request's tokens in it:
+ *     fills[r*frs + e] in 1..bs for e < nent[r]
+ * Tokens are numbered in entry order: entry e holds tokens
+ * [F_e, F_e + fills[e]) with F_e = fills[0] + ... + fills[e-1], and the j-th
+ * token of an entry sits at slot j (forward, RT) or bs-1-j (reversed, BE),
+ * exactly the in-block rule of P:711.  The request's length is F_{nent[r]}.
+ * With every non-last entry full this is the dense map above.
+ */
+static void locate_f(const int32_t *bt, int bt_stride, const uint8_t *dirs, int rs, int cs,
+                     const uint8_t *fills, int frs, int bs, int r, int64_t t,
+                     int32_t *blk, int *slot) {
+    int64_t e = 0, start = 0;
+    while (t >= start + fills[(int64_t)r * frs + e]) {   /* walk the entries in order */
+        start += fills[(int64_t)r * frs + e];
+        ++e;
+    }
+    int j = (int)(t - start);                            /* j-th token of entry e */
+    *blk = bt[(int64_t)r * bt_stride + e];
+    *slot = dir_of(dirs, rs, cs, r, (int)e) ? (bs - 1 - j) : j;
+}
+
+/*
+ * Validator of a general map: codes as bkvo_validate, plus (code 1, I4)
+ * nent[r] outside [0, bt_stride], a fill outside [1, bs] (info = r, e, fill),
+ * or lens[r] != sum of the fills (info = r, -1, lens[r], sum).
+ */
+int bkvo_validate_f(int B, const int32_t *bt, int bt_stride, const uint8_t *dirs, int rs, int cs,
+                    const uint8_t *fills, int frs, const int32_t *nent,
+                    const int32_t *lens, int num_blocks, int bs, int require_nonempty,
+                    int64_t *info) {
+    for (int k = 0; k < 4; ++k) info[k] = 0;
+    for (int r = 0; r < B; ++r) {
+        if (nent[r] < 0 || nent[r] > bt_stride) { info[0] = r; info[1] = -1; info[2] = nent[r]; return 1; }
+        int64_t sum = 0;
+        for (int e = 0; e < nent[r]; ++e) {
+            int f = fills[(int64_t)r * frs + e];
+            int32_t b = bt[(int64_t)r * bt_stride + e];
+            uint8_t d = dir_of(dirs, rs, cs, r, e);
+            if (f < 1 || f > bs) { info[0] = r; info[1] = e; info[2] = f; return 1; }
+            if (b < 0 || b >= num_blocks) { info[0] = r; info[1] = e; info[2] = b; return 1; }
+            if (d > 1) { info[0] = r; info[1] = e; info[2] = d; return 1; }
+            sum += f;
+        }
+        if (sum != lens[r] || (require_nonempty && lens[r] < 1)) {
+            info[0] = r; info[1] = -1; info[2] = lens[r]; info[3] = sum;
+            return 1;
+        }
+    }
+    int32_t *fwd_owner = malloc(sizeof(int32_t) * (size_t)num_blocks);
+    int32_t *rev_owner = malloc(sizeof(int32_t) * (size_t)num_blocks);
+    for (int b = 0; b < num_blocks; ++b) fwd_owner[b] = rev_owner[b] = -1;
+    int rc = 0;
+    for (int r = 0; r < B && !rc; ++r) {
+        for (int e = 0; e < nent[r]; ++e) {
+            int32_t b = bt[(int64_t)r * bt_stride + e];
+            uint8_t d = dir_of(dirs, rs, cs, r, e);
+            int32_t *own = d ? rev_owner : fwd_owner;
+            if (own[b] >= 0) { info[0] = b; info[1] = d; info[2] = own[b]; info[3] = r; rc = 3; break; }
+            own[b] = r;
+        }
+    }
+    free(fwd_owner); free(rev_owner);
+    if (rc) return rc;
+    int64_t nslots = (int64_t)num_blocks * bs;
+    int32_t *who_r = malloc(sizeof(int32_t) * (size_t)nslots);
+    int64_t *who_t = malloc(sizeof(int64_t) * (size_t)nslots);
+    for (int64_t s = 0; s < nslots; ++s) who_r[s] = -1;
+    for (int r = 0; r < B && !rc; ++r) {
+        for (int64_t t = 0; t < lens[r]; ++t) {
+            int32_t blk; int slot;
+            locate_f(bt, bt_stride, dirs, rs, cs, fills, frs, bs, r, t, &blk, &slot);
+            int64_t s = (int64_t)blk * bs + slot;
+            if (who_r[s] >= 0) {
+                info[0] = who_r[s]; info[1] = who_t[s]; info[2] = r; info[3] = t;
+                rc = 2; break;
+            }
+            who_r[s] = r; who_t[s] = t;
+        }
+    }
+    free(who_r); free(who_t);
+    return rc;
+}
+
+/* kv_append through a general map (same rule as bkvo_append, token located by locate_f). */
+void bkvo_append_f(uint16_t *K, uint16_t *V, int64_t sb, int64_t sh, int64_t ss,
+                   int H, int d, int bs,
+                   int B, const int32_t *bt, int bt_stride, const uint8_t *dirs, int rs, int cs,
+                   const uint8_t *fills, int frs,
+                   const int32_t *before, const int32_t *cu_new,
+                   const uint16_t *k_new, const uint16_t *v_new, int64_t *slot_mapping_out) {
+    for (int r = 0; r < B; ++r) {
+        for (int32_t i = cu_new[r]; i < cu_new[r + 1]; ++i) {
+            int64_t t = (int64_t)before[r] + (i - cu_new[r]);
+            int32_t blk; int slot;
+            locate_f(bt, bt_stride, dirs, rs, cs, fills, frs, bs, r, t, &blk, &slot);
+            for (int h = 0; h < H; ++h) {
+                int64_t dst = (int64_t)blk * sb + (int64_t)h * sh + (int64_t)slot * ss;
+                int64_t src = ((int64_t)i * H + h) * d;
+                memcpy(K + dst, k_new + src, sizeof(uint16_t) * (size_t)d);
+                memcpy(V + dst, v_new + src, sizeof(uint16_t) * (size_t)d);
+            }
+            if (slot_mapping_out) slot_mapping_out[i] = (int64_t)blk * bs + slot;
+        }
+    }
+}
+
+/* gather through a general map: dense logical-order K_r, V_r for t < L. */
+void bkvo_gather_f(const uint16_t *K, const uint16_t *V, int64_t sb, int64_t sh, int64_t ss,
+                   int H, int d, int bs,
+                   const int32_t *bt, int bt_stride, const uint8_t *dirs, int rs, int cs,
+                   const uint8_t *fills, int frs,
+                   int r, int64_t L, uint16_t *k_out, uint16_t *v_out) {
+    for (int64_t t = 0; t < L; ++t) {
+        int32_t blk; int slot;
+        locate_f(bt, bt_stride, dirs, rs, cs, fills, frs, bs, r, t, &blk, &slot);
+        for (int h = 0; h < H; ++h) {
+            int64_t src = (int64_t)blk * sb + (int64_t)h * sh + (int64_t)slot * ss;
+            memcpy(k_out + (t * H + h) * d, K + src, sizeof(uint16_t) * (size_t)d);
+            memcpy(v_out + (t * H + h) * d, V + src, sizeof(uint16_t) * (size_t)d);
+        }
+    }
+}
+
+/*
+ * Decode attention through a general map: gather_f, then exactly the fp64
+ * softmax attention of bkvo_attention (readings Q8, Q9).
+ */
+void bkvo_attention_f(const uint16_t *K, const uint16_t *V, int64_t sb, int64_t sh, int64_t ss,
+                      int H, int d, int bs,
+                      const int32_t *bt, int bt_stride, const uint8_t *dirs, int rs, int cs,
+                      const uint8_t *fills, int frs,
+                      const int32_t *lens, int r_begin, int r_end,
+                      const uint16_t *q, int Hq, double scale, double *out) {
+    int g = Hq / H;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int r = r_begin; r < r_end; ++r) {
+        int64_t L = lens[r];
+        double *o_r = out + (int64_t)r * Hq * d;
+        if (L <= 0) { memset(o_r, 0, sizeof(double) * (size_t)Hq * d); continue; }
+        uint16_t *kr = malloc(sizeof(uint16_t) * (size_t)(L * H * d));
+        uint16_t *vr = malloc(sizeof(uint16_t) * (size_t)(L * H * d));
+        double *s = malloc(sizeof(double) * (size_t)L);
+        bkvo_gather_f(K, V, sb, sh, ss, H, d, bs, bt, bt_stride, dirs, rs, cs, fills, frs, r, L, kr, vr);
+        for (int h = 0; h < Hq; ++h) {
+            int kv = h / g;
+            const uint16_t *qh = q + ((int64_t)r * Hq + h) * d;
+            double m = -INFINITY;
+            for (int64_t t = 0; t < L; ++t) {
+                const uint16_t *kt = kr + (t * H + kv) * d;
+                double acc = 0.0;
+                for (int i = 0; i < d; ++i) acc += bf16_to_f64(qh[i]) * bf16_to_f64(kt[i]);
+                s[t] = scale * acc;
+                if (s[t] > m) m = s[t];
+            }
+            double denom = 0.0;
+            double *oh = o_r + (int64_t)h * d;
+            for (int i = 0; i < d; ++i) oh[i] = 0.0;
+            for (int64_t t = 0; t < L; ++t) {
+                double p = exp(s[t] - m);
+                denom += p;
+                const uint16_t *vt = vr + (t * H + kv) * d;
+                for (int i = 0; i < d; ++i) oh[i] += p * bf16_to_f64(vt[i]);
+            }
+            for (int i = 0; i < d; ++i) oh[i] /= denom;
+        }
+        free(kr); free(vr); free(s);
+    }
+}
+
 int bkvo_num_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

@@ -36,7 +36,9 @@ class _Pool(ctypes.Structure):
 class _Map(ctypes.Structure):
     _fields_ = [("block_tables", ctypes.c_void_p), ("bt_stride", ctypes.c_int32),
                 ("dirs", ctypes.c_void_p), ("dir_row_stride", ctypes.c_int32),
-                ("dir_col_stride", ctypes.c_int32), ("num_seqs", ctypes.c_int32)]
+                ("dir_col_stride", ctypes.c_int32), ("num_seqs", ctypes.c_int32),
+                ("fills", ctypes.c_void_p), ("fill_row_stride", ctypes.c_int32),
+                ("num_entries", ctypes.c_void_p)]
 
 
 _lib = None
@@ -45,7 +47,7 @@ _lib_lock = threading.Lock()
 EXPORTS = ("bkv_kv_append", "bkv_paged_decode_attention", "bkv_decode_workspace_size",
            "bkv_validate_layout_host", "bkv_status_string", "bkv_last_error", "bkv_version",
            "bkv_kv_checkpoint", "bkv_kv_restore", "bkv_paged_decode_attention_ex",
-           "bkv_decode_step")
+           "bkv_decode_step", "bkv_validate_block_map_host", "bkv_kv_append_checkpoint")
 BKV_FLAG_PDL = 1   # include/bkv.h: programmatic dependent launch (seq_lens not written by the previous kernel)
 
 
@@ -61,6 +63,9 @@ def lib():
                 P, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
                 L.bkv_kv_append.argtypes = [ctypes.POINTER(_Pool), ctypes.POINTER(_Map), P, P, i32, P, P, P, P]
                 L.bkv_kv_append.restype = ctypes.c_int
+                L.bkv_kv_append_checkpoint.argtypes = [ctypes.POINTER(_Pool), ctypes.POINTER(_Map), P, P, i32,
+                                                       P, P, P, P, P, P, P]
+                L.bkv_kv_append_checkpoint.restype = ctypes.c_int
                 L.bkv_paged_decode_attention.argtypes = [
                     ctypes.POINTER(_Pool), ctypes.POINTER(_Map), P, i32, P, i64, i64, i32, ctypes.c_float,
                     P, i64, i64, P, ctypes.c_size_t, P]
@@ -77,6 +82,8 @@ def lib():
                 L.bkv_decode_workspace_size.restype = ctypes.c_size_t
                 L.bkv_validate_layout_host.argtypes = [P, i32, P, i32, i32, i32, P, i32, i32, i32, P]
                 L.bkv_validate_layout_host.restype = ctypes.c_int
+                L.bkv_validate_block_map_host.argtypes = [ctypes.POINTER(_Map), P, i32, i32, i32, P]
+                L.bkv_validate_block_map_host.restype = ctypes.c_int
                 L.bkv_kv_checkpoint.argtypes = [ctypes.POINTER(_Pool), P, i32, P, P, P]
                 L.bkv_kv_checkpoint.restype = ctypes.c_int
                 L.bkv_kv_restore.argtypes = [ctypes.POINTER(_Pool), P, i32, P, P, P]
@@ -142,8 +149,10 @@ class KVPool:
         return _Pool(self.k.data_ptr(), self.v.data_ptr(), nb, H, bs, d, sb, sh, ss)
 
 
-def block_map(block_tables: torch.Tensor, dirs: torch.Tensor) -> _Map:
-    """D2 + D3: int32 block tables [B][M]; uint8 dirs [B] (per request) or [B][M]."""
+def block_map(block_tables: torch.Tensor, dirs: torch.Tensor, fills=None, num_entries=None) -> _Map:
+    """D2 + D3: int32 block tables [B][M]; uint8 dirs [B] (per request) or [B][M].
+    General map: uint8 ``fills`` [B][M] (tokens per entry) and int32
+    ``num_entries`` [B]; both None for a dense map."""
     _dev(block_tables, "block_tables", torch.int32)
     _dev(dirs, "dirs", torch.uint8)
     if block_tables.dim() != 2 or block_tables.stride(1) != 1:
@@ -155,13 +164,23 @@ def block_map(block_tables: torch.Tensor, dirs: torch.Tensor) -> _Map:
         rs, cs = dirs.stride(0), dirs.stride(1)
     if dirs.shape[0] != B:
         raise BkvError("dirs must have one row per request")
-    return _Map(block_tables.data_ptr(), block_tables.stride(0), dirs.data_ptr(), rs, cs, B)
+    if (fills is None) != (num_entries is None):
+        raise BkvError("a general map needs both fills and num_entries")
+    if fills is None:
+        return _Map(block_tables.data_ptr(), block_tables.stride(0), dirs.data_ptr(), rs, cs, B,
+                    None, 0, None)
+    _dev(fills, "fills", torch.uint8)
+    _dev(num_entries, "num_entries", torch.int32)
+    if fills.dim() != 2 or fills.shape[0] != B or fills.stride(1) != 1 or num_entries.shape != (B,):
+        raise BkvError("fills must be [B][M] with unit column stride, num_entries [B]")
+    return _Map(block_tables.data_ptr(), block_tables.stride(0), dirs.data_ptr(), rs, cs, B,
+                fills.data_ptr(), fills.stride(0), num_entries.data_ptr())
 
 
 def kv_append(pool: KVPool, block_tables, dirs, seq_lens_before, cu_new_tokens, k_new, v_new,
-              slot_mapping=None, total_new_tokens=None, stream=None):
+              slot_mapping=None, total_new_tokens=None, stream=None, fills=None, num_entries=None):
     """bkv_kv_append: write new K/V rows [total_new][H][d] into their bidirectional slots."""
-    p, m = pool.c(), block_map(block_tables, dirs)
+    p, m = pool.c(), block_map(block_tables, dirs, fills, num_entries)
     _dev(seq_lens_before, "seq_lens_before", torch.int32)
     _dev(cu_new_tokens, "cu_new_tokens", torch.int32)
     _dev(k_new, "k_new", torch.bfloat16)
@@ -176,6 +195,35 @@ def kv_append(pool: KVPool, block_tables, dirs, seq_lens_before, cu_new_tokens, 
                              cu_new_tokens.data_ptr(), n, k_new.data_ptr(), v_new.data_ptr(),
                              ctypes.c_void_p(sm), _stream_ptr(stream))
     _check(rc, "bkv_kv_append")
+
+
+def kv_append_checkpoint(pool: KVPool, block_tables, dirs, seq_lens_before, cu_new_tokens, k_new, v_new,
+                         evict_rows, ckpt_k, ckpt_v, slot_mapping=None, total_new_tokens=None,
+                         stream=None, fills=None, num_entries=None):
+    """bkv_kv_append_checkpoint: kv_append that first copies the live peer rows it overwrites
+    (evict_rows[i] >= 0 -> row evict_rows[i] of ckpt_k/ckpt_v, bf16 [rows][H][d]) -- the
+    lazy checkpoint of PAPER.md P:726-728, fused into the write."""
+    p, m = pool.c(), block_map(block_tables, dirs, fills, num_entries)
+    for t, n in ((seq_lens_before, "seq_lens_before"), (cu_new_tokens, "cu_new_tokens"),
+                 (evict_rows, "evict_rows")):
+        _dev(t, n, torch.int32)
+    for t, n in ((k_new, "k_new"), (v_new, "v_new"), (ckpt_k, "ckpt_k"), (ckpt_v, "ckpt_v")):
+        if n.startswith("ckpt") and not t.is_cuda:
+            if not t.is_pinned():   # pinned host memory is device-addressable under UVA
+                raise BkvError(f"{n} must be a CUDA tensor or pinned host memory")
+            if t.dtype != torch.bfloat16:
+                raise BkvError(f"{n} must be bfloat16")
+        else:
+            _dev(t, n, torch.bfloat16)
+        if not t.is_contiguous():
+            raise BkvError(f"{n} must be contiguous")
+    n = k_new.shape[0] if total_new_tokens is None else int(total_new_tokens)
+    sm = 0 if slot_mapping is None else _dev(slot_mapping, "slot_mapping", torch.int64).data_ptr()
+    rc = lib().bkv_kv_append_checkpoint(ctypes.byref(p), ctypes.byref(m), seq_lens_before.data_ptr(),
+                                        cu_new_tokens.data_ptr(), n, k_new.data_ptr(), v_new.data_ptr(),
+                                        ctypes.c_void_p(sm), evict_rows.data_ptr(), ckpt_k.data_ptr(),
+                                        ckpt_v.data_ptr(), _stream_ptr(stream))
+    _check(rc, "bkv_kv_append_checkpoint")
 
 
 def kv_checkpoint(pool: KVPool, slot_ids, k_out=None, v_out=None, stream=None):
@@ -229,8 +277,9 @@ def workspace(num_seqs, num_q_heads, num_kv_heads, head_dim, device=None, stream
     return ws
 
 
-def _attn_args(pool, block_tables, dirs, seq_lens, q, softmax_scale, out, max_seq_len, ws, stream):
-    p, m = pool.c(), block_map(block_tables, dirs)
+def _attn_args(pool, block_tables, dirs, seq_lens, q, softmax_scale, out, max_seq_len, ws, stream,
+               fills=None, num_entries=None):
+    p, m = pool.c(), block_map(block_tables, dirs, fills, num_entries)
     _dev(seq_lens, "seq_lens", torch.int32)
     _dev(q, "q", torch.bfloat16)
     B, Hq, d = q.shape
@@ -251,11 +300,13 @@ def _attn_args(pool, block_tables, dirs, seq_lens, q, softmax_scale, out, max_se
 
 
 def paged_decode_attention(pool: KVPool, block_tables, dirs, seq_lens, q, softmax_scale=None,
-                           out=None, max_seq_len=None, ws=None, stream=None, pdl=False):
+                           out=None, max_seq_len=None, ws=None, stream=None, pdl=False,
+                           fills=None, num_entries=None):
     """bkv_paged_decode_attention.  q: bf16 [B][Hq][d] (any strides with unit last stride).
-    out: bf16 with the same indexing (allocated [B][Hq][d] if None).  Returns out."""
+    out: bf16 with the same indexing (allocated [B][Hq][d] if None).  Returns out.
+    ``fills``/``num_entries``: general map."""
     p, m, out, scale, msl, ws = _attn_args(pool, block_tables, dirs, seq_lens, q, softmax_scale,
-                                           out, max_seq_len, ws, stream)
+                                           out, max_seq_len, ws, stream, fills, num_entries)
     rc = lib().bkv_paged_decode_attention_ex(
         ctypes.byref(p), ctypes.byref(m), seq_lens.data_ptr(), int(msl), q.data_ptr(),
         q.stride(0), q.stride(1), q.shape[1], float(scale), out.data_ptr(), out.stride(0),
@@ -265,12 +316,13 @@ def paged_decode_attention(pool: KVPool, block_tables, dirs, seq_lens, q, softma
 
 
 def decode_step(pool: KVPool, block_tables, dirs, seq_lens, k_new, v_new, q, softmax_scale=None,
-                out=None, max_seq_len=None, ws=None, stream=None, pdl=False):
+                out=None, max_seq_len=None, ws=None, stream=None, pdl=False, fills=None,
+                num_entries=None):
     """bkv_decode_step: append token seq_lens[r]-1 of every request (k_new/v_new contiguous
     bf16 [B][H_kv][d]) and attend over the context including it, in one launch pair.
     Equal to kv_append(before=seq_lens-1, cu=arange(B+1)) + paged_decode_attention."""
     p, m, out, scale, msl, ws = _attn_args(pool, block_tables, dirs, seq_lens, q, softmax_scale,
-                                           out, max_seq_len, ws, stream)
+                                           out, max_seq_len, ws, stream, fills, num_entries)
     _dev(k_new, "k_new", torch.bfloat16)
     _dev(v_new, "v_new", torch.bfloat16)
     shape = (q.shape[0], pool.num_kv_heads, pool.head_dim)
@@ -300,4 +352,31 @@ def validate_layout_host(block_tables, dirs, seq_lens, num_blocks, block_size, r
                                         int(bool(require_nonempty)), info.ctypes.data)
     if rc not in (0, 4):
         _check(rc, "bkv_validate_layout_host")
+    return rc == 0, [int(x) for x in info]
+
+
+def validate_block_map_host(block_tables, dirs, seq_lens, num_blocks, block_size, fills=None,
+                            num_entries=None, require_nonempty=True):
+    """bkv_validate_block_map_host on host arrays (dense, or general with fills/num_entries).
+    Returns (ok, info[5])."""
+    import numpy as np
+    bt = np.ascontiguousarray(np.asarray(block_tables), dtype=np.int32)
+    dd = np.ascontiguousarray(np.asarray(dirs), dtype=np.uint8)
+    ln = np.ascontiguousarray(np.asarray(seq_lens), dtype=np.int32)
+    rs, cs = (1, 0) if dd.ndim == 1 else (dd.shape[1], 1)
+    keep = [bt, dd, ln]
+    if fills is None:
+        m = _Map(bt.ctypes.data, bt.shape[1], dd.ctypes.data, rs, cs, ln.shape[0], None, 0, None)
+    else:
+        f = np.ascontiguousarray(np.asarray(fills), dtype=np.uint8)
+        ne = np.ascontiguousarray(np.asarray(num_entries), dtype=np.int32)
+        keep += [f, ne]
+        m = _Map(bt.ctypes.data, bt.shape[1], dd.ctypes.data, rs, cs, ln.shape[0], f.ctypes.data,
+                 f.shape[1], ne.ctypes.data)
+    info = np.zeros(5, dtype=np.int64)
+    rc = lib().bkv_validate_block_map_host(ctypes.byref(m), ln.ctypes.data, int(num_blocks),
+                                           int(block_size), int(bool(require_nonempty)), info.ctypes.data)
+    del keep
+    if rc not in (0, 4):
+        _check(rc, "bkv_validate_block_map_host")
     return rc == 0, [int(x) for x in info]

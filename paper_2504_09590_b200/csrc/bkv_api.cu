@@ -57,6 +57,12 @@ bkv_status check_map(const bkv_block_map *map) {
   if (map->bt_stride <= 0) return fail(BKV_ERR_INVALID_ARGUMENT, "bt_stride must be positive");
   if (map->dir_row_stride < 0 || map->dir_col_stride < 0)
     return fail(BKV_ERR_INVALID_ARGUMENT, "direction strides must be >= 0");
+  if (map->fills) {   // general map
+    if (map->num_seqs > 0 && !map->num_entries)
+      return fail(BKV_ERR_INVALID_ARGUMENT, "general map: num_entries is NULL");
+    if (map->fill_row_stride < 0)
+      return fail(BKV_ERR_INVALID_ARGUMENT, "general map: fill_row_stride < 0");
+  }
   return BKV_OK;
 }
 
@@ -145,12 +151,13 @@ const char *bkv_status_string(bkv_status s) {
 
 const char *bkv_last_error(void) { return g_err; }
 
-int32_t bkv_version(void) { return 100; }
+int32_t bkv_version(void) { return 200; }
 
-bkv_status bkv_kv_append(const bkv_kv_pool *pool, const bkv_block_map *map,
-                         const int32_t *seq_lens_before, const int32_t *cu_new_tokens,
-                         int32_t total_new_tokens, const void *k_new, const void *v_new,
-                         int64_t *slot_mapping_out, bkv_stream_t stream) {
+static bkv_status append_impl(const bkv_kv_pool *pool, const bkv_block_map *map,
+                              const int32_t *seq_lens_before, const int32_t *cu_new_tokens,
+                              int32_t total_new_tokens, const void *k_new, const void *v_new,
+                              int64_t *slot_mapping_out, const int32_t *evict_rows, void *ckpt_k,
+                              void *ckpt_v, bkv_stream_t stream) {
   bkv_status s = check_pool(pool);
   if (s) return s;
   if ((s = check_map(map))) return s;
@@ -181,9 +188,41 @@ bkv_status bkv_kv_append(const bkv_kv_pool *pool, const bkv_block_map *map,
   p.v_new = static_cast<const uint16_t *>(v_new);
   p.slot_mapping = slot_mapping_out;
   p.B = map->num_seqs;
+  p.fills = map->fills;
+  p.fill_rs = map->fill_row_stride;
+  p.nent = map->num_entries;
+  p.max_entries = map->bt_stride;
+  if (p.fills && map->bt_stride > bkv::kMaxEntries)
+    return fail(BKV_ERR_UNSUPPORTED, "general map: bt_stride %d > %d", map->bt_stride, bkv::kMaxEntries);
+  p.evict = evict_rows;
+  p.ck_k = static_cast<uint16_t *>(ckpt_k);
+  p.ck_v = static_cast<uint16_t *>(ckpt_v);
   cudaError_t e = bkv::launch_kv_append(p, pool->head_dim, reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "kv_append launch");
   return BKV_OK;
+}
+
+bkv_status bkv_kv_append(const bkv_kv_pool *pool, const bkv_block_map *map,
+                         const int32_t *seq_lens_before, const int32_t *cu_new_tokens,
+                         int32_t total_new_tokens, const void *k_new, const void *v_new,
+                         int64_t *slot_mapping_out, bkv_stream_t stream) {
+  return append_impl(pool, map, seq_lens_before, cu_new_tokens, total_new_tokens, k_new, v_new,
+                     slot_mapping_out, nullptr, nullptr, nullptr, stream);
+}
+
+bkv_status bkv_kv_append_checkpoint(const bkv_kv_pool *pool, const bkv_block_map *map,
+                                    const int32_t *seq_lens_before, const int32_t *cu_new_tokens,
+                                    int32_t total_new_tokens, const void *k_new, const void *v_new,
+                                    int64_t *slot_mapping_out, const int32_t *evict_rows,
+                                    void *ckpt_k, void *ckpt_v, bkv_stream_t stream) {
+  if (total_new_tokens > 0 && map && map->num_seqs > 0) {
+    if (!evict_rows || !ckpt_k || !ckpt_v)
+      return fail(BKV_ERR_INVALID_ARGUMENT, "evict_rows/ckpt_k/ckpt_v is NULL");
+    if (!aligned16(ckpt_k) || !aligned16(ckpt_v))
+      return fail(BKV_ERR_INVALID_ARGUMENT, "ckpt_k/ckpt_v must be 16-byte aligned");
+  }
+  return append_impl(pool, map, seq_lens_before, cu_new_tokens, total_new_tokens, k_new, v_new,
+                     slot_mapping_out, evict_rows, ckpt_k, ckpt_v, stream);
 }
 
 static bkv_status slot_copy(const bkv_kv_pool *pool, const int64_t *slot_ids, int32_t n, void *kb,
@@ -304,6 +343,9 @@ static bkv_status decode_impl(const bkv_kv_pool *pool, const bkv_block_map *map,
   p.dir_rs = map->dir_row_stride;
   p.dir_cs = map->dir_col_stride;
   p.seq_lens = seq_lens;
+  p.fills = map->fills;
+  p.fill_rs = map->fill_row_stride;
+  p.nent = map->num_entries;
   p.B = B;
   p.H = H;
   p.bs = pool->block_size;
@@ -432,6 +474,88 @@ bkv_status bkv_validate_layout_host(const int32_t *block_tables, int32_t bt_stri
       }
       occ_r[k] = r;
       occ_t[k] = t;
+    }
+  }
+  return BKV_OK;
+}
+
+bkv_status bkv_validate_block_map_host(const bkv_block_map *map, const int32_t *seq_lens,
+                                       int32_t num_blocks, int32_t block_size,
+                                       int32_t require_nonempty, int64_t info[5]) {
+  if (!map) return fail(BKV_ERR_INVALID_ARGUMENT, "map is NULL");
+  if (!map->fills)
+    return bkv_validate_layout_host(map->block_tables, map->bt_stride, map->dirs,
+                                    map->dir_row_stride, map->dir_col_stride, map->num_seqs,
+                                    seq_lens, num_blocks, block_size, require_nonempty, info);
+  if (!info) return fail(BKV_ERR_INVALID_ARGUMENT, "info is NULL");
+  for (int i = 0; i < 5; ++i) info[i] = 0;
+  const int B = map->num_seqs, bt_stride = map->bt_stride;
+  if (B < 0 || block_size <= 0 || block_size > 255 || num_blocks < 0 || bt_stride <= 0 ||
+      map->fill_row_stride < 0)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "bad sizes");
+  if (B > 0 && (!map->block_tables || !map->dirs || !map->num_entries || !seq_lens))
+    return fail(BKV_ERR_INVALID_ARGUMENT, "NULL input");
+  auto entry = [&](int r, int e) { return map->block_tables[(int64_t)r * bt_stride + e]; };
+  auto dir = [&](int r, int e) {
+    return map->dirs[(int64_t)r * map->dir_row_stride + (int64_t)e * map->dir_col_stride];
+  };
+  auto fill = [&](int r, int e) { return (int)map->fills[(int64_t)r * map->fill_row_stride + e]; };
+  // I4: ranges, fills, lengths = sum of fills
+  for (int r = 0; r < B; ++r) {
+    const int E = map->num_entries[r];
+    if (E < 0 || E > bt_stride) {
+      info[0] = 1; info[1] = r; info[2] = -1; info[3] = E;
+      return fail(BKV_ERR_LAYOUT, "I4: num_entries %d of request %d out of range", E, r);
+    }
+    int64_t sum = 0;
+    for (int e = 0; e < E; ++e) {
+      if (fill(r, e) < 1 || fill(r, e) > block_size) {
+        info[0] = 1; info[1] = r; info[2] = e; info[3] = fill(r, e);
+        return fail(BKV_ERR_LAYOUT, "I4: fill %d of entry %d of request %d outside [1, %d]",
+                    fill(r, e), e, r, block_size);
+      }
+      if (entry(r, e) < 0 || entry(r, e) >= num_blocks || dir(r, e) > 1) {
+        info[0] = 1; info[1] = r; info[2] = e; info[3] = entry(r, e);
+        return fail(BKV_ERR_LAYOUT, "I4: entry %d of request %d invalid", e, r);
+      }
+      sum += fill(r, e);
+    }
+    if (sum != seq_lens[r] || (require_nonempty && seq_lens[r] == 0)) {
+      info[0] = 1; info[1] = r; info[2] = -2; info[3] = seq_lens[r];
+      return fail(BKV_ERR_LAYOUT, "I4: seq_len %d of request %d != sum of its fills %lld (or empty)",
+                  seq_lens[r], r, (long long)sum);
+    }
+  }
+  // I2: at most one forward and one reversed entry per physical block
+  std::vector<int32_t> fwd(num_blocks, -1), rev(num_blocks, -1);
+  for (int r = 0; r < B; ++r) {
+    for (int e = 0; e < map->num_entries[r]; ++e) {
+      std::vector<int32_t> &own = dir(r, e) ? rev : fwd;
+      const int32_t b = entry(r, e);
+      if (own[b] >= 0) {
+        info[0] = 3; info[1] = b; info[2] = dir(r, e); info[3] = own[b]; info[4] = r;
+        return fail(BKV_ERR_LAYOUT, "I2: block %d has two %s entries", b, dir(r, e) ? "reversed" : "forward");
+      }
+      own[b] = r;
+    }
+  }
+  // I1: entry e covers slots [0, n_e) forward or [bs-n_e, bs) reversed
+  std::vector<int32_t> occ_r((size_t)num_blocks * block_size, -1);
+  std::vector<int64_t> occ_t((size_t)num_blocks * block_size, 0);
+  for (int r = 0; r < B; ++r) {
+    int64_t t = 0;
+    for (int e = 0; e < map->num_entries[r]; ++e) {
+      for (int j = 0; j < fill(r, e); ++j, ++t) {
+        const int slot = dir(r, e) ? block_size - 1 - j : j;
+        const size_t k = (size_t)entry(r, e) * block_size + slot;
+        if (occ_r[k] >= 0) {
+          info[0] = 2; info[1] = occ_r[k]; info[2] = occ_t[k]; info[3] = r; info[4] = t;
+          return fail(BKV_ERR_LAYOUT, "I1: token %lld of request %d and token %lld of request %d share a slot",
+                      (long long)occ_t[k], occ_r[k], (long long)t, r);
+        }
+        occ_r[k] = r;
+        occ_t[k] = t;
+      }
     }
   }
   return BKV_OK;

@@ -22,6 +22,15 @@ struct AppendParams {
   const uint16_t *k_new, *v_new;
   int64_t *slot_mapping;  // optional
   int B;
+  // general map: per-entry fill counts; nullptr for a dense map
+  const uint8_t *fills;
+  int fill_rs;
+  const int32_t *nent;
+  int max_entries;        // bt_stride: sizes the per-CTA prefix table in shared memory
+  // fused lazy checkpoint: evict[i] >= 0 -> the old rows of new
+  // token i's slot go to row evict[i] of ck_k / ck_v before the overwrite
+  const int32_t *evict;
+  uint16_t *ck_k, *ck_v;
 };
 cudaError_t launch_kv_append(const AppendParams &p, int head_dim, cudaStream_t s);
 
@@ -44,6 +53,9 @@ struct DecodeParams {
   const uint8_t *dirs;
   int dir_rs, dir_cs;
   const int32_t *seq_lens;
+  const uint8_t *fills;  // general map (f3): entry fill counts, nullptr for a dense map
+  int fill_rs;
+  const int32_t *nent;   // general map: entries per request
   int B, H, bs, g;
   const uint16_t *q;
   int64_t q_ss, q_sh;
@@ -85,5 +97,6 @@ cudaError_t launch_decode(const CUtensorMap &tmK, const CUtensorMap &tmV, const 
 constexpr int kMaxSeqs = 2048;  // plan arrays live in shared memory
 constexpr int kMaxGroup = 16;   // GQA rows per MMA tile
 constexpr int kMaxKvHeads = 128; // per rank; sizes the fixed counter region of the workspace
+constexpr int kMaxEntries = 16384; // general-map append: per-request prefix table in shared memory
 
 }  // namespace bkv

@@ -101,7 +101,13 @@ __device__ __forceinline__ int bucket_of(int s, int P) {
   return 4 * s > 3 * P ? 0 : (2 * s > P ? 1 : (4 * s > P ? 2 : 3));
 }
 
-__device__ void compute_plan(const DecodeParams &p, int *Pre, int *Lsm, Plan *plan) {
+// Entries (blocks) of request r: ceil(L/bs) for a dense map, num_entries[r]
+// for a general one.
+__device__ __forceinline__ int entries_of(const DecodeParams &p, int r, int L) {
+  return p.fills ? __ldg(p.nent + r) : nblocks_of(L, p.bs);
+}
+
+__device__ void compute_plan(const DecodeParams &p, int *Pre, int *Lsm, int *NBsm, Plan *plan) {
   __shared__ long long red_ll[32];
   __shared__ int4 red4[32];
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5,
@@ -110,8 +116,10 @@ __device__ void compute_plan(const DecodeParams &p, int *Pre, int *Lsm, Plan *pl
   long long local = 0;
   for (int r = tid; r < B; r += nt) {
     const int L = __ldg(p.seq_lens + r);
+    const int nb = entries_of(p, r, L);
     Lsm[r] = L;
-    local += nblocks_of(L, p.bs);
+    NBsm[r] = nb;
+    local += nb;
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
@@ -128,7 +136,7 @@ __device__ void compute_plan(const DecodeParams &p, int *Pre, int *Lsm, Plan *pl
   const int r0 = min(B, tid * per), r1 = min(B, r0 + per);
   int4 cnt = make_int4(0, 0, 0, 0);
   for (int r = r0; r < r1; ++r) {
-    const int nb = nblocks_of(Lsm[r], p.bs);
+    const int nb = NBsm[r];
     const int n = nb > 0 ? (nb + P - 1) / P : 1;
     const int bk = bucket_of((nb + n - 1) / n, P);
     cnt.x += bk == 0 ? n : 0;
@@ -162,7 +170,7 @@ __device__ void compute_plan(const DecodeParams &p, int *Pre, int *Lsm, Plan *pl
     Pre[1 * (B + 1) + r] = e.y;
     Pre[2 * (B + 1) + r] = e.z;
     Pre[3 * (B + 1) + r] = e.w;
-    const int nb = nblocks_of(Lsm[r], p.bs);
+    const int nb = NBsm[r];
     const int n = nb > 0 ? (nb + P - 1) / P : 1;
     const int bk = bucket_of((nb + n - 1) / n, P);
     e.x += bk == 0 ? n : 0;
@@ -223,6 +231,7 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
   const uint32_t my_patch = smem_u32(patch_g + warp * S * 512);
   int *Pre = reinterpret_cast<int *>(patch_g + W * S * 512);  // [kBuckets][B + 1]
   int *Lsm = Pre + kBuckets * (p.B + 1);                      // seq_lens cache [B]
+  int *NBsm = Lsm + ((p.B + 3) & ~3);                         // entries per request [B]
 
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmK);
@@ -241,7 +250,7 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
     }
   };
   trace(0, -1);
-  compute_plan(p, Pre, Lsm, &plan);
+  compute_plan(p, Pre, Lsm, NBsm, &plan);
   // PDL: everything above read only seq_lens; wait for the preceding kernel
   // (it may have written the pool / q) before touching anything else.
   if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -281,7 +290,7 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
     return u;
   };
   struct UnitInfo {
-    int u, r, h, L, n, e0, e1;
+    int u, r, h, L, nb, n, e0, e1;
   };
   auto decode_unit = [&](int u) -> UnitInfo {
     UnitInfo x;
@@ -295,28 +304,31 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
     const int *pk = Pre + k * (p.B + 1);
     x.r = search_le(pk, p.B, j);
     x.L = Lsm[x.r];
-    const int nb = nblocks_of(x.L, bs);
+    const int nb = NBsm[x.r];
+    x.nb = nb;
     x.n = nb > 0 ? (nb + P - 1) / P : 1;
     const int sidx = j - pk[x.r];
     x.e0 = static_cast<int>(static_cast<long long>(sidx) * nb / x.n);
     x.e1 = static_cast<int>(static_cast<long long>(sidx + 1) * nb / x.n);
     return x;
   };
-  // window of 32 block-table/direction entries starting at block wb (lane i: entry wb + i)
-  auto load_window = [&](const UnitInfo &x, int wb, int &btv, int &dirv) {
+  // window of 32 block-table/direction(/fill) entries starting at block wb (lane i: entry wb + i)
+  auto load_window = [&](const UnitInfo &x, int wb, int &btv, int &dirv, int &filv) {
     const int ew = wb + lane;
     btv = 0;
     dirv = 0;
+    filv = 0;
     if (x.u < U && ew < x.e1) {
       btv = __ldg(p.bt + static_cast<int64_t>(x.r) * p.bt_stride + ew);
       dirv = __ldg(p.dirs + static_cast<int64_t>(x.r) * p.dir_rs + static_cast<int64_t>(ew) * p.dir_cs);
+      if (p.fills) filv = __ldg(p.fills + static_cast<int64_t>(x.r) * p.fill_rs + ew);
     }
   };
   UnitInfo cur{}, nxt = decode_unit(pull_unit());
-  int nx_bt = 0, nx_dir = 0;
-  load_window(nxt, nxt.e0, nx_bt, nx_dir);
+  int nx_bt = 0, nx_dir = 0, nx_fil = 0;
+  load_window(nxt, nxt.e0, nx_bt, nx_dir, nx_fil);
   bool is_active = false, is_done = false, is_first = false;
-  int is_ci = 0, is_nc = 0, is_wb = 0, bt_w = 0, dir_w = 0;
+  int is_ci = 0, is_nc = 0, is_wb = 0, bt_w = 0, dir_w = 0, fil_w = 0;
 
   // Produce the next chunk of this warp's work stream (warp-collective).
   // Chunk ci of a unit = 16 slots (sub-chunk ci % cpb) of block e0 + ci / cpb;
@@ -330,9 +342,10 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
       cur = nxt;
       bt_w = nx_bt;
       dir_w = nx_dir;
+      fil_w = nx_fil;
       is_wb = cur.e0;
-      nxt = decode_unit(pull_unit());             // look one unit ahead ...
-      load_window(nxt, nxt.e0, nx_bt, nx_dir);    // ... its loads overlap this unit
+      nxt = decode_unit(pull_unit());                     // look one unit ahead ...
+      load_window(nxt, nxt.e0, nx_bt, nx_dir, nx_fil);    // ... its loads overlap this unit
       if (lane < g) {   // the unit's q rows: pull into L2 now, the consumer loads them later
         const uint16_t *qrow = p.q + static_cast<int64_t>(cur.r) * p.q_ss +
                                static_cast<int64_t>(cur.h * g + lane) * p.q_sh;
@@ -355,20 +368,24 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
     const int c = chunks_per_block == 1 ? 0 : (is_ci & 1);
     if (e - is_wb >= 32) {  // long unit: refill the window (rare)
       is_wb = e;
-      load_window(cur, e, bt_w, dir_w);
+      load_window(cur, e, bt_w, dir_w, fil_w);
     }
     const int idx = e - is_wb;
     const int b = __shfl_sync(FULL, bt_w, idx);
     const int dr = __shfl_sync(FULL, dir_w, idx);
-    const int ne = min(bs, cur.L - e * bs);          // live tokens in this block
+    const int fl = __shfl_sync(FULL, fil_w, idx);
+    // live tokens in this block: dense map -> all but the last entry full;
+    // general map (f3) -> the entry's fill count
+    const int ne = p.fills ? fl : min(bs, cur.L - e * bs);
     const int lo_s = dr ? bs - ne : 0;               // RT from the left,
     const int hi_s = dr ? bs : ne;                   //        BE from the right
     const int lo = max(lo_s - c * 16, 0), hi = min(hi_s - c * 16, 16);
     int flags = (is_first ? F_FIRST : 0) | (lo >= hi ? F_NOKV : 0);
-    if (p.k_new != nullptr && e == (cur.L - 1) / bs) {
-      // fused decode step: token t = L-1 of (r, h) lands in
-      // this block, in its direction's slot; this warp alone owns it.
-      const int j = (cur.L - 1) - e * bs;
+    if (p.k_new != nullptr && e == cur.nb - 1) {
+      // fused decode step: token t = L-1 of (r, h) is the
+      // last token of the last entry, in its direction's slot; this
+      // warp alone owns it.
+      const int j = ne - 1;
       const int slot_new = dr ? bs - 1 - j : j;
       if ((slot_new >> 4) == c) flags |= F_NEW | (slot_new << 8);
     }
@@ -821,7 +838,7 @@ __global__ void __launch_bounds__(256) merge_kernel(const DecodeParams p) {
   const int r = rh / H, h = rh - r * H;
   const int P = p.plan_out[0];
   const int L = __ldg(p.seq_lens + r);
-  const int nb = nblocks_of(L, p.bs);
+  const int nb = entries_of(p, r, L);
   const int ns = nb > 0 ? (nb + P - 1) / P : 1;
   if (ns <= 1) return;
   const int k = bucket_of((nb + ns - 1) / ns, P);
@@ -936,7 +953,7 @@ cudaError_t decode_config(int head_dim, int group, int num_seqs, DecodeLaunch *c
   const int qb = 0;   // q is read from global (L2-prefetched), no shared-memory ring
   auto need = [&](int w, int s) {
     return 1024 + w * s * slot_bytes + w * s * (int)(sizeof(int) * 8) + w * s * 8 + w * 1024 + w * s * 512 +
-           4 * (num_seqs + 1) * (int)sizeof(int) + ((num_seqs + 3) & ~3) * 4 + 256;
+           4 * (num_seqs + 1) * (int)sizeof(int) + 2 * ((num_seqs + 3) & ~3) * 4 + 256;
   };
   const bool mma = group > 1 || mha_on_mma();
   int W = env_int("BKV_WARPS", mma ? 8 : 12);   // measured best: MMA kernels 8, CUDA-core MHA 12

@@ -14,6 +14,22 @@
 
 namespace bkv {
 
+// Fused lazy checkpoint ("only the KV tensors of a
+// specific request that are about to be overwritten by its peer need to be
+// checkpointed"): before new token i's row replaces a live peer row, the SAME
+// thread copies the old 16 bytes out to checkpoint row evict[i] (device memory
+// or the device alias of mapped pinned host memory), so program order alone
+// orders the read before the overwrite.
+template <int D>
+__device__ __forceinline__ void evict_row(const AppendParams &p, int i, int h, int which, int sub,
+                                          const uint16_t *slot_row) {
+  const int er = __ldg(p.evict + i);
+  if (er < 0) return;
+  const uint4 old = *reinterpret_cast<const uint4 *>(slot_row);
+  uint16_t *ck = which ? p.ck_v : p.ck_k;
+  *reinterpret_cast<uint4 *>(ck + (static_cast<int64_t>(er) * p.H + h) * D + sub * 8) = old;
+}
+
 template <int D>
 __global__ void __launch_bounds__(256) kv_append_kernel(AppendParams p) {
   constexpr int TPR = D / 8;  // threads per row, 16 B each
@@ -45,14 +61,110 @@ __global__ void __launch_bounds__(256) kv_append_kernel(AppendParams p) {
     const uint16_t *s = which ? p.v_new : p.k_new;
     uint16_t *d = which ? p.v : p.k;
     const uint4 val = __ldg(reinterpret_cast<const uint4 *>(s + src));
+    if (p.evict) evict_row<D>(p, first + j, h, which, sub, d + dst);
     *reinterpret_cast<uint4 *>(d + dst) = val;
     if (p.slot_mapping && which == 0 && h == 0 && sub == 0)
       p.slot_mapping[first + j] = static_cast<int64_t>(blk) * p.bs + slot;
   }
 }
 
+// General map: entry e of request r holds n_e = fills[e]
+// tokens, numbered in entry order, the j-th at slot j (forward) or bs-1-j
+// (reversed).  The CTA builds the exclusive prefix F_e of
+// the request's fills in shared memory (a block scan, 256 entries per pass);
+// new token t then lives in the entry with F_e <= t < F_{e+1} (binary search),
+// at j = t - F_e.  Copies as above: bit-exact, nothing else written.
+template <int D>
+__global__ void __launch_bounds__(256) kv_append_general_kernel(AppendParams p) {
+  constexpr int TPR = D / 8;
+  extern __shared__ int F[];   // [E + 1] exclusive prefix of the fills
+  __shared__ int wsum[8];
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int r = blockIdx.x;
+  const int32_t first = p.cu_new[r];
+  const int n = p.cu_new[r + 1] - first;
+  if (n <= 0) return;
+  const int E = p.nent[r];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint8_t *fr = p.fills + static_cast<int64_t>(r) * p.fill_rs;
+  int carry = 0;
+  for (int base = 0; base < E; base += 256) {
+    const int e = base + static_cast<int>(threadIdx.x);
+    const int v = e < E ? static_cast<int>(__ldg(fr + e)) : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    int before_w = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      before_w += w < warp ? wsum[w] : 0;
+      tot += wsum[w];
+    }
+    if (e < E) F[e] = carry + before_w + x - v;
+    carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) F[E] = carry;
+  __syncthreads();
+  const int before = p.before[r];
+  const int sub = threadIdx.x % TPR;
+  const int rows = n * p.H * 2;
+  const int64_t bt_row = static_cast<int64_t>(r) * p.bt_stride;
+  const int64_t dir_row = static_cast<int64_t>(r) * p.dir_rs;
+  for (int row = threadIdx.x / TPR; row < rows; row += blockDim.x / TPR) {
+    const int j = row / (2 * p.H);
+    const int rem = row - j * 2 * p.H;
+    const int which = rem / p.H;
+    const int h = rem - which * p.H;
+    const int t = before + j;
+    int lo = 0, hi = E - 1;   // largest e in [0, E) with F[e] <= t
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (F[mid] <= t)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    const int e = lo;
+    const int within = t - F[e];
+    const int32_t blk = __ldg(p.bt + bt_row + e);
+    const uint8_t dir = __ldg(p.dirs + dir_row + static_cast<int64_t>(e) * p.dir_cs);
+    const int slot = dir ? (p.bs - 1 - within) : within;
+    const int64_t src = (static_cast<int64_t>(first + j) * p.H + h) * D + sub * 8;
+    const int64_t dst = static_cast<int64_t>(blk) * p.sb + static_cast<int64_t>(h) * p.sh +
+                        static_cast<int64_t>(slot) * p.ss + sub * 8;
+    const uint16_t *s = which ? p.v_new : p.k_new;
+    uint16_t *d = which ? p.v : p.k;
+    const uint4 val = __ldg(reinterpret_cast<const uint4 *>(s + src));
+    if (p.evict) evict_row<D>(p, first + j, h, which, sub, d + dst);
+    *reinterpret_cast<uint4 *>(d + dst) = val;
+    if (p.slot_mapping && which == 0 && h == 0 && sub == 0)
+      p.slot_mapping[first + j] = static_cast<int64_t>(blk) * p.bs + slot;
+  }
+}
+
+template <int D>
+static cudaError_t launch_general(const AppendParams &p, cudaStream_t s) {
+  static int configured = 0;   // dynamic smem already granted
+  const int smem = 4 * (p.max_entries + 1);
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(kv_append_general_kernel<D>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  kv_append_general_kernel<D><<<p.B, 256, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_kv_append(const AppendParams &p, int head_dim, cudaStream_t s) {
   if (p.B <= 0) return cudaSuccess;
+  if (p.fills) return head_dim == 128 ? launch_general<128>(p, s) : launch_general<64>(p, s);
   dim3 grid(p.B), block(256);
   if (head_dim == 128)
     kv_append_kernel<128><<<grid, block, 0, s>>>(p);

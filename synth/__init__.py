@@ -7,13 +7,14 @@ bf16 values from a counter-based hash that has identical numpy and torch
 implementations.  Both the CPU oracle and the CUDA path consume what it
 produces; neither side imports the other.
 """
-from .workload import (CONFIGS, Shape, Layout, draw_lengths, build_layout, make_case,
+from .workload import (CONFIGS, Shape, Layout, draw_lengths, build_layout, build_general_layout,
+                       make_case,
                        Case, shard_heads)
 from .values import (key32, hash_bf16_np, hash_bf16_torch, dense_kv_np, q_np,
                      dense_kv_torch, q_torch, BF16_NAN)
 
 __all__ = [
-    "CONFIGS", "Shape", "Layout", "draw_lengths", "build_layout", "make_case", "Case",
+    "CONFIGS", "Shape", "Layout", "draw_lengths", "build_layout", "build_general_layout", "make_case", "Case",
     "shard_heads", "key32", "hash_bf16_np", "hash_bf16_torch", "dense_kv_np", "q_np",
     "dense_kv_torch", "q_torch", "BF16_NAN",
 ]

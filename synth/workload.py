@@ -117,7 +117,9 @@ class Layout:
     block_tables: np.ndarray      # int32 [B][M], -1 padded
     dirs: np.ndarray              # uint8 [B][M] per-entry direction (0 RT fwd, 1 BE rev), 0 padded
     num_blocks: int               # pool capacity in blocks
-    n_shared: int                 # number of physical blocks shared by an RT and a BE tail
+    n_shared: int                 # number of physical blocks shared by an RT and a BE request
+    fills: np.ndarray | None = None        # general map only (f3): uint8 [B][M] tokens per entry
+    num_entries: np.ndarray | None = None  # general map only (f3): int32 [B] entries in use
 
     @property
     def batch(self) -> int:
@@ -128,7 +130,13 @@ class Layout:
         return self.is_be.astype(np.uint8)
 
     def nblocks(self) -> np.ndarray:
+        if self.num_entries is not None:
+            return self.num_entries.astype(np.int64)
         return (self.lens + self.block_size - 1) // self.block_size
+
+    @property
+    def general(self) -> bool:
+        return self.fills is not None
 
 
 def build_layout(lens, is_be, block_size: int, rng: np.random.Generator, *,
@@ -174,6 +182,67 @@ def build_layout(lens, is_be, block_size: int, rng: np.random.Generator, *,
     return Layout(lens.astype(np.int32), is_be, bs, bt, dirs, max(num_blocks, 1), len(pairs))
 
 
+def build_general_layout(lens, is_be, block_size: int, rng: np.random.Generator, *,
+                         share_prob: float = 0.6, spare_blocks: int = 0, permute: bool = True,
+                         order=None) -> Layout:
+    """General map: any entry may be partly filled.
+
+    Stand-in for FindBlock (a BE prefill goes to "the blocks with
+    the maximum number of empty slots") and FindPreemptBlock (an
+    RT request takes over a BE block "from the opposite end").  Requests are
+    placed one after another (seeded random order).  Each takes blocks until
+    its tokens are placed: with probability ``share_prob`` it reuses, among the
+    blocks whose own-direction side is free and whose opposite side is in use,
+    the one with the most empty slots, putting min(remaining, empty) tokens
+    there; otherwise a fresh block takes min(remaining, bs).  The output is
+    only WHICH block each entry names and HOW MANY tokens it holds -- never a
+    slot index (that is the method's business).
+    """
+    lens = np.asarray(lens, dtype=np.int64)
+    is_be = np.asarray(is_be, dtype=bool)
+    B, bs = lens.shape[0], block_size
+    used = [[0, 0]]  # per logical block: tokens of its forward / reversed owner (0 = side free)
+    used.clear()
+    entries = [[] for _ in range(B)]
+    n_shared = 0
+    order = rng.permutation(B) if order is None else np.asarray(order)
+    for r in order:
+        d = int(is_be[r])
+        rem = int(lens[r])
+        while rem > 0:
+            blk = -1
+            if rng.random() < share_prob:
+                best = 0
+                for b, u in enumerate(used):
+                    empty = bs - u[0] - u[1]
+                    if u[d] == 0 and u[1 - d] > 0 and empty > best:
+                        best, blk = empty, b
+            if blk < 0:
+                used.append([0, 0])
+                blk = len(used) - 1
+            else:
+                n_shared += 1
+            n = min(rem, bs - used[blk][0] - used[blk][1])
+            used[blk][d] = n
+            entries[r].append((blk, n))
+            rem -= n
+    M = max(1, max((len(e) for e in entries), default=1))
+    num_blocks = len(used) + int(spare_blocks)
+    perm = rng.permutation(num_blocks) if permute else np.arange(num_blocks)
+    bt = np.full((B, M), -1, dtype=np.int32)
+    fills = np.zeros((B, M), dtype=np.uint8)
+    dirs = np.zeros((B, M), dtype=np.uint8)
+    nent = np.zeros(B, dtype=np.int32)
+    for r in range(B):
+        nent[r] = len(entries[r])
+        for e, (blk, n) in enumerate(entries[r]):
+            bt[r, e] = perm[blk]
+            fills[r, e] = n
+            dirs[r, e] = BE if is_be[r] else RT
+    return Layout(lens.astype(np.int32), is_be, bs, bt, dirs, max(num_blocks, 1), n_shared,
+                  fills=fills, num_entries=nent)
+
+
 @dataclass
 class Case:
     """One seeded batch: shape, layout and the value-stream seed."""
@@ -185,7 +254,8 @@ class Case:
 
 
 def make_case(shape: Shape | str, seed: int = 0, *, lens=None, is_be=None, share_tails=True,
-              spare_blocks: int = 3, q_scale_log2: int = 0, layer: int = 0) -> Case:
+              spare_blocks: int = 3, q_scale_log2: int = 0, layer: int = 0,
+              general: bool = False, share_prob: float = 0.6) -> Case:
     if isinstance(shape, str):
         shape = CONFIGS[shape]
     rng = np.random.default_rng(seed)
@@ -198,8 +268,12 @@ def make_case(shape: Shape | str, seed: int = 0, *, lens=None, is_be=None, share
         if is_be is None:
             is_be = np.arange(len(lens)) % 2 == 1
         shape = replace(shape, batch=len(lens))
-    lay = build_layout(lens, is_be, shape.block_size, rng, share_tails=share_tails,
-                       spare_blocks=spare_blocks)
+    if general:
+        lay = build_general_layout(lens, is_be, shape.block_size, rng, share_prob=share_prob,
+                                   spare_blocks=spare_blocks)
+    else:
+        lay = build_layout(lens, is_be, shape.block_size, rng, share_tails=share_tails,
+                           spare_blocks=spare_blocks)
     return Case(shape, lay, seed, q_scale_log2, layer)
 
 

@@ -120,3 +120,107 @@ def test_gpu_checkpoint_restore_bitwise():
         Vo = np.full_like(V, BF16_NAN)
         oracle.restore(Ko, Vo, sids, ck, cv)
         assert np.array_equal(u(pool.k), Ko) and np.array_equal(u(pool.v), Vo)
+
+
+def _grown_rt_case(seed, bs=16, H=2, d=128, B=16):
+    """Shared-tail layout whose RT requests then grow INTO their BE peer's slots."""
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(1, 120, B)
+    is_be = np.arange(B) % 2 == 1
+    lay = build_layout(lens, is_be, bs, rng, spare_blocks=2)
+    grow = np.where(~is_be, np.minimum(6, (-lens) % bs), 0).astype(np.int32)
+    K = rng.integers(0, 65535, (lay.num_blocks, H, bs, d)).astype(np.uint16)
+    V = rng.integers(0, 65535, (lay.num_blocks, H, bs, d)).astype(np.uint16)
+    n = int(grow.sum())
+    kn = rng.integers(0, 65535, (n, H, d)).astype(np.uint16)
+    vn = rng.integers(0, 65535, (n, H, d)).astype(np.uint16)
+    cu = np.concatenate([[0], np.cumsum(grow)]).astype(np.int32)
+    return lay, grow, K, V, kn, vn, cu
+
+
+def test_fused_checkpoint_reference_is_checkpoint_then_append():
+    """CPU side of the fused call's definition: the victims the oracle reports are exactly
+    the slots whose old bytes differ after the append; checkpointing them first keeps them."""
+    lay, grow, K, V, kn, vn, cu = _grown_rt_case(7, d=8)
+    before = lay.lens.astype(np.int32)
+    victims = oracle.overwritten_peers(lay.block_tables, lay.dirs, lay.lens, before, grow, lay.num_blocks, 16)
+    assert len(victims) > 0
+    sids = [s for _, _, s in victims]
+    ck, cv = oracle.checkpoint(K, V, sids)
+    K2, V2 = K.copy(), V.copy()
+    sm = oracle.append(K2, V2, lay.block_tables, lay.dirs, before, cu, kn, vn)
+    assert set(sids) <= set(sm.tolist())
+    kk, vv = oracle.checkpoint(K, V, sm)          # old contents of every written slot
+    assert np.array_equal(ck, kk[[sm.tolist().index(s) for s in sids]])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed,d", [(7, 128), (8, 64)])
+def test_gpu_append_checkpoint_fused_bitwise(seed, d):
+    """bkv_kv_append_checkpoint == oracle checkpoint(victims) + oracle append, bit for bit."""
+    import paper_2504_09590_b200 as bkv
+    lay, grow, K, V, kn, vn, cu = _grown_rt_case(seed, d=d)
+    H = K.shape[1]
+    before = lay.lens.astype(np.int32)
+    victims = oracle.overwritten_peers(lay.block_tables, lay.dirs, lay.lens, before, grow, lay.num_blocks, 16)
+    sids = [s for _, _, s in victims]
+    assert len(sids) > 0
+    ck, cv = oracle.checkpoint(K, V, sids)
+    Ko, Vo = K.copy(), V.copy()
+    sm = oracle.append(Ko, Vo, lay.block_tables, lay.dirs, before, cu, kn, vn)
+    evict = np.array([sids.index(s) if s in sids else -1 for s in sm.tolist()], np.int32)
+
+    def g(a):
+        return torch.from_numpy(np.ascontiguousarray(a).view(np.int16).copy()).cuda().view(torch.bfloat16)
+
+    def u(t):
+        return t.view(torch.int16).cpu().numpy().view(np.uint16)
+
+    pool = bkv.KVPool(g(K), g(V))
+    n_ck = len(sids) + 3                       # spare rows must stay untouched
+    gk = torch.full((n_ck, H, d), 7.0, dtype=torch.bfloat16, device="cuda")
+    gv = torch.full((n_ck, H, d), 7.0, dtype=torch.bfloat16, device="cuda")
+    gsm = torch.zeros(len(sm), dtype=torch.int64, device="cuda")
+    bkv.kv_append_checkpoint(pool, torch.from_numpy(lay.block_tables).cuda(), torch.from_numpy(lay.dirs).cuda(),
+                             torch.from_numpy(before).cuda(), torch.from_numpy(cu).cuda(), g(kn), g(vn),
+                             torch.from_numpy(evict).cuda(), gk, gv, slot_mapping=gsm)
+    torch.cuda.synchronize()
+    assert np.array_equal(u(pool.k), Ko) and np.array_equal(u(pool.v), Vo)
+    assert np.array_equal(gsm.cpu().numpy(), sm)
+    assert np.array_equal(u(gk)[:len(sids)], ck) and np.array_equal(u(gv)[:len(sids)], cv)
+    assert (gk[len(sids):].float() == 7.0).all() and (gv[len(sids):].float() == 7.0).all()
+    # swap-in after the RT request finished: the peer's tokens come back bitwise (P:730)
+    bkv.kv_restore(pool, torch.tensor(sids, dtype=torch.int64, device="cuda"), gk[:len(sids)], gv[:len(sids)])
+    torch.cuda.synchronize()
+    oracle.restore(Ko, Vo, sids, ck, cv)
+    assert np.array_equal(u(pool.k), Ko)
+
+
+@pytest.mark.gpu
+def test_gpu_append_checkpoint_into_pinned_host_memory():
+    """The checkpoint rows may land directly in pinned host memory (UVA: the pinned
+    pointer is valid on the device) -- the D2H checkpoint of P:726 with no staging copy."""
+    import paper_2504_09590_b200 as bkv
+    H, d = 2, 64
+    lay, grow, K, V, kn, vn, cu = _grown_rt_case(9, d=d, H=H)
+    before = lay.lens.astype(np.int32)
+    victims = oracle.overwritten_peers(lay.block_tables, lay.dirs, lay.lens, before, grow, lay.num_blocks, 16)
+    sids = [s for _, _, s in victims]
+    ck, cv = oracle.checkpoint(K, V, sids)
+    Ko, Vo = K.copy(), V.copy()
+    sm = oracle.append(Ko, Vo, lay.block_tables, lay.dirs, before, cu, kn, vn)
+    evict = np.array([sids.index(s) if s in sids else -1 for s in sm.tolist()], np.int32)
+
+    def g(a):
+        return torch.from_numpy(np.ascontiguousarray(a).view(np.int16).copy()).cuda().view(torch.bfloat16)
+
+    hk = torch.zeros((len(sids), H, d), dtype=torch.bfloat16).pin_memory()
+    hv = torch.zeros((len(sids), H, d), dtype=torch.bfloat16).pin_memory()
+    pool = bkv.KVPool(g(K), g(V))
+    bkv.kv_append_checkpoint(pool, torch.from_numpy(lay.block_tables).cuda(), torch.from_numpy(lay.dirs).cuda(),
+                             torch.from_numpy(before).cuda(), torch.from_numpy(cu).cuda(), g(kn), g(vn),
+                             torch.from_numpy(evict).cuda(), hk, hv)
+    torch.cuda.synchronize()
+    assert np.array_equal(hk.view(torch.int16).numpy().view(np.uint16), ck)
+    assert np.array_equal(hv.view(torch.int16).numpy().view(np.uint16), cv)
+    assert np.array_equal(pool.k.view(torch.int16).cpu().numpy().view(np.uint16), Ko)
