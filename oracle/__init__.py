@@ -70,6 +70,9 @@ def lib():
         L.bkvo_attention_f.argtypes = [P, P, i64, i64, i64, i32, i32, i32,
                                        P, i32, P, i32, i32, P, i32, P, i32, i32, P, i32, dbl, P]
         L.bkvo_attention_f.restype = None
+        L.bkvo_prefill_attention.argtypes = [P, P, i64, i64, i64, i32, i32, i32,
+                                             P, i32, P, i32, i32, P, i32, i32, P, P, P, i32, dbl, P]
+        L.bkvo_prefill_attention.restype = None
         L.bkvo_num_threads.restype = i32
         L.bkvo_set_num_threads.argtypes = [i32]
         _lib = L
@@ -204,6 +207,30 @@ def attention(K, V, block_tables, dirs, lens, q, scale: float, r_range=None, fil
     lib().bkvo_attention(_ptr(K), _ptr(V), sb, sh, ss, H, d, bs, _ptr(bt), int(bt.shape[1]),
                          _ptr(dd), rs, cs, _ptr(ln), int(r0), int(r1), _ptr(qq), int(Hq),
                          float(scale), _ptr(out))
+    return out
+
+
+def prefill_attention(K, V, block_tables, dirs, lens, cu_q, q, scale: float, fills=None,
+                      num_entries=None):
+    """fp64 causal attention of each request's LAST n = cu_q[r+1]-cu_q[r] tokens over its
+    paged context (mixed prefill + decode, SURVEY §8(f) f4).  q uint16 [total][Hq][d];
+    returns float64 [total][Hq][d]."""
+    sb, sh, ss, H, d, bs = _pool_geom(K)
+    bt = _c(block_tables, np.int32)
+    dd, rs, cs = _dirs(dirs)
+    ln = _c(lens, np.int32)
+    cu = _c(cu_q, np.int32)
+    qq = _c(q, np.uint16)
+    T, Hq, dq = qq.shape
+    B = int(ln.shape[0])
+    assert dq == d and Hq % H == 0 and cu.shape == (B + 1,) and cu[-1] == T
+    out = np.zeros((T, Hq, d), dtype=np.float64)
+    f, frs = None, 0
+    if fills is not None:
+        f, frs, _ = _fills(fills, num_entries, B)
+    lib().bkvo_prefill_attention(_ptr(K), _ptr(V), sb, sh, ss, H, d, bs, _ptr(bt), int(bt.shape[1]),
+                                 _ptr(dd), rs, cs, _ptr(f), frs, B, _ptr(ln), _ptr(cu), _ptr(qq),
+                                 int(Hq), float(scale), _ptr(out))
     return out
 
 

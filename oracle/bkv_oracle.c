@@ -481,6 +481,72 @@ void bkvo_attention_f(const uint16_t *K, const uint16_t *V, int64_t sb, int64_t 
     }
 }
 
+/*
+ * ---------------------------------------------------------------------------
+ * Mixed prefill + decode attention over the bidirectional paged cache
+ * (SURVEY §8(f) row f4).  BROS batches "the concatenated prefill requests
+ * followed by the decode requests" with a length table and dispatches each
+ * part to its attention kernel; the prefill part is standard
+ * causal self-attention over the request's tokens (the cost model's
+ * "attention score matrix ... batched GEMM and softmax").
+ *
+ * Request r has L = lens[r] resident tokens (its new tokens already appended,
+ * reading Q7); its LAST n = cu_q[r+1] - cu_q[r] tokens are queries.  Query i
+ * (0 <= i < n) is logical token p = L - n + i and attends causally to tokens
+ * t <= p:
+ *   s_t = scale * q_i[h] . K_r[t][kv],  o = sum_{t<=p} e^{s_t - m} V_r[t][kv] / sum_{t<=p} e^{s_t - m}
+ * with kv = h / g (reading Q9).  n = 1 is exactly decode attention.
+ * q is bf16 [total_q][Hq][d] (row cu_q[r] + i), out fp64 of the same shape.
+ * fills == NULL selects the dense map, else the general map (row f3).
+ */
+void bkvo_prefill_attention(const uint16_t *K, const uint16_t *V, int64_t sb, int64_t sh, int64_t ss,
+                            int H, int d, int bs,
+                            const int32_t *bt, int bt_stride, const uint8_t *dirs, int rs, int cs,
+                            const uint8_t *fills, int frs,
+                            int B, const int32_t *lens, const int32_t *cu_q,
+                            const uint16_t *q, int Hq, double scale, double *out) {
+    int g = Hq / H;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int r = 0; r < B; ++r) {
+        int64_t L = lens[r];
+        int n = cu_q[r + 1] - cu_q[r];
+        if (n <= 0) continue;
+        uint16_t *kr = malloc(sizeof(uint16_t) * (size_t)(L * H * d));
+        uint16_t *vr = malloc(sizeof(uint16_t) * (size_t)(L * H * d));
+        double *s = malloc(sizeof(double) * (size_t)L);
+        if (fills)
+            bkvo_gather_f(K, V, sb, sh, ss, H, d, bs, bt, bt_stride, dirs, rs, cs, fills, frs, r, L, kr, vr);
+        else
+            bkvo_gather(K, V, sb, sh, ss, H, d, bs, bt, bt_stride, dirs, rs, cs, r, L, kr, vr);
+        for (int i = 0; i < n; ++i) {
+            int64_t p = L - n + i;                 /* logical position of query i */
+            for (int h = 0; h < Hq; ++h) {
+                int kv = h / g;
+                const uint16_t *qh = q + ((int64_t)(cu_q[r] + i) * Hq + h) * d;
+                double *oh = out + ((int64_t)(cu_q[r] + i) * Hq + h) * d;
+                double m = -INFINITY;
+                for (int64_t t = 0; t <= p; ++t) {
+                    const uint16_t *kt = kr + (t * H + kv) * d;
+                    double acc = 0.0;
+                    for (int c = 0; c < d; ++c) acc += bf16_to_f64(qh[c]) * bf16_to_f64(kt[c]);
+                    s[t] = scale * acc;
+                    if (s[t] > m) m = s[t];
+                }
+                double denom = 0.0;
+                for (int c = 0; c < d; ++c) oh[c] = 0.0;
+                for (int64_t t = 0; t <= p; ++t) {
+                    double pt = exp(s[t] - m);
+                    denom += pt;
+                    const uint16_t *vt = vr + (t * H + kv) * d;
+                    for (int c = 0; c < d; ++c) oh[c] += pt * bf16_to_f64(vt[c]);
+                }
+                for (int c = 0; c < d; ++c) oh[c] /= denom;
+            }
+        }
+        free(kr); free(vr); free(s);
+    }
+}
+
 int bkvo_num_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

@@ -11,10 +11,10 @@ from .workload import (CONFIGS, Shape, Layout, draw_lengths, build_layout, build
                        make_case,
                        Case, shard_heads)
 from .values import (key32, hash_bf16_np, hash_bf16_torch, dense_kv_np, q_np,
-                     dense_kv_torch, q_torch, BF16_NAN)
+                     dense_kv_torch, q_torch, q_rows_np, q_rows_torch, BF16_NAN)
 
 __all__ = [
     "CONFIGS", "Shape", "Layout", "draw_lengths", "build_layout", "build_general_layout", "make_case", "Case",
     "shard_heads", "key32", "hash_bf16_np", "hash_bf16_torch", "dense_kv_np", "q_np",
-    "dense_kv_torch", "q_torch", "BF16_NAN",
+    "dense_kv_torch", "q_torch", "q_rows_np", "q_rows_torch", "BF16_NAN",
 ]

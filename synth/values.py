@@ -17,7 +17,7 @@ import numpy as np
 
 M32 = 0xFFFFFFFF
 BF16_NAN = 0x7FC0          # quiet-NaN bf16 pattern used to poison non-owned slots
-KIND_K, KIND_V, KIND_Q = 1, 2, 3
+KIND_K, KIND_V, KIND_Q, KIND_QP = 1, 2, 3, 4
 
 
 def _mul32_np(x, c: int):
@@ -141,3 +141,23 @@ def q_torch(seed: int, layer: int, req: int, heads, d: int, device, scale_log2: 
     heads = torch.as_tensor(list(heads), dtype=torch.int64, device=device)
     idx = heads[:, None] * d + torch.arange(d, dtype=torch.int64, device=device)[None, :]
     return hash_bf16_torch(_stream(seed, KIND_Q, layer, req), idx, scale_log2)
+
+
+def q_rows_np(seed: int, layer: int, req: int, n: int, heads, d: int, h_total: int,
+              scale_log2: int = 0):
+    """Query rows of a request's last ``n`` tokens (mixed prefill + decode):
+    uint16 [n][len(heads)][d]; element (i, h, c) is counter (i*h_total + h)*d + c of the
+    request's prefill-query stream (GLOBAL q-head indices)."""
+    heads = np.asarray(list(heads), dtype=np.int64)
+    i = np.arange(n, dtype=np.int64)[:, None, None]
+    idx = (i * h_total + heads[None, :, None]) * d + np.arange(d, dtype=np.int64)[None, None, :]
+    return hash_bf16_np(_stream(seed, KIND_QP, layer, req), idx, scale_log2)
+
+
+def q_rows_torch(seed: int, layer: int, req: int, n: int, heads, d: int, h_total: int, device,
+                 scale_log2: int = 0):
+    import torch
+    heads = torch.as_tensor(list(heads), dtype=torch.int64, device=device)
+    i = torch.arange(n, dtype=torch.int64, device=device)[:, None, None]
+    idx = (i * h_total + heads[None, :, None]) * d + torch.arange(d, dtype=torch.int64, device=device)[None, None, :]
+    return hash_bf16_torch(_stream(seed, KIND_QP, layer, req), idx, scale_log2)
