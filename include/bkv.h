@@ -297,6 +297,36 @@ BKV_API bkv_status bkv_decode_step(const bkv_kv_pool *pool, const bkv_block_map 
                                    int64_t o_stride_seq, int64_t o_stride_head, void *workspace,
                                    size_t workspace_bytes, uint32_t flags, bkv_stream_t stream);
 
+/*
+ * bkv_paged_prefill_attention -- mixed prefill + decode attention over the
+ * bidirectional paged cache.  BROS batches "the
+ * concatenated prefill requests followed by the decode requests" and
+ * dispatches each part by a length table; this call
+ * serves both parts from the shared blocks in one launch:
+ *   request r holds L = seq_lens[r] resident tokens (its new tokens already
+ *   appended, e.g. by bkv_kv_append; reading Q7) and its LAST
+ *   n = cu_q[r+1] - cu_q[r] tokens are queries.  Query i (0 <= i < n) is
+ *   logical token p = L - n + i and attends causally:
+ *     out[cu_q[r]+i][h] = softmax_{t <= p}(softmax_scale * q . K_r[t]) . V_r[t]
+ *   with kv head h / (num_q_heads / num_kv_heads).  n = 1 is decode attention
+ *   (same result as bkv_paged_decode_attention up to fp32 summation order);
+ *   n = L is full causal prefill; n = 0 leaves the request untouched.
+ *   cu_q        device int32 [num_seqs+1], non-decreasing, cu_q[0] = 0, n <= L
+ *   max_q_len   host upper bound of n (sizes the grid)
+ *   q, out      device bf16, element (row i, head h, dim c) at
+ *               q[i*q_stride_tok + h*q_stride_head + c] (same for out),
+ *               16-byte aligned, strides multiples of 8 elements
+ * Dense or general maps (fills).  fp32 accumulation, bf16 RNE output.  No
+ * workspace, no split-K (each 128-row query tile runs in one CTA).
+ */
+BKV_API bkv_status bkv_paged_prefill_attention(const bkv_kv_pool *pool, const bkv_block_map *map,
+                                               const int32_t *seq_lens, const int32_t *cu_q,
+                                               int32_t max_q_len, const void *q,
+                                               int64_t q_stride_tok, int64_t q_stride_head,
+                                               int32_t num_q_heads, float softmax_scale, void *out,
+                                               int64_t o_stride_tok, int64_t o_stride_head,
+                                               bkv_stream_t stream);
+
 /* Workspace bytes for bkv_paged_decode_attention on the CURRENT device
  * (depends on the SM count); 0 on error (see bkv_last_error). */
 BKV_API size_t bkv_decode_workspace_size(int32_t num_seqs, int32_t num_q_heads, int32_t num_kv_heads,

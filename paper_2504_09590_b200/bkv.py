@@ -47,7 +47,8 @@ _lib_lock = threading.Lock()
 EXPORTS = ("bkv_kv_append", "bkv_paged_decode_attention", "bkv_decode_workspace_size",
            "bkv_validate_layout_host", "bkv_status_string", "bkv_last_error", "bkv_version",
            "bkv_kv_checkpoint", "bkv_kv_restore", "bkv_paged_decode_attention_ex",
-           "bkv_decode_step", "bkv_validate_block_map_host", "bkv_kv_append_checkpoint")
+           "bkv_decode_step", "bkv_validate_block_map_host", "bkv_kv_append_checkpoint",
+           "bkv_paged_prefill_attention")
 BKV_FLAG_PDL = 1   # include/bkv.h: programmatic dependent launch (seq_lens not written by the previous kernel)
 
 
@@ -78,6 +79,10 @@ def lib():
                     ctypes.POINTER(_Pool), ctypes.POINTER(_Map), P, i32, P, P, P, i64, i64, i32,
                     ctypes.c_float, P, i64, i64, P, ctypes.c_size_t, ctypes.c_uint32, P]
                 L.bkv_decode_step.restype = ctypes.c_int
+                L.bkv_paged_prefill_attention.argtypes = [
+                    ctypes.POINTER(_Pool), ctypes.POINTER(_Map), P, P, i32, P, i64, i64, i32, ctypes.c_float,
+                    P, i64, i64, P]
+                L.bkv_paged_prefill_attention.restype = ctypes.c_int
                 L.bkv_decode_workspace_size.argtypes = [i32, i32, i32, i32]
                 L.bkv_decode_workspace_size.restype = ctypes.c_size_t
                 L.bkv_validate_layout_host.argtypes = [P, i32, P, i32, i32, i32, P, i32, i32, i32, P]
@@ -336,6 +341,35 @@ def decode_step(pool: KVPool, block_tables, dirs, seq_lens, k_new, v_new, q, sof
         out.data_ptr(), out.stride(0), out.stride(1), ws.data_ptr(), ws.numel(),
         BKV_FLAG_PDL if pdl else 0, _stream_ptr(stream))
     _check(rc, "bkv_decode_step")
+    return out
+
+
+def paged_prefill_attention(pool: KVPool, block_tables, dirs, seq_lens, cu_q, q, max_q_len=None,
+                            softmax_scale=None, out=None, stream=None, fills=None, num_entries=None):
+    """bkv_paged_prefill_attention: causal attention of every request's LAST
+    n_r = cu_q[r+1]-cu_q[r] tokens over its paged context; q/out bf16 [total][Hq][d]
+    (unit last stride).  n_r = 1 rows are decodes, so one call serves a mixed batch."""
+    p, m = pool.c(), block_map(block_tables, dirs, fills, num_entries)
+    _dev(seq_lens, "seq_lens", torch.int32)
+    _dev(cu_q, "cu_q", torch.int32)
+    _dev(q, "q", torch.bfloat16)
+    T, Hq, d = q.shape
+    if q.stride(2) != 1:
+        raise BkvError("q must have a unit stride along head_dim")
+    if out is None:
+        out = torch.empty((T, Hq, d), dtype=torch.bfloat16, device=q.device)
+    _dev(out, "out", torch.bfloat16)
+    if out.stride(2) != 1:
+        raise BkvError("out must have a unit stride along head_dim")
+    if softmax_scale is None:
+        softmax_scale = 1.0 / math.sqrt(d)
+    if max_q_len is None:
+        max_q_len = int((cu_q[1:] - cu_q[:-1]).max().item()) if cu_q.numel() > 1 else 0
+    rc = lib().bkv_paged_prefill_attention(
+        ctypes.byref(p), ctypes.byref(m), seq_lens.data_ptr(), cu_q.data_ptr(), int(max_q_len),
+        q.data_ptr(), q.stride(0), q.stride(1), Hq, float(softmax_scale), out.data_ptr(),
+        out.stride(0), out.stride(1), _stream_ptr(stream))
+    _check(rc, "bkv_paged_prefill_attention")
     return out
 
 

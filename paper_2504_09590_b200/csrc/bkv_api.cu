@@ -363,6 +363,7 @@ static bkv_status decode_impl(const bkv_kv_pool *pool, const bkv_block_map *map,
   p.part_o = reinterpret_cast<float *>(ws + w.o);
   p.target_units = bkv::decode_target_units(cfg);
   p.min_split = bkv::decode_min_split(g);
+  p.small_plan = getenv("BKV_SMALL_PLAN") ? atoi(getenv("BKV_SMALL_PLAN")) : 1;
   p.units_max = w.units_max;
   p.slots = slots;
   p.q_bytes = qb;
@@ -476,6 +477,60 @@ bkv_status bkv_validate_layout_host(const int32_t *block_tables, int32_t bt_stri
       occ_t[k] = t;
     }
   }
+  return BKV_OK;
+}
+
+bkv_status bkv_paged_prefill_attention(const bkv_kv_pool *pool, const bkv_block_map *map,
+                                       const int32_t *seq_lens, const int32_t *cu_q,
+                                       int32_t max_q_len, const void *q, int64_t q_stride_tok,
+                                       int64_t q_stride_head, int32_t num_q_heads,
+                                       float softmax_scale, void *out, int64_t o_stride_tok,
+                                       int64_t o_stride_head, bkv_stream_t stream) {
+  bkv_status s = check_pool(pool);
+  if (s) return s;
+  if ((s = check_map(map))) return s;
+  const int B = map->num_seqs, H = pool->num_kv_heads;
+  if (B == 0 || max_q_len == 0) return BKV_OK;
+  if (max_q_len < 0) return fail(BKV_ERR_INVALID_ARGUMENT, "max_q_len < 0");
+  if (B > 65535 || H > 65535) return fail(BKV_ERR_UNSUPPORTED, "num_seqs/num_kv_heads > 65535");
+  if (!seq_lens || !cu_q || !q || !out)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "seq_lens/cu_q/q/out is NULL");
+  if (num_q_heads <= 0 || num_q_heads % H)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "num_q_heads %d is not a multiple of num_kv_heads %d",
+                num_q_heads, H);
+  if (!aligned16(q) || !aligned16(out) || q_stride_tok % 8 || q_stride_head % 8 ||
+      o_stride_tok % 8 || o_stride_head % 8)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "q/out must be 16-byte aligned with strides multiple of 8");
+  if (!(softmax_scale == softmax_scale) || isinf(softmax_scale))
+    return fail(BKV_ERR_INVALID_ARGUMENT, "softmax_scale must be finite");
+  CUtensorMap tmK, tmV;
+  if ((s = encode_pool_map(&tmK, pool->k, pool))) return s;
+  if ((s = encode_pool_map(&tmV, pool->v, pool))) return s;
+  bkv::PrefillParams p;
+  p.bt = map->block_tables;
+  p.bt_stride = map->bt_stride;
+  p.dirs = map->dirs;
+  p.dir_rs = map->dir_row_stride;
+  p.dir_cs = map->dir_col_stride;
+  p.fills = map->fills;
+  p.fill_rs = map->fill_row_stride;
+  p.nent = map->num_entries;
+  p.seq_lens = seq_lens;
+  p.cu_q = cu_q;
+  p.B = B;
+  p.H = H;
+  p.bs = pool->block_size;
+  p.g = num_q_heads / H;
+  p.q = static_cast<const uint16_t *>(q);
+  p.q_st = q_stride_tok;
+  p.q_sh = q_stride_head;
+  p.out = static_cast<uint16_t *>(out);
+  p.o_st = o_stride_tok;
+  p.o_sh = o_stride_head;
+  p.scale_log2 = softmax_scale * 1.4426950408889634f;
+  cudaError_t e = bkv::launch_prefill(tmK, tmV, p, pool->head_dim, max_q_len,
+                                      reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "prefill attention launch");
   return BKV_OK;
 }
 

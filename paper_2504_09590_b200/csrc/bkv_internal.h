@@ -67,7 +67,8 @@ struct DecodeParams {
   float *part_ml;        // [units_max][g][2]  (m in log2 domain, l)
   float *part_o;         // [units_max][g][D]  un-normalised partial outputs
   int target_units;      // split plan: aim for about this many units
-  int min_split;         // split plan: at least this many blocks per unit
+  int min_split;         // split plan: at least this many blocks per unit (large problems)
+  int small_plan;        // split plan: chain-balanced P for small problems (BKV_SMALL_PLAN=0: off)
   int units_max;         // workspace capacity in units
   int slots;             // ring depth per warp (S)
   int q_bytes;           // smem bytes per q-ring entry
@@ -93,6 +94,28 @@ int decode_target_units(const DecodeLaunch &cfg);
 int decode_min_split(int group);
 cudaError_t launch_decode(const CUtensorMap &tmK, const CUtensorMap &tmV, const DecodeParams &p,
                           int head_dim, const DecodeLaunch &cfg, cudaStream_t s);
+
+// ------------------------------------------- mixed prefill + decode (f4)
+struct PrefillParams {
+  const int32_t *bt;
+  int bt_stride;
+  const uint8_t *dirs;
+  int dir_rs, dir_cs;
+  const uint8_t *fills;   // general map (f3) or nullptr
+  int fill_rs;
+  const int32_t *nent;
+  const int32_t *seq_lens;
+  const int32_t *cu_q;    // [B+1] query rows of request r: its last cu_q[r+1]-cu_q[r] tokens
+  int B, H, bs, g;
+  const uint16_t *q;
+  int64_t q_st, q_sh;
+  uint16_t *out;
+  int64_t o_st, o_sh;
+  float scale_log2;
+};
+int prefill_smem_bytes(int head_dim);
+cudaError_t launch_prefill(const CUtensorMap &tmK, const CUtensorMap &tmV, const PrefillParams &p,
+                           int head_dim, int max_q_len, cudaStream_t s);
 
 constexpr int kMaxSeqs = 2048;  // plan arrays live in shared memory
 constexpr int kMaxGroup = 16;   // GQA rows per MMA tile

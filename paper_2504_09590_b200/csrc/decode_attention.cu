@@ -90,8 +90,8 @@ __device__ __forceinline__ int search_le(const int *a, int n, int x) {
 }
 
 // Split plan, computed identically by every CTA from
-// seq_lens (no host round trip).  P = max(min_split, ceil(sum_r nb_r * H /
-// target)) blocks; request r is cut into n_r = ceil(nb_r / P) near-equal
+// seq_lens (no host round trip).  P = ceil(sum_r nb_r * H / target) blocks
+// when that is >= min_split, else the small-problem rule below; request r is cut into n_r = ceil(nb_r / P) near-equal
 // splits of s_r <= P blocks.  Requests are grouped into 4 buckets by split
 // size (largest first) and units are enumerated bucket by bucket, so the
 // dynamically scheduled work list runs roughly longest-first and the tail is
@@ -129,7 +129,27 @@ __device__ void compute_plan(const DecodeParams &p, int *Pre, int *Lsm, int *NBs
   for (int w = 0; w < nw; ++w) T += red_ll[w];
   const long long target = max(1, p.target_units);
   long long Pll = (T * p.H + target - 1) / target;
-  if (Pll < p.min_split) Pll = p.min_split;
+  if (Pll < p.min_split) {
+    // Small problem (fewer than ~3 min_split-block units per warp): the step is
+    // bounded by the longest per-warp chain, not by bandwidth.  Units number at
+    // most TH/P + BH (each (r, h) rounds up once), so P_k = ceil(TH / (kW - BH))
+    // gives every warp at most k units; pick k in {1, 2, 3} minimising the
+    // chain k * (P_k + 2) (a unit's q load + output cost about two chunks).
+    const long long TH = T * p.H, BH = static_cast<long long>(p.B) * p.H, W = p.total_warps;
+    long long best = -1, bestP = p.min_split;
+    for (int k = 1; k <= 3; ++k) {
+      const long long room = k * W - BH;
+      if (room <= 0) continue;
+      const long long Pk = max(1ll, (TH + room - 1) / room);
+      if (Pk > p.min_split) continue;
+      const long long chain = k * (Pk + 2);
+      if (best < 0 || chain < best) {
+        best = chain;
+        bestP = Pk;
+      }
+    }
+    Pll = p.small_plan ? bestP : p.min_split;
+  }
   const int P = static_cast<int>(Pll);
   // per-thread contiguous ranges -> 4-bucket exclusive scans of n_r
   const int per = (B + nt - 1) / nt;
