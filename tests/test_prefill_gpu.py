@@ -1,0 +1,107 @@
+"""GPU parity of mixed prefill + decode attention through the C ABI.
+
+bkv_paged_prefill_attention against oracle.prefill_attention on the same
+seeded inputs (synth: lengths, layouts, K/V, prefill-query stream), dense and
+general maps, MHA and GQA, d 64/128, bs 16/32, mixed decode (n = 1) and
+prefill rows, poisoned peer slots.  Tolerance: north_star's max-abs 2e-2 /
+mean-abs 2e-3 (bf16 inputs, fp32 accumulation).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2504_09590_b200 as bkv
+from synth import make_case
+from synth.values import BF16_NAN
+from synth.workload import Shape
+from tests._cases import dense_case, default_scale
+from tests.test_gpu_parity import DEV, check_close, gpu_map, gpu_pool_from_dense, t_u16, u16
+from tests.test_general_map_gpu import gmap, gpu_general_pool
+from tests.test_prefill_oracle import make_q, pools, query_counts, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(case, general, n, fill=BF16_NAN, qs=1):
+    sh, lay = case.shape, case.layout
+    ks, vs, K, V = pools(case, general)
+    q, cu = make_q(case, n, sh.num_q_heads, scale_log2=qs)
+    ref = run_oracle(case, K, V, cu, q, general)
+    if general:
+        pool, _ = gpu_general_pool(case, ks, vs, sh.num_kv_heads, fill=fill)
+        bt, dirs, lens, fills, nent = gmap(lay)
+        kw = dict(fills=fills, num_entries=nent)
+    else:
+        pool, _ = gpu_pool_from_dense(case, ks, vs, sh.num_kv_heads, fill=fill)
+        bt, dirs, lens = gpu_map(lay)
+        kw = {}
+    o = bkv.paged_prefill_attention(pool, bt, dirs, lens, torch.from_numpy(cu).to(DEV), t_u16(q),
+                                    softmax_scale=default_scale(sh.head_dim), **kw)
+    torch.cuda.synchronize()
+    return o, ref
+
+
+@pytest.mark.parametrize("cfg,seed,general,full", [("tiny", 0, False, False), ("tiny", 1, True, False),
+                                                   ("tiny_gqa", 2, False, False), ("tiny_gqa", 3, True, False),
+                                                   ("tiny", 4, False, True), ("tiny_gqa", 5, True, True)])
+def test_prefill_parity_small(cfg, seed, general, full):
+    case = make_case(cfg, seed, general=general)
+    n = query_counts(case.layout.lens, np.random.default_rng(seed), full=full)
+    o, ref = _run(case, general, n)
+    check_close(o, ref, cfg)
+
+
+@pytest.mark.parametrize("hq,hkv,d,bs,general", [(8, 1, 128, 16, False), (6, 2, 64, 32, True),
+                                                 (5, 5, 128, 32, False), (16, 2, 128, 16, True),
+                                                 (12, 4, 64, 16, False)])
+def test_prefill_parity_geometries(hq, hkv, d, bs, general):
+    sh = Shape("pg", hq, hkv, d, bs, 10, 0.5, "uniform", 900, 1, 1, uniform_max=900)
+    case = make_case(sh, hq * 3 + bs, general=general, share_prob=0.9)
+    n = query_counts(case.layout.lens, np.random.default_rng(hq), decode_frac=0.3)
+    o, ref = _run(case, general, n, qs=2)
+    check_close(o, ref, str((hq, hkv, d, bs, general)))
+
+
+def test_prefill_single_queries_match_decode_kernel():
+    """n = 1 everywhere: the prefill kernel is a decode kernel (tolerance, and vs the oracle)."""
+    case = make_case("tiny_gqa", 7)
+    sh, lay = case.shape, case.layout
+    n = np.ones(lay.batch, np.int32)
+    o, ref = _run(case, False, n, qs=0)
+    check_close(o, ref, "n=1")
+    ks, vs, q = dense_case(case)
+    pool, _ = gpu_pool_from_dense(case, ks, vs, sh.num_kv_heads)
+    bt, dirs, lens = gpu_map(lay)
+    od = bkv.paged_decode_attention(pool, bt, dirs, lens, t_u16(q))
+    cu = torch.arange(lay.batch + 1, dtype=torch.int32, device=DEV)
+    op = bkv.paged_prefill_attention(pool, bt, dirs, lens, cu, t_u16(q))
+    torch.cuda.synchronize()
+    assert (op.float() - od.float()).abs().max().item() <= 2e-2
+
+
+def test_prefill_poison_and_zero_query_requests():
+    """NaN vs zero in non-owned slots: bitwise equal output; n = 0 rows untouched."""
+    case = make_case("tiny_gqa", 8, general=True, share_prob=1.0)
+    lay = case.layout
+    n = query_counts(lay.lens, np.random.default_rng(8))
+    n[::3] = 0
+    o1, ref = _run(case, True, n, fill=BF16_NAN)
+    o2, _ = _run(case, True, n, fill=0)
+    check_close(o1, ref, "poison")
+    assert torch.equal(o1.view(torch.int16), o2.view(torch.int16))
+
+
+def test_prefill_long_context_llama_shard():
+    """Llama-70B TP8 shard (1 kv head, 8 q heads): long causal prefill chunks over a
+    ShareGPT-like context with shared tails (several 128-row tiles per request)."""
+    case = make_case("llama70b", 9)
+    sh, lay = case.shape, case.layout
+    keep = 24                                   # bounded oracle cost: first 24 requests
+    from synth.workload import build_layout, Case
+    lay2 = build_layout(lay.lens[:keep], lay.is_be[:keep], 16, np.random.default_rng(3), spare_blocks=2)
+    sh1 = Shape("l8", 8, 1, 128, 16, keep, 0.5, "sharegpt", 4096, 1, 8)
+    case2 = Case(sh1, lay2, 9)
+    n = np.minimum(lay2.lens, np.random.default_rng(4).integers(1, 300, keep)).astype(np.int32)
+    o, ref = _run(case2, False, n, qs=0)
+    check_close(o, ref, "llama shard")
