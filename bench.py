@@ -207,13 +207,15 @@ def run_ours(args):
 
     import paper_2504_09590_b200 as bkv
     from synth import CONFIGS, make_case
-    from paper_2504_09590_b200.tp import HeadShard, gather_heads
+    from paper_2504_09590_b200.tp import HeadShard, PeerReassembly, gather_heads
 
     ws, rank, local = dist_env()
     # dev-only: BKV_DIST_BACKEND=gloo runs several ranks on one GPU (smoke test of the N>1 path)
     backend = os.environ.get("BKV_DIST_BACKEND", "nccl")
     if backend != "nccl":
         local = local % max(1, torch.cuda.device_count())
+        if ws > 1 and args.reassembly == "nccl":
+            args.graphs = False      # the gloo all-gather goes through host memory: not capturable
     if ws > 1:
         torch.cuda.set_device(local)
         if backend == "nccl":
@@ -262,6 +264,10 @@ def run_ours(args):
     q_d, kn_d, vn_d = q_h.to(dev), kn_h.to(dev), vn_h.to(dev)
     out_loc = torch.empty((n_layers, Hq, B, d), dtype=torch.bfloat16, device=dev)   # head-major
     out_glob = torch.empty((n_layers, Hq * tp, B, d), dtype=torch.bfloat16, device=dev) if tp > 1 else None
+    p2p = None
+    if tp > 1 and args.reassembly == "p2p":   # f2: fused NVLink reassembly instead of the all-gather
+        p2p = PeerReassembly(shard, n_layers, B, d, dev)
+        out_glob = p2p.glob
     out_h = torch.empty((n_layers, Hq * tp, B, d), dtype=torch.bfloat16).pin_memory()
     wsb = bkv.workspace(B, Hq, H, d, dev)
     max_len = int(lay.lens.max())
@@ -271,6 +277,16 @@ def run_ours(args):
         """One decode step over all layers (append + attention [+ all-gather])."""
         launches = 0
         for l in range(n_layers):
+            if p2p is not None:   # f2: fused step + stores into every peer's output, then signal
+                bkv.decode_multi_out(pools[l], md["bt"], md["dirs"], md["lens"], qd[l],
+                                     p2p.local_out(l).permute(1, 0, 2), p2p.peer_outs(l),
+                                     k_new=knd[l], v_new=vnd[l], softmax_scale=scale,
+                                     max_seq_len=max_len, ws=wsb, pdl=args.pdl)
+                launches += 2
+                if not attn_only:
+                    p2p.barrier()
+                    launches += 1
+                continue
             o = out_loc[l].permute(1, 0, 2)                                   # [B][Hq][d] view
             if args.fused:   # f2: append fused into the attention kernel (bkv_decode_step)
                 bkv.decode_step(pools[l], md["bt"], md["dirs"], md["lens"], knd[l], vnd[l], qd[l],
@@ -355,6 +371,8 @@ def run_ours(args):
     for _ in range(2):
         e2e_step()
     ms_e2e = timed(e2e_step, args.steps) / args.steps
+    if p2p is not None:
+        p2p.check()
     clk = clocks.stop()                      # clocks sampled over all three timed regions
     h2d = sum(v.numel() * v.element_size() for v in meta_h.values()) + \
         (q_h.numel() + kn_h.numel() + vn_h.numel()) * 2
@@ -395,6 +413,8 @@ def run_ours(args):
             "attn_share_of_step": att_avg_us * n_layers / (ms_step * 1e3),
             "cuda_graphs": bool(args.graphs),
             "fused_append": bool(args.fused),
+            "reassembly": ("p2p stores + peer barrier (bkv_decode_multi_out)" if p2p is not None
+                           else "nccl all_gather_into_tensor" if tp > 1 else "none (1 GPU)"),
             "attn_layer_tokens_per_s": B / (att_avg_us * 1e-6),
             "seed": args.seed,
         },
@@ -430,6 +450,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-pdl", dest="pdl", action="store_false",
                     help="launch attention without programmatic dependent launch")
+    ap.add_argument("--reassembly", default="nccl", choices=["nccl", "p2p"],
+                    help="N>1: NCCL all-gather (default) or fused NVLink stores (symmetric memory)")
     ap.add_argument("--no-fused", dest="fused", action="store_false",
                     help="separate kv_append + attention launches instead of bkv_decode_step")
     ap.add_argument("--no-graphs", dest="graphs", action="store_false",

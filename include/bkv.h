@@ -298,6 +298,47 @@ BKV_API bkv_status bkv_decode_step(const bkv_kv_pool *pool, const bkv_block_map 
                                    size_t workspace_bytes, uint32_t flags, bkv_stream_t stream);
 
 /*
+ * bkv_decode_multi_out -- decode attention (k_new = v_new = NULL) or the fused
+ * decode step (both set, as bkv_decode_step) whose outputs are ALSO stored
+ * into n_peers further buffers: the fused reassembly of SURVEY §8(f) row f2.
+ * Under tensor parallelism by kv head (outputs moved with NCCL in the
+ * paper) every rank writes its head slice straight into every peer's
+ * global output over NVLink instead of a separate all-gather.
+ *   out          this rank's output (as bkv_paged_decode_attention)
+ *   peer_outs    HOST array of n_peers (0..8) device-accessible pointers (peer
+ *                memory mapped by CUDA IPC / symmetric memory, or local
+ *                buffers); row (r, h) goes to peer_outs[k] + r*o_stride_seq +
+ *                h*o_stride_head exactly as to out (callers bake their head-
+ *                slice offset into the pointer), 16-byte aligned
+ * The peer copies are written by the stream-ordered merge kernel with 8-byte
+ * vector stores (bit-identical to out).  Completion is visible to the peers
+ * only after bkv_peer_barrier on every rank.
+ */
+BKV_API bkv_status bkv_decode_multi_out(const bkv_kv_pool *pool, const bkv_block_map *map,
+                                        const int32_t *seq_lens, int32_t max_seq_len,
+                                        const void *k_new, const void *v_new, const void *q,
+                                        int64_t q_stride_seq, int64_t q_stride_head,
+                                        int32_t num_q_heads, float softmax_scale, void *out,
+                                        void *const *peer_outs, int32_t n_peers,
+                                        int64_t o_stride_seq, int64_t o_stride_head,
+                                        void *workspace, size_t workspace_bytes, uint32_t flags,
+                                        bkv_stream_t stream);
+
+/*
+ * bkv_peer_barrier -- stream-ordered cross-rank completion signal for the
+ * fused reassembly: rank `rank` of n stores epoch e (device counter *counter,
+ * incremented by this call, so graph replays need no host update) into
+ * pads[k][rank] for every k (release, system scope) and waits until
+ * pads[rank][k] >= e for every k (acquire).  pads = HOST array of n
+ * device-accessible uint32 arrays of n entries (zeroed before first use);
+ * every rank must call it the same number of times.  A wait longer than
+ * timeout_ns (%globaltimer) stops waiting and sets *err = 1 instead of hanging.
+ */
+BKV_API bkv_status bkv_peer_barrier(uint32_t *const *pads, int32_t n, int32_t rank,
+                                    uint32_t *counter, uint32_t *err, uint64_t timeout_ns,
+                                    bkv_stream_t stream);
+
+/*
  * bkv_paged_prefill_attention -- mixed prefill + decode attention over the
  * bidirectional paged cache.  BROS batches "the
  * concatenated prefill requests followed by the decode requests" and

@@ -48,7 +48,7 @@ EXPORTS = ("bkv_kv_append", "bkv_paged_decode_attention", "bkv_decode_workspace_
            "bkv_validate_layout_host", "bkv_status_string", "bkv_last_error", "bkv_version",
            "bkv_kv_checkpoint", "bkv_kv_restore", "bkv_paged_decode_attention_ex",
            "bkv_decode_step", "bkv_validate_block_map_host", "bkv_kv_append_checkpoint",
-           "bkv_paged_prefill_attention")
+           "bkv_paged_prefill_attention", "bkv_decode_multi_out", "bkv_peer_barrier")
 BKV_FLAG_PDL = 1   # include/bkv.h: programmatic dependent launch (seq_lens not written by the previous kernel)
 
 
@@ -83,6 +83,12 @@ def lib():
                     ctypes.POINTER(_Pool), ctypes.POINTER(_Map), P, P, i32, P, i64, i64, i32, ctypes.c_float,
                     P, i64, i64, P]
                 L.bkv_paged_prefill_attention.restype = ctypes.c_int
+                L.bkv_decode_multi_out.argtypes = [
+                    ctypes.POINTER(_Pool), ctypes.POINTER(_Map), P, i32, P, P, P, i64, i64, i32, ctypes.c_float,
+                    P, P, i32, i64, i64, P, ctypes.c_size_t, ctypes.c_uint32, P]
+                L.bkv_decode_multi_out.restype = ctypes.c_int
+                L.bkv_peer_barrier.argtypes = [P, i32, i32, P, P, ctypes.c_uint64, P]
+                L.bkv_peer_barrier.restype = ctypes.c_int
                 L.bkv_decode_workspace_size.argtypes = [i32, i32, i32, i32]
                 L.bkv_decode_workspace_size.restype = ctypes.c_size_t
                 L.bkv_validate_layout_host.argtypes = [P, i32, P, i32, i32, i32, P, i32, i32, i32, P]
@@ -371,6 +377,43 @@ def paged_prefill_attention(pool: KVPool, block_tables, dirs, seq_lens, cu_q, q,
         out.stride(0), out.stride(1), _stream_ptr(stream))
     _check(rc, "bkv_paged_prefill_attention")
     return out
+
+
+def _ptr_array(ptrs):
+    vals = [p if isinstance(p, int) else p.data_ptr() for p in ptrs]
+    return (ctypes.c_void_p * max(1, len(vals)))(*vals), len(vals)
+
+
+def decode_multi_out(pool: KVPool, block_tables, dirs, seq_lens, q, out, peer_outs, k_new=None,
+                     v_new=None, softmax_scale=None, max_seq_len=None, ws=None, stream=None, pdl=False,
+                     fills=None, num_entries=None):
+    """bkv_decode_multi_out (fused reassembly): decode attention (or the fused
+    decode step when k_new/v_new are given) whose output rows are also stored into every
+    pointer of ``peer_outs`` (ints = device-accessible peer addresses, or tensors), with
+    ``out``'s strides.  Returns out."""
+    p, m, out, scale, msl, ws = _attn_args(pool, block_tables, dirs, seq_lens, q, softmax_scale,
+                                           out, max_seq_len, ws, stream, fills, num_entries)
+    arr, n = _ptr_array(peer_outs)
+    kp = vp = None
+    if k_new is not None:
+        _dev(k_new, "k_new", torch.bfloat16)
+        _dev(v_new, "v_new", torch.bfloat16)
+        kp, vp = k_new.data_ptr(), v_new.data_ptr()
+    rc = lib().bkv_decode_multi_out(
+        ctypes.byref(p), ctypes.byref(m), seq_lens.data_ptr(), int(msl), kp, vp, q.data_ptr(),
+        q.stride(0), q.stride(1), q.shape[1], float(scale), out.data_ptr(), arr, n, out.stride(0),
+        out.stride(1), ws.data_ptr(), ws.numel(), BKV_FLAG_PDL if pdl else 0, _stream_ptr(stream))
+    _check(rc, "bkv_decode_multi_out")
+    return out
+
+
+def peer_barrier(pads, rank, counter, err, timeout_ns=5_000_000_000, stream=None):
+    """bkv_peer_barrier: stream-ordered cross-rank completion signal (``pads`` = per-rank
+    device-accessible uint32 flag arrays, ints or tensors; counter/err: int32 device tensors)."""
+    arr, n = _ptr_array(pads)
+    rc = lib().bkv_peer_barrier(arr, n, int(rank), counter.data_ptr(), err.data_ptr(), int(timeout_ns),
+                                _stream_ptr(stream))
+    _check(rc, "bkv_peer_barrier")
 
 
 def validate_layout_host(block_tables, dirs, seq_lens, num_blocks, block_size, require_nonempty=True):

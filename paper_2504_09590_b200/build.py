@@ -22,6 +22,10 @@ NVCC_FLAGS = [
 ]
 
 
+if os.environ.get("BKV_BUILD_TRACE") == "1":   # dev: compile the decode-kernel timeline tracing in
+    NVCC_FLAGS += ["-DBKV_DEV_TRACE"]
+
+
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 

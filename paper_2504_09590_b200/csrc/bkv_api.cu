@@ -299,7 +299,8 @@ static bkv_status decode_impl(const bkv_kv_pool *pool, const bkv_block_map *map,
                               int64_t q_stride_head, int32_t num_q_heads, float softmax_scale,
                               void *out, int64_t o_stride_seq, int64_t o_stride_head,
                               void *workspace, size_t workspace_bytes, uint32_t flags,
-                              bkv_stream_t stream) {
+                              bkv_stream_t stream, void *const *peer_outs = nullptr,
+                              int32_t n_peers = 0) {
   if (flags & ~BKV_FLAG_PDL) return fail(BKV_ERR_INVALID_ARGUMENT, "unknown flags 0x%x", flags);
   bkv_status s = check_pool(pool);
   if (s) return s;
@@ -376,6 +377,14 @@ static bkv_status decode_impl(const bkv_kv_pool *pool, const bkv_block_map *map,
   p.pool_sb = pool->stride_block;
   p.pool_sh = pool->stride_head;
   p.pool_ss = pool->stride_slot;
+  if (n_peers < 0 || n_peers > bkv::kMaxPeers)
+    return fail(BKV_ERR_UNSUPPORTED, "n_peers %d outside [0, %d]", n_peers, bkv::kMaxPeers);
+  p.n_peers = n_peers;
+  for (int k = 0; k < bkv::kMaxPeers; ++k) {
+    p.peer_out[k] = k < n_peers ? static_cast<uint16_t *>(peer_outs[k]) : nullptr;
+    if (k < n_peers && (!peer_outs[k] || !aligned16(peer_outs[k])))
+      return fail(BKV_ERR_INVALID_ARGUMENT, "peer output %d is NULL or not 16-byte aligned", k);
+  }
   p.debug_flags = getenv("BKV_DEBUG") ? atoi(getenv("BKV_DEBUG")) : 0;
   p.trace_cap = w.trace_cap;
   p.trace = w.trace_cap ? reinterpret_cast<unsigned long long *>(ws + w.trace) : nullptr;
@@ -411,6 +420,43 @@ bkv_status bkv_decode_step(const bkv_kv_pool *pool, const bkv_block_map *map,
   return decode_impl(pool, map, seq_lens, max_seq_len, k_new, v_new, q, q_stride_seq,
                      q_stride_head, num_q_heads, softmax_scale, out, o_stride_seq, o_stride_head,
                      workspace, workspace_bytes, flags, stream);
+}
+
+bkv_status bkv_decode_multi_out(const bkv_kv_pool *pool, const bkv_block_map *map,
+                                const int32_t *seq_lens, int32_t max_seq_len, const void *k_new,
+                                const void *v_new, const void *q, int64_t q_stride_seq,
+                                int64_t q_stride_head, int32_t num_q_heads, float softmax_scale,
+                                void *out, void *const *peer_outs, int32_t n_peers,
+                                int64_t o_stride_seq, int64_t o_stride_head, void *workspace,
+                                size_t workspace_bytes, uint32_t flags, bkv_stream_t stream) {
+  if ((k_new == nullptr) != (v_new == nullptr))
+    return fail(BKV_ERR_INVALID_ARGUMENT, "k_new and v_new must both be set or both be NULL");
+  if (k_new && (!aligned16(k_new) || !aligned16(v_new)))
+    return fail(BKV_ERR_INVALID_ARGUMENT, "k_new/v_new must be 16-byte aligned");
+  if (n_peers > 0 && !peer_outs) return fail(BKV_ERR_INVALID_ARGUMENT, "peer_outs is NULL");
+  return decode_impl(pool, map, seq_lens, max_seq_len, k_new, v_new, q, q_stride_seq,
+                     q_stride_head, num_q_heads, softmax_scale, out, o_stride_seq, o_stride_head,
+                     workspace, workspace_bytes, flags, stream, peer_outs, n_peers);
+}
+
+bkv_status bkv_peer_barrier(uint32_t *const *pads, int32_t n, int32_t rank, uint32_t *counter,
+                            uint32_t *err, uint64_t timeout_ns, bkv_stream_t stream) {
+  if (n < 1 || n > bkv::kMaxPeers) return fail(BKV_ERR_UNSUPPORTED, "n %d outside [1, 8]", n);
+  if (rank < 0 || rank >= n) return fail(BKV_ERR_INVALID_ARGUMENT, "rank %d outside [0, %d)", rank, n);
+  if (!pads || !counter || !err) return fail(BKV_ERR_INVALID_ARGUMENT, "pads/counter/err is NULL");
+  bkv::PeerBarrierParams p;
+  for (int k = 0; k < bkv::kMaxPeers; ++k) {
+    p.pads[k] = k < n ? pads[k] : nullptr;
+    if (k < n && !pads[k]) return fail(BKV_ERR_INVALID_ARGUMENT, "pad %d is NULL", k);
+  }
+  p.n = n;
+  p.rank = rank;
+  p.counter = counter;
+  p.err = err;
+  p.timeout_ns = timeout_ns;
+  cudaError_t e = bkv::launch_peer_barrier(p, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "peer barrier launch");
+  return BKV_OK;
 }
 
 bkv_status bkv_validate_layout_host(const int32_t *block_tables, int32_t bt_stride,

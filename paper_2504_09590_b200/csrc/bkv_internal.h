@@ -78,6 +78,10 @@ struct DecodeParams {
   const uint16_t *k_new, *v_new;
   uint16_t *k_pool, *v_pool;
   int64_t pool_sb, pool_sh, pool_ss;
+  // fused reassembly (f2): the merge kernel also stores every output row into
+  // these device-accessible outputs (peers' buffers over NVLink), same strides
+  uint16_t *peer_out[8];
+  int n_peers;
   int debug_flags;       // dev only: 1 = skip the math (data-movement skeleton)
   unsigned long long *trace;  // dev only (BKV_TRACE): per-warp event log, else nullptr
   int trace_cap;         // events per warp
@@ -116,6 +120,17 @@ struct PrefillParams {
 int prefill_smem_bytes(int head_dim);
 cudaError_t launch_prefill(const CUtensorMap &tmK, const CUtensorMap &tmV, const PrefillParams &p,
                            int head_dim, int max_q_len, cudaStream_t s);
+
+// cross-rank completion signal of the fused reassembly (f2)
+struct PeerBarrierParams {
+  uint32_t *pads[8];     // pads[k] = peer k's flag array (device-accessible), [n] entries
+  int n, rank;
+  uint32_t *counter;     // this rank's epoch counter (device)
+  uint32_t *err;         // set to 1 on timeout
+  unsigned long long timeout_ns;
+};
+cudaError_t launch_peer_barrier(const PeerBarrierParams &p, cudaStream_t s);
+constexpr int kMaxPeers = 8;
 
 constexpr int kMaxSeqs = 2048;  // plan arrays live in shared memory
 constexpr int kMaxGroup = 16;   // GQA rows per MMA tile

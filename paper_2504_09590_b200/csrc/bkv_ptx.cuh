@@ -95,6 +95,16 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_
       : "memory");
 }
 
+// 16-byte store into (this CTA's) shared memory through the async proxy, counted
+// as 16 transaction bytes on `bar` -- hands small metadata to the consumers of
+// an mbarrier stage with the same completion semantics as the TMA data.
+__device__ __forceinline__ void st_async_v4(uint32_t dst, int4 v, uint32_t bar) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.s32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(dst),
+      "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(bar)
+      : "memory");
+}
+
 // ---------------------------------------------------------- shared memory
 // 1-D bulk store shared -> global (async proxy, bulk-group completion)
 __device__ __forceinline__ void bulk_store(void *dst, uint32_t src, uint32_t bytes) {

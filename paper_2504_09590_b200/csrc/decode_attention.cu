@@ -44,6 +44,15 @@
 
 namespace bkv {
 
+// Dev-only timeline / cycle tracing (scripts/trace_run.py): compiled in only
+// when libbkv is built with BKV_BUILD_TRACE=1 (-DBKV_DEV_TRACE), so the product
+// kernel carries neither the code nor the registers.
+#ifdef BKV_DEV_TRACE
+constexpr bool kDevTrace = true;
+#else
+constexpr bool kDevTrace = false;
+#endif
+
 // F_NEW (fused decode step): the chunk holds this step's new token; its slot
 // in the block sits in flags bits 8..15 and the physical block in SlotMeta::aux.
 enum : int { F_FIRST = 1, F_LAST = 2, F_NOKV = 4, F_NOQ = 8, F_NEW = 16 };
@@ -260,7 +269,7 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
   // dev-only event trace: (globaltimer ns << 8 | kind), unit id in a second word
   int trace_n = 0;
   auto trace = [&](int kind, int u) {
-    if (p.trace && lane == 0 && trace_n < p.trace_cap) {
+    if (kDevTrace && p.trace && lane == 0 && trace_n < p.trace_cap) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
       unsigned long long *e = p.trace + (static_cast<int64_t>(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * p.trace_cap + trace_n) * 2;
@@ -754,7 +763,7 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
     issue(issued, m, blk, cs);
   }
   long long prof[6] = {0, 0, 0, 0, 0, 0};   // dev (BKV_TRACE): cycles wait/begin/consume/issue/end, chunks
-  const bool profiling = p.trace != nullptr;
+  const bool profiling = kDevTrace && p.trace != nullptr;
   int slot = 0;
   uint32_t phase = 0;
   for (int seq = 0; seq < issued; ++seq) {
@@ -860,7 +869,21 @@ __global__ void __launch_bounds__(256) merge_kernel(const DecodeParams p) {
   const int L = __ldg(p.seq_lens + r);
   const int nb = entries_of(p, r, L);
   const int ns = nb > 0 ? (nb + P - 1) / P : 1;
-  if (ns <= 1) return;
+  if (ns <= 1) {
+    // single split: the decode kernel wrote the local row; forward it to the
+    // peers' outputs (fused reassembly) with 16-byte stores
+    if (p.n_peers > 0) {
+      const int64_t off = static_cast<int64_t>(r) * p.o_ss + static_cast<int64_t>(h * g + row1) * p.o_sh + lane * EPL;
+      if constexpr (EPL == 4) {
+        const uint2 w = *reinterpret_cast<const uint2 *>(p.out + off);
+        for (int k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint2 *>(p.peer_out[k] + off) = w;
+      } else {
+        const uint32_t w = *reinterpret_cast<const uint32_t *>(p.out + off);
+        for (int k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint32_t *>(p.peer_out[k] + off) = w;
+      }
+    }
+    return;
+  }
   const int k = bucket_of((nb + ns - 1) / ns, P);
   // all splits of (r, h) are consecutive split slots of r's bucket: u = (slot0 + s) * H + h
   const int u0 = (p.plan_out[1 + k] + p.plan_out[16 + k * (p.B + 1) + r]) * H + h;
@@ -934,14 +957,17 @@ __global__ void __launch_bounds__(256) merge_kernel(const DecodeParams p) {
     for (int j = 0; j < 8; ++j) {
       if (j >= nr) break;
       const float inv = Lrun[j] > 0.f ? 1.f / Lrun[j] : 0.f;
-      uint16_t *o = p.out + static_cast<int64_t>(r) * p.o_ss + static_cast<int64_t>(h * g + row0 + j) * p.o_sh + lane * EPL;
+      const int64_t off = static_cast<int64_t>(r) * p.o_ss + static_cast<int64_t>(h * g + row0 + j) * p.o_sh + lane * EPL;
       if constexpr (EPL == 4) {
         uint2 w;
         w.x = pack_bf16(acc[j][0] * inv, acc[j][1] * inv);
         w.y = pack_bf16(acc[j][2] * inv, acc[j][3] * inv);
-        *reinterpret_cast<uint2 *>(o) = w;
+        *reinterpret_cast<uint2 *>(p.out + off) = w;
+        for (int k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint2 *>(p.peer_out[k] + off) = w;
       } else {
-        *reinterpret_cast<uint32_t *>(o) = pack_bf16(acc[j][0] * inv, acc[j][1] * inv);
+        const uint32_t w = pack_bf16(acc[j][0] * inv, acc[j][1] * inv);
+        *reinterpret_cast<uint32_t *>(p.out + off) = w;
+        for (int k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint32_t *>(p.peer_out[k] + off) = w;
       }
     }
   }
@@ -1031,6 +1057,46 @@ static cudaError_t launch_t(const CUtensorMap &tmK, const CUtensorMap &tmV, cons
   }
   e = cudaLaunchKernelEx(&lm, merge_kernel<D>, p);
   if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+// Cross-rank completion signal for the fused reassembly.
+// Thread k publishes "my slice of this step is in your output" to peer k
+// (release, system scope, after the stream-ordered merge kernel completed) and
+// waits for peer k's flag in its own pad (acquire).  The epoch is a device
+// counter bumped once per call, so CUDA-graph replays need no host update.
+// A bounded spin (timeout_ns of %globaltimer) reports through *err instead of
+// hanging the GPU.
+__global__ void peer_barrier_kernel(PeerBarrierParams p) {
+  __shared__ uint32_t epoch_s;
+  if (threadIdx.x == 0) {
+    epoch_s = *p.counter + 1;
+    *p.counter = epoch_s;
+  }
+  __syncthreads();
+  const uint32_t epoch = epoch_s;
+  const int k = threadIdx.x;
+  if (k >= p.n) return;
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.pads[k] + p.rank), "r"(epoch) : "memory");
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+  const uint32_t *mine = p.pads[p.rank] + k;
+  for (;;) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
+    if (static_cast<int32_t>(v - epoch) >= 0) break;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    if (t - t0 > p.timeout_ns) {
+      atomicExch(p.err, 1u);
+      break;
+    }
+  }
+}
+
+cudaError_t launch_peer_barrier(const PeerBarrierParams &p, cudaStream_t s) {
+  peer_barrier_kernel<<<1, 32, 0, s>>>(p);
   return cudaGetLastError();
 }
 

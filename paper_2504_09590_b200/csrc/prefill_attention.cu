@@ -18,8 +18,10 @@
 //    (dense map: entry e holds tokens [e*bs, ...); general map (f3): prefix of
 //    the fill counts) and streams each 16-slot chunk's K and V tiles with one
 //    5-D TMA load each (128B swizzle, same tensor maps as decode) into a 4-stage
-//    mbarrier ring; chunks whose first live token lies past the tile's last
-//    query position are never loaded.
+//    mbarrier ring (full: TMA bytes, empty: one arrive per consumer warp);
+//    chunks whose first live token lies past the tile's last query position
+//    are never loaded.  Each stage's chunk metadata (live slot range, token of
+//    slot 0, direction) is written with st.async onto the same full barrier.
 //  * 8 consumer warps, 16 rows each, FA2-style on bf16 mma.sync m16n8k16 with
 //    fp32 accumulation: S = Q.K^T (Q fragments in registers, K via ldmatrix),
 //    causal + direction mask by token index (slot s of a chunk holds token
@@ -40,10 +42,74 @@ namespace {
 constexpr int kStages = 4;
 constexpr int kConsumerWarps = 8;
 constexpr int kRowsPerTile = 16 * kConsumerWarps;
-constexpr int kLast = 1 << 8;   // meta flag: no more chunks
+constexpr int kLast = 1 << 8;   // chunk-metadata flag: no more chunks
 
 __device__ __forceinline__ uint32_t pswz(int row, int c) {
   return static_cast<uint32_t>(row * 128 + ((c ^ (row & 7)) << 4));
+}
+
+// The request's 16-slot chunks in logical entry order, skipping dead chunks
+// and chunks whose first live token lies past the tile's last query (run by the
+// producer warp).  Entries are read 32 at a time into a lane-distributed window
+// (lane i: entry wb + i) and broadcast by shuffle, keeping global-load latency
+// off the per-chunk path.
+struct ChunkWalk {
+  int e, c, F, E, wb;    // entry, chunk in entry, first token of entry, entries, window base
+  int wblk, wdir, wfill; // this lane's window entry
+  int blk, dir, fill;    // current entry (warp-uniform)
+  bool have;
+};
+
+__device__ __forceinline__ void walk_window(const PrefillParams &p, int r, int L, ChunkWalk &w, int wb) {
+  const int e = wb + static_cast<int>(threadIdx.x & 31);
+  w.wb = wb;
+  w.wblk = w.wdir = w.wfill = 0;
+  if (e < w.E) {
+    w.wblk = __ldg(p.bt + static_cast<int64_t>(r) * p.bt_stride + e);
+    w.wdir = __ldg(p.dirs + static_cast<int64_t>(r) * p.dir_rs + static_cast<int64_t>(e) * p.dir_cs);
+    w.wfill = p.fills ? static_cast<int>(__ldg(p.fills + static_cast<int64_t>(r) * p.fill_rs + e))
+                      : min(p.bs, L - e * p.bs);
+  }
+}
+
+__device__ __forceinline__ void walk_init(const PrefillParams &p, int r, int L, ChunkWalk &w) {
+  w.e = 0;
+  w.F = 0;
+  w.E = p.fills ? __ldg(p.nent + r) : (L + p.bs - 1) / p.bs;
+  w.have = false;
+  walk_window(p, r, L, w, 0);
+}
+
+__device__ __forceinline__ bool walk_next(const PrefillParams &p, int r, int L, int pos_max,
+                                          ChunkWalk &w, int &lo, int &hi, int &tb) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const int bs = p.bs;
+  while (w.e < w.E && w.F <= pos_max) {
+    if (!w.have) {
+      if (w.e - w.wb >= 32) walk_window(p, r, L, w, w.e);
+      const int idx = w.e - w.wb;
+      w.blk = __shfl_sync(FULL, w.wblk, idx);
+      w.dir = __shfl_sync(FULL, w.wdir, idx);
+      w.fill = __shfl_sync(FULL, w.wfill, idx);
+      w.c = 0;
+      w.have = true;
+    }
+    const int lo_s = w.dir ? bs - w.fill : 0, hi_s = w.dir ? bs : w.fill;
+    while (w.c < bs / 16) {
+      const int c = w.c++;
+      lo = max(lo_s - 16 * c, 0);
+      hi = min(hi_s - 16 * c, 16);
+      if (lo >= hi) continue;
+      tb = w.dir ? w.F + bs - 1 - 16 * c : w.F + 16 * c;   // token of chunk slot 0
+      const int first_tok = w.dir ? tb - (hi - 1) : tb + lo;
+      if (first_tok > pos_max) continue;
+      return true;
+    }
+    w.F += w.fill;
+    ++w.e;
+    w.have = false;
+  }
+  return false;
 }
 
 }  // namespace
@@ -75,8 +141,9 @@ __global__ void __launch_bounds__(32 * (kConsumerWarps + 1), 1)
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t *gbase = smem_raw + (base - raw);
-  int4 *metas = reinterpret_cast<int4 *>(gbase + kStages * SLOT_BYTES);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(metas + kStages);   // full[S], empty[S]
+  int4 *metas = reinterpret_cast<int4 *>(gbase + kStages * SLOT_BYTES);     // per-stage chunk metadata
+  uint64_t *bars = reinterpret_cast<uint64_t *>(metas + kStages);          // full[S], empty[S]
+  const uint32_t metas0 = smem_u32(metas);
   const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * kStages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -92,50 +159,51 @@ __global__ void __launch_bounds__(32 * (kConsumerWarps + 1), 1)
   __syncthreads();
 
   if (warp == kConsumerWarps) {
+    ChunkWalk walk;
+    walk_init(p, r, L, walk);
+    int lo, hi, tb;
     // ------------------------------------------------------------ producer
-    if (lane != 0) return;
+    // The chunk metadata rides on the stage's full barrier (st.async, 16
+    // transaction bytes), so consumers see it exactly when they see the tiles.
     const uint64_t pol = policy_evict_first();
-    const int bs = p.bs;
-    const int E = p.fills ? __ldg(p.nent + r) : (L + bs - 1) / bs;
-    const int64_t bt_row = static_cast<int64_t>(r) * p.bt_stride;
-    const int64_t dir_row = static_cast<int64_t>(r) * p.dir_rs;
-    int it = 0, F = 0;
-    auto acquire = [&](int i) {
-      const int round = i / kStages;
-      if (round > 0) mbar_wait(empty0 + 8 * (i % kStages), (round - 1) & 1);
-    };
-    for (int e = 0; e < E && F <= pos_max; ++e) {
-      const int blk = __ldg(p.bt + bt_row + e);
-      const int dir = __ldg(p.dirs + dir_row + static_cast<int64_t>(e) * p.dir_cs);
-      const int fill = p.fills ? static_cast<int>(__ldg(p.fills + static_cast<int64_t>(r) * p.fill_rs + e))
-                               : min(bs, L - e * bs);
-      const int lo_s = dir ? bs - fill : 0, hi_s = dir ? bs : fill;
-      for (int c = 0; c < bs / 16; ++c) {
-        const int lo = max(lo_s - 16 * c, 0), hi = min(hi_s - 16 * c, 16);
-        if (lo >= hi) continue;
-        const int tb = dir ? F + bs - 1 - 16 * c : F + 16 * c;   // token of chunk slot 0
-        const int first_tok = dir ? tb - (hi - 1) : tb + lo;
-        if (first_tok > pos_max) continue;
-        acquire(it);
-        const int st = it % kStages;
-        metas[st] = make_int4(lo, hi, tb, dir);
+    int it = 0;
+    for (; walk_next(p, r, L, pos_max, walk, lo, hi, tb); ++it) {
+      if (lane == 0) {
+        const int st = it % kStages, round = it / kStages;
+        if (round > 0) mbar_wait(empty0 + 8 * st, (round - 1) & 1);
         const uint32_t fb = full0 + 8 * st;
-        mbar_arrive_expect_tx(fb, SLOT_BYTES);
+        mbar_arrive_expect_tx(fb, SLOT_BYTES + 16);
+        st_async_v4(metas0 + 16 * st, make_int4(lo, hi, tb, walk.dir), fb);
         const uint32_t dk = base + st * SLOT_BYTES;
-        tma_load_5d(dk, &tmK, 0, 16 * c, 0, h, blk, fb, pol);
-        tma_load_5d(dk + KV_BYTES, &tmV, 0, 16 * c, 0, h, blk, fb, pol);
-        ++it;
+        const int c = walk.c - 1;
+        tma_load_5d(dk, &tmK, 0, 16 * c, 0, h, walk.blk, fb, pol);
+        tma_load_5d(dk + KV_BYTES, &tmV, 0, 16 * c, 0, h, walk.blk, fb, pol);
       }
-      F += fill;
+      __syncwarp();
     }
-    acquire(it);
-    metas[it % kStages] = make_int4(0, 0, 0, kLast);
-    mbar_arrive(full0 + 8 * (it % kStages));
+    if (lane == 0) {   // terminator stage: metadata only
+      const int st = it % kStages, round = it / kStages;
+      if (round > 0) mbar_wait(empty0 + 8 * st, (round - 1) & 1);
+      const uint32_t fb = full0 + 8 * st;
+      mbar_arrive_expect_tx(fb, 16);
+      st_async_v4(metas0 + 16 * st, make_int4(0, 0, 0, kLast), fb);
+    }
     return;
   }
 
   // ------------------------------------------------------------ consumers
+  if (row0 + 16 * warp >= row_end) {   // no live rows in this warp (short tile, decode rows):
+    for (int it = 0;; ++it) {          // keep the ring moving, skip the math
+      const int st = it % kStages;
+      mbar_wait(full0 + 8 * st, (it / kStages) & 1);
+      if (metas[st].w & kLast) return;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8 * st);
+    }
+  }
   const int rA = row0 + 16 * warp + (lane >> 2), rB = rA + 8;
+  // earliest query position of this warp's rows (rows are in position order)
+  const int pos_warp_min = L - n + (row0 + 16 * warp) / g;
   const bool okA = rA < row_end, okB = rB < row_end;
   const int posA = okA ? L - n + rA / g : -1, posB = okB ? L - n + rB / g : -1;
   auto qrow = [&](int row) {
@@ -179,15 +247,23 @@ __global__ void __launch_bounds__(32 * (kConsumerWarps + 1), 1)
     }
     // ---- direction + causal mask by token index, scale to the log2 domain
     float sv4[2][4] = {{s0[0], s0[1], s0[2], s0[3]}, {s1[0], s1[1], s1[2], s1[3]}};
+    const int max_tok = dir ? tb - lo : tb + hi - 1;
+    if (lo == 0 && hi == 16 && max_tok <= pos_warp_min) {   // whole chunk visible to every row
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
+      for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int col = nt * 8 + k0 + (e & 1);
-        const int tok = dir ? tb - col : tb + col;
-        const bool ok = col >= lo && col < hi && tok <= ((e >> 1) ? posB : posA);
-        sv4[nt][e] = ok ? sv4[nt][e] * p.scale_log2 : -INFINITY;
-      }
+        for (int e = 0; e < 4; ++e) sv4[nt][e] *= p.scale_log2;
+    } else {
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int col = nt * 8 + k0 + (e & 1);
+          const int tok = dir ? tb - col : tb + col;
+          const bool ok = col >= lo && col < hi && tok <= ((e >> 1) ? posB : posA);
+          sv4[nt][e] = ok ? sv4[nt][e] * p.scale_log2 : -INFINITY;
+        }
+    }
     float mxA = fmaxf(fmaxf(sv4[0][0], sv4[0][1]), fmaxf(sv4[1][0], sv4[1][1]));
     float mxB = fmaxf(fmaxf(sv4[0][2], sv4[0][3]), fmaxf(sv4[1][2], sv4[1][3]));
     mxA = fmaxf(mxA, __shfl_xor_sync(FULL, mxA, 1));

@@ -91,3 +91,63 @@ def decode_step(shard: HeadShard, pool, block_tables, dirs, seq_lens_before, cu_
     if gather and shard.tp > 1:
         return gather_heads(out_local_hm, out_global_hm, group)
     return out_local_hm
+
+
+class PeerReassembly:
+    """Fused reassembly over NVLink: every rank's decode kernels store its
+    head slice straight into every peer's global head-major output, then one stream-ordered
+    peer barrier publishes completion -- no separate all-gather.
+
+    Plumbing only: each rank allocates its global output [n_layers][H_q][B][d] and a flag
+    pad with torch, exports them with torch's CUDA IPC (``reduce_tensor``, the mechanism of
+    torch.multiprocessing) through the process group, and maps the peers' buffers (P2P over
+    NVLink between GPUs; also valid for several ranks on one GPU).  The stores and the
+    barrier are libbkv kernels (bkv_decode_multi_out, bkv_peer_barrier).
+    """
+
+    def __init__(self, shard: HeadShard, n_layers: int, batch: int, head_dim: int, device, group=None):
+        from torch.multiprocessing.reductions import reduce_tensor
+        self.shard = shard
+        hq, hl = shard.num_q_heads, len(shard.q_heads)
+        self.glob = torch.zeros((n_layers, hq, batch, head_dim), dtype=torch.bfloat16, device=device)
+        self.pads = torch.zeros((shard.tp,), dtype=torch.int32, device=device)
+        torch.cuda.synchronize(device)
+        mine = (reduce_tensor(self.glob), reduce_tensor(self.pads))
+        allh = [None] * shard.tp
+        dist.all_gather_object(allh, mine, group=group)
+        self._peer_tensors = []   # keep the mapped peer tensors alive
+        bases, pads = [], []
+        for k, (hg, hp) in enumerate(allh):
+            if k == shard.rank:
+                g_k, p_k = self.glob, self.pads
+            else:
+                g_k, p_k = hg[0](*hg[1]), hp[0](*hp[1])
+                self._peer_tensors += [g_k, p_k]
+            bases.append(g_k.data_ptr())
+            pads.append(p_k.data_ptr())
+        esz = self.glob.element_size()
+        self.layer_bytes = hq * batch * head_dim * esz
+        self.slice_off = shard.rank * hl * batch * head_dim * esz
+        self.peer_bases = [b for k, b in enumerate(bases) if k != shard.rank]
+        self.pad_ptrs = pads
+        self.counter = torch.zeros(1, dtype=torch.int32, device=device)
+        self.err = torch.zeros(1, dtype=torch.int32, device=device)
+        torch.cuda.synchronize(device)
+        dist.barrier(group)
+
+    def local_out(self, layer: int) -> torch.Tensor:
+        """This rank's slice of its own global output, head-major [H_q_local][B][d]."""
+        hl = len(self.shard.q_heads)
+        return self.glob[layer, self.shard.rank * hl:(self.shard.rank + 1) * hl]
+
+    def peer_outs(self, layer: int):
+        return [b + layer * self.layer_bytes + self.slice_off for b in self.peer_bases]
+
+    def barrier(self, timeout_ns: int = 5_000_000_000):
+        from .bkv import peer_barrier
+        peer_barrier(self.pad_ptrs, self.shard.rank, self.counter, self.err, timeout_ns)
+
+    def check(self):
+        """Raise if a peer barrier timed out (call outside timed regions)."""
+        if int(self.err.item()) != 0:
+            raise RuntimeError("bkv_peer_barrier timed out: a peer rank did not arrive")

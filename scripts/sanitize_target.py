@@ -32,3 +32,39 @@ for sh in (Shape("s1", 4, 4, 64, 16, 8, 0.5, "uniform", 300, 1, 1, uniform_max=3
     bkv.kv_restore(pool, sm[:17], ck, cv)
     torch.cuda.synchronize()
     print(sh.name, "ok", float(out.float().abs().mean()))
+
+# round r01c additions: general maps (f3), fused decode step, fused checkpoint (f1), prefill (f4)
+from tests.test_prefill_oracle import query_counts
+from synth import q_rows_np
+for sh in (Shape("g1", 4, 4, 64, 16, 8, 0.5, "uniform", 300, 1, 1, uniform_max=300),
+           Shape("g2", 8, 1, 128, 32, 8, 0.5, "uniform", 300, 1, 1, uniform_max=300)):
+    case = make_case(sh, 2, general=True, share_prob=1.0)
+    lay = case.layout
+    ks, vs, q = dense_case(case)
+    pool = bkv.KVPool.empty(lay.num_blocks, sh.num_kv_heads, sh.block_size, sh.head_dim)
+    pool.k.zero_(); pool.v.zero_()
+    bt = torch.from_numpy(lay.block_tables).cuda(); dirs = torch.from_numpy(lay.dirs).cuda()
+    fills = torch.from_numpy(lay.fills).cuda(); nent = torch.from_numpy(lay.num_entries).cuda()
+    before = np.maximum(lay.lens - 1, 0).astype(np.int32)
+    kn, vn, cu = ragged(ks, vs, before, np.zeros(lay.batch, np.int64))
+    bkv.kv_append(pool, bt, dirs, torch.zeros(lay.batch, dtype=torch.int32, device="cuda"),
+                  torch.from_numpy(cu).cuda(), g(kn), g(vn), fills=fills, num_entries=nent)
+    kd = np.stack([ks[r][lay.lens[r] - 1] for r in range(lay.batch)])
+    vd = np.stack([vs[r][lay.lens[r] - 1] for r in range(lay.batch)])
+    lens = torch.from_numpy(lay.lens).cuda()
+    out = bkv.decode_step(pool, bt, dirs, lens, g(kd), g(vd), g(q), fills=fills, num_entries=nent)
+    out2 = bkv.paged_decode_attention(pool, bt, dirs, lens, g(q), fills=fills, num_entries=nent)
+    n = query_counts(lay.lens, np.random.default_rng(0))
+    qp = np.concatenate([q_rows_np(0, 0, r, int(n[r]), range(sh.num_q_heads), sh.head_dim, sh.num_q_heads)
+                         for r in range(lay.batch)])
+    cuq = torch.from_numpy(np.concatenate([[0], np.cumsum(n)]).astype(np.int32)).cuda()
+    op = bkv.paged_prefill_attention(pool, bt, dirs, lens, cuq, g(qp), fills=fills, num_entries=nent)
+    # fused lazy checkpoint: every new token evicts into its own checkpoint row
+    ev = torch.arange(lay.batch, dtype=torch.int32, device="cuda")
+    ckk = torch.empty((lay.batch, sh.num_kv_heads, sh.head_dim), dtype=torch.bfloat16, device="cuda")
+    ckv = torch.empty_like(ckk)
+    bkv.kv_append_checkpoint(pool, bt, dirs, torch.from_numpy(before).cuda(),
+                             torch.arange(lay.batch + 1, dtype=torch.int32, device="cuda"), g(kd), g(vd),
+                             ev, ckk, ckv, fills=fills, num_entries=nent)
+    torch.cuda.synchronize()
+    print(sh.name, "general ok", float(out.float().abs().mean()), float(op.float().abs().mean()))

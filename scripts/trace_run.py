@@ -1,4 +1,7 @@
-"""Dev: run one decode launch with BKV_TRACE and summarise the per-warp timeline."""
+"""Dev: run one decode launch with BKV_TRACE and summarise the per-warp timeline.
+
+Needs a trace build: BKV_BUILD_TRACE=1 python paper_2504_09590_b200/build.py --force
+"""
 import os, sys
 os.environ.setdefault("BKV_TRACE", "64")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
