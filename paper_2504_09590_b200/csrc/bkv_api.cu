@@ -434,6 +434,8 @@ bkv_status bkv_decode_multi_out(const bkv_kv_pool *pool, const bkv_block_map *ma
   if (k_new && (!aligned16(k_new) || !aligned16(v_new)))
     return fail(BKV_ERR_INVALID_ARGUMENT, "k_new/v_new must be 16-byte aligned");
   if (n_peers > 0 && !peer_outs) return fail(BKV_ERR_INVALID_ARGUMENT, "peer_outs is NULL");
+  if (n_peers < 0 || n_peers > bkv::kMaxPeers)
+    return fail(BKV_ERR_UNSUPPORTED, "n_peers %d outside [0, %d]", n_peers, bkv::kMaxPeers);
   return decode_impl(pool, map, seq_lens, max_seq_len, k_new, v_new, q, q_stride_seq,
                      q_stride_head, num_q_heads, softmax_scale, out, o_stride_seq, o_stride_head,
                      workspace, workspace_bytes, flags, stream, peer_outs, n_peers);

@@ -95,16 +95,6 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_
       : "memory");
 }
 
-// 16-byte store into (this CTA's) shared memory through the async proxy, counted
-// as 16 transaction bytes on `bar` -- hands small metadata to the consumers of
-// an mbarrier stage with the same completion semantics as the TMA data.
-__device__ __forceinline__ void st_async_v4(uint32_t dst, int4 v, uint32_t bar) {
-  asm volatile(
-      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.s32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(dst),
-      "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(bar)
-      : "memory");
-}
-
 // ---------------------------------------------------------- shared memory
 // 1-D bulk store shared -> global (async proxy, bulk-group completion)
 __device__ __forceinline__ void bulk_store(void *dst, uint32_t src, uint32_t bytes) {
@@ -188,9 +178,15 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint3
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-// named barrier over `n` threads (a multiple of 32), id 1..15 (0 = __syncthreads)
+// named barrier over `n` threads (a multiple of 32), id 1..15 (0 = __syncthreads).
+// Non-.aligned forms: the participating warps reach the barrier from different
+// code sites (bar.sync / bar.arrive are the .aligned variants).
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+// arrive without waiting (the producer side of a named-barrier handoff)
+__device__ __forceinline__ void named_bar_arrive(int id, int n) {
+  asm volatile("barrier.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
 // ------------------------------------------------------- gpu-scope sync

@@ -21,7 +21,7 @@
 //    mbarrier ring (full: TMA bytes, empty: one arrive per consumer warp);
 //    chunks whose first live token lies past the tile's last query position
 //    are never loaded.  Each stage's chunk metadata (live slot range, token of
-//    slot 0, direction) is written with st.async onto the same full barrier.
+//    slot 0, direction) is handed to the consumers through a named barrier.
 //  * 8 consumer warps, 16 rows each, FA2-style on bf16 mma.sync m16n8k16 with
 //    fp32 accumulation: S = Q.K^T (Q fragments in registers, K via ldmatrix),
 //    causal + direction mask by token index (slot s of a chunk holds token
@@ -143,7 +143,6 @@ __global__ void __launch_bounds__(32 * (kConsumerWarps + 1), 1)
   uint8_t *gbase = smem_raw + (base - raw);
   int4 *metas = reinterpret_cast<int4 *>(gbase + kStages * SLOT_BYTES);     // per-stage chunk metadata
   uint64_t *bars = reinterpret_cast<uint64_t *>(metas + kStages);          // full[S], empty[S]
-  const uint32_t metas0 = smem_u32(metas);
   const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * kStages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -163,31 +162,35 @@ __global__ void __launch_bounds__(32 * (kConsumerWarps + 1), 1)
     walk_init(p, r, L, walk);
     int lo, hi, tb;
     // ------------------------------------------------------------ producer
-    // The chunk metadata rides on the stage's full barrier (st.async, 16
-    // transaction bytes), so consumers see it exactly when they see the tiles.
+    // Each stage's chunk metadata is handed over through named barrier
+    // 1 + stage (producer bar.arrive, consumers bar.sync: release/acquire at
+    // CTA scope); the tiles themselves complete on the stage's full mbarrier.
     const uint64_t pol = policy_evict_first();
     int it = 0;
     for (; walk_next(p, r, L, pos_max, walk, lo, hi, tb); ++it) {
+      const int st = it % kStages;
       if (lane == 0) {
-        const int st = it % kStages, round = it / kStages;
+        const int round = it / kStages;
         if (round > 0) mbar_wait(empty0 + 8 * st, (round - 1) & 1);
+        metas[st] = make_int4(lo, hi, tb, walk.dir);
         const uint32_t fb = full0 + 8 * st;
-        mbar_arrive_expect_tx(fb, SLOT_BYTES + 16);
-        st_async_v4(metas0 + 16 * st, make_int4(lo, hi, tb, walk.dir), fb);
+        mbar_arrive_expect_tx(fb, SLOT_BYTES);
         const uint32_t dk = base + st * SLOT_BYTES;
         const int c = walk.c - 1;
         tma_load_5d(dk, &tmK, 0, 16 * c, 0, h, walk.blk, fb, pol);
         tma_load_5d(dk + KV_BYTES, &tmV, 0, 16 * c, 0, h, walk.blk, fb, pol);
       }
       __syncwarp();
+      named_bar_arrive(1 + st, 32 * (kConsumerWarps + 1));
     }
-    if (lane == 0) {   // terminator stage: metadata only
-      const int st = it % kStages, round = it / kStages;
+    const int st = it % kStages;   // terminator stage: metadata only
+    if (lane == 0) {
+      const int round = it / kStages;
       if (round > 0) mbar_wait(empty0 + 8 * st, (round - 1) & 1);
-      const uint32_t fb = full0 + 8 * st;
-      mbar_arrive_expect_tx(fb, 16);
-      st_async_v4(metas0 + 16 * st, make_int4(0, 0, 0, kLast), fb);
+      metas[st] = make_int4(0, 0, 0, kLast);
     }
+    __syncwarp();
+    named_bar_arrive(1 + st, 32 * (kConsumerWarps + 1));
     return;
   }
 
@@ -195,8 +198,9 @@ __global__ void __launch_bounds__(32 * (kConsumerWarps + 1), 1)
   if (row0 + 16 * warp >= row_end) {   // no live rows in this warp (short tile, decode rows):
     for (int it = 0;; ++it) {          // keep the ring moving, skip the math
       const int st = it % kStages;
-      mbar_wait(full0 + 8 * st, (it / kStages) & 1);
+      named_bar_sync(1 + st, 32 * (kConsumerWarps + 1));
       if (metas[st].w & kLast) return;
+      mbar_wait(full0 + 8 * st, (it / kStages) & 1);
       __syncwarp();
       if (lane == 0) mbar_arrive(empty0 + 8 * st);
     }
@@ -230,9 +234,10 @@ __global__ void __launch_bounds__(32 * (kConsumerWarps + 1), 1)
 
   for (int it = 0;; ++it) {
     const int st = it % kStages;
-    mbar_wait(full0 + 8 * st, (it / kStages) & 1);
+    named_bar_sync(1 + st, 32 * (kConsumerWarps + 1));
     const int4 meta = metas[st];
     if (meta.w & kLast) break;
+    mbar_wait(full0 + 8 * st, (it / kStages) & 1);
     const int lo = meta.x, hi = meta.y, tb = meta.z, dir = meta.w;
     const uint32_t sk = base + st * SLOT_BYTES, sv = sk + KV_BYTES;
     // ---- S = Q.K^T (16 rows x 16 slots)
