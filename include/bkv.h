@@ -368,6 +368,29 @@ BKV_API bkv_status bkv_paged_prefill_attention(const bkv_kv_pool *pool, const bk
                                                int64_t o_stride_tok, int64_t o_stride_head,
                                                bkv_stream_t stream);
 
+/*
+ * bkv_paged_mixed_attention -- the paper's dispatch of a mixed batch
+ * ("the concatenated prefill requests followed by the
+ * decode requests", a length table, each part routed to its kernel).
+ * Requests [0, num_prefill_seqs) are served by bkv_paged_prefill_attention
+ * (their query rows: cu_q as there, num_prefill_rows = cu_q[num_prefill_seqs]
+ * given on the host); requests [num_prefill_seqs, num_seqs) are decodes with
+ * ONE query row each, stored contiguously after the prefill rows (request
+ * num_prefill_seqs + j at row num_prefill_rows + j), served by the split-K
+ * decode kernel (workspace, flags as bkv_paged_decode_attention_ex).  Same
+ * results as one bkv_paged_prefill_attention over the whole batch (up to fp32
+ * summation order); two launches on `stream`.
+ */
+BKV_API bkv_status bkv_paged_mixed_attention(const bkv_kv_pool *pool, const bkv_block_map *map,
+                                             const int32_t *seq_lens, const int32_t *cu_q,
+                                             int32_t num_prefill_seqs, int32_t num_prefill_rows,
+                                             int32_t max_q_len, int32_t max_seq_len, const void *q,
+                                             int64_t q_stride_tok, int64_t q_stride_head,
+                                             int32_t num_q_heads, float softmax_scale, void *out,
+                                             int64_t o_stride_tok, int64_t o_stride_head,
+                                             void *workspace, size_t workspace_bytes,
+                                             uint32_t flags, bkv_stream_t stream);
+
 /* Workspace bytes for bkv_paged_decode_attention on the CURRENT device
  * (depends on the SM count); 0 on error (see bkv_last_error). */
 BKV_API size_t bkv_decode_workspace_size(int32_t num_seqs, int32_t num_q_heads, int32_t num_kv_heads,

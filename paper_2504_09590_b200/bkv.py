@@ -48,7 +48,8 @@ EXPORTS = ("bkv_kv_append", "bkv_paged_decode_attention", "bkv_decode_workspace_
            "bkv_validate_layout_host", "bkv_status_string", "bkv_last_error", "bkv_version",
            "bkv_kv_checkpoint", "bkv_kv_restore", "bkv_paged_decode_attention_ex",
            "bkv_decode_step", "bkv_validate_block_map_host", "bkv_kv_append_checkpoint",
-           "bkv_paged_prefill_attention", "bkv_decode_multi_out", "bkv_peer_barrier")
+           "bkv_paged_prefill_attention", "bkv_decode_multi_out", "bkv_peer_barrier",
+           "bkv_paged_mixed_attention")
 BKV_FLAG_PDL = 1   # include/bkv.h: programmatic dependent launch (seq_lens not written by the previous kernel)
 
 
@@ -89,6 +90,10 @@ def lib():
                 L.bkv_decode_multi_out.restype = ctypes.c_int
                 L.bkv_peer_barrier.argtypes = [P, i32, i32, P, P, ctypes.c_uint64, P]
                 L.bkv_peer_barrier.restype = ctypes.c_int
+                L.bkv_paged_mixed_attention.argtypes = [
+                    ctypes.POINTER(_Pool), ctypes.POINTER(_Map), P, P, i32, i32, i32, i32, P, i64, i64, i32,
+                    ctypes.c_float, P, i64, i64, P, ctypes.c_size_t, ctypes.c_uint32, P]
+                L.bkv_paged_mixed_attention.restype = ctypes.c_int
                 L.bkv_decode_workspace_size.argtypes = [i32, i32, i32, i32]
                 L.bkv_decode_workspace_size.restype = ctypes.c_size_t
                 L.bkv_validate_layout_host.argtypes = [P, i32, P, i32, i32, i32, P, i32, i32, i32, P]
@@ -414,6 +419,40 @@ def peer_barrier(pads, rank, counter, err, timeout_ns=5_000_000_000, stream=None
     rc = lib().bkv_peer_barrier(arr, n, int(rank), counter.data_ptr(), err.data_ptr(), int(timeout_ns),
                                 _stream_ptr(stream))
     _check(rc, "bkv_peer_barrier")
+
+
+def paged_mixed_attention(pool: KVPool, block_tables, dirs, seq_lens, cu_q, q, num_prefill_seqs,
+                          num_prefill_rows, max_q_len=None, max_seq_len=None, softmax_scale=None,
+                          out=None, ws=None, stream=None, pdl=False, fills=None, num_entries=None):
+    """bkv_paged_mixed_attention (P:762-765 dispatch): requests [0, P) prefill through the causal
+    kernel, requests [P, B) decode (one row each, rows after the prefill rows) through the
+    split-K decode kernel.  q/out bf16 [total][Hq][d]."""
+    p, m = pool.c(), block_map(block_tables, dirs, fills, num_entries)
+    for t, n in ((seq_lens, "seq_lens"), (cu_q, "cu_q")):
+        _dev(t, n, torch.int32)
+    _dev(q, "q", torch.bfloat16)
+    T, Hq, d = q.shape
+    if out is None:
+        out = torch.empty((T, Hq, d), dtype=torch.bfloat16, device=q.device)
+    _dev(out, "out", torch.bfloat16)
+    if q.stride(2) != 1 or out.stride(2) != 1:
+        raise BkvError("q/out must have a unit stride along head_dim")
+    if softmax_scale is None:
+        softmax_scale = 1.0 / math.sqrt(d)
+    if max_q_len is None:
+        max_q_len = int((cu_q[1:] - cu_q[:-1]).max().item()) if cu_q.numel() > 1 else 0
+    if max_seq_len is None:
+        max_seq_len = block_tables.shape[1] * pool.block_size
+    B = block_tables.shape[0]
+    if ws is None:
+        ws = workspace(max(1, B - int(num_prefill_seqs)), Hq, pool.num_kv_heads, d, q.device, stream)
+    rc = lib().bkv_paged_mixed_attention(
+        ctypes.byref(p), ctypes.byref(m), seq_lens.data_ptr(), cu_q.data_ptr(), int(num_prefill_seqs),
+        int(num_prefill_rows), int(max_q_len), int(max_seq_len), q.data_ptr(), q.stride(0), q.stride(1), Hq,
+        float(softmax_scale), out.data_ptr(), out.stride(0), out.stride(1), ws.data_ptr(), ws.numel(),
+        BKV_FLAG_PDL if pdl else 0, _stream_ptr(stream))
+    _check(rc, "bkv_paged_mixed_attention")
+    return out
 
 
 def validate_layout_host(block_tables, dirs, seq_lens, num_blocks, block_size, require_nonempty=True):

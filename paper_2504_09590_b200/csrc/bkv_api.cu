@@ -582,6 +582,49 @@ bkv_status bkv_paged_prefill_attention(const bkv_kv_pool *pool, const bkv_block_
   return BKV_OK;
 }
 
+bkv_status bkv_paged_mixed_attention(const bkv_kv_pool *pool, const bkv_block_map *map,
+                                     const int32_t *seq_lens, const int32_t *cu_q,
+                                     int32_t num_prefill_seqs, int32_t num_prefill_rows,
+                                     int32_t max_q_len, int32_t max_seq_len, const void *q,
+                                     int64_t q_stride_tok, int64_t q_stride_head,
+                                     int32_t num_q_heads, float softmax_scale, void *out,
+                                     int64_t o_stride_tok, int64_t o_stride_head, void *workspace,
+                                     size_t workspace_bytes, uint32_t flags, bkv_stream_t stream) {
+  bkv_status s = check_map(map);
+  if (s) return s;
+  const int B = map->num_seqs;
+  if (num_prefill_seqs < 0 || num_prefill_seqs > B || num_prefill_rows < 0)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "num_prefill_seqs %d / num_prefill_rows %d out of range",
+                num_prefill_seqs, num_prefill_rows);
+  if (!aligned16(q) || !aligned16(out) || q_stride_tok % 8 || o_stride_tok % 8)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "q/out must be 16-byte aligned with strides multiple of 8");
+  // part 1: prefill requests [0, P) -- the causal kernel
+  bkv_block_map mp = *map;
+  mp.num_seqs = num_prefill_seqs;
+  if (num_prefill_seqs > 0 && max_q_len > 0) {
+    s = bkv_paged_prefill_attention(pool, &mp, seq_lens, cu_q, max_q_len, q, q_stride_tok,
+                                    q_stride_head, num_q_heads, softmax_scale, out, o_stride_tok,
+                                    o_stride_head, stream);
+    if (s) return s;
+  }
+  // part 2: decode requests [P, B), one query row each at rows num_prefill_rows + (r - P)
+  const int nd = B - num_prefill_seqs;
+  if (nd == 0) return BKV_OK;
+  bkv_block_map md = *map;
+  md.num_seqs = nd;
+  md.block_tables = map->block_tables + (int64_t)num_prefill_seqs * map->bt_stride;
+  md.dirs = map->dirs + (int64_t)num_prefill_seqs * map->dir_row_stride;
+  if (map->fills) {
+    md.fills = map->fills + (int64_t)num_prefill_seqs * map->fill_row_stride;
+    md.num_entries = map->num_entries + num_prefill_seqs;
+  }
+  const uint16_t *qd = static_cast<const uint16_t *>(q) + (int64_t)num_prefill_rows * q_stride_tok;
+  uint16_t *od = static_cast<uint16_t *>(out) + (int64_t)num_prefill_rows * o_stride_tok;
+  return decode_impl(pool, &md, seq_lens + num_prefill_seqs, max_seq_len, nullptr, nullptr, qd,
+                     q_stride_tok, q_stride_head, num_q_heads, softmax_scale, od, o_stride_tok,
+                     o_stride_head, workspace, workspace_bytes, flags, stream);
+}
+
 bkv_status bkv_validate_block_map_host(const bkv_block_map *map, const int32_t *seq_lens,
                                        int32_t num_blocks, int32_t block_size,
                                        int32_t require_nonempty, int64_t info[5]) {

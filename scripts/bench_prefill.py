@@ -77,7 +77,7 @@ def time_graph(fn, layers, iters, warmup=3):
     return float(np.median(ts)), ts
 
 
-def setup(shape, lay, tp, layers, n, seed=0, device="cuda"):
+def setup(shape, lay, tp, layers, n, seed=0, device="cuda", n_prefill=None):
     import torch
     import paper_2504_09590_b200 as bkv
     from synth import q_rows_torch
@@ -94,6 +94,17 @@ def setup(shape, lay, tp, layers, n, seed=0, device="cuda"):
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)
     args = (t(lay.block_tables), t(lay.dirs), t(lay.lens.astype(np.int32)), t(cu))
     max_n = int(n.max())
+    if n_prefill is not None:   # P:762-765 dispatch: prefill rows first, then one-row decodes
+        rows_p = int(cu[n_prefill])
+        max_np = int(n[:n_prefill].max()) if n_prefill else 0
+        ws = bkv.workspace(max(1, lay.batch - n_prefill), Hq, H, d, torch.device(device))
+        max_len = int(lay.lens.max())
+
+        def fn():
+            for p in pools:
+                bkv.paged_mixed_attention(p, *args, q, n_prefill, rows_p, max_q_len=max_np,
+                                          max_seq_len=max_len, out=out, ws=ws, pdl=True)
+        return fn, H, Hq, d
 
     def fn():
         for p in pools:
@@ -106,6 +117,10 @@ def main():
     ap.add_argument("--config", default="llama70b")
     ap.add_argument("--tp", type=int, default=1)
     ap.add_argument("--prefill", type=int, default=16, help="BE requests prefilling their whole prompt")
+    ap.add_argument("--no-decodes", action="store_true", help="only the prefill rows (n = 0 elsewhere)")
+    ap.add_argument("--one-kernel", action="store_true",
+                    help="serve the whole mixed batch with the prefill kernel (default: P:762-765 dispatch, "
+                         "prefill kernel + split-K decode kernel via bkv_paged_mixed_attention)")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cost-model", default=None, help="write phase,l_n,l_a,latency_us samples here")
@@ -119,11 +134,18 @@ def main():
     rng = np.random.default_rng(a.seed + 1)
     be = np.flatnonzero(lay.is_be)
     pre = rng.choice(be, size=min(a.prefill, be.size), replace=False)
-    n = np.ones(lay.batch, np.int32)
+    n = np.zeros(lay.batch, np.int32) if a.no_decodes else np.ones(lay.batch, np.int32)
     n[pre] = lay.lens[pre]
     kv_bytes = float(lay.lens.astype(np.int64).sum()) * 4 * shape.head_dim * (shape.num_kv_heads // a.tp)
     layers = max(4, int(math.ceil(500e6 / kv_bytes)))
-    fn, H, Hq, d = setup(shape, lay, a.tp, layers, n, a.seed)
+    dispatch = not a.one_kernel and not a.no_decodes
+    if dispatch:   # reorder the batch: prefill requests first (the paper's batch layout)
+        from dataclasses import replace
+        perm = np.concatenate([pre, np.setdiff1d(np.arange(lay.batch), pre)])
+        lay = replace(lay, lens=lay.lens[perm], is_be=lay.is_be[perm], block_tables=lay.block_tables[perm],
+                      dirs=lay.dirs[perm])
+        n = n[perm]
+    fn, H, Hq, d = setup(shape, lay, a.tp, layers, n, a.seed, n_prefill=len(pre) if dispatch else None)
     med, ts = time_graph(fn, layers, a.steps)
     flops = causal_flops(lay.lens.astype(np.int64), n.astype(np.int64), Hq, d)
     tpk, hbm, src = peaks()
@@ -134,11 +156,14 @@ def main():
         "dtype": "bf16", "data": "synthetic",
         "config": {"workload": f"{a.config} TP{a.tp} shard: {H} kv / {Hq} q heads x d{d}, bs{shape.block_size}, "
                                f"batch {lay.batch}: {len(pre)} BE requests prefilling their whole prompt "
-                               f"(n = L), {lay.batch - len(pre)} decodes (n = 1)",
-                   "prefill_tokens": int(n[pre].sum()), "decode_tokens": int(lay.batch - len(pre)),
-                   "layers_rotated": layers, "l2": "pools rotated, > L2", "cuda_graphs": True},
+                               f"(n = L), {int((n == 1).sum())} decodes (n = 1)",
+                   "prefill_tokens": int(n[pre].sum()), "decode_tokens": int((n == 1).sum()),
+                   "layers_rotated": layers, "l2": "pools rotated, > L2", "cuda_graphs": True,
+                   "dispatch": ("bkv_paged_mixed_attention: prefill kernel + split-K decode kernel"
+                                if dispatch else "bkv_paged_prefill_attention for every row")},
         "us_per_layer": med, "p10_us": float(np.percentile(ts, 10)), "p90_us": float(np.percentile(ts, 90)),
-        "roofline": {"bound": "tensor", "kernel": "bkv::prefill_kernel (mma.sync m16n8k16 bf16)",
+        "roofline": {"bound": "tensor", "kernel": "bkv::prefill_kernel (mma.sync m16n8k16 bf16)"
+                     + (" + bkv::decode_kernel" if dispatch else ""),
                      "achieved": achieved, "peak": tpk, "unit": "TFLOP/s", "frac": achieved / tpk,
                      "peak_source": src, "flops_per_launch": flops},
         "hbm_view": {"kv_bytes_per_launch": kv_bytes, "achieved_gbs": kv_bytes / (med * 1e-6) / 1e9,

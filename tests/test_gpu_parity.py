@@ -224,9 +224,13 @@ def test_gqa_equals_mha_with_repeated_kv_heads():
 
 
 # --------------------------------------- full-size configs, sampled requests
-def _full_size(cfg, tp=1, rank=0, sample=6, seed=0):
-    sh = CONFIGS[cfg]
-    case = make_case(cfg, seed)
+def _full_size(cfg, tp=1, rank=0, sample=6, seed=0, mode="attn", pdl=False):
+    """Full BASELINE-size batch on the GPU; the oracle checks a sample of requests one by one.
+    mode "attn": bkv_paged_decode_attention over the resident context; mode "step": the
+    bench's launch configuration -- the fused decode step (bkv_decode_step, PDL) appending
+    token L-1 of every request and attending over all L."""
+    sh = CONFIGS[cfg] if isinstance(cfg, str) else cfg
+    case = make_case(sh, seed)
     lay = case.layout
     kv_heads, q_heads = shard_heads(sh, tp, rank)
     Hl = len(kv_heads)
@@ -234,17 +238,26 @@ def _full_size(cfg, tp=1, rank=0, sample=6, seed=0):
     pool.k.zero_()
     pool.v.zero_()
     bt, dirs, lens = gpu_map(lay)
+    resident = lay.lens - (1 if mode == "step" else 0)
+    last_k, last_v = [], []
     for r0 in range(0, lay.batch, 32):   # generate on the GPU in request batches
         rs = range(r0, min(lay.batch, r0 + 32))
         kk, vv = zip(*[dense_kv_torch(case.seed, 0, r, int(lay.lens[r]), kv_heads, sh.head_dim,
                                       sh.num_kv_heads, DEV) for r in rs])
-        kn, vn = torch.cat(kk), torch.cat(vv)
-        cu = torch.tensor(np.concatenate([[0], np.cumsum(lay.lens[list(rs)])]), dtype=torch.int32, device=DEV)
+        last_k += [k[-1] for k in kk]
+        last_v += [v[-1] for v in vv]
+        kn = torch.cat([k[:resident[r]] for k, r in zip(kk, rs)])
+        vn = torch.cat([v[:resident[r]] for v, r in zip(vv, rs)])
+        cu = torch.tensor(np.concatenate([[0], np.cumsum(resident[list(rs)])]), dtype=torch.int32, device=DEV)
         sub_bt = bt[r0:r0 + len(rs)].contiguous()
         sub_dirs = dirs[r0:r0 + len(rs)].contiguous()
         bkv.kv_append(pool, sub_bt, sub_dirs, torch.zeros(len(rs), dtype=torch.int32, device=DEV), cu, kn, vn)
     q = torch.stack([q_torch(case.seed, 0, r, q_heads, sh.head_dim, DEV) for r in range(lay.batch)])
-    o = bkv.paged_decode_attention(pool, bt, dirs, lens, q)
+    if mode == "step":
+        o = bkv.decode_step(pool, bt, dirs, lens, torch.stack(last_k).contiguous(),
+                            torch.stack(last_v).contiguous(), q, pdl=pdl)
+    else:
+        o = bkv.paged_decode_attention(pool, bt, dirs, lens, q, pdl=pdl)
     torch.cuda.synchronize()
     # oracle on a sample of requests (longest, shortest, shared tails, random)
     rng = np.random.default_rng(seed + 100)
@@ -259,13 +272,34 @@ def _full_size(cfg, tp=1, rank=0, sample=6, seed=0):
         oracle.append(K, V, sub.block_tables, sub.dirs, np.zeros(1, np.int32), np.array([0, L], np.int32), k, v)
         qr = q_np(case.seed, 0, r, q_heads, sh.head_dim)[None]
         ref = oracle.attention(K, V, sub.block_tables, sub.dirs, sub.lens, qr, default_scale(sh.head_dim))
-        check_close(o[r:r + 1], ref, f"{cfg} r{r} L{L}")
+        check_close(o[r:r + 1], ref, f"{sh.name} r{r} L{L}")
     return o
 
 
 @pytest.mark.parametrize("cfg,tp,rank", [("opt13b", 1, 0), ("opt30b", 4, 2), ("llama70b", 1, 0), ("llama70b", 8, 7)])
 def test_full_size_sampled_parity(cfg, tp, rank):
     _full_size(cfg, tp, rank)
+
+
+@pytest.mark.parametrize("cfg,tp", [("opt13b", 1), ("llama70b", 8), ("opt30b", 1)])
+def test_full_size_bench_launch_config(cfg, tp):
+    """What bench.py times: the fused decode step with PDL at the full BASELINE batch."""
+    _full_size(cfg, tp, 0, mode="step", pdl=True, seed=1)
+
+
+@pytest.mark.parametrize("L0,bs,rt", [(8192, 32, 0.25), (8192, 16, 1.0), (512, 16, 0.0), (2048, 32, 0.75)])
+def test_sweep_config_sampled_parity(L0, bs, rt):
+    """BASELINE configs[4]: Llama-2-70B shape, context sweep 512-8K, block 16/32, RT:BE mix
+    (TP8 shard: 1 kv head / 8 q heads), full batch 256, sampled requests vs the oracle."""
+    from synth.workload import sweep_shape
+    _full_size(sweep_shape(L0, bs, rt), tp=8, rank=3, sample=4, seed=2, mode="step", pdl=True)
+
+
+def test_max_batch_2048():
+    """num_seqs at the ABI maximum (2048): the in-kernel plan arrays are full."""
+    sh = Shape("maxb", 4, 2, 64, 16, 2048, 0.5, "uniform", 96, 1, 1, uniform_max=96)
+    _full_size(sh, 1, 0, sample=8, seed=3, mode="step")
+    _full_size(sh, 1, 0, sample=8, seed=4, mode="attn")
 
 
 # ---------------------------------------------------------------- ABI errors

@@ -105,3 +105,29 @@ def test_prefill_long_context_llama_shard():
     n = np.minimum(lay2.lens, np.random.default_rng(4).integers(1, 300, keep)).astype(np.int32)
     o, ref = _run(case2, False, n, qs=0)
     check_close(o, ref, "llama shard")
+
+
+@pytest.mark.parametrize("cfg,general", [("tiny_gqa", False), ("tiny", True)])
+def test_mixed_dispatch_matches_oracle(cfg, general):
+    """bkv_paged_mixed_attention: prefill requests first, then one-row decodes."""
+    case = make_case(cfg, 12, general=general)
+    sh, lay = case.shape, case.layout
+    B = lay.batch
+    P = B // 2
+    n = np.ones(B, np.int32)
+    n[:P] = np.minimum(lay.lens[:P], 1 + np.arange(P) * 37)
+    ks, vs, K, V = pools(case, general)
+    q, cu = make_q(case, n, sh.num_q_heads, scale_log2=1)
+    ref = run_oracle(case, K, V, cu, q, general)
+    if general:
+        pool, _ = gpu_general_pool(case, ks, vs, sh.num_kv_heads)
+        bt, dirs, lens, fills, nent = gmap(lay)
+        kw = dict(fills=fills, num_entries=nent)
+    else:
+        pool, _ = gpu_pool_from_dense(case, ks, vs, sh.num_kv_heads)
+        bt, dirs, lens = gpu_map(lay)
+        kw = {}
+    o = bkv.paged_mixed_attention(pool, bt, dirs, lens, torch.from_numpy(cu).to(DEV), t_u16(q), P, int(cu[P]),
+                                  softmax_scale=default_scale(sh.head_dim), **kw)
+    torch.cuda.synchronize()
+    check_close(o, ref, cfg)
