@@ -120,6 +120,8 @@ struct PrefillParams {
 int prefill_smem_bytes(int head_dim);
 cudaError_t launch_prefill(const CUtensorMap &tmK, const CUtensorMap &tmV, const PrefillParams &p,
                            int head_dim, int max_q_len, cudaStream_t s);
+cudaError_t launch_prefill_tc(const CUtensorMap &tmK, const CUtensorMap &tmV, const PrefillParams &p,
+                              int max_q_len, cudaStream_t s);
 
 // cross-rank completion signal of the fused reassembly (f2)
 struct PeerBarrierParams {

@@ -31,6 +31,7 @@
 //    combined arithmetically: their scores are selected to -inf and their V
 //    fragment halves are masked to zero before the MMA (reading Q10).
 #include <math.h>
+#include <stdlib.h>
 
 #include "bkv_internal.h"
 #include "bkv_ptx.cuh"
@@ -362,6 +363,9 @@ static cudaError_t launch_prefill_t(const CUtensorMap &tmK, const CUtensorMap &t
 cudaError_t launch_prefill(const CUtensorMap &tmK, const CUtensorMap &tmV, const PrefillParams &p,
                            int head_dim, int max_q_len, cudaStream_t s) {
   if (p.B <= 0 || max_q_len <= 0) return cudaSuccess;
+  // head_dim 128: the tcgen05 / TMEM kernel (prefill_tc.cu); BKV_PREFILL_MMA_SYNC=1 (dev) keeps this one
+  static const bool mma_sync = getenv("BKV_PREFILL_MMA_SYNC") && atoi(getenv("BKV_PREFILL_MMA_SYNC"));
+  if (head_dim == 128 && !mma_sync) return launch_prefill_tc(tmK, tmV, p, max_q_len, s);
   return head_dim == 128 ? launch_prefill_t<128>(tmK, tmV, p, max_q_len, s)
                          : launch_prefill_t<64>(tmK, tmV, p, max_q_len, s);
 }

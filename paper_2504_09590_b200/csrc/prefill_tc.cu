@@ -1,0 +1,459 @@
+// prefill_tc.cu -- mixed prefill + decode attention on the 5th-generation
+// tensor cores (tcgen05.mma, TMEM accumulators) for head_dim 128
+// (PAPER.md P:762-765).  Same contract and tiling as
+// prefill_attention.cu (which remains the head_dim-64 path and the dev
+// reference, BKV_PREFILL_MMA_SYNC=1): one CTA per (128-row query tile, kv head,
+// request), rows = (token, q head of the group) pairs, causal over the
+// request's paged tokens, dense or general block maps.
+//
+// Roles (192 threads):
+//   warps 0-3  softmax warpgroup: thread t owns query row t of the tile and TMEM
+//              lane t (tcgen05.ld 32x32b gives a whole row to one thread: no
+//              shuffles); loads Q, masks (direction + causal by token index,
+//              P:711), online softmax in the log2 domain with a lazy rescale
+//              (the running max is only moved when it grows by > 8, so O in
+//              TMEM is rarely touched), writes P (bf16) to shared memory,
+//              zeroes dead V rows, and runs the epilogue;
+//   warp 4     producer: walks the request's entries in logical order and TMA-
+//              streams each 16-slot chunk's K and V tiles into an 8-stage ring;
+//   warp 5     MMA issuer (one lane) + TMEM owner: per key tile of up to four
+//              chunks, S = Q.K^T (M 128, N 16 per chunk, K 128) into one of two
+//              TMEM S buffers, then O += P.V (M 128, N 128, K 16 per chunk) into
+//              the TMEM O accumulator; tcgen05.commit releases stages/buffers.
+// Operands: Q, K and P are K-major 128B-swizzled, V is MN-major 128B-swizzled
+// -- exactly the layout the 5-D TMA boxes of the pool land in.
+#include <math.h>
+
+#include "bkv_internal.h"
+#include "bkv_ptx.cuh"
+
+namespace bkv {
+
+namespace {
+
+constexpr int kTcStages = 8;       // K/V chunk ring (two key tiles in flight)
+constexpr int kTcChunks = 4;       // chunks (16 keys each) per key tile
+constexpr int kTcRows = 128;       // query rows per CTA = TMEM lanes
+constexpr int kTcThreads = 192;
+constexpr int kTcLast = 1 << 8;
+
+__device__ __forceinline__ uint32_t tswz(int row, int c) {
+  return static_cast<uint32_t>(row * 128 + ((c ^ (row & 7)) << 4));
+}
+
+// SM100 shared-memory matrix descriptor, 128B swizzle (start, leading and
+// stride byte offsets in 16-byte units; version 1).
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// instruction descriptor: bf16 x bf16 -> fp32, shape M x N, A/B major (0 K, 1 MN)
+__host__ __device__ constexpr uint32_t idesc(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(id), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float *v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// the chunk walk (see prefill_attention.cu): entries in logical order, 32 at a
+// time in a lane-distributed window
+struct TcWalk {
+  int e, c, F, E, wb;
+  int wblk, wdir, wfill;
+  int blk, dir, fill;
+  bool have;
+};
+__device__ __forceinline__ void tc_window(const PrefillParams &p, int r, int L, TcWalk &w, int wb) {
+  const int e = wb + static_cast<int>(threadIdx.x & 31);
+  w.wb = wb;
+  w.wblk = w.wdir = w.wfill = 0;
+  if (e < w.E) {
+    w.wblk = __ldg(p.bt + static_cast<int64_t>(r) * p.bt_stride + e);
+    w.wdir = __ldg(p.dirs + static_cast<int64_t>(r) * p.dir_rs + static_cast<int64_t>(e) * p.dir_cs);
+    w.wfill = p.fills ? static_cast<int>(__ldg(p.fills + static_cast<int64_t>(r) * p.fill_rs + e))
+                      : min(p.bs, L - e * p.bs);
+  }
+}
+__device__ __forceinline__ bool tc_next(const PrefillParams &p, int r, int L, int pos_max, TcWalk &w,
+                                        int &lo, int &hi, int &tb) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const int bs = p.bs;
+  while (w.e < w.E && w.F <= pos_max) {
+    if (!w.have) {
+      if (w.e - w.wb >= 32) tc_window(p, r, L, w, w.e);
+      const int idx = w.e - w.wb;
+      w.blk = __shfl_sync(FULL, w.wblk, idx);
+      w.dir = __shfl_sync(FULL, w.wdir, idx);
+      w.fill = __shfl_sync(FULL, w.wfill, idx);
+      w.c = 0;
+      w.have = true;
+    }
+    const int lo_s = w.dir ? bs - w.fill : 0, hi_s = w.dir ? bs : w.fill;
+    while (w.c < bs / 16) {
+      const int c = w.c++;
+      lo = max(lo_s - 16 * c, 0);
+      hi = min(hi_s - 16 * c, 16);
+      if (lo >= hi) continue;
+      tb = w.dir ? w.F + bs - 1 - 16 * c : w.F + 16 * c;
+      const int first_tok = w.dir ? tb - (hi - 1) : tb + lo;
+      if (first_tok > pos_max) continue;
+      return true;
+    }
+    w.F += w.fill;
+    ++w.e;
+    w.have = false;
+  }
+  return false;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+    prefill_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                      const PrefillParams p) {
+  constexpr int D = 128;
+  constexpr int KV_BYTES = 2 * 2048;          // one 16-slot x 128-d tile (two 64-d halves)
+  constexpr int SLOT_BYTES = 2 * KV_BYTES;    // K + V
+  constexpr unsigned FULL = 0xffffffffu;
+
+  const int r = blockIdx.z, h = blockIdx.y;
+  const int q0 = __ldg(p.cu_q + r);
+  const int n = __ldg(p.cu_q + r + 1) - q0;
+  const int g = p.g;
+  const int rows = n * g;
+  const int ntiles = (rows + kTcRows - 1) / kTcRows;
+  const int tile = ntiles - 1 - static_cast<int>(blockIdx.x);
+  if (tile < 0) return;
+  const int L = __ldg(p.seq_lens + r);
+  const int row0 = tile * kTcRows;
+  const int row_end = min(rows, row0 + kTcRows);
+  const int pos_max = L - n + (row_end - 1) / g;
+
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t *gb = smem_raw + (base - raw);
+  const uint32_t sQ = base;                                  // 2 x 128 x 128 B
+  const uint32_t sStage = sQ + 2 * kTcRows * 128;            // kTcStages x 8 KB
+  const uint32_t sP = sStage + kTcStages * SLOT_BYTES;       // 2 x 128 x 128 B
+  int4 *metas = reinterpret_cast<int4 *>(gb + (sP - base) + 2 * kTcRows * 128);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(metas + kTcStages);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * kTcStages + 9);
+  const uint32_t bar0 = smem_u32(bars);
+  const uint32_t full0 = bar0, empty0 = bar0 + 8 * kTcStages;
+  // s_full/s_free: S buffer handoff; p_full/p_free: P buffer handoff (p_free also
+  // marks "every P.V up to this tile has landed in O"); q_full: Q staged
+  const uint32_t s_full0 = bar0 + 16 * kTcStages, s_free0 = s_full0 + 16, p_full0 = s_full0 + 32,
+                 p_free0 = s_full0 + 48, q_full = s_full0 + 64;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&tmK);
+    prefetch_tmap(&tmV);
+    for (int i = 0; i < kTcStages; ++i) {
+      mbar_init(full0 + 8 * i, 1);
+      mbar_init(empty0 + 8 * i, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(s_full0 + 8 * b, 1);
+      mbar_init(s_free0 + 8 * b, 4);
+      mbar_init(p_full0 + 8 * b, 4);
+      mbar_init(p_free0 + 8 * b, 1);
+    }
+    mbar_init(q_full, 4);
+    fence_mbar_init();
+  }
+  if (warp == 5) {   // TMEM: S buffers at columns [0, 64) and [64, 128), O at [128, 256)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 4) {
+    // ------------------------------------------------------------ producer
+    TcWalk w;
+    w.e = 0;
+    w.F = 0;
+    w.E = p.fills ? __ldg(p.nent + r) : (L + p.bs - 1) / p.bs;
+    w.have = false;
+    tc_window(p, r, L, w, 0);
+    const uint64_t pol = policy_evict_first();
+    int it = 0, lo, hi, tb;
+    for (; tc_next(p, r, L, pos_max, w, lo, hi, tb); ++it) {
+      if (lane == 0) {
+        const int st = it % kTcStages, round = it / kTcStages;
+        if (round > 0) mbar_wait(empty0 + 8 * st, (round - 1) & 1);
+        metas[st] = make_int4(lo, hi, tb, w.dir);
+        const uint32_t fb = full0 + 8 * st;
+        mbar_arrive_expect_tx(fb, SLOT_BYTES);
+        const uint32_t dk = sStage + st * SLOT_BYTES;
+        tma_load_5d(dk, &tmK, 0, 16 * (w.c - 1), 0, h, w.blk, fb, pol);
+        tma_load_5d(dk + KV_BYTES, &tmV, 0, 16 * (w.c - 1), 0, h, w.blk, fb, pol);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {   // terminator: metadata only
+      const int st = it % kTcStages, round = it / kTcStages;
+      if (round > 0) mbar_wait(empty0 + 8 * st, (round - 1) & 1);
+      metas[st] = make_int4(0, 0, 0, kTcLast);
+      mbar_arrive(full0 + 8 * st);
+    }
+  } else if (warp == 5) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idS = idesc(128, 16, 0, 0), idO = idesc(128, 128, 0, 1);
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      int it = 0, prev_nch = 0, prev_it0 = 0;
+      bool first_pv = true;
+      auto issue_pv = [&](int t, int it0, int nch) {
+        const int pb = t & 1;
+        mbar_wait(p_full0 + 8 * pb, (t >> 1) & 1);
+        tc_fence_after();
+        for (int j = 0; j < nch; ++j) {
+          const int st = (it0 + j) % kTcStages;
+          const uint64_t a = sdesc(sP + pb * (kTcRows * 128) + j * 32, 16, 1024);
+          const uint64_t b = sdesc(sStage + st * SLOT_BYTES + KV_BYTES, 2048, 1024);
+          umma(tmem + 128, a, b, idO, first_pv ? 0u : 1u);
+          first_pv = false;
+        }
+        for (int j = 0; j < nch; ++j) umma_commit(empty0 + 8 * ((it0 + j) % kTcStages));
+        umma_commit(p_free0 + 8 * pb);
+      };
+      for (int t = 0;; ++t) {
+        const int sb = t & 1;
+        if (t >= 2) mbar_wait(s_free0 + 8 * sb, ((t - 2) >> 1) & 1);
+        tc_fence_after();
+        int nch = 0;
+        const int it0 = it;
+        bool done = false;
+        for (int j = 0; j < kTcChunks; ++j, ++it) {
+          const int st = it % kTcStages;
+          mbar_wait(full0 + 8 * st, (it / kTcStages) & 1);
+          if (metas[st].w & kTcLast) {
+            done = true;
+            break;
+          }
+          const uint32_t sk = sStage + st * SLOT_BYTES;
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t off = (k >> 2) * (kTcRows * 128) + (k & 3) * 32;
+            const uint64_t a = sdesc(sQ + off, 16, 1024);
+            const uint64_t b = sdesc(sk + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024);
+            umma(tmem + sb * 64 + 16 * j, a, b, idS, k > 0);
+          }
+          ++nch;
+        }
+        if (nch > 0) umma_commit(s_full0 + 8 * sb);
+        if (t >= 1) issue_pv(t - 1, prev_it0, prev_nch);   // P.V of the previous tile overlaps S of this one
+        if (nch == 0) break;
+        prev_nch = nch;
+        prev_it0 = it0;
+        if (done) {
+          issue_pv(t, it0, nch);
+          break;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax warpgroup
+    const int row = threadIdx.x;               // 0..127: query row of the tile = TMEM lane
+    const int grow = row0 + row;
+    const bool ok = grow < row_end;
+    const int tok = ok ? grow / g : 0, jh = ok ? grow - tok * g : 0;
+    const int pos = ok ? L - n + tok : -1;
+    // Q row -> shared memory (K-major, 128B swizzle, two 64-d halves)
+    {
+      const uint4 *qs = reinterpret_cast<const uint4 *>(p.q + static_cast<int64_t>(q0 + tok) * p.q_st +
+                                                        static_cast<int64_t>(h * g + jh) * p.q_sh);
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const uint4 v = ok ? __ldg(qs + c) : make_uint4(0u, 0u, 0u, 0u);
+        st_shared_v4(sQ + (c >> 3) * (kTcRows * 128) + tswz(row, c & 7), v);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(q_full);
+    }
+    const uint32_t lane_addr = static_cast<uint32_t>(warp * 32) << 16;
+    float m_ref = -INFINITY, l = 0.f;
+    int it = 0, ntile = 0;
+    for (;;) {
+      const int t = ntile, sb = t & 1;
+      // chunk metadata of this key tile (visible once each stage's TMA completed)
+      int4 meta[kTcChunks];
+      int nch = 0;
+      bool done = false;
+      for (int j = 0; j < kTcChunks; ++j) {
+        const int st = (it + j) % kTcStages;
+        mbar_wait(full0 + 8 * st, ((it + j) / kTcStages) & 1);
+        meta[j] = metas[st];
+        if (meta[j].w & kTcLast) {
+          done = true;
+          break;
+        }
+        ++nch;
+      }
+      if (nch == 0) break;
+      // dead V rows of partly live chunks -> zero (P = 0 must never meet NaN, reading Q10)
+      for (int j = 0; j < nch; ++j) {
+        if (meta[j].x > 0 || meta[j].y < 16) {
+          const uint32_t sv = sStage + ((it + j) % kTcStages) * SLOT_BYTES + KV_BYTES;
+          for (int q = row; q < 256; q += kTcRows) {   // 16 slots x 2 halves x 8 pieces
+            const int slot = q >> 4, rest = q & 15;
+            if (slot < meta[j].x || slot >= meta[j].y) sts128_zero(sv + (rest >> 3) * 2048 + slot * 128 + (rest & 7) * 16);
+          }
+        }
+      }
+      // S tile -> registers
+      mbar_wait(s_full0 + 8 * sb, (t >> 1) & 1);
+      tc_fence_after();
+      float s[kTcChunks * 16];
+#pragma unroll
+      for (int j = 0; j < kTcChunks; ++j)
+        if (j < nch) tmem_ld16(tmem + lane_addr + sb * 64 + 16 * j, s + 16 * j);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_free0 + 8 * sb);
+      // mask (direction + causal by token index) and scale
+      float mx = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < kTcChunks; ++j) {
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const bool live = j < nch && c >= meta[j].x && c < meta[j].y &&
+                            (meta[j].w ? meta[j].z - c : meta[j].z + c) <= pos;
+          s[16 * j + c] = live ? s[16 * j + c] * p.scale_log2 : -INFINITY;
+          mx = fmaxf(mx, s[16 * j + c]);
+        }
+      }
+      // lazy rescale: the reference max moves only when it grows by more than 8
+      // (2^8 headroom for p); O in TMEM is rescaled warp-collectively, and only
+      // once every earlier P.V has landed (p_free of the previous tile)
+      const bool grow = mx > m_ref + 8.f;
+      const bool resc = grow && m_ref != -INFINITY;
+      if (__any_sync(FULL, resc)) {
+        const float alpha = resc ? ex2(m_ref - mx) : 1.f;
+        l *= alpha;
+        mbar_wait(p_free0 + 8 * ((t - 1) & 1), ((t - 1) >> 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < D; c += 16) {
+          float o[16];
+          tmem_ld16(tmem + lane_addr + 128 + c, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[i] *= alpha;
+          tmem_st16(tmem + lane_addr + 128 + c, o);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+      }
+      if (grow) m_ref = mx;
+      const float base_m = m_ref == -INFINITY ? 0.f : m_ref;
+      // P -> shared memory buffer sb (K-major, 128B swizzle)
+      if (t >= 2) mbar_wait(p_free0 + 8 * sb, ((t - 2) >> 1) & 1);
+      const uint32_t prow = sP + sb * (kTcRows * 128);
+#pragma unroll
+      for (int j = 0; j < kTcChunks; ++j) {
+        uint32_t w[8];
+#pragma unroll
+        for (int c = 0; c < 16; c += 2) {
+          const float p0 = ex2(s[16 * j + c] - base_m), p1 = ex2(s[16 * j + c + 1] - base_m);
+          l += p0 + p1;
+          w[c >> 1] = pack_bf16(p0, p1);
+        }
+        st_shared_v4(prow + tswz(row, 2 * j), make_uint4(w[0], w[1], w[2], w[3]));
+        st_shared_v4(prow + tswz(row, 2 * j + 1), make_uint4(w[4], w[5], w[6], w[7]));
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full0 + 8 * sb);
+      it += nch;
+      ++ntile;
+      if (done) break;
+    }
+    // ---- epilogue: O / l -> bf16 rows, once the last P.V landed
+    mbar_wait(p_free0 + 8 * ((ntile - 1) & 1), ((ntile - 1) >> 1) & 1);
+    tc_fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    uint4 *orow = reinterpret_cast<uint4 *>(p.out + static_cast<int64_t>(q0 + tok) * p.o_st +
+                                            static_cast<int64_t>(h * g + jh) * p.o_sh);
+#pragma unroll 1
+    for (int c = 0; c < D; c += 16) {
+      float o[16];
+      tmem_ld16(tmem + lane_addr + 128 + c, o);
+      tmem_wait_ld();
+      if (ok) {
+        orow[c / 8] = make_uint4(pack_bf16(o[0] * inv, o[1] * inv), pack_bf16(o[2] * inv, o[3] * inv),
+                                 pack_bf16(o[4] * inv, o[5] * inv), pack_bf16(o[6] * inv, o[7] * inv));
+        orow[c / 8 + 1] = make_uint4(pack_bf16(o[8] * inv, o[9] * inv), pack_bf16(o[10] * inv, o[11] * inv),
+                                     pack_bf16(o[12] * inv, o[13] * inv), pack_bf16(o[14] * inv, o[15] * inv));
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  }
+}
+
+int prefill_tc_smem_bytes() {
+  return 1024 + 2 * kTcRows * 128 + kTcStages * 2 * 4096 + 2 * kTcRows * 128 + kTcStages * 16 +
+         (2 * kTcStages + 9) * 8 + 16;   // barriers + TMEM address slot
+}
+
+cudaError_t launch_prefill_tc(const CUtensorMap &tmK, const CUtensorMap &tmV, const PrefillParams &p,
+                              int max_q_len, cudaStream_t s) {
+  const int smem = prefill_tc_smem_bytes();
+  static int configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  const long long tiles = (static_cast<long long>(max_q_len) * p.g + kTcRows - 1) / kTcRows;
+  dim3 grid(static_cast<unsigned>(tiles), p.H, p.B);
+  prefill_tc_kernel<<<grid, kTcThreads, smem, s>>>(tmK, tmV, p);
+  return cudaGetLastError();
+}
+
+}  // namespace bkv
