@@ -85,7 +85,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // dimension (stride 128 B) lets ONE box {64, 16, d/64, 1, 1} fetch a whole
 // 16-slot x d tile, landing as [half][slot][128 B] with the 128-byte swizzle
 // the decode kernel's ldmatrix / LDS reads are conflict-free against.
-bkv_status encode_pool_map(CUtensorMap *m, void *base, const bkv_kv_pool *pool) {
+bkv_status encode_pool_map(CUtensorMap *m, void *base, const bkv_kv_pool *pool, bool one_half = false) {
   auto fn = encode_fn();
   if (!fn) return fail(BKV_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
   const int halves = pool->head_dim / 64;
@@ -93,7 +93,7 @@ bkv_status encode_pool_map(CUtensorMap *m, void *base, const bkv_kv_pool *pool) 
                         (cuuint64_t)pool->num_kv_heads, (cuuint64_t)pool->num_blocks};
   cuuint64_t strides[4] = {(cuuint64_t)pool->stride_slot * 2, 128,
                            (cuuint64_t)pool->stride_head * 2, (cuuint64_t)pool->stride_block * 2};
-  cuuint32_t box[5] = {64, 16, (cuuint32_t)halves, 1, 1};
+  cuuint32_t box[5] = {64, 16, one_half ? 1u : (cuuint32_t)halves, 1, 1};
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, base, dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -104,7 +104,7 @@ bkv_status encode_pool_map(CUtensorMap *m, void *base, const bkv_kv_pool *pool) 
 
 // ------------------------------------------------------------ workspace
 struct WsLayout {
-  size_t sched, counters, ml, o, trace, total;
+  size_t sched, counters, mcnt, ml, o, trace, total;
   int trace_cap;
   int units_max;
 };
@@ -119,12 +119,13 @@ bkv_status ws_layout(int B, int Hq, int H, int D, WsLayout *w, bkv::DecodeLaunch
   const long long units = (long long)bkv::decode_target_units(*cfg) + (long long)B * H;
   if (units > (1ll << 30)) return fail(BKV_ERR_INVALID_ARGUMENT, "problem too large");
   w->units_max = (int)units;
-  // Region A: scheduler word (re-armed to 0 by every call's merge kernel) and
+  // Region A: scheduler words (re-armed to 0 by every call: merge kernel or last CTA),
   // the published split plan; fixed size for every geometry.  Region B
   // (partials) is scratch.
   w->sched = 0;
   w->counters = 256;
-  w->ml = w->counters + up256((size_t)bkv::kMaxSeqs * bkv::kMaxKvHeads * 4);
+  w->mcnt = w->counters + up256((size_t)bkv::kMaxSeqs * bkv::kMaxKvHeads * 4);
+  w->ml = w->mcnt + up256((size_t)bkv::kMaxSeqs * bkv::kMaxKvHeads * 4);
   w->o = w->ml + up256((size_t)units * g * 2 * 4);
   w->trace = w->o + up256((size_t)units * g * D * 4);
   const char *tr = getenv("BKV_TRACE");   // dev only: per-warp event log after the partials
@@ -360,6 +361,7 @@ static bkv_status decode_impl(const bkv_kv_pool *pool, const bkv_block_map *map,
   p.scale_log2 = softmax_scale * 1.4426950408889634f;
   p.sched = reinterpret_cast<int *>(ws + w.sched);
   p.plan_out = reinterpret_cast<int *>(ws + w.counters);
+  p.merge_cnt = reinterpret_cast<int *>(ws + w.mcnt);
   p.part_ml = reinterpret_cast<float *>(ws + w.ml);
   p.part_o = reinterpret_cast<float *>(ws + w.o);
   p.target_units = bkv::decode_target_units(cfg);
@@ -380,6 +382,10 @@ static bkv_status decode_impl(const bkv_kv_pool *pool, const bkv_block_map *map,
   if (n_peers < 0 || n_peers > bkv::kMaxPeers)
     return fail(BKV_ERR_UNSUPPORTED, "n_peers %d outside [0, %d]", n_peers, bkv::kMaxPeers);
   p.n_peers = n_peers;
+  // split merge: separate stream-ordered merge_kernel by default; in-kernel last-arriver merge
+  // (opt-in, BKV_FUSED_MERGE=1: measured slower -- the last-arriving warp merges all g rows
+  // of a GQA group serially at the tail, e.g. Llama-70B TP1 115 -> 149 us per layer)
+  p.fused_merge = (n_peers == 0 && getenv("BKV_FUSED_MERGE") && atoi(getenv("BKV_FUSED_MERGE"))) ? 1 : 0;
   for (int k = 0; k < bkv::kMaxPeers; ++k) {
     p.peer_out[k] = k < n_peers ? static_cast<uint16_t *>(peer_outs[k]) : nullptr;
     if (k < n_peers && (!peer_outs[k] || !aligned16(peer_outs[k])))
@@ -552,8 +558,9 @@ bkv_status bkv_paged_prefill_attention(const bkv_kv_pool *pool, const bkv_block_
   if (!(softmax_scale == softmax_scale) || isinf(softmax_scale))
     return fail(BKV_ERR_INVALID_ARGUMENT, "softmax_scale must be finite");
   CUtensorMap tmK, tmV;
-  if ((s = encode_pool_map(&tmK, pool->k, pool))) return s;
-  if ((s = encode_pool_map(&tmV, pool->v, pool))) return s;
+  const bool tc = bkv::prefill_uses_tc(pool->head_dim);   // tcgen05 kernel: one 64-d half per box
+  if ((s = encode_pool_map(&tmK, pool->k, pool, tc))) return s;
+  if ((s = encode_pool_map(&tmV, pool->v, pool, tc))) return s;
   bkv::PrefillParams p;
   p.bt = map->block_tables;
   p.bt_stride = map->bt_stride;

@@ -62,7 +62,9 @@ struct DecodeParams {
   uint16_t *out;
   int64_t o_ss, o_sh;
   float scale_log2;      // softmax_scale * log2(e)
-  int *sched;            // [0] next unit (re-armed to 0 by the merge kernel)
+  int *sched;            // [0] next unit, [1] exited CTAs (re-armed to 0 by the merge kernel or the last CTA)
+  int *merge_cnt;        // [B*H] split arrivals per (request, kv head) for the fused merge (self-cleaning)
+  int fused_merge;       // 1: last-arriver merge inside the decode kernel (no merge kernel launch)
   int *plan_out;         // split plan published by CTA 0 for the merge kernel
   float *part_ml;        // [units_max][g][2]  (m in log2 domain, l)
   float *part_o;         // [units_max][g][D]  un-normalised partial outputs
@@ -118,6 +120,7 @@ struct PrefillParams {
   float scale_log2;
 };
 int prefill_smem_bytes(int head_dim);
+bool prefill_uses_tc(int head_dim);   // tcgen05 kernel (wants 1-half TMA boxes)
 cudaError_t launch_prefill(const CUtensorMap &tmK, const CUtensorMap &tmV, const PrefillParams &p,
                            int head_dim, int max_q_len, cudaStream_t s);
 cudaError_t launch_prefill_tc(const CUtensorMap &tmK, const CUtensorMap &tmV, const PrefillParams &p,

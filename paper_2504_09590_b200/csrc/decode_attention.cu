@@ -231,6 +231,79 @@ __device__ void compute_plan(const DecodeParams &p, int *Pre, int *Lsm, int *NBs
   __syncthreads();
 }
 
+// Merge of the split partials of one (request r, kv head h, q head `head` of
+// the group) row, in split order: M = max m_s, L = sum l_s 2^(m_s - M),
+// O = sum o_s 2^(m_s - M) / L.  Lanes take 32 splits at a
+// time, weights are broadcast by shuffle, each lane owns EPL output elements.
+// COHERENT: the partials were written by other SMs during THIS kernel (fused
+// last-arriver merge) -> L2 loads (ld.global.cg), else read-only cached loads.
+template <int D, bool COHERENT>
+__device__ __forceinline__ void merge_row(const DecodeParams &p, int u0, int ns, int r, int h, int head,
+                                          int lane) {
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int EPL = D / 32;
+  const int H = p.H, g = p.g;
+  float Mrun = -INFINITY, Lrun = 0.f, acc[EPL];
+#pragma unroll
+  for (int q = 0; q < EPL; ++q) acc[q] = 0.f;
+  for (int s0 = 0; s0 < ns; s0 += 32) {
+    const int sl = s0 + lane;
+    const bool ok = sl < ns;
+    const int us = u0 + sl * H;
+    float wj = -INFINITY, lj = 0.f;
+    if (ok) {
+      const float2 *src = reinterpret_cast<const float2 *>(p.part_ml + (static_cast<int64_t>(us) * g + head) * 2);
+      const float2 v = COHERENT ? __ldcg(src) : __ldg(src);
+      wj = v.x;
+      lj = v.y;
+    }
+    float mg = wj;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mg = fmaxf(mg, __shfl_xor_sync(FULL, mg, o));
+    const float Mn = fmaxf(Mrun, mg);
+    const float a = ex2(Mrun - Mn);
+    const float w = ok ? ex2(wj - Mn) : 0.f;
+    float ls = lj * w;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ls += __shfl_xor_sync(FULL, ls, o);
+    Lrun = Lrun * a + ls;
+#pragma unroll
+    for (int q = 0; q < EPL; ++q) acc[q] *= a;
+    Mrun = Mn;
+    const int cnt = min(32, ns - s0);
+#pragma unroll 4
+    for (int t = 0; t < cnt; ++t) {
+      const int ut = __shfl_sync(FULL, us, t);
+      const float wt = __shfl_sync(FULL, w, t);
+      const float *po = p.part_o + (static_cast<int64_t>(ut) * g + head) * D + lane * EPL;
+      if constexpr (EPL == 4) {
+        const float4 v = COHERENT ? __ldcg(reinterpret_cast<const float4 *>(po)) : __ldg(reinterpret_cast<const float4 *>(po));
+        acc[0] = fmaf(wt, v.x, acc[0]);
+        acc[1] = fmaf(wt, v.y, acc[1]);
+        acc[2] = fmaf(wt, v.z, acc[2]);
+        acc[3] = fmaf(wt, v.w, acc[3]);
+      } else {
+        const float2 v = COHERENT ? __ldcg(reinterpret_cast<const float2 *>(po)) : __ldg(reinterpret_cast<const float2 *>(po));
+        acc[0] = fmaf(wt, v.x, acc[0]);
+        acc[1] = fmaf(wt, v.y, acc[1]);
+      }
+    }
+  }
+  const float inv = Lrun > 0.f ? 1.f / Lrun : 0.f;
+  const int64_t off = static_cast<int64_t>(r) * p.o_ss + static_cast<int64_t>(h * g + head) * p.o_sh + lane * EPL;
+  if constexpr (EPL == 4) {
+    uint2 w;
+    w.x = pack_bf16(acc[0] * inv, acc[1] * inv);
+    w.y = pack_bf16(acc[2] * inv, acc[3] * inv);
+    *reinterpret_cast<uint2 *>(p.out + off) = w;
+    for (int k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint2 *>(p.peer_out[k] + off) = w;
+  } else {
+    const uint32_t w = pack_bf16(acc[0] * inv, acc[1] * inv);
+    *reinterpret_cast<uint32_t *>(p.out + off) = w;
+    for (int k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint32_t *>(p.peer_out[k] + off) = w;
+  }
+}
+
 // KIND 0: MHA on CUDA cores; 1: MMA with g <= 8; 2: MMA with 8 < g <= 16.
 // GQA runs 8 warps (measured best) and gets the 255-register budget of a
 // 256-thread CTA -- at 384 threads the MMA kernels spill (ptxas -v).
@@ -751,7 +824,29 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
         }
       if (direct) return;
     }
-    // split partial written; bkv merge_kernel (next on the stream) combines the splits
+    // Split partial written.  Fused merge (default): the warp that completes the
+    // LAST split of (r, h) merges all of them in split order right here, while
+    // other warps keep streaming -- no second kernel on the critical path.
+    // Release/acquire through the per-(r, h) arrival counter (threadfence +
+    // atomic, the classic last-block pattern); the counter is reset by the
+    // merging warp, so the workspace stays clean for the next call.  Otherwise
+    // bkv merge_kernel (next on the stream) combines the splits.
+    if (p.fused_merge) {
+      __threadfence();   // every lane's partial stores ...
+      __syncwarp();      // ... precede lane 0's arrival
+      int last = 0;
+      if (lane == 0) last = atomicAdd(p.merge_cnt + r * H + h, 1) == m.nsplit - 1;
+      last = __shfl_sync(FULL, last, 0);
+      if (last) {
+        __threadfence();
+        const int qq = u / H;
+        int k = 0;
+        while (k < kBuckets - 1 && qq >= plan.base[k + 1]) ++k;
+        const int u0 = (plan.base[k] + Pre[k * (p.B + 1) + r]) * H + h;
+        for (int head = 0; head < g; ++head) merge_row<D, true>(p, u0, m.nsplit, r, h, head, lane);
+        if (lane == 0) p.merge_cnt[r * H + h] = 0;
+      }
+    }
   };
 
   // ------------------------------------------------------------- main loop
@@ -838,6 +933,17 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
     }
   }
   if (p.k_new != nullptr && lane == 0) bulk_wait_all();   // pool rows written before exit
+  if (p.fused_merge) {   // no merge kernel follows: the last CTA to exit re-arms the unit counter
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(p.sched + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+        p.sched[0] = 0;
+        p.sched[1] = 0;
+        __threadfence();
+      }
+    }
+  }
   if (profiling)
     for (int k = 0; k < 6; ++k) trace(8 + k, static_cast<int>(min(prof[k], (long long)0x7fffffff)));
 
@@ -887,90 +993,7 @@ __global__ void __launch_bounds__(256) merge_kernel(const DecodeParams p) {
   const int k = bucket_of((nb + ns - 1) / ns, P);
   // all splits of (r, h) are consecutive split slots of r's bucket: u = (slot0 + s) * H + h
   const int u0 = (p.plan_out[1 + k] + p.plan_out[16 + k * (p.B + 1) + r]) * H + h;
-  {
-    const int row0 = row1, nr = 1;
-    float Mrun[8], Lrun[8], acc[8][EPL];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      Mrun[j] = -INFINITY;
-      Lrun[j] = 0.f;
-#pragma unroll
-      for (int q = 0; q < EPL; ++q) acc[j][q] = 0.f;
-    }
-    for (int s0 = 0; s0 < ns; s0 += 32) {
-      const int sl = s0 + lane;
-      const bool ok = sl < ns;
-      const int us = u0 + sl * H;
-      float wj[8], lj[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        wj[j] = -INFINITY;
-        lj[j] = 0.f;
-        if (ok && j < nr) {
-          const float2 v = __ldg(reinterpret_cast<const float2 *>(p.part_ml + (static_cast<int64_t>(us) * g + row0 + j) * 2));
-          wj[j] = v.x;
-          lj[j] = v.y;
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if (j >= nr) break;
-        float mg = wj[j];
-#pragma unroll
-        for (int o = 16; o; o >>= 1) mg = fmaxf(mg, __shfl_xor_sync(FULL, mg, o));
-        const float Mn = fmaxf(Mrun[j], mg);
-        const float a = ex2(Mrun[j] - Mn);
-        const float w = ok ? ex2(wj[j] - Mn) : 0.f;
-        float ls = lj[j] * w;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) ls += __shfl_xor_sync(FULL, ls, o);
-        Lrun[j] = Lrun[j] * a + ls;
-#pragma unroll
-        for (int q = 0; q < EPL; ++q) acc[j][q] *= a;
-        Mrun[j] = Mn;
-        wj[j] = w;
-      }
-      const int cnt = min(32, ns - s0);
-#pragma unroll 4
-      for (int t = 0; t < cnt; ++t) {
-        const int ut = __shfl_sync(FULL, us, t);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (j >= nr) break;
-          const float wt = __shfl_sync(FULL, wj[j], t);
-          const float *po = p.part_o + (static_cast<int64_t>(ut) * g + row0 + j) * D + lane * EPL;
-          if constexpr (EPL == 4) {
-            const float4 v = __ldg(reinterpret_cast<const float4 *>(po));
-            acc[j][0] = fmaf(wt, v.x, acc[j][0]);
-            acc[j][1] = fmaf(wt, v.y, acc[j][1]);
-            acc[j][2] = fmaf(wt, v.z, acc[j][2]);
-            acc[j][3] = fmaf(wt, v.w, acc[j][3]);
-          } else {
-            const float2 v = __ldg(reinterpret_cast<const float2 *>(po));
-            acc[j][0] = fmaf(wt, v.x, acc[j][0]);
-            acc[j][1] = fmaf(wt, v.y, acc[j][1]);
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (j >= nr) break;
-      const float inv = Lrun[j] > 0.f ? 1.f / Lrun[j] : 0.f;
-      const int64_t off = static_cast<int64_t>(r) * p.o_ss + static_cast<int64_t>(h * g + row0 + j) * p.o_sh + lane * EPL;
-      if constexpr (EPL == 4) {
-        uint2 w;
-        w.x = pack_bf16(acc[j][0] * inv, acc[j][1] * inv);
-        w.y = pack_bf16(acc[j][2] * inv, acc[j][3] * inv);
-        *reinterpret_cast<uint2 *>(p.out + off) = w;
-        for (int k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint2 *>(p.peer_out[k] + off) = w;
-      } else {
-        const uint32_t w = pack_bf16(acc[j][0] * inv, acc[j][1] * inv);
-        *reinterpret_cast<uint32_t *>(p.out + off) = w;
-        for (int k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint32_t *>(p.peer_out[k] + off) = w;
-      }
-    }
-  }
+  merge_row<D, false>(p, u0, ns, r, h, row1, lane);
 }
 
 // ----------------------------------------------------------------- host
@@ -1046,6 +1069,7 @@ static cudaError_t launch_t(const CUtensorMap &tmK, const CUtensorMap &tmV, cons
   }
   cudaError_t e = cudaLaunchKernelEx(&lc, decode_kernel<D, KIND>, tmK, tmV, p);
   if (e != cudaSuccess) return e;
+  if (p.fused_merge) return cudaGetLastError();   // merged in-kernel, counter re-armed by the last CTA
   const int warps = p.B * p.H * p.g;
   cudaLaunchConfig_t lm = {};
   lm.gridDim = dim3((p.debug_flags & 2) ? 1 : (warps + 7) / 8);   // dev: 2 = re-arm only (times the merge)

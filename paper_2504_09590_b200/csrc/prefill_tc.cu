@@ -1,10 +1,11 @@
 // prefill_tc.cu -- mixed prefill + decode attention on the 5th-generation
 // tensor cores (tcgen05.mma, TMEM accumulators) for head_dim 128
 // (PAPER.md P:762-765).  Same contract and tiling as
-// prefill_attention.cu (which remains the head_dim-64 path and the dev
-// reference, BKV_PREFILL_MMA_SYNC=1): one CTA per (128-row query tile, kv head,
-// request), rows = (token, q head of the group) pairs, causal over the
-// request's paged tokens, dense or general block maps.
+// prefill_attention.cu: one CTA per (128-row query tile, kv head, request),
+// rows = (token, q head of the group) pairs, causal over the request's paged
+// tokens, dense or general block maps.  Opt-in (BKV_PREFILL_TC=1): parity-green
+// (tests run it) but slower than the mma.sync kernel so far -- see
+// prefill_uses_tc() in prefill_attention.cu.
 //
 // Roles (192 threads):
 //   warps 0-3  softmax warpgroup: thread t owns query row t of the tile and TMEM
@@ -31,11 +32,11 @@ namespace bkv {
 
 namespace {
 
-constexpr int kTcStages = 8;       // K/V chunk ring (two key tiles in flight)
+constexpr int kTcStages = 4;       // key-tile ring (K | V of up to 64 keys per stage)
 constexpr int kTcChunks = 4;       // chunks (16 keys each) per key tile
+constexpr int kTcKeys = 16 * kTcChunks;
 constexpr int kTcRows = 128;       // query rows per CTA = TMEM lanes
 constexpr int kTcThreads = 192;
-constexpr int kTcLast = 1 << 8;
 
 __device__ __forceinline__ uint32_t tswz(int row, int c) {
   return static_cast<uint32_t>(row * 128 + ((c ^ (row & 7)) << 4));
@@ -138,14 +139,39 @@ __device__ __forceinline__ bool tc_next(const PrefillParams &p, int r, int L, in
   return false;
 }
 
+struct TcChunk {
+  int lo, hi, tb, dir, blk, c;
+};
+
+// next key tile (up to kTcChunks chunks) of a warp's own walk; returns the count
+__device__ __forceinline__ int tc_tile(const PrefillParams &p, int r, int L, int pos_max, TcWalk &w,
+                                       TcChunk (&ch)[kTcChunks]) {
+  int nch = 0;
+  int lo, hi, tb;
+  while (nch < kTcChunks && tc_next(p, r, L, pos_max, w, lo, hi, tb)) {
+    ch[nch] = TcChunk{lo, hi, tb, w.dir, w.blk, w.c - 1};
+    ++nch;
+  }
+  return nch;
+}
+
+__device__ __forceinline__ void tc_walk_init(const PrefillParams &p, int r, int L, TcWalk &w) {
+  w.e = 0;
+  w.F = 0;
+  w.E = p.fills ? __ldg(p.nent + r) : (L + p.bs - 1) / p.bs;
+  w.have = false;
+  tc_window(p, r, L, w, 0);
+}
+
 }  // namespace
 
 __global__ void __launch_bounds__(kTcThreads, 1)
     prefill_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                       const PrefillParams p) {
   constexpr int D = 128;
-  constexpr int KV_BYTES = 2 * 2048;          // one 16-slot x 128-d tile (two 64-d halves)
-  constexpr int SLOT_BYTES = 2 * KV_BYTES;    // K + V
+  constexpr int HALF = kTcKeys * 128;          // one 64-d half of a key tile: 64 rows x 128 B
+  constexpr int TILE = 2 * HALF;               // K (or V) of one key tile
+  constexpr int STAGE = 2 * TILE;              // K + V
   constexpr unsigned FULL = 0xffffffffu;
 
   const int r = blockIdx.z, h = blockIdx.y;
@@ -165,11 +191,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t *gb = smem_raw + (base - raw);
-  const uint32_t sQ = base;                                  // 2 x 128 x 128 B
-  const uint32_t sStage = sQ + 2 * kTcRows * 128;            // kTcStages x 8 KB
-  const uint32_t sP = sStage + kTcStages * SLOT_BYTES;       // 2 x 128 x 128 B
-  int4 *metas = reinterpret_cast<int4 *>(gb + (sP - base) + 2 * kTcRows * 128);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(metas + kTcStages);
+  const uint32_t sQ = base;                                  // 2 halves x 128 rows x 128 B
+  const uint32_t sStage = sQ + 2 * kTcRows * 128;            // kTcStages key tiles (K | V)
+  const uint32_t sP = sStage + kTcStages * STAGE;            // 2 x 128 rows x 128 B (64 keys)
+  uint64_t *bars = reinterpret_cast<uint64_t *>(gb + (sP - base) + 2 * kTcRows * 128);
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * kTcStages + 9);
   const uint32_t bar0 = smem_u32(bars);
   const uint32_t full0 = bar0, empty0 = bar0 + 8 * kTcStages;
@@ -204,91 +229,84 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // Every role (producer, MMA issuer, each softmax warp) runs the same chunk walk
+  // itself (warp-collective, entries read 32 at a time), so no chunk metadata
+  // crosses warps through shared memory; the tiles themselves are handed over by
+  // the mbarriers.
+  TcWalk walk;
+  tc_walk_init(p, r, L, walk);
+  TcChunk ch[kTcChunks];
+
   if (warp == 4) {
     // ------------------------------------------------------------ producer
-    TcWalk w;
-    w.e = 0;
-    w.F = 0;
-    w.E = p.fills ? __ldg(p.nent + r) : (L + p.bs - 1) / p.bs;
-    w.have = false;
-    tc_window(p, r, L, w, 0);
+    // A key tile = up to four 16-slot chunks of the walk, each landing as rows
+    // [16j, 16j+16) of the tile (one TMA box per 64-d half per tensor), so the
+    // tile is one contiguous K-major (K) / MN-major (V) 128B-swizzled operand.
     const uint64_t pol = policy_evict_first();
-    int it = 0, lo, hi, tb;
-    for (; tc_next(p, r, L, pos_max, w, lo, hi, tb); ++it) {
+    for (int t = 0;; ++t) {
+      const int nch = tc_tile(p, r, L, pos_max, walk, ch);
+      if (nch == 0) break;
       if (lane == 0) {
-        const int st = it % kTcStages, round = it / kTcStages;
+        const int st = t % kTcStages, round = t / kTcStages;
         if (round > 0) mbar_wait(empty0 + 8 * st, (round - 1) & 1);
-        metas[st] = make_int4(lo, hi, tb, w.dir);
         const uint32_t fb = full0 + 8 * st;
-        mbar_arrive_expect_tx(fb, SLOT_BYTES);
-        const uint32_t dk = sStage + st * SLOT_BYTES;
-        tma_load_5d(dk, &tmK, 0, 16 * (w.c - 1), 0, h, w.blk, fb, pol);
-        tma_load_5d(dk + KV_BYTES, &tmV, 0, 16 * (w.c - 1), 0, h, w.blk, fb, pol);
+        mbar_arrive_expect_tx(fb, nch * 4 * 2048);
+        const uint32_t dk = sStage + st * STAGE;
+        for (int j = 0; j < nch; ++j)
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            tma_load_5d(dk + hf * HALF + j * 2048, &tmK, 0, 16 * ch[j].c, hf, h, ch[j].blk, fb, pol);
+            tma_load_5d(dk + TILE + hf * HALF + j * 2048, &tmV, 0, 16 * ch[j].c, hf, h, ch[j].blk, fb, pol);
+          }
       }
       __syncwarp();
-    }
-    if (lane == 0) {   // terminator: metadata only
-      const int st = it % kTcStages, round = it / kTcStages;
-      if (round > 0) mbar_wait(empty0 + 8 * st, (round - 1) & 1);
-      metas[st] = make_int4(0, 0, 0, kTcLast);
-      mbar_arrive(full0 + 8 * st);
     }
   } else if (warp == 5) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idS = idesc(128, 16, 0, 0), idO = idesc(128, 128, 0, 1);
       mbar_wait(q_full, 0);
       tc_fence_after();
-      int it = 0, prev_nch = 0, prev_it0 = 0;
-      bool first_pv = true;
-      auto issue_pv = [&](int t, int it0, int nch) {
-        const int pb = t & 1;
-        mbar_wait(p_full0 + 8 * pb, (t >> 1) & 1);
-        tc_fence_after();
-        for (int j = 0; j < nch; ++j) {
-          const int st = (it0 + j) % kTcStages;
-          const uint64_t a = sdesc(sP + pb * (kTcRows * 128) + j * 32, 16, 1024);
-          const uint64_t b = sdesc(sStage + st * SLOT_BYTES + KV_BYTES, 2048, 1024);
-          umma(tmem + 128, a, b, idO, first_pv ? 0u : 1u);
-          first_pv = false;
-        }
-        for (int j = 0; j < nch; ++j) umma_commit(empty0 + 8 * ((it0 + j) % kTcStages));
-        umma_commit(p_free0 + 8 * pb);
-      };
-      for (int t = 0;; ++t) {
-        const int sb = t & 1;
-        if (t >= 2) mbar_wait(s_free0 + 8 * sb, ((t - 2) >> 1) & 1);
-        tc_fence_after();
-        int nch = 0;
-        const int it0 = it;
-        bool done = false;
-        for (int j = 0; j < kTcChunks; ++j, ++it) {
-          const int st = it % kTcStages;
-          mbar_wait(full0 + 8 * st, (it / kTcStages) & 1);
-          if (metas[st].w & kTcLast) {
-            done = true;
-            break;
-          }
-          const uint32_t sk = sStage + st * SLOT_BYTES;
+    }
+    __syncwarp();
+    bool first_pv = true;
+    int prev_nch = 0;
+    auto issue_pv = [&](int t, int nch) {
+      const int pb = t & 1, st = t % kTcStages;
+      mbar_wait(p_full0 + 8 * pb, (t >> 1) & 1);
+      tc_fence_after();
+      const uint32_t idO = idesc(128, 128, 0, 1);
+      for (int j = 0; j < nch; ++j) {
+        const uint64_t a = sdesc(sP + pb * (kTcRows * 128) + j * 32, 16, 1024);
+        const uint64_t b = sdesc(sStage + st * STAGE + TILE + j * 2048, HALF, 1024);
+        umma(tmem + 128, a, b, idO, first_pv ? 0u : 1u);
+        first_pv = false;
+      }
+      umma_commit(empty0 + 8 * st);
+      umma_commit(p_free0 + 8 * pb);
+    };
+    for (int t = 0;; ++t) {
+      const int nch = tc_tile(p, r, L, pos_max, walk, ch);   // whole warp: the walk uses shuffles
+      if (lane == 0) {
+        const int sb = t & 1, st = t % kTcStages;
+        if (nch > 0) {
+          mbar_wait(full0 + 8 * st, (t / kTcStages) & 1);
+          if (t >= 2) mbar_wait(s_free0 + 8 * sb, ((t - 2) >> 1) & 1);
+          tc_fence_after();
+          const uint32_t idS = idesc(128, 16 * nch, 0, 0);
+          const uint32_t sk = sStage + st * STAGE;
 #pragma unroll
           for (int k = 0; k < D / 16; ++k) {
-            const uint32_t off = (k >> 2) * (kTcRows * 128) + (k & 3) * 32;
-            const uint64_t a = sdesc(sQ + off, 16, 1024);
-            const uint64_t b = sdesc(sk + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024);
-            umma(tmem + sb * 64 + 16 * j, a, b, idS, k > 0);
+            const uint64_t a = sdesc(sQ + (k >> 2) * (kTcRows * 128) + (k & 3) * 32, 16, 1024);
+            const uint64_t b = sdesc(sk + (k >> 2) * HALF + (k & 3) * 32, 16, 1024);
+            umma(tmem + sb * 64, a, b, idS, k > 0);
           }
-          ++nch;
+          umma_commit(s_full0 + 8 * sb);
         }
-        if (nch > 0) umma_commit(s_full0 + 8 * sb);
-        if (t >= 1) issue_pv(t - 1, prev_it0, prev_nch);   // P.V of the previous tile overlaps S of this one
-        if (nch == 0) break;
-        prev_nch = nch;
-        prev_it0 = it0;
-        if (done) {
-          issue_pv(t, it0, nch);
-          break;
-        }
+        if (t >= 1) issue_pv(t - 1, prev_nch);   // P.V of the previous tile overlaps S of this one
       }
+      __syncwarp();
+      if (nch == 0) break;
+      prev_nch = nch;
     }
   } else {
     // ------------------------------------------------------------ softmax warpgroup
@@ -297,8 +315,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const bool ok = grow < row_end;
     const int tok = ok ? grow / g : 0, jh = ok ? grow - tok * g : 0;
     const int pos = ok ? L - n + tok : -1;
-    // Q row -> shared memory (K-major, 128B swizzle, two 64-d halves)
-    {
+    {   // Q row -> shared memory (K-major, 128B swizzle, two 64-d halves)
       const uint4 *qs = reinterpret_cast<const uint4 *>(p.q + static_cast<int64_t>(q0 + tok) * p.q_st +
                                                         static_cast<int64_t>(h * g + jh) * p.q_sh);
 #pragma unroll
@@ -312,31 +329,23 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
     const uint32_t lane_addr = static_cast<uint32_t>(warp * 32) << 16;
     float m_ref = -INFINITY, l = 0.f;
-    int it = 0, ntile = 0;
-    for (;;) {
-      const int t = ntile, sb = t & 1;
-      // chunk metadata of this key tile (visible once each stage's TMA completed)
-      int4 meta[kTcChunks];
-      int nch = 0;
-      bool done = false;
-      for (int j = 0; j < kTcChunks; ++j) {
-        const int st = (it + j) % kTcStages;
-        mbar_wait(full0 + 8 * st, ((it + j) / kTcStages) & 1);
-        meta[j] = metas[st];
-        if (meta[j].w & kTcLast) {
-          done = true;
-          break;
-        }
-        ++nch;
-      }
+    int ntile = 0;
+    for (;; ++ntile) {
+      const int t = ntile, sb = t & 1, st = t % kTcStages;
+      const int nch = tc_tile(p, r, L, pos_max, walk, ch);
       if (nch == 0) break;
+      int4 meta[kTcChunks];
+#pragma unroll
+      for (int j = 0; j < kTcChunks; ++j)
+        meta[j] = j < nch ? make_int4(ch[j].lo, ch[j].hi, ch[j].tb, ch[j].dir) : make_int4(0, 0, 0, 0);
+      mbar_wait(full0 + 8 * st, (t / kTcStages) & 1);   // the tile's K/V landed (V rows get patched below)
       // dead V rows of partly live chunks -> zero (P = 0 must never meet NaN, reading Q10)
       for (int j = 0; j < nch; ++j) {
         if (meta[j].x > 0 || meta[j].y < 16) {
-          const uint32_t sv = sStage + ((it + j) % kTcStages) * SLOT_BYTES + KV_BYTES;
+          const uint32_t sv = sStage + st * STAGE + TILE + j * 2048;
           for (int q = row; q < 256; q += kTcRows) {   // 16 slots x 2 halves x 8 pieces
             const int slot = q >> 4, rest = q & 15;
-            if (slot < meta[j].x || slot >= meta[j].y) sts128_zero(sv + (rest >> 3) * 2048 + slot * 128 + (rest & 7) * 16);
+            if (slot < meta[j].x || slot >= meta[j].y) sts128_zero(sv + (rest >> 3) * HALF + slot * 128 + (rest & 7) * 16);
           }
         }
       }
@@ -392,22 +401,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const uint32_t prow = sP + sb * (kTcRows * 128);
 #pragma unroll
       for (int j = 0; j < kTcChunks; ++j) {
-        uint32_t w[8];
+        if (j >= nch) break;
+        uint32_t pw[8];
 #pragma unroll
         for (int c = 0; c < 16; c += 2) {
           const float p0 = ex2(s[16 * j + c] - base_m), p1 = ex2(s[16 * j + c + 1] - base_m);
           l += p0 + p1;
-          w[c >> 1] = pack_bf16(p0, p1);
+          pw[c >> 1] = pack_bf16(p0, p1);
         }
-        st_shared_v4(prow + tswz(row, 2 * j), make_uint4(w[0], w[1], w[2], w[3]));
-        st_shared_v4(prow + tswz(row, 2 * j + 1), make_uint4(w[4], w[5], w[6], w[7]));
+        st_shared_v4(prow + tswz(row, 2 * j), make_uint4(pw[0], pw[1], pw[2], pw[3]));
+        st_shared_v4(prow + tswz(row, 2 * j + 1), make_uint4(pw[4], pw[5], pw[6], pw[7]));
       }
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full0 + 8 * sb);
-      it += nch;
-      ++ntile;
-      if (done) break;
     }
     // ---- epilogue: O / l -> bf16 rows, once the last P.V landed
     mbar_wait(p_free0 + 8 * ((ntile - 1) & 1), ((ntile - 1) >> 1) & 1);
@@ -437,8 +444,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 }
 
 int prefill_tc_smem_bytes() {
-  return 1024 + 2 * kTcRows * 128 + kTcStages * 2 * 4096 + 2 * kTcRows * 128 + kTcStages * 16 +
-         (2 * kTcStages + 9) * 8 + 16;   // barriers + TMEM address slot
+  return 1024 + 2 * kTcRows * 128 + kTcStages * 4 * kTcKeys * 128 + 2 * kTcRows * 128 +
+         (2 * kTcStages + 9) * 8 + 16;
 }
 
 cudaError_t launch_prefill_tc(const CUtensorMap &tmK, const CUtensorMap &tmV, const PrefillParams &p,
