@@ -118,6 +118,7 @@ struct PrefillParams {
   uint16_t *out;
   int64_t o_st, o_sh;
   float scale_log2;
+  int tiles_max;          // 128-row query tiles of the longest request (persistent kernels)
 };
 int prefill_smem_bytes(int head_dim);
 bool prefill_uses_tc(int head_dim);   // tcgen05 kernel (wants 1-half TMA boxes)

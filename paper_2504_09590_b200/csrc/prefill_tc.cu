@@ -174,19 +174,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   constexpr int STAGE = 2 * TILE;              // K + V
   constexpr unsigned FULL = 0xffffffffu;
 
-  const int r = blockIdx.z, h = blockIdx.y;
-  const int q0 = __ldg(p.cu_q + r);
-  const int n = __ldg(p.cu_q + r + 1) - q0;
-  const int g = p.g;
-  const int rows = n * g;
-  const int ntiles = (rows + kTcRows - 1) / kTcRows;
-  const int tile = ntiles - 1 - static_cast<int>(blockIdx.x);
-  if (tile < 0) return;
-  const int L = __ldg(p.seq_lens + r);
-  const int row0 = tile * kTcRows;
-  const int row_end = min(rows, row0 + kTcRows);
-  const int pos_max = L - n + (row_end - 1) / g;
-
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -204,9 +191,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                  p_free0 = s_full0 + 48, q_full = s_full0 + 64;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  if (threadIdx.x == 0) {
-    prefetch_tmap(&tmK);
-    prefetch_tmap(&tmV);
+  auto init_barriers = [&]() {
     for (int i = 0; i < kTcStages; ++i) {
       mbar_init(full0 + 8 * i, 1);
       mbar_init(empty0 + 8 * i, 1);
@@ -219,6 +204,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
     mbar_init(q_full, 4);
     fence_mbar_init();
+  };
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&tmK);
+    prefetch_tmap(&tmV);
+    init_barriers();
   }
   if (warp == 5) {   // TMEM: S buffers at columns [0, 64) and [64, 128), O at [128, 256)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot)));
@@ -228,6 +218,30 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+
+  // Persistent over work items (x, h, r), x = tile counted from the END of the
+  // request (its latest, longest rows first): only existing tiles cost a pass;
+  // no CTA is launched for an empty tile.  TMEM stays allocated and every
+  // barrier keeps running phases across items: all roles number key tiles with
+  // the same CTA-global counter gt (stage = gt % stages, S/P buffer = gt & 1),
+  // so the producer already streams the next item while the current one drains.
+  const int g = p.g;
+  int gt0 = 0;           // key tiles of earlier items (identical in every role)
+  int items_done = 0;
+  const int n_items = p.tiles_max * p.H * p.B;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+  const int x = item / (p.H * p.B), hr = item - x * (p.H * p.B);
+  const int r = hr / p.H, h = hr - r * p.H;
+  const int q0 = __ldg(p.cu_q + r);
+  const int n = __ldg(p.cu_q + r + 1) - q0;
+  const int rows = n * g;
+  const int ntiles = (rows + kTcRows - 1) / kTcRows;
+  const int tile = ntiles - 1 - x;
+  if (tile < 0) continue;
+  const int L = __ldg(p.seq_lens + r);
+  const int row0 = tile * kTcRows;
+  const int row_end = min(rows, row0 + kTcRows);
+  const int pos_max = L - n + (row_end - 1) / g;
 
   // Every role (producer, MMA issuer, each softmax warp) runs the same chunk walk
   // itself (warp-collective, entries read 32 at a time), so no chunk metadata
@@ -245,9 +259,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const uint64_t pol = policy_evict_first();
     for (int t = 0;; ++t) {
       const int nch = tc_tile(p, r, L, pos_max, walk, ch);
-      if (nch == 0) break;
+      if (nch == 0) {
+        gt0 += t;
+        break;
+      }
       if (lane == 0) {
-        const int st = t % kTcStages, round = t / kTcStages;
+        const int gt = gt0 + t, st = gt % kTcStages, round = gt / kTcStages;
         if (round > 0) mbar_wait(empty0 + 8 * st, (round - 1) & 1);
         const uint32_t fb = full0 + 8 * st;
         mbar_arrive_expect_tx(fb, nch * 4 * 2048);
@@ -264,15 +281,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   } else if (warp == 5) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      mbar_wait(q_full, 0);
+      mbar_wait(q_full, items_done & 1);
       tc_fence_after();
     }
     __syncwarp();
     bool first_pv = true;
     int prev_nch = 0;
-    auto issue_pv = [&](int t, int nch) {
-      const int pb = t & 1, st = t % kTcStages;
-      mbar_wait(p_full0 + 8 * pb, (t >> 1) & 1);
+    auto issue_pv = [&](int gt, int nch) {
+      const int pb = gt & 1, st = gt % kTcStages;
+      mbar_wait(p_full0 + 8 * pb, (gt >> 1) & 1);
       tc_fence_after();
       const uint32_t idO = idesc(128, 128, 0, 1);
       for (int j = 0; j < nch; ++j) {
@@ -286,11 +303,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     };
     for (int t = 0;; ++t) {
       const int nch = tc_tile(p, r, L, pos_max, walk, ch);   // whole warp: the walk uses shuffles
+      const int gt = gt0 + t;
       if (lane == 0) {
-        const int sb = t & 1, st = t % kTcStages;
+        const int sb = gt & 1, st = gt % kTcStages;
         if (nch > 0) {
-          mbar_wait(full0 + 8 * st, (t / kTcStages) & 1);
-          if (t >= 2) mbar_wait(s_free0 + 8 * sb, ((t - 2) >> 1) & 1);
+          mbar_wait(full0 + 8 * st, (gt / kTcStages) & 1);
+          if (gt >= 2) mbar_wait(s_free0 + 8 * sb, ((gt - 2) >> 1) & 1);
           tc_fence_after();
           const uint32_t idS = idesc(128, 16 * nch, 0, 0);
           const uint32_t sk = sStage + st * STAGE;
@@ -302,10 +320,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           }
           umma_commit(s_full0 + 8 * sb);
         }
-        if (t >= 1) issue_pv(t - 1, prev_nch);   // P.V of the previous tile overlaps S of this one
+        if (t >= 1) issue_pv(gt - 1, prev_nch);   // P.V of the previous tile overlaps S of this one
       }
       __syncwarp();
-      if (nch == 0) break;
+      if (nch == 0) {
+        gt0 += t;
+        break;
+      }
       prev_nch = nch;
     }
   } else {
@@ -331,7 +352,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     float m_ref = -INFINITY, l = 0.f;
     int ntile = 0;
     for (;; ++ntile) {
-      const int t = ntile, sb = t & 1, st = t % kTcStages;
+      const int t = gt0 + ntile, sb = t & 1, st = t % kTcStages;   // CTA-global key tile number
       const int nch = tc_tile(p, r, L, pos_max, walk, ch);
       if (nch == 0) break;
       int4 meta[kTcChunks];
@@ -380,7 +401,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       if (__any_sync(FULL, resc)) {
         const float alpha = resc ? ex2(m_ref - mx) : 1.f;
         l *= alpha;
-        mbar_wait(p_free0 + 8 * ((t - 1) & 1), ((t - 1) >> 1) & 1);
+        mbar_wait(p_free0 + 8 * ((t - 1) & 1), ((t - 1) >> 1) & 1);   // (t >= 1: m_ref set by an earlier tile)
         tc_fence_after();
 #pragma unroll 1
         for (int c = 0; c < D; c += 16) {
@@ -417,7 +438,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       if (lane == 0) mbar_arrive(p_full0 + 8 * sb);
     }
     // ---- epilogue: O / l -> bf16 rows, once the last P.V landed
-    mbar_wait(p_free0 + 8 * ((ntile - 1) & 1), ((ntile - 1) >> 1) & 1);
+    gt0 += ntile;
+    mbar_wait(p_free0 + 8 * ((gt0 - 1) & 1), ((gt0 - 1) >> 1) & 1);
     tc_fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
     uint4 *orow = reinterpret_cast<uint4 *>(p.out + static_cast<int64_t>(q0 + tok) * p.o_st +
@@ -436,6 +458,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
     tc_fence_before();
   }
+  ++items_done;
+  }   // work items
   __syncthreads();
   if (warp == 5) {
     tc_fence_after();
@@ -458,8 +482,14 @@ cudaError_t launch_prefill_tc(const CUtensorMap &tmK, const CUtensorMap &tmV, co
     configured = smem;
   }
   const long long tiles = (static_cast<long long>(max_q_len) * p.g + kTcRows - 1) / kTcRows;
-  dim3 grid(static_cast<unsigned>(tiles), p.H, p.B);
-  prefill_tc_kernel<<<grid, kTcThreads, smem, s>>>(tmK, tmV, p);
+  PrefillParams q = p;
+  q.tiles_max = static_cast<int>(tiles);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long items = tiles * p.H * p.B;
+  const int grid = static_cast<int>(items < sms ? items : sms);   // one persistent CTA per SM
+  prefill_tc_kernel<<<grid, kTcThreads, smem, s>>>(tmK, tmV, q);
   return cudaGetLastError();
 }
 
