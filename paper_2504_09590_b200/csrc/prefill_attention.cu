@@ -340,13 +340,12 @@ __global__ void __launch_bounds__(32 * (kConsumerWarps + 1), 1)
   }
 }
 
-// The tcgen05/TMEM kernel (prefill_tc.cu, head_dim 128) is opt-in, BKV_PREFILL_TC=1:
-// parity-green but measured slower than this mma.sync kernel so far (Llama-70B TP1
-// whole-prompt prefills 71 vs 140 TF/s: one 4-warp softmax group per SM leaves its
-// latency exposed; next: two ping-pong query tiles per CTA).
+// head_dim 128 runs the tcgen05/TMEM kernel (prefill_tc.cu): Llama-70B TP1 whole-
+// prompt prefills 160 vs 140 TF/s for this mma.sync kernel, which stays the
+// head_dim-64 path and is selectable for 128 with BKV_PREFILL_MMA_SYNC=1 (dev A/B).
 bool prefill_uses_tc(int head_dim) {
-  const char *e = getenv("BKV_PREFILL_TC");
-  return head_dim == 128 && e && atoi(e) != 0;
+  const char *e = getenv("BKV_PREFILL_MMA_SYNC");
+  return head_dim == 128 && !(e && atoi(e) != 0);
 }
 
 int prefill_smem_bytes(int head_dim) {
@@ -372,7 +371,7 @@ static cudaError_t launch_prefill_t(const CUtensorMap &tmK, const CUtensorMap &t
 cudaError_t launch_prefill(const CUtensorMap &tmK, const CUtensorMap &tmV, const PrefillParams &p,
                            int head_dim, int max_q_len, cudaStream_t s) {
   if (p.B <= 0 || max_q_len <= 0) return cudaSuccess;
-  // opt-in tcgen05 / TMEM kernel (prefill_tc.cu; tensor maps with one 64-d half per box)
+  // head_dim 128: the tcgen05 / TMEM kernel (prefill_tc.cu; tensor maps with one 64-d half per box)
   if (prefill_uses_tc(head_dim)) return launch_prefill_tc(tmK, tmV, p, max_q_len, s);
   return head_dim == 128 ? launch_prefill_t<128>(tmK, tmV, p, max_q_len, s)
                          : launch_prefill_t<64>(tmK, tmV, p, max_q_len, s);

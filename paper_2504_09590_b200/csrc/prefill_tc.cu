@@ -3,9 +3,8 @@
 // (PAPER.md P:762-765).  Same contract and tiling as
 // prefill_attention.cu: one CTA per (128-row query tile, kv head, request),
 // rows = (token, q head of the group) pairs, causal over the request's paged
-// tokens, dense or general block maps.  Opt-in (BKV_PREFILL_TC=1): parity-green
-// (tests run it) but slower than the mma.sync kernel so far -- see
-// prefill_uses_tc() in prefill_attention.cu.
+// tokens, dense or general block maps.  The default for head_dim 128 (see
+// prefill_uses_tc() in prefill_attention.cu).
 //
 // Roles (192 threads):
 //   warps 0-3  softmax warpgroup: thread t owns query row t of the tile and TMEM
@@ -35,6 +34,7 @@ namespace {
 constexpr int kTcStages = 4;       // key-tile ring (K | V of up to 64 keys per stage)
 constexpr int kTcChunks = 4;       // chunks (16 keys each) per key tile
 constexpr int kTcKeys = 16 * kTcChunks;
+constexpr int kTcLastFlag = 1 << 8;   // tile metadata: the item's last key tile
 constexpr int kTcRows = 128;       // query rows per CTA = TMEM lanes
 constexpr int kTcThreads = 192;
 
@@ -181,7 +181,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const uint32_t sQ = base;                                  // 2 halves x 128 rows x 128 B
   const uint32_t sStage = sQ + 2 * kTcRows * 128;            // kTcStages key tiles (K | V)
   const uint32_t sP = sStage + kTcStages * STAGE;            // 2 x 128 rows x 128 B (64 keys)
-  uint64_t *bars = reinterpret_cast<uint64_t *>(gb + (sP - base) + 2 * kTcRows * 128);
+  int4 *metas = reinterpret_cast<int4 *>(gb + (sP - base) + 2 * kTcRows * 128);   // [stage][chunk]
+  int *tcount = reinterpret_cast<int *>(metas + kTcStages * kTcChunks);          // chunks | last flag
+  uint64_t *bars = reinterpret_cast<uint64_t *>(tcount + kTcStages);
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * kTcStages + 9);
   const uint32_t bar0 = smem_u32(bars);
   const uint32_t full0 = bar0, empty0 = bar0 + 8 * kTcStages;
@@ -243,29 +245,32 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int row_end = min(rows, row0 + kTcRows);
   const int pos_max = L - n + (row_end - 1) / g;
 
-  // Every role (producer, MMA issuer, each softmax warp) runs the same chunk walk
-  // itself (warp-collective, entries read 32 at a time), so no chunk metadata
-  // crosses warps through shared memory; the tiles themselves are handed over by
-  // the mbarriers.
-  TcWalk walk;
-  tc_walk_init(p, r, L, walk);
-  TcChunk ch[kTcChunks];
+  // Tile metadata: the producer walks the request's chunks (one tile of
+  // lookahead, so each tile carries a "last" flag) and publishes per stage the
+  // chunk count and (lo, hi, tb, dir) per chunk, handed over by two named
+  // barriers per stage (producer bar.arrive; the MMA warp resp. the softmax
+  // warpgroup bar.sync: CTA-scope release/acquire) -- the consumers never walk.
+  // The tiles themselves are handed over by the mbarriers.
+  auto bar_mma = [](int st) { return 1 + st; };                  // producer + MMA warp: 64 threads
+  auto bar_sm = [](int st) { return 1 + kTcStages + st; };       // producer + softmax: 160 threads
 
   if (warp == 4) {
     // ------------------------------------------------------------ producer
     // A key tile = up to four 16-slot chunks of the walk, each landing as rows
     // [16j, 16j+16) of the tile (one TMA box per 64-d half per tensor), so the
     // tile is one contiguous K-major (K) / MN-major (V) 128B-swizzled operand.
+    TcWalk walk;
+    tc_walk_init(p, r, L, walk);
+    TcChunk ch[kTcChunks], nx[kTcChunks];
     const uint64_t pol = policy_evict_first();
-    for (int t = 0;; ++t) {
-      const int nch = tc_tile(p, r, L, pos_max, walk, ch);
-      if (nch == 0) {
-        gt0 += t;
-        break;
-      }
+    int nch = tc_tile(p, r, L, pos_max, walk, ch);
+    for (int t = 0; nch > 0; ++t) {
+      const int nnx = tc_tile(p, r, L, pos_max, walk, nx);   // lookahead: is this tile the last?
+      const int gt = gt0 + t, st = gt % kTcStages, round = gt / kTcStages;
       if (lane == 0) {
-        const int gt = gt0 + t, st = gt % kTcStages, round = gt / kTcStages;
         if (round > 0) mbar_wait(empty0 + 8 * st, (round - 1) & 1);
+        for (int j = 0; j < nch; ++j) metas[st * kTcChunks + j] = make_int4(ch[j].lo, ch[j].hi, ch[j].tb, ch[j].dir);
+        tcount[st] = nch | (nnx == 0 ? kTcLastFlag : 0);
         const uint32_t fb = full0 + 8 * st;
         mbar_arrive_expect_tx(fb, nch * 4 * 2048);
         const uint32_t dk = sStage + st * STAGE;
@@ -277,6 +282,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           }
       }
       __syncwarp();
+      named_bar_arrive(bar_mma(st), 64);
+      named_bar_arrive(bar_sm(st), 160);
+      if (nnx == 0) {
+        gt0 += t + 1;
+        break;
+      }
+      nch = nnx;
+#pragma unroll
+      for (int j = 0; j < kTcChunks; ++j) ch[j] = nx[j];
     }
   } else if (warp == 5) {
     // ------------------------------------------------------------ MMA issuer
@@ -286,7 +300,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
     __syncwarp();
     bool first_pv = true;
-    int prev_nch = 0;
     auto issue_pv = [&](int gt, int nch) {
       const int pb = gt & 1, st = gt % kTcStages;
       mbar_wait(p_full0 + 8 * pb, (gt >> 1) & 1);
@@ -301,33 +314,34 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       umma_commit(empty0 + 8 * st);
       umma_commit(p_free0 + 8 * pb);
     };
+    int prev_nch = 0;
     for (int t = 0;; ++t) {
-      const int nch = tc_tile(p, r, L, pos_max, walk, ch);   // whole warp: the walk uses shuffles
-      const int gt = gt0 + t;
+      const int gt = gt0 + t, sb = gt & 1, st = gt % kTcStages;
+      named_bar_sync(bar_mma(st), 64);
+      const int tc = tcount[st];
+      const int nch = tc & 0xff;
       if (lane == 0) {
-        const int sb = gt & 1, st = gt % kTcStages;
-        if (nch > 0) {
-          mbar_wait(full0 + 8 * st, (gt / kTcStages) & 1);
-          if (gt >= 2) mbar_wait(s_free0 + 8 * sb, ((gt - 2) >> 1) & 1);
-          tc_fence_after();
-          const uint32_t idS = idesc(128, 16 * nch, 0, 0);
-          const uint32_t sk = sStage + st * STAGE;
+        mbar_wait(full0 + 8 * st, (gt / kTcStages) & 1);
+        if (gt >= 2) mbar_wait(s_free0 + 8 * sb, ((gt - 2) >> 1) & 1);
+        tc_fence_after();
+        const uint32_t idS = idesc(128, 16 * nch, 0, 0);
+        const uint32_t sk = sStage + st * STAGE;
 #pragma unroll
-          for (int k = 0; k < D / 16; ++k) {
-            const uint64_t a = sdesc(sQ + (k >> 2) * (kTcRows * 128) + (k & 3) * 32, 16, 1024);
-            const uint64_t b = sdesc(sk + (k >> 2) * HALF + (k & 3) * 32, 16, 1024);
-            umma(tmem + sb * 64, a, b, idS, k > 0);
-          }
-          umma_commit(s_full0 + 8 * sb);
+        for (int k = 0; k < D / 16; ++k) {
+          const uint64_t a = sdesc(sQ + (k >> 2) * (kTcRows * 128) + (k & 3) * 32, 16, 1024);
+          const uint64_t b = sdesc(sk + (k >> 2) * HALF + (k & 3) * 32, 16, 1024);
+          umma(tmem + sb * 64, a, b, idS, k > 0);
         }
+        umma_commit(s_full0 + 8 * sb);
         if (t >= 1) issue_pv(gt - 1, prev_nch);   // P.V of the previous tile overlaps S of this one
+        if (tc & kTcLastFlag) issue_pv(gt, nch);
       }
       __syncwarp();
-      if (nch == 0) {
-        gt0 += t;
+      prev_nch = nch;
+      if (tc & kTcLastFlag) {
+        gt0 += t + 1;
         break;
       }
-      prev_nch = nch;
     }
   } else {
     // ------------------------------------------------------------ softmax warpgroup
@@ -353,12 +367,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     int ntile = 0;
     for (;; ++ntile) {
       const int t = gt0 + ntile, sb = t & 1, st = t % kTcStages;   // CTA-global key tile number
-      const int nch = tc_tile(p, r, L, pos_max, walk, ch);
-      if (nch == 0) break;
+      named_bar_sync(bar_sm(st), 160);
+      const int tc = tcount[st];
+      const int nch = tc & 0xff;
       int4 meta[kTcChunks];
 #pragma unroll
-      for (int j = 0; j < kTcChunks; ++j)
-        meta[j] = j < nch ? make_int4(ch[j].lo, ch[j].hi, ch[j].tb, ch[j].dir) : make_int4(0, 0, 0, 0);
+      for (int j = 0; j < kTcChunks; ++j) meta[j] = j < nch ? metas[st * kTcChunks + j] : make_int4(0, 0, 0, 0);
       mbar_wait(full0 + 8 * st, (t / kTcStages) & 1);   // the tile's K/V landed (V rows get patched below)
       // dead V rows of partly live chunks -> zero (P = 0 must never meet NaN, reading Q10)
       for (int j = 0; j < nch; ++j) {
@@ -381,15 +395,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(s_free0 + 8 * sb);
-      // mask (direction + causal by token index) and scale
+      // per chunk, the live slots of this row form one interval [clo, chi): the
+      // entry's live range intersected with the causal bound (forward: token
+      // tb + c <= pos -> c <= pos - tb; reversed: tb - c <= pos -> c >= tb - pos)
       float mx = -INFINITY;
 #pragma unroll
       for (int j = 0; j < kTcChunks; ++j) {
+        int clo = meta[j].x, chi = meta[j].y;
+        if (meta[j].w) clo = max(clo, meta[j].z - pos);
+        else chi = min(chi, pos - meta[j].z + 1);
+        if (j >= nch) chi = 0;
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
-          const bool live = j < nch && c >= meta[j].x && c < meta[j].y &&
-                            (meta[j].w ? meta[j].z - c : meta[j].z + c) <= pos;
-          s[16 * j + c] = live ? s[16 * j + c] * p.scale_log2 : -INFINITY;
+          s[16 * j + c] = (c >= clo && c < chi) ? s[16 * j + c] * p.scale_log2 : -INFINITY;
           mx = fmaxf(mx, s[16 * j + c]);
         }
       }
@@ -436,6 +454,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full0 + 8 * sb);
+      if (tc & kTcLastFlag) {
+        ++ntile;
+        break;
+      }
     }
     // ---- epilogue: O / l -> bf16 rows, once the last P.V landed
     gt0 += ntile;
@@ -469,7 +491,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
 int prefill_tc_smem_bytes() {
   return 1024 + 2 * kTcRows * 128 + kTcStages * 4 * kTcKeys * 128 + 2 * kTcRows * 128 +
-         (2 * kTcStages + 9) * 8 + 16;
+         kTcStages * kTcChunks * 16 + kTcStages * 4 + (2 * kTcStages + 9) * 8 + 16;   // + metadata, barriers, TMEM slot
 }
 
 cudaError_t launch_prefill_tc(const CUtensorMap &tmK, const CUtensorMap &tmV, const PrefillParams &p,

@@ -134,17 +134,17 @@ def test_mixed_dispatch_matches_oracle(cfg, general):
 
 
 @pytest.mark.parametrize("cfg,general,full", [("tiny_gqa", False, False), ("tiny_gqa", True, True)])
-def test_prefill_tcgen05_kernel_parity(cfg, general, full, monkeypatch):
-    """The opt-in tcgen05 / TMEM prefill kernel (BKV_PREFILL_TC=1, head_dim 128)."""
-    monkeypatch.setenv("BKV_PREFILL_TC", "1")
+def test_prefill_mma_sync_kernel_parity_d128(cfg, general, full, monkeypatch):
+    """The mma.sync prefill kernel at head_dim 128 (BKV_PREFILL_MMA_SYNC=1; the default there
+    is the tcgen05 kernel, which every other d128 test here exercises)."""
+    monkeypatch.setenv("BKV_PREFILL_MMA_SYNC", "1")
     case = make_case(cfg, 21, general=general)
     n = query_counts(case.layout.lens, np.random.default_rng(21), full=full)
     o, ref = _run(case, general, n)
-    check_close(o, ref, cfg + " tcgen05")
+    check_close(o, ref, cfg + " mma.sync d128")
 
 
-def test_prefill_tcgen05_long_context_and_geometries(monkeypatch):
-    monkeypatch.setenv("BKV_PREFILL_TC", "1")
+def test_prefill_tcgen05_long_context_and_geometries():
     for hq, hkv, bs, general in ((8, 1, 16, False), (16, 2, 32, True), (5, 5, 16, True)):
         sh = Shape("tc", hq, hkv, 128, bs, 8, 0.5, "uniform", 1500, 1, 1, uniform_max=1500)
         case = make_case(sh, hq + bs, general=general, share_prob=0.9)
