@@ -102,6 +102,35 @@ bkv_status encode_pool_map(CUtensorMap *m, void *base, const bkv_kv_pool *pool, 
   return BKV_OK;
 }
 
+// Combined view of K and V (decode): when the pool is contiguous over (block,
+// head) and V sits a multiple of 16 bytes away from K, one 5-D box
+// {64 d, 16 slots, d/64 halves, 2 (K, V), 1 (block*H + head)} fetches both
+// tiles of a chunk -- one TMA instruction per chunk instead of two.
+// Returns 0 (not applicable), 1 (K first) or 2 (V first, V below K).
+int encode_pool_map_kv(CUtensorMap *m, const bkv_kv_pool *pool) {
+  const char *e = getenv("BKV_KV_COMBINED");
+  if (e && atoi(e) == 0) return 0;
+  auto fn = encode_fn();
+  if (!fn) return 0;
+  if (pool->stride_block != (int64_t)pool->num_kv_heads * pool->stride_head) return 0;
+  const int64_t diff = static_cast<const char *>(pool->v) - static_cast<const char *>(pool->k);
+  const int64_t ad = diff < 0 ? -diff : diff;
+  if (ad == 0 || (ad & 15) || ad >= (int64_t(1) << 40)) return 0;
+  void *base = diff > 0 ? pool->k : pool->v;
+  const int halves = pool->head_dim / 64;
+  cuuint64_t dims[5] = {64, (cuuint64_t)pool->block_size, (cuuint64_t)halves, 2,
+                        (cuuint64_t)pool->num_blocks * pool->num_kv_heads};
+  cuuint64_t strides[4] = {(cuuint64_t)pool->stride_slot * 2, 128, (cuuint64_t)ad,
+                           (cuuint64_t)pool->stride_head * 2};
+  cuuint32_t box[5] = {64, 16, (cuuint32_t)halves, 2, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, base, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return 0;
+  return diff > 0 ? 1 : 2;
+}
+
 // ------------------------------------------------------------ workspace
 struct WsLayout {
   size_t sched, counters, mcnt, ml, o, trace, total;
@@ -337,6 +366,9 @@ static bkv_status decode_impl(const bkv_kv_pool *pool, const bkv_block_map *map,
   CUtensorMap tmK, tmV;
   if ((s = encode_pool_map(&tmK, pool->k, pool))) return s;
   if ((s = encode_pool_map(&tmV, pool->v, pool))) return s;
+  CUtensorMap tmKV;
+  const int kv_mode = encode_pool_map_kv(&tmKV, pool);
+  if (kv_mode) tmK = tmKV;   // the kernel then issues one box per chunk from tmK
   uint8_t *ws = static_cast<uint8_t *>(workspace);
   bkv::DecodeParams p;
   p.bt = map->block_tables;
@@ -391,6 +423,7 @@ static bkv_status decode_impl(const bkv_kv_pool *pool, const bkv_block_map *map,
     if (k < n_peers && (!peer_outs[k] || !aligned16(peer_outs[k])))
       return fail(BKV_ERR_INVALID_ARGUMENT, "peer output %d is NULL or not 16-byte aligned", k);
   }
+  p.kv_mode = kv_mode;
   p.debug_flags = getenv("BKV_DEBUG") ? atoi(getenv("BKV_DEBUG")) : 0;
   p.trace_cap = w.trace_cap;
   p.trace = w.trace_cap ? reinterpret_cast<unsigned long long *>(ws + w.trace) : nullptr;

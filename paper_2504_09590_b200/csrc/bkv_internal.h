@@ -65,6 +65,7 @@ struct DecodeParams {
   int *sched;            // [0] next unit, [1] exited CTAs (re-armed to 0 by the merge kernel or the last CTA)
   int *merge_cnt;        // [B*H] split arrivals per (request, kv head) for the fused merge (self-cleaning)
   int fused_merge;       // 1: last-arriver merge inside the decode kernel (no merge kernel launch)
+  int kv_mode;           // 0: separate K and V boxes; 1/2: one K|V box (tmK = combined map), K resp. V first
   int *plan_out;         // split plan published by CTA 0 for the merge kernel
   float *part_ml;        // [units_max][g][2]  (m in log2 domain, l)
   float *part_o;         // [units_max][g][D]  un-normalised partial outputs

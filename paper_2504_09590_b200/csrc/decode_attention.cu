@@ -304,6 +304,79 @@ __device__ __forceinline__ void merge_row(const DecodeParams &p, int u0, int ns,
   }
 }
 
+// Merge of ALL g rows of (r, h) by one warp (the fused last-arriver path, g <= 8):
+// the (m, l) of every (split, row) pair are loaded at once into the warp's
+// shared scratch, lanes < g turn them into normalised weights
+// w = 2^(m - M) / L, then each lane accumulates its EPL output elements of
+// every row with all partial loads of a split issued together (no per-row
+// dependent chain).  Same result as merge_row up to fp32 rounding order.
+template <int D>
+__device__ __forceinline__ void merge_group(const DecodeParams &p, int u0, int ns, int r, int h, int lane,
+                                            uint32_t scr) {
+  constexpr int EPL = D / 32;
+  const int H = p.H, g = p.g;
+  for (int idx = lane; idx < ns * g; idx += 32) {
+    const int sp = idx / g, j = idx - sp * g;
+    const float2 v = __ldcg(reinterpret_cast<const float2 *>(
+        p.part_ml + (static_cast<int64_t>(u0 + sp * H) * g + j) * 2));
+    st_shared_v2f(scr + idx * 8, v.x, v.y);
+  }
+  __syncwarp();
+  if (lane < g) {
+    float M = -INFINITY;
+    for (int sp = 0; sp < ns; ++sp) M = fmaxf(M, __uint_as_float(lds32(scr + (sp * g + lane) * 8)));
+    float Ls = 0.f;
+    for (int sp = 0; sp < ns; ++sp) {
+      const uint32_t a = scr + (sp * g + lane) * 8;
+      Ls += __uint_as_float(lds32(a + 4)) * ex2(__uint_as_float(lds32(a)) - M);
+    }
+    const float inv = Ls > 0.f ? 1.f / Ls : 0.f;
+    for (int sp = 0; sp < ns; ++sp) {
+      const uint32_t a = scr + (sp * g + lane) * 8;
+      st_shared_f32(a, ex2(__uint_as_float(lds32(a)) - M) * inv);   // weight replaces m
+    }
+  }
+  __syncwarp();
+  float acc[8][EPL];
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+#pragma unroll
+    for (int q = 0; q < EPL; ++q) acc[j][q] = 0.f;
+  for (int sp = 0; sp < ns; ++sp) {
+    const float *po = p.part_o + static_cast<int64_t>(u0 + sp * H) * g * D + lane * EPL;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j >= g) break;
+      const float w = __uint_as_float(lds32(scr + (sp * g + j) * 8));
+      if constexpr (EPL == 4) {
+        const float4 v = __ldcg(reinterpret_cast<const float4 *>(po + j * D));
+        acc[j][0] = fmaf(w, v.x, acc[j][0]);
+        acc[j][1] = fmaf(w, v.y, acc[j][1]);
+        acc[j][2] = fmaf(w, v.z, acc[j][2]);
+        acc[j][3] = fmaf(w, v.w, acc[j][3]);
+      } else {
+        const float2 v = __ldcg(reinterpret_cast<const float2 *>(po + j * D));
+        acc[j][0] = fmaf(w, v.x, acc[j][0]);
+        acc[j][1] = fmaf(w, v.y, acc[j][1]);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (j >= g) break;
+    uint16_t *o = p.out + static_cast<int64_t>(r) * p.o_ss + static_cast<int64_t>(h * g + j) * p.o_sh + lane * EPL;
+    if constexpr (EPL == 4) {
+      uint2 w2;
+      w2.x = pack_bf16(acc[j][0], acc[j][1]);
+      w2.y = pack_bf16(acc[j][2], acc[j][3]);
+      *reinterpret_cast<uint2 *>(o) = w2;
+    } else {
+      *reinterpret_cast<uint32_t *>(o) = pack_bf16(acc[j][0], acc[j][1]);
+    }
+  }
+  __syncwarp();
+}
+
 // KIND 0: MHA on CUDA cores; 1: MMA with g <= 8; 2: MMA with 8 < g <= 16.
 // GQA runs 8 warps (measured best) and gets the 255-register budget of a
 // 256-thread CTA -- at 384 threads the MMA kernels spill (ptxas -v).
@@ -521,8 +594,12 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
       if (kv) {
         // one 5-D box = the whole 16-slot x d tile, laid out [half][slot][128 B] swizzled
         const uint32_t dk = my_slots + i * G::SLOT_BYTES, dv = dk + G::KV_BYTES;
-        tma_load_5d(dk, &tmK, 0, csub * 16, 0, m.h, blk, bar, pol);
-        tma_load_5d(dv, &tmV, 0, csub * 16, 0, m.h, blk, bar, pol);
+        if (p.kv_mode) {   // one box = K and V tiles of (block, head): [kv][half][slot][128 B]
+          tma_load_5d(dk, &tmK, 0, csub * 16, 0, 0, blk * H + m.h, bar, pol);
+        } else {
+          tma_load_5d(dk, &tmK, 0, csub * 16, 0, m.h, blk, bar, pol);
+          tma_load_5d(dv, &tmV, 0, csub * 16, 0, m.h, blk, bar, pol);
+        }
       }
     }
   };
@@ -591,8 +668,10 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
 
   // One chunk: loads are placed right before their use, and the slot is handed
   // back to the issuer (`release`) as soon as both tiles sit in registers.
-  auto consume = [&](uint32_t sk, int lo, int hi, auto &&release) {
-    const uint32_t sv = sk + G::KV_BYTES;
+  // combined K|V boxes land in address order: V first when the V pool lies below K
+  const uint32_t k_off = p.kv_mode == 2 ? G::KV_BYTES : 0u, v_off = G::KV_BYTES - k_off;
+  auto consume = [&](uint32_t s0, int lo, int hi, auto &&release) {
+    const uint32_t sk = s0 + k_off, sv = s0 + v_off;
     if (lo > 0 || hi < 16) zero_dead_rows(sv, lo, hi);   // P = 0 must never meet NaN (Q10)
     if constexpr (!MMA) {
       // ---- s_t = q.k_t : lane = (token t, half hf of d); q from the warp scratch
@@ -843,7 +922,10 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
         int k = 0;
         while (k < kBuckets - 1 && qq >= plan.base[k + 1]) ++k;
         const int u0 = (plan.base[k] + Pre[k * (p.B + 1) + r]) * H + h;
-        for (int head = 0; head < g; ++head) merge_row<D, true>(p, u0, m.nsplit, r, h, head, lane);
+        if (g <= 8 && m.nsplit * g <= 128)
+          merge_group<D>(p, u0, m.nsplit, r, h, lane, my_scr);
+        else
+          for (int head = 0; head < g; ++head) merge_row<D, true>(p, u0, m.nsplit, r, h, head, lane);
         if (lane == 0) p.merge_cnt[r * H + h] = 0;
       }
     }
@@ -880,7 +962,7 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
       const int which = lane >> 4, pc = lane & 15, slot_new = (m.flags >> 8) & 0xff;
       if (pc < TPR) {
         const uint4 v = lds128(my_patch + slot * 512 + which * 2 * D + pc * 16);
-        const uint32_t tile = my_slots + slot * G::SLOT_BYTES + which * G::KV_BYTES;
+        const uint32_t tile = my_slots + slot * G::SLOT_BYTES + (which ? v_off : k_off);
         st_shared_v4(tile + (pc >> 3) * G::HALF_BYTES + swz(slot_new & 15, pc & 7), v);
       }
       if (lane == 0) {   // pool rows: async bulk stores straight from the patch area
