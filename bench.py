@@ -321,10 +321,17 @@ def run_ours(args):
     barrier()
     g_step, g_attn = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
     if args.graphs:
-        with torch.cuda.graph(g_step):
-            step(meta_d, q_d, kn_d, vn_d)
-        with torch.cuda.graph(g_attn):
-            step(meta_d, q_d, kn_d, vn_d, attn_only=True)
+        try:
+            with torch.cuda.graph(g_step):
+                step(meta_d, q_d, kn_d, vn_d)
+            with torch.cuda.graph(g_attn):
+                step(meta_d, q_d, kn_d, vn_d, attn_only=True)
+        except Exception as e:   # e.g. a collective that cannot be captured: time the eager launches
+            print(f"bench: CUDA graph capture failed ({type(e).__name__}: {e}); running eagerly",
+                  file=sys.stderr, flush=True)
+            torch.cuda.synchronize(dev)
+            args.graphs = False
+    if args.graphs:
         run_step, run_attn = g_step.replay, g_attn.replay
     else:
         run_step = lambda: step(meta_d, q_d, kn_d, vn_d)
