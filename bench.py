@@ -122,10 +122,11 @@ def algorithmic_bytes(lay, H, Hq, d, bs):
     token for the local kv heads, q and out rows, block-table + direction entries
     and seq_lens."""
     L = lay.lens.astype(np.int64)
-    nb = (L + bs - 1) // bs
+    nb = lay.nblocks().astype(np.int64)        # entries: ceil(L/bs), or num_entries of a general map
     kv = float(L.sum()) * 2 * H * d * 2
     qo = 2.0 * lay.batch * Hq * d * 2
-    meta = float(nb.sum()) * (4 + 1) + 4.0 * lay.batch
+    per_entry = 4 + 1 + (1 if lay.general else 0)   # block id, direction (+ fill count)
+    meta = float(nb.sum()) * per_entry + (8.0 if lay.general else 4.0) * lay.batch
     return kv + qo + meta, kv
 
 
@@ -228,7 +229,7 @@ def run_ours(args):
     tp = ws
     if sh.num_kv_heads % tp:
         raise SystemExit(f"{args.config}: {sh.num_kv_heads} kv heads do not shard over {tp} GPUs")
-    case = make_case(args.config, args.seed)
+    case = make_case(args.config, args.seed, general=args.general_map)
     lay = case.layout
     shard = HeadShard(sh.num_q_heads, sh.num_kv_heads, tp, rank)
     kv_heads, q_heads = list(shard.kv_heads), list(shard.q_heads)
@@ -256,6 +257,9 @@ def run_ours(args):
         "before": before_h.pin_memory(),
         "cu": cu_h.pin_memory(),
     }
+    if args.general_map:   # per-entry fill counts travel with the map
+        meta_h["fills"] = torch.from_numpy(lay.fills).pin_memory()
+        meta_h["nent"] = torch.from_numpy(lay.num_entries).pin_memory()
     g_cpu = torch.Generator().manual_seed(99)
     q_h = torch.randn((n_layers, B, Hq, d), generator=g_cpu).to(torch.bfloat16).pin_memory()
     kn_h = torch.randn((n_layers, B, H, d), generator=g_cpu).to(torch.bfloat16).pin_memory()
@@ -276,12 +280,13 @@ def run_ours(args):
     def step(md, qd, knd, vnd, attn_only=False):
         """One decode step over all layers (append + attention [+ all-gather])."""
         launches = 0
+        gm = dict(fills=md["fills"], num_entries=md["nent"]) if args.general_map else {}
         for l in range(n_layers):
             if p2p is not None:   # f2: fused step + stores into every peer's output, then signal
                 bkv.decode_multi_out(pools[l], md["bt"], md["dirs"], md["lens"], qd[l],
                                      p2p.local_out(l).permute(1, 0, 2), p2p.peer_outs(l),
                                      k_new=knd[l], v_new=vnd[l], softmax_scale=scale,
-                                     max_seq_len=max_len, ws=wsb, pdl=args.pdl)
+                                     max_seq_len=max_len, ws=wsb, pdl=args.pdl, **gm)
                 launches += 2
                 if not attn_only:
                     p2p.barrier()
@@ -290,14 +295,14 @@ def run_ours(args):
             o = out_loc[l].permute(1, 0, 2)                                   # [B][Hq][d] view
             if args.fused:   # f2: append fused into the attention kernel (bkv_decode_step)
                 bkv.decode_step(pools[l], md["bt"], md["dirs"], md["lens"], knd[l], vnd[l], qd[l],
-                                scale, out=o, max_seq_len=max_len, ws=wsb, pdl=args.pdl)
+                                scale, out=o, max_seq_len=max_len, ws=wsb, pdl=args.pdl, **gm)
             else:
                 if not attn_only:
                     bkv.kv_append(pools[l], md["bt"], md["dirs"], md["before"], md["cu"], knd[l],
-                                  vnd[l], total_new_tokens=B)
+                                  vnd[l], total_new_tokens=B, **gm)
                     launches += 1
                 bkv.paged_decode_attention(pools[l], md["bt"], md["dirs"], md["lens"], qd[l], scale,
-                                           out=o, max_seq_len=max_len, ws=wsb, pdl=args.pdl)
+                                           out=o, max_seq_len=max_len, ws=wsb, pdl=args.pdl, **gm)
             launches += 2                                                     # decode + merge kernels
             if tp > 1 and not attn_only:
                 gather_heads(out_loc[l], out_glob[l])
@@ -414,6 +419,7 @@ def run_ours(args):
             "kv_heads_per_gpu": H, "q_heads_per_gpu": Hq, "head_dim": d, "block_size": bs,
             "mean_ctx": float(lay.lens.mean()), "max_ctx": int(lay.lens.max()),
             "shared_blocks": int(lay.n_shared),
+            "block_map": "general (per-entry fills, f3)" if args.general_map else "dense",
             "l2": f"inputs larger than L2: each step reads {n_layers} layers x {kv_bytes / 1e6:.0f} MB of KV per GPU",
             "per_layer_us": ms_step * 1e3 / n_layers,
             "attn_us_per_layer": att_avg_us,
@@ -457,6 +463,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-pdl", dest="pdl", action="store_false",
                     help="launch attention without programmatic dependent launch")
+    ap.add_argument("--general-map", action="store_true",
+                    help="FindBlock-style general block map (partly filled entries, SURVEY §8(f) f3)")
     ap.add_argument("--reassembly", default="nccl", choices=["nccl", "p2p"],
                     help="N>1: NCCL all-gather (default) or fused NVLink stores (symmetric memory)")
     ap.add_argument("--no-fused", dest="fused", action="store_false",
