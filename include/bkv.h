@@ -14,7 +14,14 @@
  *   bkv_kv_append               -- write this step's new K/V rows into their slots
  *   bkv_paged_decode_attention  -- per-request decode attention over the pool
  *
- * plus host helpers (workspace sizing, a host-side layout validator, status
+ * and the SURVEY §8(f) rows built on them:
+ *
+ *   bkv_kv_append_checkpoint, bkv_kv_checkpoint, bkv_kv_restore   (f1 lazy checkpoint)
+ *   bkv_decode_step, bkv_decode_multi_out, bkv_peer_barrier       (f2 fused step / reassembly)
+ *   bkv_block_map.fills / num_entries in every call               (f3 general maps)
+ *   bkv_paged_prefill_attention, bkv_paged_mixed_attention        (f4 mixed prefill + decode)
+ *
+ * plus host helpers (workspace sizing, host-side layout validators, status
  * strings).
  *
  * Conventions (all entry points):

@@ -11,23 +11,26 @@
 // why the paper's PTX value-vector reversal has no counterpart here.
 //
 // Design (B200, DESIGN.md §6 "decode attention"):
-//  * Persistent grid, one CTA per SM, W independent warps per CTA (12 MHA, 8
-//    GQA).  Each warp is its own producer: lane 0 streams 16-slot "chunks" (K
-//    and V tile of one (block, kv head), 2*d*32 bytes) through a private 2-deep
-//    ring of 128B-swizzled shared-memory slots with ONE 5-D TMA tensor load per
-//    tile and mbarrier completion; the consumer moves the tile to registers
-//    and refills the slot before doing the math.
+//  * Persistent grid, one CTA per SM, 8 independent warps per CTA.  Each warp
+//    is its own producer: lane 0 streams 16-slot "chunks" (K and V tile of one
+//    (block, kv head), 2*d*32 bytes) through a private 2-deep ring of
+//    128B-swizzled shared-memory slots -- ONE 5-D TMA box per chunk when the
+//    pool allows a combined K|V view, else one per tile -- with mbarrier
+//    completion; the consumer moves the tile to registers and refills the
+//    slot before doing the math.
 //  * Work units = (request, kv head, split of <= P blocks), pulled from a
 //    global atomic counter (first unit static), enumerated longest-first by a
-//    4-bucket split plan computed in-kernel from seq_lens; the issuer decodes
+//    4-bucket split plan computed in-kernel from seq_lens (entry counts for
+//    general maps); small problems get a chain-balanced P.  The issuer decodes
 //    the next unit one unit ahead (block-table window loads, q L2 prefetch).
-//  * MHA (g = 1): CUDA-core fp32 (FFMA2), lanes = (token, half of d), q in smem.
-//  * GQA (g >= 2): tokens on the MMA M dimension: S^T = K.Q^T and
-//    O^T += V^T.P^T with bf16 mma.sync m16n8k16 (K via ldmatrix, V via
-//    ldmatrix.trans, P^T re-laid through 256 B of smem).
+//  * Tensor cores for every group size (the CUDA-core FFMA2 MHA variant is a
+//    dev switch, BKV_MHA_CUDA_CORES=1): tokens on the MMA M dimension,
+//    S^T = K.Q^T and O^T += V^T.P^T with bf16 mma.sync m16n8k16 (K via
+//    ldmatrix, V via ldmatrix.trans, P^T re-laid through 256 B of smem).
 //  * A unit's output is written directly when the request has one split;
 //    otherwise fp32 (m, l, o) partials go to the workspace and merge_kernel,
-//    stream-ordered after this kernel, combines them in split order.
+//    stream-ordered after this kernel, combines them in split order (an
+//    in-kernel last-arriver merge exists behind BKV_FUSED_MERGE=1).
 //  * Fused decode step (bkv_decode_step): the chunk that
 //    holds a unit's new token t = L-1 also bulk-loads the token's K/V rows
 //    (from k_new/v_new) into a per-slot patch area on the same mbarrier; the

@@ -9,7 +9,8 @@
 // One CTA per request; each (token, head, K|V) row of head_dim bf16 is moved
 // by head_dim/8 threads with one 16-byte load and one 16-byte store each, so a
 // warp touches whole 128-byte lines on both sides.  The step is launch-latency
-// bound (a decode step moves 4*B*H*d bytes); NEXT f2 fuses it into attention.
+// bound (a decode step moves 4*B*H*d bytes); bkv_decode_step (f2) fuses the
+// decode-step append into the attention kernel instead.
 #include "bkv_internal.h"
 
 namespace bkv {
