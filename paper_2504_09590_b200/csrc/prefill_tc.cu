@@ -165,6 +165,16 @@ __device__ __forceinline__ void tc_walk_init(const PrefillParams &p, int r, int 
 
 }  // namespace
 
+// Dev-only cycle accounting (trace builds, -DBKV_DEV_TRACE): per CTA and role,
+// cycles spent in each phase of the tile loop, read by bkv_dev_prefill_prof.
+#ifdef BKV_DEV_TRACE
+constexpr bool kTcProf = true;
+#else
+constexpr bool kTcProf = false;
+#endif
+constexpr int kProfSlots = 8;
+__device__ unsigned long long g_tc_prof[148 * 3 * kProfSlots];
+
 __global__ void __launch_bounds__(kTcThreads, 1)
     prefill_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                       const PrefillParams p) {
@@ -317,12 +327,23 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     int prev_nch = 0;
     for (int t = 0;; ++t) {
       const int gt = gt0 + t, sb = gt & 1, st = gt % kTcStages;
+      long long pc0 = kTcProf ? clock64() : 0;
+      auto prof = [&](int slot) {
+        if (kTcProf && lane == 0 && blockIdx.x < 148) {
+          const long long c = clock64();
+          atomicAdd(&g_tc_prof[(blockIdx.x * 3 + 1) * kProfSlots + slot], static_cast<unsigned long long>(c - pc0));
+          pc0 = c;
+        }
+      };
       named_bar_sync(bar_mma(st), 64);
+      prof(0);
       const int tc = tcount[st];
       const int nch = tc & 0xff;
       if (lane == 0) {
         mbar_wait(full0 + 8 * st, (gt / kTcStages) & 1);
+        prof(1);
         if (gt >= 2) mbar_wait(s_free0 + 8 * sb, ((gt - 2) >> 1) & 1);
+        prof(2);
         tc_fence_after();
         const uint32_t idS = idesc(128, 16 * nch, 0, 0);
         const uint32_t sk = sStage + st * STAGE;
@@ -333,7 +354,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           umma(tmem + sb * 64, a, b, idS, k > 0);
         }
         umma_commit(s_full0 + 8 * sb);
+        prof(3);
         if (t >= 1) issue_pv(gt - 1, prev_nch);   // P.V of the previous tile overlaps S of this one
+        prof(4);
         if (tc & kTcLastFlag) issue_pv(gt, nch);
       }
       __syncwarp();
@@ -367,13 +390,23 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     int ntile = 0;
     for (;; ++ntile) {
       const int t = gt0 + ntile, sb = t & 1, st = t % kTcStages;   // CTA-global key tile number
+      long long pc0 = kTcProf ? clock64() : 0;
+      auto prof = [&](int slot) {
+        if (kTcProf && threadIdx.x == 0 && blockIdx.x < 148) {
+          const long long c = clock64();
+          atomicAdd(&g_tc_prof[(blockIdx.x * 3 + 0) * kProfSlots + slot], static_cast<unsigned long long>(c - pc0));
+          pc0 = c;
+        }
+      };
       named_bar_sync(bar_sm(st), 160);
+      prof(0);
       const int tc = tcount[st];
       const int nch = tc & 0xff;
       int4 meta[kTcChunks];
 #pragma unroll
       for (int j = 0; j < kTcChunks; ++j) meta[j] = j < nch ? metas[st * kTcChunks + j] : make_int4(0, 0, 0, 0);
       mbar_wait(full0 + 8 * st, (t / kTcStages) & 1);   // the tile's K/V landed (V rows get patched below)
+      prof(1);
       // dead V rows of partly live chunks -> zero (P = 0 must never meet NaN, reading Q10)
       for (int j = 0; j < nch; ++j) {
         if (meta[j].x > 0 || meta[j].y < 16) {
@@ -385,7 +418,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
       }
       // S tile -> registers
+      prof(2);
       mbar_wait(s_full0 + 8 * sb, (t >> 1) & 1);
+      prof(3);
       tc_fence_after();
       float s[kTcChunks * 16];
 #pragma unroll
@@ -436,7 +471,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       if (grow) m_ref = mx;
       const float base_m = m_ref == -INFINITY ? 0.f : m_ref;
       // P -> shared memory buffer sb (K-major, 128B swizzle)
+      prof(4);
       if (t >= 2) mbar_wait(p_free0 + 8 * sb, ((t - 2) >> 1) & 1);
+      prof(5);
       const uint32_t prow = sP + sb * (kTcRows * 128);
 #pragma unroll
       for (int j = 0; j < kTcChunks; ++j) {
@@ -454,6 +491,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full0 + 8 * sb);
+      prof(6);
+      if (kTcProf && threadIdx.x == 0 && blockIdx.x < 148) atomicAdd(&g_tc_prof[(blockIdx.x * 3 + 0) * kProfSlots + 7], 1ull);
       if (tc & kTcLastFlag) {
         ++ntile;
         break;
@@ -488,6 +527,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
   }
 }
+
+}  // namespace bkv
+
+extern "C" __attribute__((visibility("default"))) int bkv_dev_prefill_prof(unsigned long long *host, int reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(host, bkv::g_tc_prof, sizeof(bkv::g_tc_prof));
+  if (reset) {
+    static unsigned long long zeros[148 * 3 * bkv::kProfSlots] = {};
+    cudaMemcpyToSymbol(bkv::g_tc_prof, zeros, sizeof(zeros));
+  }
+  return e == cudaSuccess ? (bkv::kTcProf ? 1 : 2) : -1;
+}
+
+namespace bkv {
 
 int prefill_tc_smem_bytes() {
   return 1024 + 2 * kTcRows * 128 + kTcStages * 4 * kTcKeys * 128 + 2 * kTcRows * 128 +

@@ -22,6 +22,6 @@ ncu --set full --clock-control none --import-source on -k regex:merge_kernel -s 
     -o $OUT/merge_llama70b_tp1 python scripts/ncu_target.py llama70b 1 8 > /dev/null 2>&1
 ncu --set full --clock-control none -k regex:kv_append -s 6 -c 1 -o $OUT/append_opt13b_tp1 \
     python scripts/ncu_target.py opt13b 1 8 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:prefill_kernel -s 2 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:prefill -s 2 -c 1 \
     -o $OUT/prefill_llama70b_tp1 python scripts/bench_prefill.py --config llama70b --tp 1 --no-decodes --steps 1 > /dev/null 2>&1
 ls -la $OUT

@@ -21,7 +21,7 @@ os.makedirs(DST, exist_ok=True)
 
 def short(name):
     for k in ("decode_kernel", "merge_kernel", "kv_append_kernel", "kv_append_general_kernel", "slot_copy_kernel",
-              "prefill_kernel", "peer_barrier_kernel"):
+              "prefill_tc_kernel", "prefill_kernel", "peer_barrier_kernel"):
         if k in name:
             return "bkv::" + k + name[name.index(k) + len(k):].split("(")[0]
     return name.split("(")[0][:60]
