@@ -65,6 +65,12 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
+// K/V tiles re-read by many query tiles of the same request (prefill): keep them in L2
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 // 4-D tiled tensor load global -> shared, completion counted on `bar` (bytes).
 __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap *m, int c0, int c1,
                                             int c2, int c3, uint32_t bar, uint64_t policy) {

@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(32 * (kConsumerWarps + 1), 1)
     // Each stage's chunk metadata is handed over through named barrier
     // 1 + stage (producer bar.arrive, consumers bar.sync: release/acquire at
     // CTA scope); the tiles themselves complete on the stage's full mbarrier.
-    const uint64_t pol = policy_evict_first();
+    const uint64_t pol = policy_evict_last();   // every query tile of the request re-reads these
     int it = 0;
     for (; walk_next(p, r, L, pos_max, walk, lo, hi, tb); ++it) {
       const int st = it % kStages;

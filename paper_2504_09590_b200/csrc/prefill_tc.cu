@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     TcWalk walk;
     tc_walk_init(p, r, L, walk);
     TcChunk ch[kTcChunks], nx[kTcChunks];
-    const uint64_t pol = policy_evict_first();
+    const uint64_t pol = policy_evict_last();   // every query tile of the request re-reads these
     int nch = tc_tile(p, r, L, pos_max, walk, ch);
     for (int t = 0; nch > 0; ++t) {
       const int nnx = tc_tile(p, r, L, pos_max, walk, nx);   // lookahead: is this tile the last?
