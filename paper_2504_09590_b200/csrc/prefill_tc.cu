@@ -36,7 +36,7 @@ constexpr int kTcChunks = 4;       // chunks (16 keys each) per key tile
 constexpr int kTcKeys = 16 * kTcChunks;
 constexpr int kTcLastFlag = 1 << 8;   // tile metadata: the item's last key tile
 constexpr int kTcRows = 128;       // query rows per CTA = TMEM lanes
-constexpr int kTcThreads = 192;
+constexpr int kTcThreads = 224;   // softmax 0-3, K producer 4, MMA 5, V producer 6
 
 __device__ __forceinline__ uint32_t tswz(int row, int c) {
   return static_cast<uint32_t>(row * 128 + ((c ^ (row & 7)) << 4));
@@ -87,6 +87,20 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float *v) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// 2^x on the FMA pipe (half of the softmax exponentials, FA4-style, so the
+// MUFU unit and the FMA pipe share the work): round-to-nearest via the
+// 1.5 * 2^23 magic number, a degree-3 polynomial for 2^f on [-1/2, 1/2]
+// (max relative error 1.0e-4, far below the bf16 rounding of P), exponent by
+// an integer add.  x < -125 (incl. -inf, masked scores) gives 0.
+__device__ __forceinline__ float ex2_poly(float x) {
+  const float xc = fmaxf(x, -125.f);
+  const float t = xc + 12582912.f;
+  const float f = xc - (t - 12582912.f);
+  const float pl = fmaf(fmaf(fmaf(0.0550086178f, f, 0.2422102978f), f, 0.6932828819f), f, 1.f);
+  const float r = __int_as_float(__float_as_int(pl) + ((__float_as_int(t) - 0x4B400000) << 23));
+  return x < -125.f ? 0.f : r;
+}
 
 // the chunk walk (see prefill_attention.cu): entries in logical order, 32 at a
 // time in a lane-distributed window
@@ -205,7 +219,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
   auto init_barriers = [&]() {
     for (int i = 0; i < kTcStages; ++i) {
-      mbar_init(full0 + 8 * i, 1);
+      mbar_init(full0 + 8 * i, 2);   // the K and the V producer each arm their bytes
       mbar_init(empty0 + 8 * i, 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -264,11 +278,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   auto bar_mma = [](int st) { return 1 + st; };                  // producer + MMA warp: 64 threads
   auto bar_sm = [](int st) { return 1 + kTcStages + st; };       // producer + softmax: 160 threads
 
-  if (warp == 4) {
-    // ------------------------------------------------------------ producer
+  if (warp == 4 || warp == 6) {
+    // ------------------------------------------------------------ producers
     // A key tile = up to four 16-slot chunks of the walk, each landing as rows
     // [16j, 16j+16) of the tile (one TMA box per 64-d half per tensor), so the
     // tile is one contiguous K-major (K) / MN-major (V) 128B-swizzled operand.
+    // Warp 4 streams K and publishes the tile metadata (before its copies, so
+    // the consumers can prepare), warp 6 streams V: 8 boxes per warp per tile.
+    const bool is_k = warp == 4;
     TcWalk walk;
     tc_walk_init(p, r, L, walk);
     TcChunk ch[kTcChunks], nx[kTcChunks];
@@ -279,21 +296,26 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const int gt = gt0 + t, st = gt % kTcStages, round = gt / kTcStages;
       if (lane == 0) {
         if (round > 0) mbar_wait(empty0 + 8 * st, (round - 1) & 1);
-        for (int j = 0; j < nch; ++j) metas[st * kTcChunks + j] = make_int4(ch[j].lo, ch[j].hi, ch[j].tb, ch[j].dir);
-        tcount[st] = nch | (nnx == 0 ? kTcLastFlag : 0);
-        const uint32_t fb = full0 + 8 * st;
-        mbar_arrive_expect_tx(fb, nch * 4 * 2048);
-        const uint32_t dk = sStage + st * STAGE;
-        for (int j = 0; j < nch; ++j)
-#pragma unroll
-          for (int hf = 0; hf < 2; ++hf) {
-            tma_load_5d(dk + hf * HALF + j * 2048, &tmK, 0, 16 * ch[j].c, hf, h, ch[j].blk, fb, pol);
-            tma_load_5d(dk + TILE + hf * HALF + j * 2048, &tmV, 0, 16 * ch[j].c, hf, h, ch[j].blk, fb, pol);
-          }
+        if (is_k) {
+          for (int j = 0; j < nch; ++j) metas[st * kTcChunks + j] = make_int4(ch[j].lo, ch[j].hi, ch[j].tb, ch[j].dir);
+          tcount[st] = nch | (nnx == 0 ? kTcLastFlag : 0);
+        }
       }
       __syncwarp();
-      named_bar_arrive(bar_mma(st), 64);
-      named_bar_arrive(bar_sm(st), 160);
+      if (is_k) {
+        named_bar_arrive(bar_mma(st), 64);
+        named_bar_arrive(bar_sm(st), 160);
+      }
+      if (lane == 0) {
+        const uint32_t fb = full0 + 8 * st;
+        mbar_arrive_expect_tx(fb, nch * 2 * 2048);
+        const uint32_t dst = sStage + st * STAGE + (is_k ? 0 : TILE);
+        const CUtensorMap *tm = is_k ? &tmK : &tmV;
+        for (int j = 0; j < nch; ++j)
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) tma_load_5d(dst + hf * HALF + j * 2048, tm, 0, 16 * ch[j].c, hf, h, ch[j].blk, fb, pol);
+      }
+      __syncwarp();
       if (nnx == 0) {
         gt0 += t + 1;
         break;
@@ -433,19 +455,37 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       // per chunk, the live slots of this row form one interval [clo, chi): the
       // entry's live range intersected with the causal bound (forward: token
       // tb + c <= pos -> c <= pos - tb; reversed: tb - c <= pos -> c >= tb - pos)
-      float mx = -INFINITY;
+      // With a positive scale the max commutes with the scaling, which is then
+      // folded into the exponent (p = 2^(s*scale - m)); a tile every row of the
+      // warp sees whole (four full chunks before its first query) skips the masks.
+      const bool fold = p.scale_log2 > 0.f;
+      bool whole = nch == kTcChunks;
+      int clo[kTcChunks], chi[kTcChunks];
 #pragma unroll
       for (int j = 0; j < kTcChunks; ++j) {
-        int clo = meta[j].x, chi = meta[j].y;
-        if (meta[j].w) clo = max(clo, meta[j].z - pos);
-        else chi = min(chi, pos - meta[j].z + 1);
-        if (j >= nch) chi = 0;
+        clo[j] = meta[j].x;
+        chi[j] = meta[j].y;
+        if (meta[j].w) clo[j] = max(clo[j], meta[j].z - pos);
+        else chi[j] = min(chi[j], pos - meta[j].z + 1);
+        if (j >= nch) chi[j] = 0;
+        whole = whole && clo[j] == 0 && chi[j] == 16;
+      }
+      float mx = -INFINITY;
+      if (fold && __all_sync(FULL, whole)) {
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          s[16 * j + c] = (c >= clo && c < chi) ? s[16 * j + c] * p.scale_log2 : -INFINITY;
-          mx = fmaxf(mx, s[16 * j + c]);
+        for (int c = 0; c < kTcChunks * 16; ++c) mx = fmaxf(mx, s[c]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < kTcChunks; ++j) {
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            const float v = fold ? s[16 * j + c] : s[16 * j + c] * p.scale_log2;
+            s[16 * j + c] = (c >= clo[j] && c < chi[j]) ? v : -INFINITY;
+            mx = fmaxf(mx, s[16 * j + c]);
+          }
         }
       }
+      if (fold) mx *= p.scale_log2;   // (-inf stays -inf)
       // lazy rescale: the reference max moves only when it grows by more than 8
       // (2^8 headroom for p); O in TMEM is rescaled warp-collectively, and only
       // once every earlier P.V has landed (p_free of the previous tile)
@@ -481,7 +521,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         uint32_t pw[8];
 #pragma unroll
         for (int c = 0; c < 16; c += 2) {
-          const float p0 = ex2(s[16 * j + c] - base_m), p1 = ex2(s[16 * j + c + 1] - base_m);
+          const float x0 = fold ? fmaf(s[16 * j + c], p.scale_log2, -base_m) : s[16 * j + c] - base_m;
+          const float x1 = fold ? fmaf(s[16 * j + c + 1], p.scale_log2, -base_m) : s[16 * j + c + 1] - base_m;
+          const float p0 = ex2(x0), p1 = ex2_poly(x1);   // MUFU and FMA pipe in parallel
           l += p0 + p1;
           pw[c >> 1] = pack_bf16(p0, p1);
         }

@@ -224,13 +224,13 @@ def test_gqa_equals_mha_with_repeated_kv_heads():
 
 
 # --------------------------------------- full-size configs, sampled requests
-def _full_size(cfg, tp=1, rank=0, sample=6, seed=0, mode="attn", pdl=False):
+def _full_size(cfg, tp=1, rank=0, sample=6, seed=0, mode="attn", pdl=False, spare_blocks=3):
     """Full BASELINE-size batch on the GPU; the oracle checks a sample of requests one by one.
     mode "attn": bkv_paged_decode_attention over the resident context; mode "step": the
     bench's launch configuration -- the fused decode step (bkv_decode_step, PDL) appending
     token L-1 of every request and attending over all L."""
     sh = CONFIGS[cfg] if isinstance(cfg, str) else cfg
-    case = make_case(sh, seed)
+    case = make_case(sh, seed, spare_blocks=spare_blocks)
     lay = case.layout
     kv_heads, q_heads = shard_heads(sh, tp, rank)
     Hl = len(kv_heads)
@@ -293,6 +293,16 @@ def test_sweep_config_sampled_parity(L0, bs, rt):
     (TP8 shard: 1 kv head / 8 q heads), full batch 256, sampled requests vs the oracle."""
     from synth.workload import sweep_shape
     _full_size(sweep_shape(L0, bs, rt), tp=8, rank=3, sample=4, seed=2, mode="step", pdl=True)
+
+
+def test_int64_offsets_tp1_8k_pool():
+    """Llama-70B TP1 at 8K contexts: the pool holds > 2^31 elements per tensor, so every
+    kernel's block/head/slot offsets must be 64-bit (sampled requests vs the oracle)."""
+    from synth.workload import sweep_shape
+    sh = sweep_shape(8192, 16, 0.5)
+    lay = make_case(sh, 5, spare_blocks=4000).layout
+    assert int(lay.block_tables.max()) * sh.num_kv_heads * sh.block_size * sh.head_dim > 2 ** 31
+    _full_size(sh, tp=1, rank=0, sample=3, seed=5, mode="step", pdl=True, spare_blocks=4000)
 
 
 def test_max_batch_2048():
