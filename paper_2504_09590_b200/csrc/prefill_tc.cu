@@ -88,20 +88,6 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float *v) {
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-// 2^x on the FMA pipe (half of the softmax exponentials, FA4-style, so the
-// MUFU unit and the FMA pipe share the work): round-to-nearest via the
-// 1.5 * 2^23 magic number, a degree-3 polynomial for 2^f on [-1/2, 1/2]
-// (max relative error 1.0e-4, far below the bf16 rounding of P), exponent by
-// an integer add.  x < -125 (incl. -inf, masked scores) gives 0.
-__device__ __forceinline__ float ex2_poly(float x) {
-  const float xc = fmaxf(x, -125.f);
-  const float t = xc + 12582912.f;
-  const float f = xc - (t - 12582912.f);
-  const float pl = fmaf(fmaf(fmaf(0.0550086178f, f, 0.2422102978f), f, 0.6932828819f), f, 1.f);
-  const float r = __int_as_float(__float_as_int(pl) + ((__float_as_int(t) - 0x4B400000) << 23));
-  return x < -125.f ? 0.f : r;
-}
-
 // the chunk walk (see prefill_attention.cu): entries in logical order, 32 at a
 // time in a lane-distributed window
 struct TcWalk {
@@ -523,7 +509,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         for (int c = 0; c < 16; c += 2) {
           const float x0 = fold ? fmaf(s[16 * j + c], p.scale_log2, -base_m) : s[16 * j + c] - base_m;
           const float x1 = fold ? fmaf(s[16 * j + c + 1], p.scale_log2, -base_m) : s[16 * j + c + 1] - base_m;
-          const float p0 = ex2(x0), p1 = ex2_poly(x1);   // MUFU and FMA pipe in parallel
+          const float p0 = ex2(x0), p1 = ex2(x1);
           l += p0 + p1;
           pw[c >> 1] = pack_bf16(p0, p1);
         }
