@@ -416,11 +416,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       mbar_wait(full0 + 8 * st, (t / kTcStages) & 1);   // the tile's K/V landed (V rows get patched below)
       prof(1);
       // dead V rows of partly live chunks -> zero (P = 0 must never meet NaN, reading Q10)
-      for (int j = 0; j < nch; ++j) {
-        if (meta[j].x > 0 || meta[j].y < 16) {
+#pragma unroll
+      for (int j = 0; j < kTcChunks; ++j) {   // unrolled: meta[] stays in registers
+        if (j < nch && (meta[j].x > 0 || meta[j].y < 16)) {
           const uint32_t sv = sStage + st * STAGE + TILE + j * 2048;
-          for (int q = row; q < 256; q += kTcRows) {   // 16 slots x 2 halves x 8 pieces
-            const int slot = q >> 4, rest = q & 15;
+#pragma unroll
+          for (int q = 0; q < 256; q += kTcRows) {   // 16 slots x 2 halves x 8 pieces
+            const int slot = (q + row) >> 4, rest = (q + row) & 15;
             if (slot < meta[j].x || slot >= meta[j].y) sts128_zero(sv + (rest >> 3) * HALF + slot * 128 + (rest & 7) * 16);
           }
         }
@@ -456,10 +458,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (j >= nch) chi[j] = 0;
         whole = whole && clo[j] == 0 && chi[j] == 16;
       }
-      float mx = -INFINITY;
+      // eight independent max chains (a single running max is a 64-deep
+      // dependency chain on one thread)
+      float mx8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mx8[i] = -INFINITY;
       if (fold && __all_sync(FULL, whole)) {
 #pragma unroll
-        for (int c = 0; c < kTcChunks * 16; ++c) mx = fmaxf(mx, s[c]);
+        for (int c = 0; c < kTcChunks * 16; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], s[c]);
       } else {
 #pragma unroll
         for (int j = 0; j < kTcChunks; ++j) {
@@ -467,10 +473,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           for (int c = 0; c < 16; ++c) {
             const float v = fold ? s[16 * j + c] : s[16 * j + c] * p.scale_log2;
             s[16 * j + c] = (c >= clo[j] && c < chi[j]) ? v : -INFINITY;
-            mx = fmaxf(mx, s[16 * j + c]);
+            mx8[c & 7] = fmaxf(mx8[c & 7], s[16 * j + c]);
           }
         }
       }
+      float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                       fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
       if (fold) mx *= p.scale_log2;   // (-inf stays -inf)
       // lazy rescale: the reference max moves only when it grows by more than 8
       // (2^8 headroom for p); O in TMEM is rescaled warp-collectively, and only
@@ -501,6 +509,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       if (t >= 2) mbar_wait(p_free0 + 8 * sb, ((t - 2) >> 1) & 1);
       prof(5);
       const uint32_t prow = sP + sb * (kTcRows * 128);
+      float l4[4] = {0.f, 0.f, 0.f, 0.f};   // independent row-sum chains, folded into l below
 #pragma unroll
       for (int j = 0; j < kTcChunks; ++j) {
         if (j >= nch) break;
@@ -510,12 +519,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           const float x0 = fold ? fmaf(s[16 * j + c], p.scale_log2, -base_m) : s[16 * j + c] - base_m;
           const float x1 = fold ? fmaf(s[16 * j + c + 1], p.scale_log2, -base_m) : s[16 * j + c + 1] - base_m;
           const float p0 = ex2(x0), p1 = ex2(x1);
-          l += p0 + p1;
+          l4[(c >> 1) & 3] += p0 + p1;
           pw[c >> 1] = pack_bf16(p0, p1);
         }
         st_shared_v4(prow + tswz(row, 2 * j), make_uint4(pw[0], pw[1], pw[2], pw[3]));
         st_shared_v4(prow + tswz(row, 2 * j + 1), make_uint4(pw[4], pw[5], pw[6], pw[7]));
       }
+      l += (l4[0] + l4[1]) + (l4[2] + l4[3]);
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full0 + 8 * sb);
