@@ -277,8 +277,10 @@ def run_ours(args):
     max_len = int(lay.lens.max())
     scale = 1.0 / math.sqrt(d)
 
-    def step(md, qd, knd, vnd, attn_only=False):
+    def step(md, qd, knd, vnd, attn_only=False, ol=None, og=None):
         """One decode step over all layers (append + attention [+ all-gather])."""
+        ol = out_loc if ol is None else ol
+        og = out_glob if og is None else og
         launches = 0
         gm = dict(fills=md["fills"], num_entries=md["nent"]) if args.general_map else {}
         for l in range(n_layers):
@@ -292,7 +294,7 @@ def run_ours(args):
                     p2p.barrier()
                     launches += 1
                 continue
-            o = out_loc[l].permute(1, 0, 2)                                   # [B][Hq][d] view
+            o = ol[l].permute(1, 0, 2)                                        # [B][Hq][d] view
             if args.fused:   # f2: append fused into the attention kernel (bkv_decode_step)
                 bkv.decode_step(pools[l], md["bt"], md["dirs"], md["lens"], knd[l], vnd[l], qd[l],
                                 scale, out=o, max_seq_len=max_len, ws=wsb, pdl=args.pdl, **gm)
@@ -305,7 +307,7 @@ def run_ours(args):
                                            out=o, max_seq_len=max_len, ws=wsb, pdl=args.pdl, **gm)
             launches += 2                                                     # decode + merge kernels
             if tp > 1 and not attn_only:
-                gather_heads(out_loc[l], out_glob[l])
+                gather_heads(ol[l], og[l])
         return launches
 
     def barrier():
@@ -380,9 +382,74 @@ def run_ours(args):
         run_step()
         out_h.copy_(src_out, non_blocking=True)
 
-    for _ in range(2):
-        e2e_step()
-    ms_e2e = timed(e2e_step, args.steps) / args.steps
+    pipelined = args.graphs and p2p is None and args.e2e_pipeline
+    if pipelined:
+        # Serving pipeline: two input/output buffer sets, one captured graph per set; a
+        # copy stream moves step i+1's inputs host -> device while step i computes, and
+        # step i's outputs device -> host while step i+1 computes.  Every step still
+        # moves all of its inputs and outputs through PCIe inside the timed region.
+        meta_d2 = {k: torch.empty_like(v) for k, v in meta_d.items()}
+        q_d2, kn_d2, vn_d2 = torch.empty_like(q_d), torch.empty_like(kn_d), torch.empty_like(vn_d)
+        out_loc2 = torch.empty_like(out_loc)
+        out_glob2 = torch.empty_like(out_glob) if out_glob is not None else None
+        for k in meta_d:
+            meta_d2[k].copy_(meta_d[k])
+        q_d2.copy_(q_d), kn_d2.copy_(kn_d), vn_d2.copy_(vn_d)
+        step(meta_d2, q_d2, kn_d2, vn_d2, ol=out_loc2, og=out_glob2)   # eager warm-up of set 2
+        torch.cuda.synchronize(dev)
+        g_step2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_step2):
+            step(meta_d2, q_d2, kn_d2, vn_d2, ol=out_loc2, og=out_glob2)
+        sets = [(meta_d, q_d, kn_d, vn_d, g_step, src_out),
+                (meta_d2, q_d2, kn_d2, vn_d2, g_step2, out_glob2 if tp > 1 else out_loc2)]
+        copy = torch.cuda.Stream(dev)
+        ev_h2d = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_comp = [torch.cuda.Event(), torch.cuda.Event()]
+
+        def h2d(si):
+            md, qd, knd, vnd, _, _ = sets[si]
+            with torch.cuda.stream(copy):
+                for k, v in meta_h.items():
+                    md[k].copy_(v, non_blocking=True)
+                qd.copy_(q_h, non_blocking=True)
+                knd.copy_(kn_h, non_blocking=True)
+                vnd.copy_(vn_h, non_blocking=True)
+                ev_h2d[si].record(copy)
+
+        def run_pipeline(n):
+            copy.wait_stream(stream)
+            h2d(0)
+            for i in range(n):
+                si = i % 2
+                stream.wait_event(ev_h2d[si])
+                sets[si][4].replay()
+                ev_comp[si].record(stream)
+                if i + 1 < n:                      # inputs of step i+1 (its set was last read by step i-1)
+                    sj = 1 - si
+                    if i >= 1:
+                        copy.wait_event(ev_comp[sj])
+                    h2d(sj)
+                with torch.cuda.stream(copy):      # outputs of step i, overlapping step i+1
+                    copy.wait_event(ev_comp[si])
+                    out_h.copy_(sets[si][5], non_blocking=True)
+            stream.wait_stream(copy)
+
+        def timed_pipeline(n):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            barrier()
+            e0.record(stream)
+            run_pipeline(n)
+            e1.record(stream)
+            barrier()
+            return max_over_ranks(e0.elapsed_time(e1))
+
+        run_pipeline(2)
+        ms_e2e = timed_pipeline(args.steps) / args.steps
+    else:
+        for _ in range(2):
+            e2e_step()
+        ms_e2e = timed(e2e_step, args.steps) / args.steps
     if p2p is not None:
         p2p.check()
     clk = clocks.stop()                      # clocks sampled over all three timed regions
@@ -439,6 +506,8 @@ def run_ours(args):
         },
         "cpu_baseline": cpu,
         "e2e": {"value": B / (ms_e2e * 1e-3), "unit": "tokens/s", "ms_per_step": ms_e2e,
+                "pipeline": ("copy stream overlaps step i+1 H2D and step i D2H with compute (2 buffer sets)"
+                             if pipelined else "serial H2D, step, D2H on one stream"),
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": launches,
         "clocks": clk,
@@ -463,6 +532,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-pdl", dest="pdl", action="store_false",
                     help="launch attention without programmatic dependent launch")
+    ap.add_argument("--no-e2e-pipeline", dest="e2e_pipeline", action="store_false",
+                    help="e2e leg: serial H2D/step/D2H instead of the double-buffered copy-stream pipeline")
     ap.add_argument("--general-map", action="store_true",
                     help="FindBlock-style general block map (partly filled entries, SURVEY §8(f) f3)")
     ap.add_argument("--reassembly", default="nccl", choices=["nccl", "p2p"],
