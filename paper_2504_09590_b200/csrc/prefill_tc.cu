@@ -1,27 +1,34 @@
 // prefill_tc.cu -- mixed prefill + decode attention on the 5th-generation
 // tensor cores (tcgen05.mma, TMEM accumulators) for head_dim 128
-// (PAPER.md P:762-765).  Same contract and tiling as
-// prefill_attention.cu: one CTA per (128-row query tile, kv head, request),
-// rows = (token, q head of the group) pairs, causal over the request's paged
-// tokens, dense or general block maps.  The default for head_dim 128 (see
-// prefill_uses_tc() in prefill_attention.cu).
+// (PAPER.md P:762-765).  Same contract as
+// prefill_attention.cu: rows = (token, q head of the group) pairs, causal over
+// the request's paged tokens, dense or general block maps.  The default for
+// head_dim 128 (see prefill_uses_tc() in prefill_attention.cu).
 //
-// Roles (192 threads):
-//   warps 0-3  softmax warpgroup: thread t owns query row t of the tile and TMEM
-//              lane t (tcgen05.ld 32x32b gives a whole row to one thread: no
-//              shuffles); loads Q, masks (direction + causal by token index,
-//              P:711), online softmax in the log2 domain with a lazy rescale
-//              (the running max is only moved when it grows by > 8, so O in
-//              TMEM is rarely touched), writes P (bf16) to shared memory,
-//              zeroes dead V rows, and runs the epilogue;
-//   warp 4     producer: walks the request's entries in logical order and TMA-
-//              streams each 16-slot chunk's K and V tiles into an 8-stage ring;
-//   warp 5     MMA issuer (one lane) + TMEM owner: per key tile of up to four
-//              chunks, S = Q.K^T (M 128, N 16 per chunk, K 128) into one of two
-//              TMEM S buffers, then O += P.V (M 128, N 128, K 16 per chunk) into
-//              the TMEM O accumulator; tcgen05.commit releases stages/buffers.
+// Persistent CTAs (one per SM) walk work items = QT consecutive 128-row query
+// tiles of one (request, kv head), latest rows first; QT = 2 by default
+// ("ping-pong": both tiles share every streamed K/V tile).  Roles, for
+// QT = 2 (352 threads):
+//   warps 0-3, 4-7  one softmax warpgroup per query tile: thread t owns row t
+//              of its tile and TMEM lane t (tcgen05.ld 32x32b gives a whole
+//              row to one thread: no shuffles); loads Q, masks (direction +
+//              causal by token index; a mask-free path for whole
+//              tiles), online softmax in the log2 domain with a lazy rescale
+//              (the running max moves only when it grows by > 8, so O in TMEM
+//              is rarely touched), writes P (bf16) to shared memory, zeroes
+//              dead V rows (group 0), runs the epilogue;
+//   warp 8     K producer: walks the request's entries in logical order and
+//              publishes each 64-key tile's chunk metadata through named
+//              barriers, then TMA-streams the K tile (four 16-slot chunks as
+//              rows of one 128B-swizzled operand) into a 3-stage ring;
+//   warp 9     MMA issuer (one lane) + TMEM owner: per key tile, for each
+//              query tile S = Q.K^T (M 128, N <= 64, K 128) into one of two
+//              TMEM S buffers, then O += P.V (M 128, N 128, K 16 per chunk)
+//              into that tile's TMEM O accumulator; tcgen05.commit releases
+//              S/P buffers and stages;
+//   warp 10    V producer (same walk, V tiles).
 // Operands: Q, K and P are K-major 128B-swizzled, V is MN-major 128B-swizzled
-// -- exactly the layout the 5-D TMA boxes of the pool land in.
+// -- exactly the layout the TMA boxes of the pool land in.
 #include <math.h>
 
 #include "bkv_internal.h"
@@ -175,10 +182,16 @@ constexpr bool kTcProf = false;
 constexpr int kProfSlots = 8;
 __device__ unsigned long long g_tc_prof[148 * 3 * kProfSlots];
 
-__global__ void __launch_bounds__(kTcThreads, 1)
+// QT = query tiles of 128 rows per CTA (1, or 2 "ping-pong" groups sharing every
+// K/V tile: two softmax warpgroups, twice the MMA work per streamed byte).
+template <int QT>
+__global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
     prefill_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                       const PrefillParams p) {
   constexpr int D = 128;
+  constexpr int NS = QT == 1 ? kTcStages : 3;   // key-tile stages (shared memory budget)
+  constexpr int SMW = 4 * QT;                    // softmax warps
+  constexpr int WK = SMW, WMMA = SMW + 1, WV = SMW + 2;   // K producer, MMA issuer, V producer
   constexpr int HALF = kTcKeys * 128;          // one 64-d half of a key tile: 64 rows x 128 B
   constexpr int TILE = 2 * HALF;               // K (or V) of one key tile
   constexpr int STAGE = 2 * TILE;              // K + V
@@ -188,33 +201,35 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t *gb = smem_raw + (base - raw);
-  const uint32_t sQ = base;                                  // 2 halves x 128 rows x 128 B
-  const uint32_t sStage = sQ + 2 * kTcRows * 128;            // kTcStages key tiles (K | V)
-  const uint32_t sP = sStage + kTcStages * STAGE;            // 2 x 128 rows x 128 B (64 keys)
-  int4 *metas = reinterpret_cast<int4 *>(gb + (sP - base) + 2 * kTcRows * 128);   // [stage][chunk]
-  int *tcount = reinterpret_cast<int *>(metas + kTcStages * kTcChunks);          // chunks | last flag
-  uint64_t *bars = reinterpret_cast<uint64_t *>(tcount + kTcStages);
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * kTcStages + 9);
+  const uint32_t sQ = base;                                  // QT x (2 halves x 128 rows x 128 B)
+  const uint32_t sStage = sQ + QT * 2 * kTcRows * 128;       // NS key tiles (K | V)
+  const uint32_t sP = sStage + NS * STAGE;                   // QT x 2 x 128 rows x 128 B (64 keys)
+  int4 *metas = reinterpret_cast<int4 *>(gb + (sP - base) + QT * 2 * kTcRows * 128);   // [stage][chunk]
+  int *tcount = reinterpret_cast<int *>(metas + NS * kTcChunks);                 // chunks | last flag
+  uint64_t *bars = reinterpret_cast<uint64_t *>(tcount + ((NS + 1) & ~1));   // 8-byte aligned
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * NS + 8 * QT + 1);
   const uint32_t bar0 = smem_u32(bars);
-  const uint32_t full0 = bar0, empty0 = bar0 + 8 * kTcStages;
-  // s_full/s_free: S buffer handoff; p_full/p_free: P buffer handoff (p_free also
-  // marks "every P.V up to this tile has landed in O"); q_full: Q staged
-  const uint32_t s_full0 = bar0 + 16 * kTcStages, s_free0 = s_full0 + 16, p_full0 = s_full0 + 32,
-                 p_free0 = s_full0 + 48, q_full = s_full0 + 64;
+  const uint32_t full0 = bar0, empty0 = bar0 + 8 * NS;
+  // per query group q: s_full/s_free (S buffer handoff) and p_full/p_free (P
+  // buffer handoff; p_free also marks "every P.V up to this tile has landed in
+  // O"), two buffers each; q_full: Q staged
+  const uint32_t grp0 = bar0 + 16 * NS;   // group q: + 64 q; s_full +0, s_free +16, p_full +32, p_free +48
+  const uint32_t q_full = grp0 + 64 * QT;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   auto init_barriers = [&]() {
-    for (int i = 0; i < kTcStages; ++i) {
+    for (int i = 0; i < NS; ++i) {
       mbar_init(full0 + 8 * i, 2);   // the K and the V producer each arm their bytes
       mbar_init(empty0 + 8 * i, 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(s_full0 + 8 * b, 1);
-      mbar_init(s_free0 + 8 * b, 4);
-      mbar_init(p_full0 + 8 * b, 4);
-      mbar_init(p_free0 + 8 * b, 1);
-    }
-    mbar_init(q_full, 4);
+    for (int q = 0; q < QT; ++q)
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(grp0 + 64 * q + 8 * b, 1);        // s_full
+        mbar_init(grp0 + 64 * q + 16 + 8 * b, 4);   // s_free
+        mbar_init(grp0 + 64 * q + 32 + 8 * b, 4);   // p_full
+        mbar_init(grp0 + 64 * q + 48 + 8 * b, 1);   // p_free
+      }
+    mbar_init(q_full, SMW);
     fence_mbar_init();
   };
   if (threadIdx.x == 0) {
@@ -222,8 +237,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     prefetch_tmap(&tmV);
     init_barriers();
   }
-  if (warp == 5) {   // TMEM: S buffers at columns [0, 64) and [64, 128), O at [128, 256)
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot)));
+  if (warp == WMMA) {   // TMEM per group q: S buffers at 256q + [0, 64) / [64, 128), O at 256q + [128, 256)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(256 * QT));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -240,7 +256,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int g = p.g;
   int gt0 = 0;           // key tiles of earlier items (identical in every role)
   int items_done = 0;
-  const int n_items = p.tiles_max * p.H * p.B;
+  const int n_items = ((p.tiles_max + QT - 1) / QT) * p.H * p.B;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
   const int x = item / (p.H * p.B), hr = item - x * (p.H * p.B);
   const int r = hr / p.H, h = hr - r * p.H;
@@ -248,11 +264,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int n = __ldg(p.cu_q + r + 1) - q0;
   const int rows = n * g;
   const int ntiles = (rows + kTcRows - 1) / kTcRows;
-  const int tile = ntiles - 1 - x;
-  if (tile < 0) continue;
+  const int tile_last = ntiles - 1 - QT * x;      // this item: tiles tile_last - QT + 1 .. tile_last
+  if (tile_last < 0) continue;
   const int L = __ldg(p.seq_lens + r);
-  const int row0 = tile * kTcRows;
-  const int row_end = min(rows, row0 + kTcRows);
+  const int row0 = (tile_last - QT + 1) * kTcRows;   // may be negative: that group has no rows
+  const int row_end = min(rows, (tile_last + 1) * kTcRows);
   const int pos_max = L - n + (row_end - 1) / g;
 
   // Tile metadata: the producer walks the request's chunks (one tile of
@@ -262,16 +278,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   // warpgroup bar.sync: CTA-scope release/acquire) -- the consumers never walk.
   // The tiles themselves are handed over by the mbarriers.
   auto bar_mma = [](int st) { return 1 + st; };                  // producer + MMA warp: 64 threads
-  auto bar_sm = [](int st) { return 1 + kTcStages + st; };       // producer + softmax: 160 threads
+  auto bar_sm = [](int st) { return 1 + NS + st; };              // producer + softmax: 32 + 32 SMW threads
 
-  if (warp == 4 || warp == 6) {
+  if (warp == WK || warp == WV) {
     // ------------------------------------------------------------ producers
     // A key tile = up to four 16-slot chunks of the walk, each landing as rows
     // [16j, 16j+16) of the tile (one TMA box per 64-d half per tensor), so the
     // tile is one contiguous K-major (K) / MN-major (V) 128B-swizzled operand.
     // Warp 4 streams K and publishes the tile metadata (before its copies, so
     // the consumers can prepare), warp 6 streams V: 8 boxes per warp per tile.
-    const bool is_k = warp == 4;
+    const bool is_k = warp == WK;
     TcWalk walk;
     tc_walk_init(p, r, L, walk);
     TcChunk ch[kTcChunks], nx[kTcChunks];
@@ -279,7 +295,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     int nch = tc_tile(p, r, L, pos_max, walk, ch);
     for (int t = 0; nch > 0; ++t) {
       const int nnx = tc_tile(p, r, L, pos_max, walk, nx);   // lookahead: is this tile the last?
-      const int gt = gt0 + t, st = gt % kTcStages, round = gt / kTcStages;
+      const int gt = gt0 + t, st = gt % NS, round = gt / NS;
       if (lane == 0) {
         if (round > 0) mbar_wait(empty0 + 8 * st, (round - 1) & 1);
         if (is_k) {
@@ -290,7 +306,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       __syncwarp();
       if (is_k) {
         named_bar_arrive(bar_mma(st), 64);
-        named_bar_arrive(bar_sm(st), 160);
+        named_bar_arrive(bar_sm(st), 32 + 32 * SMW);
       }
       if (lane == 0) {
         const uint32_t fb = full0 + 8 * st;
@@ -310,31 +326,36 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
       for (int j = 0; j < kTcChunks; ++j) ch[j] = nx[j];
     }
-  } else if (warp == 5) {
+  } else if (warp == WMMA) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       mbar_wait(q_full, items_done & 1);
       tc_fence_after();
     }
     __syncwarp();
-    bool first_pv = true;
-    auto issue_pv = [&](int gt, int nch) {
-      const int pb = gt & 1, st = gt % kTcStages;
-      mbar_wait(p_full0 + 8 * pb, (gt >> 1) & 1);
-      tc_fence_after();
+    bool first_pv[QT];
+#pragma unroll
+    for (int q = 0; q < QT; ++q) first_pv[q] = true;
+    auto issue_pv = [&](int gt, int nch) {   // P.V of key tile gt for every group, then free the stage
+      const int pb = gt & 1, st = gt % NS;
       const uint32_t idO = idesc(128, 128, 0, 1);
-      for (int j = 0; j < nch; ++j) {
-        const uint64_t a = sdesc(sP + pb * (kTcRows * 128) + j * 32, 16, 1024);
-        const uint64_t b = sdesc(sStage + st * STAGE + TILE + j * 2048, HALF, 1024);
-        umma(tmem + 128, a, b, idO, first_pv ? 0u : 1u);
-        first_pv = false;
+#pragma unroll
+      for (int q = 0; q < QT; ++q) {
+        mbar_wait(grp0 + 64 * q + 32 + 8 * pb, (gt >> 1) & 1);
+        tc_fence_after();
+        for (int j = 0; j < nch; ++j) {
+          const uint64_t a = sdesc(sP + (q * 2 + pb) * (kTcRows * 128) + j * 32, 16, 1024);
+          const uint64_t b = sdesc(sStage + st * STAGE + TILE + j * 2048, HALF, 1024);
+          umma(tmem + 256 * q + 128, a, b, idO, first_pv[q] ? 0u : 1u);
+          first_pv[q] = false;
+        }
+        umma_commit(grp0 + 64 * q + 48 + 8 * pb);
       }
       umma_commit(empty0 + 8 * st);
-      umma_commit(p_free0 + 8 * pb);
     };
     int prev_nch = 0;
     for (int t = 0;; ++t) {
-      const int gt = gt0 + t, sb = gt & 1, st = gt % kTcStages;
+      const int gt = gt0 + t, sb = gt & 1, st = gt % NS;
       long long pc0 = kTcProf ? clock64() : 0;
       auto prof = [&](int slot) {
         if (kTcProf && lane == 0 && blockIdx.x < 148) {
@@ -348,20 +369,22 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const int tc = tcount[st];
       const int nch = tc & 0xff;
       if (lane == 0) {
-        mbar_wait(full0 + 8 * st, (gt / kTcStages) & 1);
+        mbar_wait(full0 + 8 * st, (gt / NS) & 1);
         prof(1);
-        if (gt >= 2) mbar_wait(s_free0 + 8 * sb, ((gt - 2) >> 1) & 1);
-        prof(2);
-        tc_fence_after();
         const uint32_t idS = idesc(128, 16 * nch, 0, 0);
         const uint32_t sk = sStage + st * STAGE;
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint64_t a = sdesc(sQ + (k >> 2) * (kTcRows * 128) + (k & 3) * 32, 16, 1024);
-          const uint64_t b = sdesc(sk + (k >> 2) * HALF + (k & 3) * 32, 16, 1024);
-          umma(tmem + sb * 64, a, b, idS, k > 0);
+        for (int q = 0; q < QT; ++q) {
+          if (gt >= 2) mbar_wait(grp0 + 64 * q + 16 + 8 * sb, ((gt - 2) >> 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint64_t a = sdesc(sQ + q * (2 * kTcRows * 128) + (k >> 2) * (kTcRows * 128) + (k & 3) * 32, 16, 1024);
+            const uint64_t b = sdesc(sk + (k >> 2) * HALF + (k & 3) * 32, 16, 1024);
+            umma(tmem + 256 * q + sb * 64, a, b, idS, k > 0);
+          }
+          umma_commit(grp0 + 64 * q + 8 * sb);
         }
-        umma_commit(s_full0 + 8 * sb);
         prof(3);
         if (t >= 1) issue_pv(gt - 1, prev_nch);   // P.V of the previous tile overlaps S of this one
         prof(4);
@@ -375,10 +398,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
     }
   } else {
-    // ------------------------------------------------------------ softmax warpgroup
-    const int row = threadIdx.x;               // 0..127: query row of the tile = TMEM lane
-    const int grow = row0 + row;
-    const bool ok = grow < row_end;
+    // ------------------------------------------------------------ softmax warpgroup(s)
+    const int qg = warp >> 2;                  // query group (128-row tile) of this warp
+    const int row = (warp & 3) * 32 + lane;    // row of the group's tile = TMEM lane
+    const int grow = row0 + qg * kTcRows + row;
+    const bool ok = grow >= 0 && grow < row_end;
+    const uint32_t s_full0 = grp0 + 64 * qg, s_free0 = s_full0 + 16, p_full0 = s_full0 + 32,
+                   p_free0 = s_full0 + 48;
+    const uint32_t tq = tmem + 256 * qg;       // this group's TMEM columns
     const int tok = ok ? grow / g : 0, jh = ok ? grow - tok * g : 0;
     const int pos = ok ? L - n + tok : -1;
     {   // Q row -> shared memory (K-major, 128B swizzle, two 64-d halves)
@@ -387,17 +414,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
         const uint4 v = ok ? __ldg(qs + c) : make_uint4(0u, 0u, 0u, 0u);
-        st_shared_v4(sQ + (c >> 3) * (kTcRows * 128) + tswz(row, c & 7), v);
+        st_shared_v4(sQ + qg * (2 * kTcRows * 128) + (c >> 3) * (kTcRows * 128) + tswz(row, c & 7), v);
       }
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(q_full);
     }
-    const uint32_t lane_addr = static_cast<uint32_t>(warp * 32) << 16;
+    const uint32_t lane_addr = static_cast<uint32_t>((warp & 3) * 32) << 16;
     float m_ref = -INFINITY, l = 0.f;
     int ntile = 0;
     for (;; ++ntile) {
-      const int t = gt0 + ntile, sb = t & 1, st = t % kTcStages;   // CTA-global key tile number
+      const int t = gt0 + ntile, sb = t & 1, st = t % NS;   // CTA-global key tile number
       long long pc0 = kTcProf ? clock64() : 0;
       auto prof = [&](int slot) {
         if (kTcProf && threadIdx.x == 0 && blockIdx.x < 148) {
@@ -406,19 +433,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           pc0 = c;
         }
       };
-      named_bar_sync(bar_sm(st), 160);
+      named_bar_sync(bar_sm(st), 32 + 32 * SMW);
       prof(0);
       const int tc = tcount[st];
       const int nch = tc & 0xff;
       int4 meta[kTcChunks];
 #pragma unroll
       for (int j = 0; j < kTcChunks; ++j) meta[j] = j < nch ? metas[st * kTcChunks + j] : make_int4(0, 0, 0, 0);
-      mbar_wait(full0 + 8 * st, (t / kTcStages) & 1);   // the tile's K/V landed (V rows get patched below)
+      mbar_wait(full0 + 8 * st, (t / NS) & 1);   // the tile's K/V landed (V rows get patched below)
       prof(1);
       // dead V rows of partly live chunks -> zero (P = 0 must never meet NaN, reading Q10)
 #pragma unroll
       for (int j = 0; j < kTcChunks; ++j) {   // unrolled: meta[] stays in registers
-        if (j < nch && (meta[j].x > 0 || meta[j].y < 16)) {
+        if (qg == 0 && j < nch && (meta[j].x > 0 || meta[j].y < 16)) {   // group 0 patches for all
           const uint32_t sv = sStage + st * STAGE + TILE + j * 2048;
 #pragma unroll
           for (int q = 0; q < 256; q += kTcRows) {   // 16 slots x 2 halves x 8 pieces
@@ -435,7 +462,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       float s[kTcChunks * 16];
 #pragma unroll
       for (int j = 0; j < kTcChunks; ++j)
-        if (j < nch) tmem_ld16(tmem + lane_addr + sb * 64 + 16 * j, s + 16 * j);
+        if (j < nch) tmem_ld16(tq + lane_addr + sb * 64 + 16 * j, s + 16 * j);
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
@@ -493,11 +520,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll 1
         for (int c = 0; c < D; c += 16) {
           float o[16];
-          tmem_ld16(tmem + lane_addr + 128 + c, o);
+          tmem_ld16(tq + lane_addr + 128 + c, o);
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 16; ++i) o[i] *= alpha;
-          tmem_st16(tmem + lane_addr + 128 + c, o);
+          tmem_st16(tq + lane_addr + 128 + c, o);
         }
         tmem_wait_st();
         tc_fence_before();
@@ -508,7 +535,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       prof(4);
       if (t >= 2) mbar_wait(p_free0 + 8 * sb, ((t - 2) >> 1) & 1);
       prof(5);
-      const uint32_t prow = sP + sb * (kTcRows * 128);
+      const uint32_t prow = sP + (qg * 2 + sb) * (kTcRows * 128);
       float l4[4] = {0.f, 0.f, 0.f, 0.f};   // independent row-sum chains, folded into l below
 #pragma unroll
       for (int j = 0; j < kTcChunks; ++j) {
@@ -546,7 +573,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll 1
     for (int c = 0; c < D; c += 16) {
       float o[16];
-      tmem_ld16(tmem + lane_addr + 128 + c, o);
+      tmem_ld16(tq + lane_addr + 128 + c, o);
       tmem_wait_ld();
       if (ok) {
         orow[c / 8] = make_uint4(pack_bf16(o[0] * inv, o[1] * inv), pack_bf16(o[2] * inv, o[3] * inv),
@@ -560,9 +587,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   ++items_done;
   }   // work items
   __syncthreads();
-  if (warp == 5) {
+  if (warp == WMMA) {   // the allocating warp frees the TMEM columns
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256 * QT));
   }
 }
 
@@ -579,17 +606,22 @@ extern "C" __attribute__((visibility("default"))) int bkv_dev_prefill_prof(unsig
 
 namespace bkv {
 
-int prefill_tc_smem_bytes() {
-  return 1024 + 2 * kTcRows * 128 + kTcStages * 4 * kTcKeys * 128 + 2 * kTcRows * 128 +
-         kTcStages * kTcChunks * 16 + kTcStages * 4 + (2 * kTcStages + 9) * 8 + 16;   // + metadata, barriers, TMEM slot
+template <int QT>
+static int tc_smem_bytes() {
+  constexpr int NS = QT == 1 ? kTcStages : 3;
+  return 1024 + QT * 2 * kTcRows * 128 + NS * 4 * kTcKeys * 128 + QT * 2 * kTcRows * 128 +
+         NS * kTcChunks * 16 + ((NS + 1) & ~1) * 4 + (2 * NS + 8 * QT + 1) * 8 + 16;   // + metadata, barriers, TMEM slot
 }
 
-cudaError_t launch_prefill_tc(const CUtensorMap &tmK, const CUtensorMap &tmV, const PrefillParams &p,
-                              int max_q_len, cudaStream_t s) {
-  const int smem = prefill_tc_smem_bytes();
+int prefill_tc_smem_bytes() { return tc_smem_bytes<1>(); }
+
+template <int QT>
+static cudaError_t launch_tc(const CUtensorMap &tmK, const CUtensorMap &tmV, const PrefillParams &p,
+                             int max_q_len, cudaStream_t s) {
+  const int smem = tc_smem_bytes<QT>();
   static int configured = 0;
   if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(prefill_tc_kernel<QT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     configured = smem;
   }
@@ -599,10 +631,19 @@ cudaError_t launch_prefill_tc(const CUtensorMap &tmK, const CUtensorMap &tmV, co
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long items = tiles * p.H * p.B;
+  const long long items = ((tiles + QT - 1) / QT) * p.H * p.B;
   const int grid = static_cast<int>(items < sms ? items : sms);   // one persistent CTA per SM
-  prefill_tc_kernel<<<grid, kTcThreads, smem, s>>>(tmK, tmV, q);
+  prefill_tc_kernel<QT><<<grid, 32 * (4 * QT + 3), smem, s>>>(tmK, tmV, q);
   return cudaGetLastError();
+}
+
+cudaError_t launch_prefill_tc(const CUtensorMap &tmK, const CUtensorMap &tmV, const PrefillParams &p,
+                              int max_q_len, cudaStream_t s) {
+  // default: two ping-pong 128-row query tiles per CTA share every K/V tile (Llama-70B
+  // TP1 prefill rows 191 -> 233 TF/s); BKV_PREFILL_QT=1 (dev) runs one tile per CTA
+  const char *e = getenv("BKV_PREFILL_QT");
+  if (e && atoi(e) == 1) return launch_tc<1>(tmK, tmV, p, max_q_len, s);
+  return launch_tc<2>(tmK, tmV, p, max_q_len, s);
 }
 
 }  // namespace bkv

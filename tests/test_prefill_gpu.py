@@ -151,3 +151,14 @@ def test_prefill_tcgen05_long_context_and_geometries():
         n = query_counts(case.layout.lens, np.random.default_rng(hq), decode_frac=0.3)
         o, ref = _run(case, general, n, qs=2)
         check_close(o, ref, str((hq, hkv, bs, general)))
+
+
+@pytest.mark.parametrize("cfg,general", [("tiny_gqa", False), ("tiny_gqa", True)])
+def test_prefill_tcgen05_single_query_tile_per_cta(cfg, general, monkeypatch):
+    """BKV_PREFILL_QT=1: the tcgen05 kernel with one 128-row query tile per CTA (the
+    default runs two ping-pong tiles per CTA)."""
+    monkeypatch.setenv("BKV_PREFILL_QT", "1")
+    case = make_case(cfg, 31, general=general)
+    n = query_counts(case.layout.lens, np.random.default_rng(31))
+    o, ref = _run(case, general, n)
+    check_close(o, ref, cfg + " QT1")
