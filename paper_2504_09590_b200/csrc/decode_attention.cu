@@ -66,6 +66,7 @@ struct SlotMeta {
 };
 
 constexpr int kBuckets = 4;
+constexpr int kFastSplits = 8;   // merge: rows with <= this many splits preload every partial
 
 struct Plan {
   int P;                  // target blocks per split
@@ -249,7 +250,53 @@ __device__ __forceinline__ void merge_row(const DecodeParams &p, int u0, int ns,
   float Mrun = -INFINITY, Lrun = 0.f, acc[EPL];
 #pragma unroll
   for (int q = 0; q < EPL; ++q) acc[q] = 0.f;
-  for (int s0 = 0; s0 < ns; s0 += 32) {
+  if (!COHERENT && ns <= kFastSplits) {   // (the fused in-kernel merge keeps the register-light loop)
+    // Few splits (the common case): every partial load -- all (m, l) pairs and
+    // all o slices -- is issued before any of them is used, so the row costs
+    // one memory round trip instead of two.
+    float ov[kFastSplits][EPL];
+#pragma unroll
+    for (int t = 0; t < kFastSplits; ++t) {
+      if (t < ns) {
+        const float *po = p.part_o + (static_cast<int64_t>(u0 + t * H) * g + head) * D + lane * EPL;
+        if constexpr (EPL == 4) {
+          const float4 v = COHERENT ? __ldcg(reinterpret_cast<const float4 *>(po)) : __ldg(reinterpret_cast<const float4 *>(po));
+          ov[t][0] = v.x;
+          ov[t][1] = v.y;
+          ov[t][2] = v.z;
+          ov[t][3] = v.w;
+        } else {
+          const float2 v = COHERENT ? __ldcg(reinterpret_cast<const float2 *>(po)) : __ldg(reinterpret_cast<const float2 *>(po));
+          ov[t][0] = v.x;
+          ov[t][1] = v.y;
+        }
+      }
+    }
+    float wj = -INFINITY, lj = 0.f;
+    if (lane < ns) {
+      const float2 *src = reinterpret_cast<const float2 *>(p.part_ml + (static_cast<int64_t>(u0 + lane * H) * g + head) * 2);
+      const float2 v = COHERENT ? __ldcg(src) : __ldg(src);
+      wj = v.x;
+      lj = v.y;
+    }
+    float mg = wj;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mg = fmaxf(mg, __shfl_xor_sync(FULL, mg, o));
+    const float w = lane < ns ? ex2(wj - mg) : 0.f;
+    float ls = lj * w;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ls += __shfl_xor_sync(FULL, ls, o);
+    Lrun = ls;
+#pragma unroll
+    for (int t = 0; t < kFastSplits; ++t) {
+      const float wt = __shfl_sync(FULL, w, t);
+      if (t < ns) {
+#pragma unroll
+        for (int q = 0; q < EPL; ++q) acc[q] = fmaf(wt, ov[t][q], acc[q]);
+      }
+    }
+  }
+  for (int s0 = 0; (COHERENT || ns > kFastSplits) && s0 < ns; s0 += 32) {
     const int sl = s0 + lane;
     const bool ok = sl < ns;
     const int us = u0 + sl * H;
@@ -438,7 +485,13 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
       for (int k = 0; k <= kBuckets; ++k) p.plan_out[1 + k] = plan.base[k];
       p.plan_out[6] = plan.U;
     }
-    for (int i = threadIdx.x; i < kBuckets * (p.B + 1); i += blockDim.x) p.plan_out[16 + i] = Pre[i];
+    // per request: (first split slot, split count) -> the merge kernel needs one load per row
+    for (int r = threadIdx.x; r < p.B; r += blockDim.x) {
+      const int nb = NBsm[r];
+      const int ns = nb > 0 ? (nb + plan.P - 1) / plan.P : 1;
+      const int k = bucket_of((nb + ns - 1) / ns, plan.P);
+      reinterpret_cast<int2 *>(p.plan_out + 16)[r] = make_int2(plan.base[k] + Pre[k * (p.B + 1) + r], ns);
+    }
   }
   trace(1, -1);
   const int P = plan.P, U = plan.U;
@@ -1036,17 +1089,17 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
 }
 
 // Split merge, a second, stream-ordered kernel: one warp
-// per (request, kv head).  Requests with one split were written by the decode
-// kernel directly; for the others the fp32 (m, l, o) partials of all splits
-// are combined in split order -- M = max m_s, L = sum l_s 2^(m_s - M),
-// O = sum o_s 2^(m_s - M) / L -- so the result is deterministic.  Lanes take 32
-// splits at a time (their (m, l) loads issue together), weights are broadcast
-// by shuffle and each lane accumulates EPL consecutive output elements.  Being
+// per (request, kv head, q head).  Requests with one split were written by the
+// decode kernel directly; for the others the fp32 (m, l, o) partials of all
+// splits are combined in split order -- M = max m_s, L = sum l_s 2^(m_s - M),
+// O = sum o_s 2^(m_s - M) / L -- so the result is deterministic.  CTA 0 of the
+// decode kernel publishes (first split slot, split count) per request, so a
+// row's dependent chain is: that one load, all its partial loads (issued
+// together for <= kFastSplits splits), the store.  Being
 // stream-ordered after the decode kernel, it needs no atomics or fences; it
 // also re-arms the decode kernel's unit counter for the next call.
 template <int D>
 __global__ void __launch_bounds__(256) merge_kernel(const DecodeParams p) {
-  constexpr unsigned FULL = 0xffffffffu;
   constexpr int EPL = D / 32;
   if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");   // decode results complete
   if (blockIdx.x == 0 && threadIdx.x == 0) p.sched[0] = 0;
@@ -1056,10 +1109,8 @@ __global__ void __launch_bounds__(256) merge_kernel(const DecodeParams p) {
   if (wid >= p.B * H * g) return;   // one warp per (request, kv head, q head of the group)
   const int rh = wid / g, row1 = wid - rh * g;
   const int r = rh / H, h = rh - r * H;
-  const int P = p.plan_out[0];
-  const int L = __ldg(p.seq_lens + r);
-  const int nb = entries_of(p, r, L);
-  const int ns = nb > 0 ? (nb + P - 1) / P : 1;
+  const int2 mp = reinterpret_cast<const int2 *>(p.plan_out + 16)[r];   // (first split slot, splits)
+  const int ns = mp.y;
   if (ns <= 1) {
     // single split: the decode kernel wrote the local row; forward it to the
     // peers' outputs (fused reassembly) with 16-byte stores
@@ -1075,9 +1126,8 @@ __global__ void __launch_bounds__(256) merge_kernel(const DecodeParams p) {
     }
     return;
   }
-  const int k = bucket_of((nb + ns - 1) / ns, P);
   // all splits of (r, h) are consecutive split slots of r's bucket: u = (slot0 + s) * H + h
-  const int u0 = (p.plan_out[1 + k] + p.plan_out[16 + k * (p.B + 1) + r]) * H + h;
+  const int u0 = mp.x * H + h;
   merge_row<D, false>(p, u0, ns, r, h, row1, lane);
 }
 

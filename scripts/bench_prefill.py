@@ -162,7 +162,9 @@ def main():
                    "dispatch": ("bkv_paged_mixed_attention: prefill kernel + split-K decode kernel"
                                 if dispatch else "bkv_paged_prefill_attention for every row")},
         "us_per_layer": med, "p10_us": float(np.percentile(ts, 10)), "p90_us": float(np.percentile(ts, 90)),
-        "roofline": {"bound": "tensor", "kernel": "bkv::prefill_kernel (mma.sync m16n8k16 bf16)"
+        "roofline": {"bound": "tensor", "kernel": ("bkv::prefill_tc_kernel (tcgen05, TMEM accumulators)"
+                                                   if d == 128 and os.environ.get("BKV_PREFILL_MMA_SYNC") != "1"
+                                                   else "bkv::prefill_kernel (mma.sync m16n8k16 bf16)")
                      + (" + bkv::decode_kernel" if dispatch else ""),
                      "achieved": achieved, "peak": tpk, "unit": "TFLOP/s", "frac": achieved / tpk,
                      "peak_source": src, "flops_per_launch": flops},
