@@ -253,11 +253,15 @@ BKV_API bkv_status bkv_kv_append_checkpoint(const bkv_kv_pool *pool, const bkv_b
  * bkv_paged_decode_attention_ex -- the same call with launch flags.
  *   BKV_FLAG_PDL  launch the attention and merge kernels with programmatic
  *                 dependent launch: the split-plan prologue (which reads only
- *                 seq_lens) overlaps the tail of the preceding kernel on the
- *                 stream, e.g. bkv_kv_append.  Contract: seq_lens must NOT be
- *                 written by the kernel that immediately precedes this call on
- *                 the stream (host copies and earlier kernels are fine); every
- *                 other input is read only after that kernel has completed.
+ *                 seq_lens, and num_entries for a general map) overlaps the
+ *                 tail of the preceding kernel on the stream, e.g.
+ *                 bkv_kv_append or the previous call's merge; both kernels
+ *                 trigger their dependents early, so the next kernel's CTAs
+ *                 are scheduled as SMs free up.  Contract: seq_lens (and
+ *                 num_entries) must NOT be written by the kernel that
+ *                 immediately precedes this call on the stream (host copies
+ *                 and earlier kernels are fine); every other input is read
+ *                 only after that kernel has completed.
  * Unknown flag bits return BKV_ERR_INVALID_ARGUMENT.
  */
 #define BKV_FLAG_PDL 1u

@@ -85,7 +85,7 @@ struct DecodeParams {
   // these device-accessible outputs (peers' buffers over NVLink), same strides
   uint16_t *peer_out[8];
   int n_peers;
-  int debug_flags;       // dev only: 1 = skip the math (data-movement skeleton)
+  int debug_flags;       // dev only: 1 = skip the math (data-movement skeleton), 2 = merge re-arm only, 4 = CTA-major first units, 8 = exit after the plan, 16 = exit at entry, 32 = no early PDL trigger
   unsigned long long *trace;  // dev only (BKV_TRACE): per-warp event log, else nullptr
   int trace_cap;         // events per warp
 };

@@ -120,7 +120,27 @@ __device__ __forceinline__ int entries_of(const DecodeParams &p, int r, int L) {
   return p.fills ? __ldg(p.nent + r) : nblocks_of(L, p.bs);
 }
 
-__device__ void compute_plan(const DecodeParams &p, int *Pre, int *Lsm, int *NBsm, Plan *plan) {
+// ceil(a / b), 0 <= a, 1 <= b: a 32-bit unsigned division when both fit (the
+// usual case -- the 64-bit one is a software routine of several hundred cycles
+// on the prologue's critical path)
+__device__ __forceinline__ long long cdiv_ll(long long a, long long b) {
+  if (((static_cast<unsigned long long>(a) | static_cast<unsigned long long>(b)) >> 32) == 0) {
+    const unsigned ua = static_cast<unsigned>(a), ub = static_cast<unsigned>(b);
+    const unsigned q = ua / ub;
+    return q + (q * ub != ua ? 1 : 0);
+  }
+  return (a + b - 1) / b;
+}
+
+// splits of a request with nb entries and its size bucket, packed (n << 2 | bucket)
+__device__ __forceinline__ int split_code(int nb, int P) {
+  const unsigned n = nb > 0 ? (static_cast<unsigned>(nb) + P - 1) / static_cast<unsigned>(P) : 1u;
+  const unsigned sz = (static_cast<unsigned>(nb) + n - 1) / n;
+  return static_cast<int>(n << 2) | bucket_of(static_cast<int>(sz), P);
+}
+
+__device__ void compute_plan(const DecodeParams &p, int *Pre, int *Lsm, int *NBsm, Plan *plan,
+                             long long *pc = nullptr) {   // pc: dev trace clocks
   __shared__ long long red_ll[32];
   __shared__ int4 red4[32];
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5,
@@ -134,14 +154,16 @@ __device__ void compute_plan(const DecodeParams &p, int *Pre, int *Lsm, int *NBs
     NBsm[r] = nb;
     local += nb;
   }
+  if (kDevTrace && pc) pc[0] = clock64();
 #pragma unroll
   for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
   if (lane == 0) red_ll[warp] = local;
   __syncthreads();
+  if (kDevTrace && pc) pc[1] = clock64();
   long long T = 0;
   for (int w = 0; w < nw; ++w) T += red_ll[w];
   const long long target = max(1, p.target_units);
-  long long Pll = (T * p.H + target - 1) / target;
+  long long Pll = cdiv_ll(T * p.H, target);
   if (Pll < p.min_split) {
     // Small problem (fewer than ~3 min_split-block units per warp): the step is
     // bounded by the longest per-warp chain, not by bandwidth.  Units number at
@@ -153,7 +175,7 @@ __device__ void compute_plan(const DecodeParams &p, int *Pre, int *Lsm, int *NBs
     for (int k = 1; k <= 3; ++k) {
       const long long room = k * W - BH;
       if (room <= 0) continue;
-      const long long Pk = max(1ll, (TH + room - 1) / room);
+      const long long Pk = max(1ll, cdiv_ll(TH, room));
       if (Pk > p.min_split) continue;
       const long long chain = k * (Pk + 2);
       if (best < 0 || chain < best) {
@@ -164,14 +186,16 @@ __device__ void compute_plan(const DecodeParams &p, int *Pre, int *Lsm, int *NBs
     Pll = p.small_plan ? bestP : p.min_split;
   }
   const int P = static_cast<int>(Pll);
+  if (kDevTrace && pc) pc[2] = clock64();
   // per-thread contiguous ranges -> 4-bucket exclusive scans of n_r
   const int per = (B + nt - 1) / nt;
   const int r0 = min(B, tid * per), r1 = min(B, r0 + per);
   int4 cnt = make_int4(0, 0, 0, 0);
+  int *code = Pre + 3 * (B + 1);   // split codes, parked in Pre[3][r] until this thread overwrites them
   for (int r = r0; r < r1; ++r) {
-    const int nb = NBsm[r];
-    const int n = nb > 0 ? (nb + P - 1) / P : 1;
-    const int bk = bucket_of((nb + n - 1) / n, P);
+    const int c = split_code(NBsm[r], P);
+    code[r] = c;
+    const int n = c >> 2, bk = c & 3;
     cnt.x += bk == 0 ? n : 0;
     cnt.y += bk == 1 ? n : 0;
     cnt.z += bk == 2 ? n : 0;
@@ -191,6 +215,7 @@ __device__ void compute_plan(const DecodeParams &p, int *Pre, int *Lsm, int *NBs
   }
   if (lane == 31) red4[warp] = inc;
   __syncthreads();
+  if (kDevTrace && pc) pc[3] = clock64();
   int4 e = make_int4(inc.x - cnt.x, inc.y - cnt.y, inc.z - cnt.z, inc.w - cnt.w);
   for (int w = 0; w < warp; ++w) {
     e.x += red4[w].x;
@@ -199,13 +224,12 @@ __device__ void compute_plan(const DecodeParams &p, int *Pre, int *Lsm, int *NBs
     e.w += red4[w].w;
   }
   for (int r = r0; r < r1; ++r) {
+    const int c = code[r];
+    const int n = c >> 2, bk = c & 3;
     Pre[0 * (B + 1) + r] = e.x;
     Pre[1 * (B + 1) + r] = e.y;
     Pre[2 * (B + 1) + r] = e.z;
     Pre[3 * (B + 1) + r] = e.w;
-    const int nb = NBsm[r];
-    const int n = nb > 0 ? (nb + P - 1) / P : 1;
-    const int bk = bucket_of((nb + n - 1) / n, P);
     e.x += bk == 0 ? n : 0;
     e.y += bk == 1 ? n : 0;
     e.z += bk == 2 ? n : 0;
@@ -475,7 +499,17 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
     }
   };
   trace(0, -1);
-  compute_plan(p, Pre, Lsm, NBsm, &plan);
+  // PDL: let the stream's next kernel (the merge) be scheduled onto SMs as
+  // this grid's CTAs exit; it still waits for this whole grid to complete
+  if (p.pdl && !(p.debug_flags & 32)) asm volatile("griddepcontrol.launch_dependents;");
+  if (p.debug_flags & 16) return;   // dev: launch cost only
+  long long pc[6];
+  pc[5] = kDevTrace ? clock64() : 0;
+  compute_plan(p, Pre, Lsm, NBsm, &plan, kDevTrace ? pc : nullptr);
+  if (kDevTrace) {
+    pc[4] = clock64();
+    for (int k = 0; k < 5; ++k) trace(16 + k, static_cast<int>(pc[k] - pc[5]));
+  }
   // PDL: everything above read only seq_lens; wait for the preceding kernel
   // (it may have written the pool / q) before touching anything else.
   if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -487,13 +521,12 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
     }
     // per request: (first split slot, split count) -> the merge kernel needs one load per row
     for (int r = threadIdx.x; r < p.B; r += blockDim.x) {
-      const int nb = NBsm[r];
-      const int ns = nb > 0 ? (nb + plan.P - 1) / plan.P : 1;
-      const int k = bucket_of((nb + ns - 1) / ns, plan.P);
-      reinterpret_cast<int2 *>(p.plan_out + 16)[r] = make_int2(plan.base[k] + Pre[k * (p.B + 1) + r], ns);
+      const int c = split_code(NBsm[r], plan.P), k = c & 3;
+      reinterpret_cast<int2 *>(p.plan_out + 16)[r] = make_int2(plan.base[k] + Pre[k * (p.B + 1) + r], c >> 2);
     }
   }
   trace(1, -1);
+  if (p.debug_flags & 8) return;    // dev: launch + plan prologue only
   const int P = plan.P, U = plan.U;
 
   const uint32_t my_slots = slots_base + warp * S * G::SLOT_BYTES;
@@ -1101,7 +1134,12 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
 template <int D>
 __global__ void __launch_bounds__(256) merge_kernel(const DecodeParams p) {
   constexpr int EPL = D / 32;
-  if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");   // decode results complete
+  if (p.pdl) {
+    // the next decode call's CTAs may start their seq_lens-only prologue as
+    // SMs free up; they wait for this grid before touching anything else
+    if (!(p.debug_flags & 32)) asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // decode results complete
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) p.sched[0] = 0;
   const int lane = threadIdx.x & 31;
   const int wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);

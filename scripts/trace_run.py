@@ -64,3 +64,13 @@ names = ["wait", "begin-unit", "consume", "issue", "end-unit"]
 tot = v[:, :5].sum(1)
 print("  per-warp cycles (active warps, median): " + ", ".join(f"{n} {np.median(v[:, i]):.0f}" for i, n in enumerate(names)) +
       f"; chunks {np.median(v[:, 5]):.0f}; per chunk: " + ", ".join(f"{n} {np.median(v[:, i] / np.maximum(v[:, 5], 1)):.0f}" for i, n in enumerate(names)))
+
+# prologue clocks (kinds 16..20: after seq_lens loads, after the total reduction,
+# after P, after the bucket scans, plan done -- cycles since kernel entry)
+pro = []
+for kk in range(16, 21):
+    sel = (k == kk) & valid
+    if sel.any():
+        pro.append(np.median(tr[:, :, 1][sel]))
+if pro:
+    print("  prologue cycles since entry (median over warps): loads %.0f, reduce %.0f, P %.0f, scans %.0f, done %.0f" % tuple(pro))
