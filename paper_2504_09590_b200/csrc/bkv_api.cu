@@ -330,7 +330,7 @@ static bkv_status decode_impl(const bkv_kv_pool *pool, const bkv_block_map *map,
                               void *out, int64_t o_stride_seq, int64_t o_stride_head,
                               void *workspace, size_t workspace_bytes, uint32_t flags,
                               bkv_stream_t stream, void *const *peer_outs = nullptr,
-                              int32_t n_peers = 0) {
+                              int32_t n_peers = 0, bool after_own_prefill = false) {
   if (flags & ~BKV_FLAG_PDL) return fail(BKV_ERR_INVALID_ARGUMENT, "unknown flags 0x%x", flags);
   bkv_status s = check_pool(pool);
   if (s) return s;
@@ -404,6 +404,11 @@ static bkv_status decode_impl(const bkv_kv_pool *pool, const bkv_block_map *map,
   p.q_bytes = qb;
   p.total_warps = cfg.grid * cfg.warps;
   p.pdl = (flags & BKV_FLAG_PDL) ? 1 : 0;
+  // mixed dispatch: the preceding kernel is our own prefill kernel, which
+  // writes only the prefill rows of `out` and was itself launched in stream
+  // order -- the decode part may run alongside its tail (no grid wait)
+  const char *ov = getenv("BKV_MIXED_OVERLAP");   // dev: 0 = keep the grid wait
+  p.pdl_nowait = (p.pdl && after_own_prefill && !(ov && atoi(ov) == 0)) ? 1 : 0;
   p.k_new = static_cast<const uint16_t *>(k_new);
   p.v_new = static_cast<const uint16_t *>(v_new);
   p.k_pool = static_cast<uint16_t *>(pool->k);
@@ -662,7 +667,7 @@ bkv_status bkv_paged_mixed_attention(const bkv_kv_pool *pool, const bkv_block_ma
   uint16_t *od = static_cast<uint16_t *>(out) + (int64_t)num_prefill_rows * o_stride_tok;
   return decode_impl(pool, &md, seq_lens + num_prefill_seqs, max_seq_len, nullptr, nullptr, qd,
                      q_stride_tok, q_stride_head, num_q_heads, softmax_scale, od, o_stride_tok,
-                     o_stride_head, workspace, workspace_bytes, flags, stream);
+                     o_stride_head, workspace, workspace_bytes, flags, stream, nullptr, 0, num_prefill_seqs > 0 && max_q_len > 0);
 }
 
 bkv_status bkv_validate_block_map_host(const bkv_block_map *map, const int32_t *seq_lens,

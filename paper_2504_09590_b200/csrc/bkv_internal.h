@@ -77,6 +77,7 @@ struct DecodeParams {
   int q_bytes;           // smem bytes per q-ring entry
   int total_warps;       // grid * warps per CTA
   int pdl;               // launched with programmatic dependent launch (BKV_FLAG_PDL)
+  int pdl_nowait;        // PDL, and the preceding kernel is independent (mixed dispatch): skip the grid wait
   // fused decode step (bkv_decode_step): new token rows [B][H][D] + pool for the write; k_new == nullptr otherwise
   const uint16_t *k_new, *v_new;
   uint16_t *k_pool, *v_pool;

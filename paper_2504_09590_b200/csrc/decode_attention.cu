@@ -512,7 +512,7 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
   }
   // PDL: everything above read only seq_lens; wait for the preceding kernel
   // (it may have written the pool / q) before touching anything else.
-  if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (p.pdl && !p.pdl_nowait) asm volatile("griddepcontrol.wait;" ::: "memory");
   if (blockIdx.x == 0) {   // publish the split plan for the merge kernel
     if (threadIdx.x == 0) {
       p.plan_out[0] = plan.P;
@@ -1248,8 +1248,9 @@ static cudaError_t launch_t(const CUtensorMap &tmK, const CUtensorMap &tmV, cons
   // 114 vs 124 us, TP8 26 vs 45 us per layer)
   const int warps = p.B * p.H * p.g;
   cudaLaunchConfig_t lm = {};
-  lm.gridDim = dim3((p.debug_flags & 2) ? 1 : (warps + 7) / 8);   // dev: 2 = re-arm only (times the merge)
-  lm.blockDim = dim3(256);
+  const int mw = std::max(1, std::min(8, env_int("BKV_MERGE_WARPS", 8)));   // warps per merge CTA
+  lm.gridDim = dim3((p.debug_flags & 2) ? 1 : (warps + mw - 1) / mw);   // dev: 2 = re-arm only (times the merge)
+  lm.blockDim = dim3(32 * mw);
   lm.stream = s;
   if (p.pdl) {
     lm.attrs = attr;

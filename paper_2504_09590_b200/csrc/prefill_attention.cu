@@ -123,6 +123,9 @@ __global__ void __launch_bounds__(32 * (kConsumerWarps + 1), 1)
   constexpr int KV_BYTES = (D / 64) * HALF_BYTES;
   constexpr int SLOT_BYTES = 2 * KV_BYTES;
   constexpr int MT = D / 16;   // k-steps of Q.K^T, pairs of 8-wide d tiles of P.V
+  // a PDL-launched successor (the mixed dispatch's decode kernel, which reads
+  // nothing this kernel writes) may take SMs as this grid's CTAs finish
+  asm volatile("griddepcontrol.launch_dependents;");
   constexpr unsigned FULL = 0xffffffffu;
 
   const int r = blockIdx.z, h = blockIdx.y;

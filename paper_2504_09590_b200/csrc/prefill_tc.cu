@@ -198,6 +198,9 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
   constexpr unsigned FULL = 0xffffffffu;
 
   extern __shared__ uint8_t smem_raw[];
+  // a PDL-launched successor (the mixed dispatch's decode kernel, which reads
+  // nothing this kernel writes) may take SMs as this grid's CTAs finish
+  asm volatile("griddepcontrol.launch_dependents;");
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t *gb = smem_raw + (base - raw);
