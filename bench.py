@@ -135,6 +135,15 @@ def append_bytes(B, H, d):
 
 
 # --------------------------------------------------------- reference (oracle) arm
+def host_cores(oracle):
+    """Let the oracle use every core this process may run on."""
+    try:
+        n = len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        n = os.cpu_count() or 1
+    oracle.set_num_threads(max(1, n))
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -152,20 +161,22 @@ def run_reference(args):
     K = (rng.standard_normal((lay.num_blocks, heads, bs, d), dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
     V = (rng.standard_normal((lay.num_blocks, heads, bs, d), dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
     q = (rng.standard_normal((B, heads * g, d), dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
+    host_cores(oracle)   # rank 0 runs alone: all host cores (torchrun sets OMP_NUM_THREADS=1)
     cores = oracle.num_threads()
+    W = args.warmup if args.warmup_ref is None else args.warmup_ref
     times = []
-    for i in range(args.warmup_ref + args.steps):
+    for i in range(W + args.steps):
         t0 = time.perf_counter()
         oracle.attention(K, V, lay.block_tables, lay.dirs, lay.lens, q, 1.0 / math.sqrt(d))
         dt = time.perf_counter() - t0
-        if i >= args.warmup_ref:
+        if i >= W:
             times.append(dt)
     t_layer_full = statistics.median(times) * (H / heads)        # scale the head sample to all heads
     t_step = t_layer_full * sh.n_layers
     value = B / t_step
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
-        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup_ref, "ms_per_step": t_step * 1e3,
+        "n_gpus": ws, "steps": args.steps, "warmup": W, "ms_per_step": t_step * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": WORKLOADS.get(args.config, args.config), "name": args.config,
@@ -185,6 +196,7 @@ def cpu_baseline(args, lay, sh):
     H, Hq, d, bs, B = sh.num_kv_heads, sh.num_q_heads, sh.head_dim, sh.block_size, lay.batch
     heads = max(1, min(H, args.ref_heads))
     g = sh.group
+    host_cores(oracle)
     rng = np.random.default_rng(2)
     K = (rng.standard_normal((lay.num_blocks, heads, bs, d), dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
     V = (rng.standard_normal((lay.num_blocks, heads, bs, d), dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
@@ -527,7 +539,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--layers", type=int, default=0, help="override the model's layer count")
     ap.add_argument("--ref-heads", type=int, default=4, help="kv heads in the oracle's bounded sample")
-    ap.add_argument("--warmup-ref", type=int, default=1)
+    ap.add_argument("--warmup-ref", type=int, default=None, help="reference-arm warm-ups (default: --warmup)")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-pdl", dest="pdl", action="store_false",

@@ -1,7 +1,5 @@
-# dev: A/B of the mixed dispatch overlap (decode part alongside the prefill tail)
-for ov in 1 0 1 0; do
-  echo "overlap $ov"
-  BKV_MIXED_OVERLAP=$ov python scripts/bench_prefill.py --config llama70b --tp 1 | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('llama tp1', round(d['value'],1), d['us_per_layer'])"
-  BKV_MIXED_OVERLAP=$ov python scripts/bench_prefill.py --config llama70b --tp 8 | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('llama tp8', round(d['value'],1), d['us_per_layer'])"
-  BKV_MIXED_OVERLAP=$ov python scripts/bench_prefill.py --config opt13b --tp 2 | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('opt13b tp2', round(d['value'],1), d['us_per_layer'])"
+# dev: A/B of decode variants on the per-layer time (CUDA graph, PDL)
+for env in "BKV_FUSED_MERGE=0" "BKV_FUSED_MERGE=1" "BKV_SMALL_PLAN=0" "BKV_UNITS_PER_WARP=2"; do
+  echo "== $env"
+  env $env python scripts/quick_perf.py llama70b:8:fused llama70b:4:fused opt13b:8:fused llama70b:1:fused 2>&1 | grep -v Warn
 done
