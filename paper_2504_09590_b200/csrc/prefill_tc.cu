@@ -260,7 +260,26 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
   int gt0 = 0;           // key tiles of earlier items (identical in every role)
   int items_done = 0;
   const int n_items = ((p.tiles_max + QT - 1) / QT) * p.H * p.B;
-  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+  // First non-empty item >= from in this CTA's progression (from, from + G, ...):
+  // the lanes of each warp test 32 candidates at once (warp-uniform result), so
+  // the empty items of short or decode-only requests cost ~nothing.
+  const int G = static_cast<int>(gridDim.x);
+  auto next_item = [&](int from) -> int {
+    const int HB = p.H * p.B;
+    for (; from < n_items; from += 32 * G) {
+      const int c = from + lane * G;
+      bool live = false;
+      if (c < n_items) {
+        const int cx = c / HB, cr = (c - cx * HB) / p.H;
+        const int cn = __ldg(p.cu_q + cr + 1) - __ldg(p.cu_q + cr);
+        live = (cn * g + kTcRows - 1) / kTcRows - 1 - QT * cx >= 0;
+      }
+      const unsigned m = __ballot_sync(FULL, live);
+      if (m) return from + (__ffs(m) - 1) * G;
+    }
+    return n_items;
+  };
+  for (int item = next_item(blockIdx.x); item < n_items; item = next_item(item + G)) {
   const int x = item / (p.H * p.B), hr = item - x * (p.H * p.B);
   const int r = hr / p.H, h = hr - r * p.H;
   const int q0 = __ldg(p.cu_q + r);

@@ -1,5 +1,6 @@
-# dev: A/B of decode variants on the per-layer time (CUDA graph, PDL)
-for env in "BKV_FUSED_MERGE=0" "BKV_FUSED_MERGE=1" "BKV_SMALL_PLAN=0" "BKV_UNITS_PER_WARP=2"; do
-  echo "== $env"
-  env $env python scripts/quick_perf.py llama70b:8:fused llama70b:4:fused opt13b:8:fused llama70b:1:fused 2>&1 | grep -v Warn
-done
+# dev: prefill lines after the warp-parallel empty-item skip
+python scripts/bench_prefill.py --config llama70b --tp 1 --no-decodes | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('llama tp1 prefill-only', round(d['value'],1), d['us_per_layer'])"
+python scripts/bench_prefill.py --config llama70b --tp 1 | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('llama tp1 mixed', round(d['value'],1), d['us_per_layer'])"
+python scripts/bench_prefill.py --config llama70b --tp 1 --one-kernel | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('llama tp1 one-kernel', round(d['value'],1), d['us_per_layer'])"
+python scripts/bench_prefill.py --config llama70b --tp 8 | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('llama tp8 mixed', round(d['value'],1), d['us_per_layer'])"
+python scripts/bench_prefill.py --config opt13b --tp 2 | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('opt13b tp2 mixed', round(d['value'],1), d['us_per_layer'])"
