@@ -390,7 +390,11 @@ BKV_API bkv_status bkv_paged_prefill_attention(const bkv_kv_pool *pool, const bk
  * num_prefill_seqs + j at row num_prefill_rows + j), served by the split-K
  * decode kernel (workspace, flags as bkv_paged_decode_attention_ex).  Same
  * results as one bkv_paged_prefill_attention over the whole batch (up to fp32
- * summation order); two launches on `stream`.
+ * summation order); two launches on `stream` (three with the split merge).
+ * With BKV_FLAG_PDL the decode part is launched as a programmatic dependent
+ * of the prefill kernel and runs alongside its tail: it reads nothing the
+ * prefill writes (disjoint output rows), and the prefill kernel itself starts
+ * in plain stream order, after everything before the call.
  */
 BKV_API bkv_status bkv_paged_mixed_attention(const bkv_kv_pool *pool, const bkv_block_map *map,
                                              const int32_t *seq_lens, const int32_t *cu_q,

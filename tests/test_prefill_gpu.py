@@ -107,9 +107,11 @@ def test_prefill_long_context_llama_shard():
     check_close(o, ref, "llama shard")
 
 
-@pytest.mark.parametrize("cfg,general", [("tiny_gqa", False), ("tiny", True)])
-def test_mixed_dispatch_matches_oracle(cfg, general):
-    """bkv_paged_mixed_attention: prefill requests first, then one-row decodes."""
+@pytest.mark.parametrize("cfg,general,pdl", [("tiny_gqa", False, False), ("tiny", True, False),
+                                             ("tiny_gqa", False, True), ("tiny", True, True)])
+def test_mixed_dispatch_matches_oracle(cfg, general, pdl):
+    """bkv_paged_mixed_attention: prefill requests first, then one-row decodes.
+    pdl=True: the decode part runs alongside the prefill kernel's tail (no grid wait)."""
     case = make_case(cfg, 12, general=general)
     sh, lay = case.shape, case.layout
     B = lay.batch
@@ -128,9 +130,28 @@ def test_mixed_dispatch_matches_oracle(cfg, general):
         bt, dirs, lens = gpu_map(lay)
         kw = {}
     o = bkv.paged_mixed_attention(pool, bt, dirs, lens, torch.from_numpy(cu).to(DEV), t_u16(q), P, int(cu[P]),
-                                  softmax_scale=default_scale(sh.head_dim), **kw)
+                                  softmax_scale=default_scale(sh.head_dim), pdl=pdl, **kw)
     torch.cuda.synchronize()
     check_close(o, ref, cfg)
+    if pdl:   # replayed in a CUDA graph, back to back: bit-identical to the eager call
+        cu_d, q_d = torch.from_numpy(cu).to(DEV), t_u16(q)
+        ws = bkv.workspace(max(1, B - P), sh.num_q_heads, sh.num_kv_heads, sh.head_dim, torch.device(DEV))
+        og = torch.empty_like(o)
+        mq = int((cu[1:] - cu[:-1]).max())
+        fn = lambda: bkv.paged_mixed_attention(pool, bt, dirs, lens, cu_d, q_d, P, int(cu[P]), out=og, ws=ws,
+                                               max_q_len=mq, max_seq_len=int(lay.lens.max()),
+                                               softmax_scale=default_scale(sh.head_dim), pdl=True, **kw)
+        fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(3):
+                fn()
+        og.zero_()
+        g.replay()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(og, o), "graph replay of the PDL mixed dispatch differs from the eager call"
 
 
 @pytest.mark.parametrize("cfg,general,full", [("tiny_gqa", False, False), ("tiny_gqa", True, True)])
