@@ -1000,13 +1000,16 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
     // merging warp, so the workspace stays clean for the next call.  Otherwise
     // bkv merge_kernel (next on the stream) combines the splits.
     if (p.fused_merge) {
-      __threadfence();   // every lane's partial stores ...
-      __syncwarp();      // ... precede lane 0's arrival
-      int last = 0;
-      if (lane == 0) last = atomicAdd(p.merge_cnt + r * H + h, 1) == m.nsplit - 1;
+      __syncwarp();      // every lane's partial stores precede lane 0's arrival, which
+      int last = 0;      // releases them (and acquires the other splits') at gpu scope
+      if (lane == 0) {
+        int old;
+        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
+                     : "=r"(old) : "l"(p.merge_cnt + r * H + h) : "memory");
+        last = old == m.nsplit - 1;
+      }
       last = __shfl_sync(FULL, last, 0);
       if (last) {
-        __threadfence();
         const int qq = u / H;
         int k = 0;
         while (k < kBuckets - 1 && qq >= plan.base[k + 1]) ++k;

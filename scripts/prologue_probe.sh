@@ -1,4 +1,4 @@
-python scripts/bench_prefill.py --config llama70b --tp 1 --no-decodes | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('llama tp1 prefill-only', round(d['value'],1), d['us_per_layer'])"
-python scripts/bench_prefill.py --config llama70b --tp 1 | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('llama tp1 mixed', round(d['value'],1), d['us_per_layer'])"
-python scripts/bench_prefill.py --config llama70b --tp 8 | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('llama tp8 mixed', round(d['value'],1), d['us_per_layer'])"
-python scripts/bench_prefill.py --config opt13b --tp 2 | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('opt13b tp2 mixed', round(d['value'],1), d['us_per_layer'])"
+for env in "BKV_FUSED_MERGE=0" "BKV_FUSED_MERGE=1"; do
+  echo "== $env"
+  env $env python scripts/quick_perf.py llama70b:8:fused llama70b:4:fused opt13b:8:fused llama70b:1:fused opt13b:1:fused 2>&1 | grep -v Warn
+done

@@ -287,6 +287,21 @@ def test_full_size_bench_launch_config(cfg, tp):
     _full_size(cfg, tp, 0, mode="step", pdl=True, seed=1)
 
 
+@pytest.mark.parametrize("cfg,tp", [("llama70b", 8), ("opt13b", 4)])
+def test_fused_merge_opt_in(cfg, tp, monkeypatch):
+    """BKV_FUSED_MERGE=1, the opt-in in-kernel last-arriver merge (group merge for GQA, row
+    merge for MHA): sampled oracle parity, twice on one workspace (the arrival counters and
+    the unit counter must be re-armed by the kernel itself), and the same result as the
+    default split merge up to fp32 summation order."""
+    monkeypatch.setenv("BKV_FUSED_MERGE", "1")
+    o1 = _full_size(cfg, tp, 0, mode="step", pdl=True, seed=3)
+    o2 = _full_size(cfg, tp, 0, mode="step", pdl=True, seed=3)
+    assert torch.equal(o1, o2)
+    monkeypatch.setenv("BKV_FUSED_MERGE", "0")
+    o0 = _full_size(cfg, tp, 0, mode="step", pdl=True, seed=3, sample=2)
+    assert (o0.float() - o1.float()).abs().max().item() <= 2e-2
+
+
 @pytest.mark.parametrize("L0,bs,rt", [(8192, 32, 0.25), (8192, 16, 1.0), (512, 16, 0.0), (2048, 32, 0.75)])
 def test_sweep_config_sampled_parity(L0, bs, rt):
     """BASELINE configs[4]: Llama-2-70B shape, context sweep 512-8K, block 16/32, RT:BE mix
