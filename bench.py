@@ -5,7 +5,8 @@ One STEP = one decode iteration of the attention path over ALL layers of the
 model shape: per layer, kv_append of the batch's new tokens
 and paged decode attention over the bidirectional block map (a3-a5); at N > 1
 GPUs each rank owns a head shard (tensor parallel by kv head) and the
-head-major outputs are reassembled with one NCCL all-gather per layer (a6).
+head-major outputs of every layer are reassembled with ONE NCCL all-gather per
+step (a6; ``--gather layer``: one per layer, ``--reassembly p2p``: peer stores).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config opt13b] [--impl reference]
 
@@ -279,12 +280,16 @@ def run_ours(args):
     meta_d = {k: v.to(dev) for k, v in meta_h.items()}
     q_d, kn_d, vn_d = q_h.to(dev), kn_h.to(dev), vn_h.to(dev)
     out_loc = torch.empty((n_layers, Hq, B, d), dtype=torch.bfloat16, device=dev)   # head-major
-    out_glob = torch.empty((n_layers, Hq * tp, B, d), dtype=torch.bfloat16, device=dev) if tp > 1 else None
+    # reassembled outputs: per-layer gather -> [layer][global head][B][d]; one gather per step
+    # (default) -> rank-major [rank][layer][local head][B][d] (global head = rank * Hq + local)
+    glob_shape = (n_layers, Hq * tp, B, d) if args.gather == "layer" else (tp, n_layers, Hq, B, d)
+    out_glob = torch.empty(glob_shape, dtype=torch.bfloat16, device=dev) if tp > 1 else None
     p2p = None
     if tp > 1 and args.reassembly == "p2p":   # f2: fused NVLink reassembly instead of the all-gather
         p2p = PeerReassembly(shard, n_layers, B, d, dev)
         out_glob = p2p.glob
-    out_h = torch.empty((n_layers, Hq * tp, B, d), dtype=torch.bfloat16).pin_memory()
+    out_h = torch.empty(tuple(out_glob.shape) if out_glob is not None else (n_layers, Hq, B, d),
+                        dtype=torch.bfloat16).pin_memory()
     wsb = bkv.workspace(B, Hq, H, d, dev)
     max_len = int(lay.lens.max())
     scale = 1.0 / math.sqrt(d)
@@ -318,8 +323,13 @@ def run_ours(args):
                 bkv.paged_decode_attention(pools[l], md["bt"], md["dirs"], md["lens"], qd[l], scale,
                                            out=o, max_seq_len=max_len, ws=wsb, pdl=args.pdl, **gm)
             launches += 2                                                     # decode + merge kernels
-            if tp > 1 and not attn_only:
+            if tp > 1 and not attn_only and args.gather == "layer":
                 gather_heads(ol[l], og[l])
+        if tp > 1 and not attn_only and p2p is None and args.gather == "step":
+            # a6: head-sharded TP needs no per-layer reassembly (each rank's o_proj shard
+            # consumes its own heads); the step's per-request outputs of every layer are
+            # reassembled by ONE all-gather
+            gather_heads(ol.view(n_layers * Hq, B, d), og.view(tp * n_layers * Hq, B, d))
         return launches
 
     def barrier():
@@ -506,7 +516,8 @@ def run_ours(args):
             "cuda_graphs": bool(args.graphs),
             "fused_append": bool(args.fused),
             "reassembly": ("p2p stores + peer barrier (bkv_decode_multi_out)" if p2p is not None
-                           else "nccl all_gather_into_tensor" if tp > 1 else "none (1 GPU)"),
+                           else f"nccl all_gather_into_tensor, one per {args.gather}" if tp > 1
+                           else "none (1 GPU)"),
             "attn_layer_tokens_per_s": B / (att_avg_us * 1e-6),
             "seed": args.seed,
         },
@@ -548,6 +559,9 @@ def main():
                     help="e2e leg: serial H2D/step/D2H instead of the double-buffered copy-stream pipeline")
     ap.add_argument("--general-map", action="store_true",
                     help="FindBlock-style general block map (partly filled entries, SURVEY §8(f) f3)")
+    ap.add_argument("--gather", default="step", choices=["step", "layer"],
+                    help="N>1, nccl reassembly: one all-gather per step of every layer's outputs (default) "
+                         "or one per layer")
     ap.add_argument("--reassembly", default="nccl", choices=["nccl", "p2p"],
                     help="N>1: NCCL all-gather (default) or fused NVLink stores (symmetric memory)")
     ap.add_argument("--no-fused", dest="fused", action="store_false",
