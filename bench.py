@@ -406,9 +406,9 @@ def run_ours(args):
 
     pipelined = args.graphs and p2p is None and args.e2e_pipeline
     if pipelined:
-        # Serving pipeline: two input/output buffer sets, one captured graph per set; a
-        # copy stream moves step i+1's inputs host -> device while step i computes, and
-        # step i's outputs device -> host while step i+1 computes.  Every step still
+        # Serving pipeline: two input/output buffer sets, one captured graph per set; one
+        # copy stream moves step i+1's inputs host -> device while step i computes, another
+        # step i's outputs device -> host while step i+1 computes (both copy engines busy).  Every step still
         # moves all of its inputs and outputs through PCIe inside the timed region.
         meta_d2 = {k: torch.empty_like(v) for k, v in meta_d.items()}
         q_d2, kn_d2, vn_d2 = torch.empty_like(q_d), torch.empty_like(kn_d), torch.empty_like(vn_d)
@@ -424,37 +424,44 @@ def run_ours(args):
             step(meta_d2, q_d2, kn_d2, vn_d2, ol=out_loc2, og=out_glob2)
         sets = [(meta_d, q_d, kn_d, vn_d, g_step, src_out),
                 (meta_d2, q_d2, kn_d2, vn_d2, g_step2, out_glob2 if tp > 1 else out_loc2)]
-        copy = torch.cuda.Stream(dev)
+        up = torch.cuda.Stream(dev)     # host -> device (one copy engine) ...
+        down = torch.cuda.Stream(dev)   # ... and device -> host (the other), concurrently
         ev_h2d = [torch.cuda.Event(), torch.cuda.Event()]
         ev_comp = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_d2h = [torch.cuda.Event(), torch.cuda.Event()]
 
         def h2d(si):
             md, qd, knd, vnd, _, _ = sets[si]
-            with torch.cuda.stream(copy):
+            with torch.cuda.stream(up):
                 for k, v in meta_h.items():
                     md[k].copy_(v, non_blocking=True)
                 qd.copy_(q_h, non_blocking=True)
                 knd.copy_(kn_h, non_blocking=True)
                 vnd.copy_(vn_h, non_blocking=True)
-                ev_h2d[si].record(copy)
+                ev_h2d[si].record(up)
 
         def run_pipeline(n):
-            copy.wait_stream(stream)
+            up.wait_stream(stream)
+            down.wait_stream(stream)
             h2d(0)
             for i in range(n):
                 si = i % 2
                 stream.wait_event(ev_h2d[si])
+                if i >= 2:                         # step i-2's outputs (same set) are on the host
+                    stream.wait_event(ev_d2h[si])
                 sets[si][4].replay()
                 ev_comp[si].record(stream)
                 if i + 1 < n:                      # inputs of step i+1 (its set was last read by step i-1)
                     sj = 1 - si
                     if i >= 1:
-                        copy.wait_event(ev_comp[sj])
+                        up.wait_event(ev_comp[sj])
                     h2d(sj)
-                with torch.cuda.stream(copy):      # outputs of step i, overlapping step i+1
-                    copy.wait_event(ev_comp[si])
+                with torch.cuda.stream(down):      # outputs of step i, overlapping step i+1
+                    down.wait_event(ev_comp[si])
                     out_h.copy_(sets[si][5], non_blocking=True)
-            stream.wait_stream(copy)
+                    ev_d2h[si].record(down)
+            stream.wait_stream(up)
+            stream.wait_stream(down)
 
         def timed_pipeline(n):
             e0 = torch.cuda.Event(enable_timing=True)
@@ -529,7 +536,7 @@ def run_ours(args):
         },
         "cpu_baseline": cpu,
         "e2e": {"value": B / (ms_e2e * 1e-3), "unit": "tokens/s", "ms_per_step": ms_e2e,
-                "pipeline": ("copy stream overlaps step i+1 H2D and step i D2H with compute (2 buffer sets)"
+                "pipeline": ("two copy streams overlap step i+1 H2D and step i D2H with compute (2 buffer sets)"
                              if pipelined else "serial H2D, step, D2H on one stream"),
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": launches,
