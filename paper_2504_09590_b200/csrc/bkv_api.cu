@@ -399,6 +399,7 @@ static bkv_status decode_impl(const bkv_kv_pool *pool, const bkv_block_map *map,
   p.target_units = bkv::decode_target_units(cfg);
   p.min_split = bkv::decode_min_split(g);
   p.small_plan = getenv("BKV_SMALL_PLAN") ? atoi(getenv("BKV_SMALL_PLAN")) : 1;
+  p.streamk = getenv("BKV_STREAMK") ? atoi(getenv("BKV_STREAMK")) : 1;   // 0 off, 1 auto, 2 always (dev)
   p.units_max = w.units_max;
   p.slots = slots;
   p.q_bytes = qb;
@@ -423,6 +424,7 @@ static bkv_status decode_impl(const bkv_kv_pool *pool, const bkv_block_map *map,
   // (opt-in, BKV_FUSED_MERGE=1: measured slower -- the last-arriving warp merges all g rows
   // of a GQA group serially at the tail, e.g. Llama-70B TP1 115 -> 149 us per layer)
   p.fused_merge = (n_peers == 0 && getenv("BKV_FUSED_MERGE") && atoi(getenv("BKV_FUSED_MERGE"))) ? 1 : 0;
+  if (p.fused_merge) p.streamk = 0;   // the in-kernel merge knows only the split plan
   for (int k = 0; k < bkv::kMaxPeers; ++k) {
     p.peer_out[k] = k < n_peers ? static_cast<uint16_t *>(peer_outs[k]) : nullptr;
     if (k < n_peers && (!peer_outs[k] || !aligned16(peer_outs[k])))

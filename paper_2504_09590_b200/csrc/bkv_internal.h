@@ -72,6 +72,7 @@ struct DecodeParams {
   int target_units;      // split plan: aim for about this many units
   int min_split;         // split plan: at least this many blocks per unit (large problems)
   int small_plan;        // split plan: chain-balanced P for small problems (BKV_SMALL_PLAN=0: off)
+  int streamk;           // small problems: equal contiguous block ranges per warp (rows cut across warps)
   int units_max;         // workspace capacity in units
   int slots;             // ring depth per warp (S)
   int q_bytes;           // smem bytes per q-ring entry

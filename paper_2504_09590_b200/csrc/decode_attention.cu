@@ -67,11 +67,13 @@ struct SlotMeta {
 
 constexpr int kBuckets = 4;
 constexpr int kFastSplits = 8;   // merge: rows with <= this many splits preload every partial
+constexpr int kStreamKMinRange = 12;   // stream-K plan only when warp ranges are at least this long
 
 struct Plan {
   int P;                  // target blocks per split
   int base[kBuckets + 1]; // split-slot offset of each size bucket (largest first)
-  int U;                  // units = base[kBuckets] * H
+  int U;                  // units = base[kBuckets] * H (stream-K: 2 partial slots per warp)
+  int streamk;            // 1: stream-K plan -- P = blocks per warp range, Pre[0] = prefix of nb
 };
 
 template <int D>
@@ -184,8 +186,18 @@ __device__ void compute_plan(const DecodeParams &p, int *Pre, int *Lsm, int *NBs
       }
     }
     Pll = p.small_plan ? bestP : p.min_split;
+    // stream-K when a warp's range holds >= kStreamKMinRange blocks (measured:
+    // Llama-70B TP2 65.3 -> 60.5 us, TP4 37.7 -> 35.1, OPT-13B TP4 39.0 -> 37.5; with
+    // ~8-block ranges (TP8 shards) the extra segments cost more than the balance gains)
+    if (p.streamk == 1 && TH >= static_cast<long long>(kStreamKMinRange) * W) Pll = -1;
   }
-  const int P = static_cast<int>(Pll);
+  if (p.streamk == 2) Pll = -1;   // dev: stream-K for every problem size
+  const bool sk = Pll < 0;
+  // stream-K (small problems): the flattened (request, kv head, block)
+  // sequence is cut into equal ranges of P blocks, one per warp; the scans below then
+  // give Pre[0][r] = sum of nb over requests before r (all "splits" in bucket 0)
+  const int P = sk ? static_cast<int>(max(1ll, cdiv_ll(T * p.H, static_cast<long long>(p.total_warps))))
+                   : static_cast<int>(Pll);
   if (kDevTrace && pc) pc[2] = clock64();
   // per-thread contiguous ranges -> 4-bucket exclusive scans of n_r
   const int per = (B + nt - 1) / nt;
@@ -193,7 +205,7 @@ __device__ void compute_plan(const DecodeParams &p, int *Pre, int *Lsm, int *NBs
   int4 cnt = make_int4(0, 0, 0, 0);
   int *code = Pre + 3 * (B + 1);   // split codes, parked in Pre[3][r] until this thread overwrites them
   for (int r = r0; r < r1; ++r) {
-    const int c = split_code(NBsm[r], P);
+    const int c = sk ? (NBsm[r] << 2) : split_code(NBsm[r], P);
     code[r] = c;
     const int n = c >> 2, bk = c & 3;
     cnt.x += bk == 0 ? n : 0;
@@ -254,7 +266,8 @@ __device__ void compute_plan(const DecodeParams &p, int *Pre, int *Lsm, int *NBs
     const int acc = tot.x + tot.y + tot.z + tot.w;
     plan->base[kBuckets] = acc;
     plan->P = P;
-    plan->U = acc * p.H;
+    plan->U = sk ? 2 * p.total_warps : acc * p.H;
+    plan->streamk = sk ? 1 : 0;
   }
   __syncthreads();
 }
@@ -267,10 +280,12 @@ __device__ void compute_plan(const DecodeParams &p, int *Pre, int *Lsm, int *NBs
 // last-arriver merge) -> L2 loads (ld.global.cg), else read-only cached loads.
 template <int D, bool COHERENT>
 __device__ __forceinline__ void merge_row(const DecodeParams &p, int u0, int ns, int r, int h, int head,
-                                          int lane) {
+                                          int lane, int u_first, int ustride) {
+  // split s of the row lives in unit slot (s == 0 ? u_first : u0 + s * ustride)
+  auto unit_of = [&](int sidx) { return sidx == 0 ? u_first : u0 + sidx * ustride; };
   constexpr unsigned FULL = 0xffffffffu;
   constexpr int EPL = D / 32;
-  const int H = p.H, g = p.g;
+  const int g = p.g;
   float Mrun = -INFINITY, Lrun = 0.f, acc[EPL];
 #pragma unroll
   for (int q = 0; q < EPL; ++q) acc[q] = 0.f;
@@ -282,7 +297,7 @@ __device__ __forceinline__ void merge_row(const DecodeParams &p, int u0, int ns,
 #pragma unroll
     for (int t = 0; t < kFastSplits; ++t) {
       if (t < ns) {
-        const float *po = p.part_o + (static_cast<int64_t>(u0 + t * H) * g + head) * D + lane * EPL;
+        const float *po = p.part_o + (static_cast<int64_t>(unit_of(t)) * g + head) * D + lane * EPL;
         if constexpr (EPL == 4) {
           const float4 v = COHERENT ? __ldcg(reinterpret_cast<const float4 *>(po)) : __ldg(reinterpret_cast<const float4 *>(po));
           ov[t][0] = v.x;
@@ -298,7 +313,7 @@ __device__ __forceinline__ void merge_row(const DecodeParams &p, int u0, int ns,
     }
     float wj = -INFINITY, lj = 0.f;
     if (lane < ns) {
-      const float2 *src = reinterpret_cast<const float2 *>(p.part_ml + (static_cast<int64_t>(u0 + lane * H) * g + head) * 2);
+      const float2 *src = reinterpret_cast<const float2 *>(p.part_ml + (static_cast<int64_t>(unit_of(lane)) * g + head) * 2);
       const float2 v = COHERENT ? __ldcg(src) : __ldg(src);
       wj = v.x;
       lj = v.y;
@@ -323,7 +338,7 @@ __device__ __forceinline__ void merge_row(const DecodeParams &p, int u0, int ns,
   for (int s0 = 0; (COHERENT || ns > kFastSplits) && s0 < ns; s0 += 32) {
     const int sl = s0 + lane;
     const bool ok = sl < ns;
-    const int us = u0 + sl * H;
+    const int us = unit_of(sl);
     float wj = -INFINITY, lj = 0.f;
     if (ok) {
       const float2 *src = reinterpret_cast<const float2 *>(p.part_ml + (static_cast<int64_t>(us) * g + head) * 2);
@@ -518,9 +533,15 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
       p.plan_out[0] = plan.P;
       for (int k = 0; k <= kBuckets; ++k) p.plan_out[1 + k] = plan.base[k];
       p.plan_out[6] = plan.U;
+      p.plan_out[7] = plan.streamk;
     }
     // per request: (first split slot, split count) -> the merge kernel needs one load per row
+    // (stream-K: (blocks before the request, its blocks))
     for (int r = threadIdx.x; r < p.B; r += blockDim.x) {
+      if (plan.streamk) {
+        reinterpret_cast<int2 *>(p.plan_out + 16)[r] = make_int2(Pre[r], NBsm[r]);
+        continue;
+      }
       const int c = split_code(NBsm[r], plan.P), k = c & 3;
       reinterpret_cast<int2 *>(p.plan_out + 16)[r] = make_int2(plan.base[k] + Pre[k * (p.B + 1) + r], c >> 2);
     }
@@ -588,7 +609,35 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
       if (p.fills) filv = __ldg(p.fills + static_cast<int64_t>(x.r) * p.fill_rs + ew);
     }
   };
-  UnitInfo cur{}, nxt = decode_unit(pull_unit());
+  // stream-K plan: this warp's range of the flattened (request, kv head, block)
+  // sequence, cut into segments at row boundaries; each segment is a unit
+  const int gw = u_pref;   // the warp's static first unit = its range index
+  int sk_beg = 0, sk_pos = 0, sk_end = 0;
+  if (plan.streamk) {
+    const int N = Pre[p.B] * H;   // total blocks x kv heads (Pre[0][B])
+    sk_beg = min(N, gw * P);
+    sk_pos = sk_beg;
+    sk_end = min(N, sk_beg + P);
+  }
+  auto next_unit = [&]() -> UnitInfo {
+    if (!plan.streamk) return decode_unit(pull_unit());
+    UnitInfo x;
+    x.u = U;
+    if (sk_pos >= sk_end) return x;
+    const int a = sk_pos;
+    x.r = search_le(Pre, p.B, a / H);   // largest r with H * Pre[0][r] <= a (so nb_r > 0)
+    x.nb = NBsm[x.r];
+    x.L = Lsm[x.r];
+    const int off = a - H * Pre[x.r];
+    x.h = off / x.nb;
+    x.e0 = off - x.h * x.nb;
+    x.e1 = min(x.nb, x.e0 + (sk_end - a));
+    x.n = (x.e0 == 0 && x.e1 == x.nb) ? 1 : 2;   // whole row: direct output, else a partial
+    x.u = 2 * gw + (a == sk_beg ? 0 : 1);        // slot: the range's first / last segment
+    sk_pos = a + (x.e1 - x.e0);
+    return x;
+  };
+  UnitInfo cur{}, nxt = next_unit();
   int nx_bt = 0, nx_dir = 0, nx_fil = 0;
   load_window(nxt, nxt.e0, nx_bt, nx_dir, nx_fil);
   bool is_active = false, is_done = false, is_first = false;
@@ -608,7 +657,7 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
       dir_w = nx_dir;
       fil_w = nx_fil;
       is_wb = cur.e0;
-      nxt = decode_unit(pull_unit());                     // look one unit ahead ...
+      nxt = next_unit();                                  // look one unit ahead ...
       load_window(nxt, nxt.e0, nx_bt, nx_dir, nx_fil);    // ... its loads overlap this unit
       if (lane < g) {   // the unit's q rows: pull into L2 now, the consumer loads them later
         const uint16_t *qrow = p.q + static_cast<int64_t>(cur.r) * p.q_ss +
@@ -1017,7 +1066,7 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
         if (g <= 8 && m.nsplit * g <= 128)
           merge_group<D>(p, u0, m.nsplit, r, h, lane, my_scr);
         else
-          for (int head = 0; head < g; ++head) merge_row<D, true>(p, u0, m.nsplit, r, h, head, lane);
+          for (int head = 0; head < g; ++head) merge_row<D, true>(p, u0, m.nsplit, r, h, head, lane, u0, H);
         if (lane == 0) p.merge_cnt[r * H + h] = 0;
       }
     }
@@ -1150,13 +1199,43 @@ __global__ void __launch_bounds__(256) merge_kernel(const DecodeParams p) {
   if (wid >= p.B * H * g) return;   // one warp per (request, kv head, q head of the group)
   const int rh = wid / g, row1 = wid - rh * g;
   const int r = rh / H, h = rh - r * H;
-  const int2 mp = reinterpret_cast<const int2 *>(p.plan_out + 16)[r];   // (first split slot, splits)
-  const int ns = mp.y;
+  const int2 mp = reinterpret_cast<const int2 *>(p.plan_out + 16)[r];
+  const int sk = p.plan_out[7];
+  const int64_t off = static_cast<int64_t>(r) * p.o_ss + static_cast<int64_t>(h * g + row1) * p.o_sh + lane * EPL;
+  int ns, u0, u_first, ustride;
+  if (sk) {
+    // stream-K plan: mp = (blocks of the requests before r, r's blocks); warp range w
+    // covers flattened blocks [w * per, (w + 1) * per); a row cut across ranges w0..w1
+    // left its pieces in slot 2 w + 0 (the range's first segment) or 2 w + 1 (its last)
+    const int per = p.plan_out[0], nb = mp.y;
+    if (nb == 0) {   // empty context (reading Q8): zeros; no range ever touched the row
+      if constexpr (EPL == 4) {
+        *reinterpret_cast<uint2 *>(p.out + off) = make_uint2(0u, 0u);
+        for (int k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint2 *>(p.peer_out[k] + off) = make_uint2(0u, 0u);
+      } else {
+        *reinterpret_cast<uint32_t *>(p.out + off) = 0u;
+        for (int k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint32_t *>(p.peer_out[k] + off) = 0u;
+      }
+      return;
+    }
+    const int S = H * mp.x + h * nb;   // small problems only: fits in int
+    const int w0 = S / per, w1 = (S + nb - 1) / per;
+    ns = w1 - w0 + 1;
+    u0 = 2 * w0;
+    u_first = 2 * w0 + (S == w0 * per ? 0 : 1);
+    ustride = 2;
+  } else {
+    // split plan: (first split slot, splits); all splits of (r, h) are consecutive
+    // split slots of r's bucket: u = (slot0 + s) * H + h
+    ns = mp.y;
+    u0 = mp.x * H + h;
+    u_first = u0;
+    ustride = H;
+  }
   if (ns <= 1) {
     // single split: the decode kernel wrote the local row; forward it to the
     // peers' outputs (fused reassembly) with 16-byte stores
     if (p.n_peers > 0) {
-      const int64_t off = static_cast<int64_t>(r) * p.o_ss + static_cast<int64_t>(h * g + row1) * p.o_sh + lane * EPL;
       if constexpr (EPL == 4) {
         const uint2 w = *reinterpret_cast<const uint2 *>(p.out + off);
         for (int k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint2 *>(p.peer_out[k] + off) = w;
@@ -1167,9 +1246,7 @@ __global__ void __launch_bounds__(256) merge_kernel(const DecodeParams p) {
     }
     return;
   }
-  // all splits of (r, h) are consecutive split slots of r's bucket: u = (slot0 + s) * H + h
-  const int u0 = mp.x * H + h;
-  merge_row<D, false>(p, u0, ns, r, h, row1, lane);
+  merge_row<D, false>(p, u0, ns, r, h, row1, lane, u_first, ustride);
 }
 
 // ----------------------------------------------------------------- host

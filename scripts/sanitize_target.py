@@ -28,6 +28,9 @@ for sh in (Shape("s1", 4, 4, 64, 16, 8, 0.5, "uniform", 300, 1, 1, uniform_max=3
                   torch.from_numpy(cu).cuda(), g(kn), g(vn), slot_mapping=sm)
     for pdl in (False, True):
         out = bkv.paged_decode_attention(pool, bt, dirs, torch.from_numpy(lay.lens).cuda(), g(q), pdl=pdl)
+    os.environ["BKV_STREAMK"] = "2"   # stream-K plan (rows cut across warp ranges) on the same case
+    out = bkv.paged_decode_attention(pool, bt, dirs, torch.from_numpy(lay.lens).cuda(), g(q), pdl=True)
+    os.environ["BKV_STREAMK"] = "1"
     ck, cv = bkv.kv_checkpoint(pool, sm[:17])
     bkv.kv_restore(pool, sm[:17], ck, cv)
     torch.cuda.synchronize()

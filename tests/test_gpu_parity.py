@@ -149,6 +149,31 @@ def test_edge_lengths(direction):
     check_close(o, ref, f"mha dir{direction}")
 
 
+def test_streamk_plan_forced_on_small_cases(monkeypatch):
+    """Stream-K split plan (equal contiguous block ranges per warp, rows cut across warps,
+    pieces merged from per-range slots) forced on for problems the auto rule leaves to the
+    bucket plan: MHA and GQA, both directions, empty and ragged contexts, bs 16/32."""
+    monkeypatch.setenv("BKV_STREAMK", "2")
+    for cfg, seed, qs in ATT_CASES:
+        case = make_case(cfg, seed, q_scale_log2=qs)
+        o, ref, _ = _run_case(case)
+        check_close(o, ref, "stream-K " + cfg)
+    lens = [0, 1, 2, 15, 16, 17, 33, 0, 64, 65, 257, 1000, 2049, 0]
+    for hq, hkv, d, bs in ((8, 2, 128, 16), (4, 4, 64, 32), (16, 1, 128, 32)):
+        sh = Shape("skedge", hq, hkv, d, bs, len(lens), 0.5, "uniform", 4096, 1, 1)
+        for direction in (0, 1):
+            case = make_case(sh, 6 + direction, lens=lens, is_be=[bool(direction)] * len(lens))
+            o, ref, _ = _run_case(case)
+            check_close(o, ref, f"stream-K {(hq, hkv, d, bs)} dir{direction}")
+
+
+@pytest.mark.parametrize("cfg,tp,rank", [("llama70b", 4, 1), ("opt13b", 4, 3), ("llama70b", 2, 0)])
+def test_full_size_streamk_auto(cfg, tp, rank):
+    """Shards where the auto rule picks the stream-K plan (warp ranges >= 12 blocks), in the
+    bench's launch configuration (fused step, PDL), sampled against the oracle."""
+    _full_size(cfg, tp, rank, mode="step", pdl=True, seed=4)
+
+
 def test_single_token_is_exact_v0():
     """Closed form P3(i): L = 1 => out = v_0 bitwise (softmax weight exactly 1)."""
     for hq, hkv, d in ((4, 4, 64), (8, 1, 128), (16, 2, 128)):
