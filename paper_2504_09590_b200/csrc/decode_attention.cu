@@ -21,8 +21,14 @@
 //  * Work units = (request, kv head, split of <= P blocks), pulled from a
 //    global atomic counter (first unit static), enumerated longest-first by a
 //    4-bucket split plan computed in-kernel from seq_lens (entry counts for
-//    general maps); small problems get a chain-balanced P.  The issuer decodes
-//    the next unit one unit ahead (block-table window loads, q L2 prefetch).
+//    general maps); small problems get a chain-balanced P, or -- when warp
+//    ranges would hold >= 12 blocks -- the stream-K plan: the flattened
+//    (request, kv head, block) sequence cut into equal contiguous ranges, one
+//    per warp, whose row segments are the units (rows cut across ranges leave
+//    per-range partial slots).  The issuer decodes the next unit one unit
+//    ahead (block-table window loads, q L2 prefetch).
+//  * PDL: both kernels trigger their dependents at entry; the plan prologue
+//    reads only seq_lens (and entry counts) before griddepcontrol.wait.
 //  * Tensor cores for every group size (the CUDA-core FFMA2 MHA variant is a
 //    dev switch, BKV_MHA_CUDA_CORES=1): tokens on the MMA M dimension,
 //    S^T = K.Q^T and O^T += V^T.P^T with bf16 mma.sync m16n8k16 (K via
