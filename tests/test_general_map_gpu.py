@@ -171,3 +171,11 @@ def test_dense_map_as_general_is_bitwise_dense():
                                     num_entries=torch.from_numpy(nb).to(DEV))
     torch.cuda.synchronize()
     assert torch.equal(o1.view(torch.int16), o2.view(torch.int16))
+
+
+@pytest.mark.parametrize("cfg,seed", [("tiny_gqa", 6), ("llama70b", 7)])
+def test_general_fused_step_streamk(cfg, seed, monkeypatch):
+    """The stream-K split plan (forced on) over general maps with the fused append:
+    segments follow entry counts, the new token's entry is owned by exactly one range."""
+    monkeypatch.setenv("BKV_STREAMK", "2")
+    test_general_fused_decode_step(cfg, seed)
