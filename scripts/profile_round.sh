@@ -13,7 +13,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/
     python bench.py --steps 2 --warmup 3 --no-cpu > $OUT/launches_bench.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_llama70b.csv \
     python bench.py --config llama70b --layers 8 --steps 2 --warmup 3 --no-cpu > $OUT/launches_bench_llama.log 2>&1
-for c in "opt13b 1" "opt13b 2" "opt30b 4" "llama70b 8" "llama70b 1"; do
+for c in "opt13b 1" "opt13b 2" "opt30b 4" "llama70b 8" "llama70b 4" "llama70b 1"; do
   set -- $c
   ncu --set full --clock-control none --import-source on -k regex:decode_kernel -s 6 -c 1 \
       -o $OUT/decode_$1_tp$2 python scripts/ncu_target.py $1 $2 8 > /dev/null 2>&1
