@@ -417,3 +417,24 @@ def test_mha_cuda_core_kernel_parity(monkeypatch):
     sh = Shape("cc", 5, 5, 128, 32, 20, 0.5, "uniform", 900, 1, 1, uniform_max=900)
     o, ref, _ = _run_case(make_case(sh, 42))
     check_close(o, ref, "cuda-core d128 bs32")
+
+
+@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("streamk", ["0", "2"])
+def test_random_geometry_fuzz(seed, streamk, monkeypatch):
+    """Seeded random geometries (group size, head_dim, block size, batch, lengths including
+    empty contexts, RT/BE mix), both split plans, against the oracle."""
+    monkeypatch.setenv("BKV_STREAMK", streamk)
+    rng = np.random.default_rng(1000 + seed)
+    hkv = int(rng.choice([1, 2, 4]))
+    g = int(rng.choice([1, 2, 4, 8, 16]))
+    d = int(rng.choice([64, 128]))
+    bs = int(rng.choice([16, 32]))
+    B = int(rng.integers(1, 48))
+    lens = rng.integers(0, 1500, B)
+    lens[rng.random(B) < 0.1] = 0
+    is_be = (rng.random(B) < 0.5).tolist()
+    sh = Shape("fuzz", hkv * g, hkv, d, bs, B, 0.5, "uniform", 1500, 1, 1)
+    case = make_case(sh, seed, lens=lens.tolist(), is_be=is_be, q_scale_log2=int(rng.integers(0, 4)))
+    o, ref, _ = _run_case(case)
+    check_close(o, ref, f"fuzz{seed} g{g} hkv{hkv} d{d} bs{bs} B{B} sk{streamk}")
