@@ -179,3 +179,19 @@ def test_general_fused_step_streamk(cfg, seed, monkeypatch):
     segments follow entry counts, the new token's entry is owned by exactly one range."""
     monkeypatch.setenv("BKV_STREAMK", "2")
     test_general_fused_decode_step(cfg, seed)
+
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("streamk", ["0", "2"])
+def test_general_fused_step_fuzz(seed, streamk, monkeypatch):
+    """Seeded random geometries on FindBlock-style general maps through the fused decode
+    step (pool bit-exact, output vs the oracle, equal to append + attention), both plans."""
+    monkeypatch.setenv("BKV_STREAMK", streamk)
+    rng = np.random.default_rng(2000 + seed)
+    hkv = int(rng.choice([1, 2, 4]))
+    g = int(rng.choice([1, 2, 4, 8]))
+    d = int(rng.choice([64, 128]))
+    bs = int(rng.choice([16, 32]))
+    B = int(rng.integers(2, 40))
+    sh = Shape(f"gfuzz{seed}", hkv * g, hkv, d, bs, B, 0.5, "uniform", 1200, 1, 1, uniform_max=1200)
+    test_general_fused_decode_step(sh, seed)
