@@ -183,3 +183,24 @@ def test_prefill_tcgen05_single_query_tile_per_cta(cfg, general, monkeypatch):
     n = query_counts(case.layout.lens, np.random.default_rng(31))
     o, ref = _run(case, general, n)
     check_close(o, ref, cfg + " QT1")
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_prefill_random_geometry_fuzz(seed, monkeypatch):
+    """Seeded random geometries (group size, head_dim 64/128 -> mma.sync / tcgen05 kernels,
+    block size, batch, dense or general map, whole-prompt / suffix / decode rows), and on
+    odd seeds the tcgen05 kernel with one query tile per CTA, against the oracle."""
+    if seed % 2:
+        monkeypatch.setenv("BKV_PREFILL_QT", "1")
+    rng = np.random.default_rng(3000 + seed)
+    hkv = int(rng.choice([1, 2, 4]))
+    g = int(rng.choice([1, 2, 4, 8, 16]))
+    d = int(rng.choice([64, 128]))
+    bs = int(rng.choice([16, 32]))
+    B = int(rng.integers(1, 24))
+    general = bool(rng.random() < 0.5)
+    sh = Shape(f"pfuzz{seed}", hkv * g, hkv, d, bs, B, 0.5, "uniform", 900, 1, 1, uniform_max=900)
+    case = make_case(sh, seed, general=general)
+    n = query_counts(case.layout.lens, rng, full=bool(rng.random() < 0.3))
+    o, ref = _run(case, general, n, qs=int(rng.integers(0, 3)))
+    check_close(o, ref, f"pfuzz{seed} g{g} hkv{hkv} d{d} bs{bs} B{B} general{general}")
