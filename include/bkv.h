@@ -21,8 +21,9 @@
  *   bkv_block_map.fills / num_entries in every call               (f3 general maps)
  *   bkv_paged_prefill_attention, bkv_paged_mixed_attention        (f4 mixed prefill + decode)
  *
- * plus host helpers (workspace sizing, host-side layout validators, status
- * strings).
+ * and the planned decode of the same path (host-built split plan, one launch
+ * per layer): bkv_decode_plan, bkv_decode_planned; plus host helpers
+ * (workspace sizing, host-side layout validators, status strings).
  *
  * Conventions (all entry points):
  *   - Device pointers are caller-owned (allocated by PyTorch or cudaMalloc);
@@ -33,8 +34,9 @@
  *     thread-local one-line explanation.  Launch failures return BKV_ERR_CUDA.
  *     Device-side faults (e.g. a block id out of range that the caller did not
  *     validate) surface asynchronously, as for any CUDA kernel.
- *   - No global mutable state besides a per-device cache of immutable device
- *     properties: calls are thread-safe.
+ *   - No global mutable state besides per-device caches of immutable device
+ *     properties and of kernel shared-memory opt-ins (mutex-guarded), and the
+ *     developer switches read once per process: calls are thread-safe.
  *   - Element type of K, V, Q, out, k_new, v_new is bf16 (IEEE bfloat16 bits);
  *     all strides are in ELEMENTS.  Reading Q1: the paper never states the
  *     precision; this library stores bf16 and accumulates in fp32.
@@ -265,6 +267,13 @@ BKV_API bkv_status bkv_kv_append_checkpoint(const bkv_kv_pool *pool, const bkv_b
  * Unknown flag bits return BKV_ERR_INVALID_ARGUMENT.
  */
 #define BKV_FLAG_PDL 1u
+/* bkv_decode_planned only, with BKV_FLAG_PDL: the RESIDENT KV of the pool (every
+ * token except the ones this call appends) is not written by the immediately
+ * preceding kernel either -- true when that kernel is e.g. the layer's QKV
+ * projection or another layer's decode call -- so the first tiles of every
+ * warp's ring are requested before the grid wait; q, k_new, v_new and the
+ * workspace are still read after it. */
+#define BKV_FLAG_KV_EARLY 2u
 BKV_API bkv_status bkv_paged_decode_attention_ex(const bkv_kv_pool *pool, const bkv_block_map *map,
                                                  const int32_t *seq_lens, int32_t max_seq_len,
                                                  const void *q, int64_t q_stride_seq,
@@ -438,9 +447,86 @@ BKV_API bkv_status bkv_validate_block_map_host(const bkv_block_map *map, const i
                                                int32_t num_blocks, int32_t block_size,
                                                int32_t require_nonempty, int64_t info[5]);
 
+/*
+ * ------------------------------------------------------------------------
+ * Planned decode: the split plan made on the HOST once per step, one kernel
+ * launch per layer ("computed on device or host").
+ *
+ * The host scheduler builds each step's length table before it
+ * uploads it, so it can also build the split plan there, once, and every
+ * layer of the step reuses it.  The plan cuts the flattened sequence of
+ * (request r, kv head h, block e) -- r-major, then h, then e -- into equal
+ * contiguous ranges, one per warp of a persistent grid (one CTA per SM);
+ * rows cut across warps are merged inside the kernel (shared memory within a
+ * CTA, a last-arriver merge of one piece per CTA across CTAs) in an order
+ * fixed by the plan, so results are run-to-run bitwise identical.  The plan
+ * depends only on the lengths (and entry counts) and on the device's SM
+ * count: identical on every rank of a head-sharded TP group.
+ *
+ * bkv_decode_plan_bytes -- an upper bound on the plan size (bytes) for
+ *   num_seqs requests and num_kv_heads local kv heads on a device with num_sms
+ *   SMs (0: the CURRENT device).  Returns 0 on an invalid argument (see
+ *   bkv_last_error).
+ *
+ * bkv_decode_plan -- host only; no CUDA call unless num_sms = 0 (then one
+ *   cached query of the current device's SM count).
+ *   seq_lens     HOST int32 [num_seqs]: resident lengths the layer calls will
+ *                receive (after this step's append), >= 0
+ *   num_entries  HOST int32 [num_seqs] for a general map (f3), else NULL
+ *   bt_stride    the block map's bt_stride (bounds the entries per request)
+ *   num_kv_heads, num_q_heads, head_dim, block_size: the layer geometry
+ *   num_sms      SM count of the device that will run it (0: current device);
+ *                bkv_decode_planned rejects a plan made for another count
+ *   plan         HOST buffer, 16-byte aligned, plan_bytes long, written
+ *   *plan_bytes_used (optional) bytes of the plan (also on
+ *                BKV_ERR_WORKSPACE_TOO_SMALL: the size needed)
+ *   The caller copies plan[0, *plan_bytes_used) to device memory (one H2D
+ *   with the step's other metadata) and passes both copies to every layer.
+ *   Errors: BKV_ERR_INVALID_ARGUMENT (negative length, entries > bt_stride,
+ *   problem >= 2^30 blocks x heads), BKV_ERR_UNSUPPORTED (geometry outside
+ *   the built set), BKV_ERR_WORKSPACE_TOO_SMALL (plan_bytes too small).
+ *
+ * bkv_decode_planned -- one layer: decode attention (k_new = v_new = NULL,
+ *   semantics of bkv_paged_decode_attention_ex) or the fused decode step
+ *   (both set, semantics of bkv_decode_step), with optional peer outputs
+ *   (semantics of bkv_decode_multi_out; n_peers = 0, peer_outs = NULL for
+ *   none).  ONE kernel launch.
+ *   plan_host    the buffer bkv_decode_plan wrote (only its header is read)
+ *   plan_dev     device copy of it, 16-byte aligned
+ *   seq_lens     device int32 [num_seqs], the lengths the plan was built from
+ *   workspace    as bkv_paged_decode_attention (bkv_decode_workspace_size;
+ *                zero-initialised once: the kernel leaves its counters zero)
+ *   flags        BKV_FLAG_PDL (| BKV_FLAG_KV_EARLY): programmatic dependent launch; the plan,
+ *                seq_lens and the block map (block_tables, dirs, fills,
+ *                num_entries) are read BEFORE the preceding kernel on the
+ *                stream completes, so none of them may be written by that
+ *                kernel (host copies and earlier kernels are fine); q, k_new,
+ *                v_new, the pool and the workspace are read after it.
+ *   Errors: as bkv_decode_multi_out, plus BKV_ERR_INVALID_ARGUMENT when the
+ *   plan's geometry (num_seqs, heads, group, head_dim, block_size, dense or
+ *   general map, SM count) does not match the call.
+ */
+BKV_API size_t bkv_decode_plan_bytes(int32_t num_seqs, int32_t num_kv_heads, int32_t num_sms);
+BKV_API bkv_status bkv_decode_plan(const int32_t *seq_lens, const int32_t *num_entries, int32_t num_seqs,
+                                   int32_t bt_stride, int32_t num_kv_heads, int32_t num_q_heads,
+                                   int32_t head_dim, int32_t block_size, int32_t num_sms, void *plan,
+                                   size_t plan_bytes, size_t *plan_bytes_used);
+BKV_API bkv_status bkv_decode_planned(const bkv_kv_pool *pool, const bkv_block_map *map,
+                                      const int32_t *seq_lens, const void *plan_host, const void *plan_dev,
+                                      const void *k_new, const void *v_new, const void *q,
+                                      int64_t q_stride_seq, int64_t q_stride_head, int32_t num_q_heads,
+                                      float softmax_scale, void *out, int64_t o_stride_seq,
+                                      int64_t o_stride_head, void *const *peer_outs, int32_t n_peers,
+                                      void *workspace, size_t workspace_bytes, uint32_t flags,
+                                      bkv_stream_t stream);
+
+/* Developer switches (BKV_* environment variables) are read once
+ * per process; this re-reads them (tests and A/B runs; not concurrent-safe). */
+BKV_API void bkv_reload_dev_switches(void);
+
 BKV_API const char *bkv_status_string(bkv_status s);
 BKV_API const char *bkv_last_error(void); /* thread-local detail of the last failure */
-BKV_API int32_t bkv_version(void);        /* MAJOR*10000 + MINOR*100 + PATCH (0.2.0: general maps) */
+BKV_API int32_t bkv_version(void);        /* MAJOR*10000 + MINOR*100 + PATCH (0.3.0: planned decode) */
 
 #ifdef __cplusplus
 } /* extern "C" */

@@ -51,6 +51,7 @@ EXPORTS = ("bkv_kv_append", "bkv_paged_decode_attention", "bkv_decode_workspace_
            "bkv_paged_prefill_attention", "bkv_decode_multi_out", "bkv_peer_barrier",
            "bkv_paged_mixed_attention")
 BKV_FLAG_PDL = 1   # include/bkv.h: programmatic dependent launch (seq_lens not written by the previous kernel)
+BKV_FLAG_KV_EARLY = 2   # planned decode: resident KV not written by the previous kernel either
 
 
 def lib():
@@ -104,6 +105,17 @@ def lib():
                 L.bkv_kv_checkpoint.restype = ctypes.c_int
                 L.bkv_kv_restore.argtypes = [ctypes.POINTER(_Pool), P, i32, P, P, P]
                 L.bkv_kv_restore.restype = ctypes.c_int
+                L.bkv_decode_plan_bytes.argtypes = [i32, i32, i32]
+                L.bkv_decode_plan_bytes.restype = ctypes.c_size_t
+                L.bkv_decode_plan.argtypes = [P, P, i32, i32, i32, i32, i32, i32, i32, P, ctypes.c_size_t,
+                                              ctypes.POINTER(ctypes.c_size_t)]
+                L.bkv_decode_plan.restype = ctypes.c_int
+                L.bkv_decode_planned.argtypes = [
+                    ctypes.POINTER(_Pool), ctypes.POINTER(_Map), P, P, P, P, P, P, i64, i64, i32,
+                    ctypes.c_float, P, i64, i64, P, i32, P, ctypes.c_size_t, ctypes.c_uint32, P]
+                L.bkv_decode_planned.restype = ctypes.c_int
+                L.bkv_reload_dev_switches.argtypes = []
+                L.bkv_reload_dev_switches.restype = None
                 L.bkv_status_string.argtypes = [ctypes.c_int]
                 L.bkv_status_string.restype = ctypes.c_char_p
                 L.bkv_last_error.restype = ctypes.c_char_p
@@ -253,6 +265,11 @@ def kv_checkpoint(pool: KVPool, slot_ids, k_out=None, v_out=None, stream=None):
         k_out = torch.empty(shape, dtype=torch.bfloat16, device=pool.k.device)
     if v_out is None:
         v_out = torch.empty(shape, dtype=torch.bfloat16, device=pool.k.device)
+    for t, nm in ((k_out, "k_out"), (v_out, "v_out")):
+        if not t.is_cuda and not t.is_pinned():   # pinned host memory is device-addressable (UVA)
+            raise BkvError(f"{nm} must be a CUDA tensor or pinned host memory")
+        if t.dtype != torch.bfloat16 or not t.is_contiguous() or tuple(t.shape) != shape:
+            raise BkvError(f"{nm} must be contiguous bfloat16 {list(shape)}")
     rc = lib().bkv_kv_checkpoint(ctypes.byref(p), slot_ids.data_ptr(), n, k_out.data_ptr(), v_out.data_ptr(),
                                  _stream_ptr(stream))
     _check(rc, "bkv_kv_checkpoint")
@@ -263,6 +280,13 @@ def kv_restore(pool: KVPool, slot_ids, k_in, v_in, stream=None):
     """bkv_kv_restore: scatter checkpointed rows back into their slots (swap-in)."""
     p = pool.c()
     _dev(slot_ids, "slot_ids", torch.int64)
+    n = slot_ids.numel()
+    shape = (n, pool.num_kv_heads, pool.head_dim)
+    for t, nm in ((k_in, "k_in"), (v_in, "v_in")):
+        if not t.is_cuda and not t.is_pinned():   # pinned host memory is device-addressable (UVA)
+            raise BkvError(f"{nm} must be a CUDA tensor or pinned host memory")
+        if t.dtype != torch.bfloat16 or not t.is_contiguous() or tuple(t.shape) != shape:
+            raise BkvError(f"{nm} must be contiguous bfloat16 {list(shape)}")
     rc = lib().bkv_kv_restore(ctypes.byref(p), slot_ids.data_ptr(), slot_ids.numel(), k_in.data_ptr(),
                               v_in.data_ptr(), _stream_ptr(stream))
     _check(rc, "bkv_kv_restore")
@@ -288,7 +312,10 @@ def workspace(num_seqs, num_q_heads, num_kv_heads, head_dim, device=None, stream
     with _ws_lock:
         ws = _ws_cache.get(key)
         if ws is None or ws.numel() < need:
-            ws = torch.zeros(max(need, 1 << 20), dtype=torch.uint8, device=dev)
+            # allocated and zeroed ON the stream that will use it, so its first kernel is
+            # ordered after the zero-fill and the allocator ties the block to that stream
+            with torch.cuda.stream(s):
+                ws = torch.zeros(max(need, 1 << 20), dtype=torch.uint8, device=dev)
             _ws_cache[key] = ws
     return ws
 
@@ -298,12 +325,21 @@ def _attn_args(pool, block_tables, dirs, seq_lens, q, softmax_scale, out, max_se
     p, m = pool.c(), block_map(block_tables, dirs, fills, num_entries)
     _dev(seq_lens, "seq_lens", torch.int32)
     _dev(q, "q", torch.bfloat16)
+    if q.dim() != 3:
+        raise BkvError("q must be [B][Hq][d]")
     B, Hq, d = q.shape
     if q.stride(2) != 1:
         raise BkvError("q must have a unit stride along head_dim")
+    if B != block_tables.shape[0] or seq_lens.dim() != 1 or seq_lens.numel() != B:
+        raise BkvError(f"q has {B} rows but block_tables has {block_tables.shape[0]} and "
+                       f"seq_lens {seq_lens.numel()}: one row per request in each")
+    if d != pool.head_dim:
+        raise BkvError(f"q head_dim {d} != pool head_dim {pool.head_dim}")
     if out is None:
         out = torch.empty((B, Hq, d), dtype=torch.bfloat16, device=q.device)
     _dev(out, "out", torch.bfloat16)
+    if out.dim() != 3 or tuple(out.shape) != (B, Hq, d):
+        raise BkvError(f"out must be [B][Hq][d] = {[B, Hq, d]}, got {list(out.shape)}")
     if out.stride(2) != 1:
         raise BkvError("out must have a unit stride along head_dim")
     if softmax_scale is None:
@@ -359,7 +395,9 @@ def paged_prefill_attention(pool: KVPool, block_tables, dirs, seq_lens, cu_q, q,
                             softmax_scale=None, out=None, stream=None, fills=None, num_entries=None):
     """bkv_paged_prefill_attention: causal attention of every request's LAST
     n_r = cu_q[r+1]-cu_q[r] tokens over its paged context; q/out bf16 [total][Hq][d]
-    (unit last stride).  n_r = 1 rows are decodes, so one call serves a mixed batch."""
+    (unit last stride).  n_r = 1 rows are decodes, so one call serves a mixed batch.
+    ``max_q_len``: host bound of max n_r (sizes the grid); None uses the total row count, a
+    valid but looser bound -- pass the scheduler's value, no device reduction is ever run."""
     p, m = pool.c(), block_map(block_tables, dirs, fills, num_entries)
     _dev(seq_lens, "seq_lens", torch.int32)
     _dev(cu_q, "cu_q", torch.int32)
@@ -374,8 +412,8 @@ def paged_prefill_attention(pool: KVPool, block_tables, dirs, seq_lens, cu_q, q,
         raise BkvError("out must have a unit stride along head_dim")
     if softmax_scale is None:
         softmax_scale = 1.0 / math.sqrt(d)
-    if max_q_len is None:
-        max_q_len = int((cu_q[1:] - cu_q[:-1]).max().item()) if cu_q.numel() > 1 else 0
+    if max_q_len is None:   # a host upper bound with no device reduction or sync: n_r <= total rows
+        max_q_len = T
     rc = lib().bkv_paged_prefill_attention(
         ctypes.byref(p), ctypes.byref(m), seq_lens.data_ptr(), cu_q.data_ptr(), int(max_q_len),
         q.data_ptr(), q.stride(0), q.stride(1), Hq, float(softmax_scale), out.data_ptr(),
@@ -439,8 +477,8 @@ def paged_mixed_attention(pool: KVPool, block_tables, dirs, seq_lens, cu_q, q, n
         raise BkvError("q/out must have a unit stride along head_dim")
     if softmax_scale is None:
         softmax_scale = 1.0 / math.sqrt(d)
-    if max_q_len is None:
-        max_q_len = int((cu_q[1:] - cu_q[:-1]).max().item()) if cu_q.numel() > 1 else 0
+    if max_q_len is None:   # host upper bound, no device op: a prefill's n_r <= the prefill rows
+        max_q_len = int(num_prefill_rows)
     if max_seq_len is None:
         max_seq_len = block_tables.shape[1] * pool.block_size
     B = block_tables.shape[0]
@@ -452,6 +490,107 @@ def paged_mixed_attention(pool: KVPool, block_tables, dirs, seq_lens, cu_q, q, n
         float(softmax_scale), out.data_ptr(), out.stride(0), out.stride(1), ws.data_ptr(), ws.numel(),
         BKV_FLAG_PDL if pdl else 0, _stream_ptr(stream))
     _check(rc, "bkv_paged_mixed_attention")
+    return out
+
+
+def reload_dev_switches():
+    """Re-read the BKV_* developer switches (read once per process otherwise)."""
+    lib().bkv_reload_dev_switches()
+
+
+class DecodePlan:
+    """A host-built split plan of one decode step (bkv_decode_plan) and its device copy.
+
+    Built from the scheduler's HOST lengths once per step; every layer's
+    :func:`decode_planned` call reuses it."""
+
+    def __init__(self, host, dev, nbytes):
+        self.host = host          # numpy int32 buffer (the header is read by each call)
+        self.dev = dev            # torch uint8 device tensor holding the same bytes
+        self.nbytes = nbytes
+
+    @property
+    def header(self):
+        names = ("magic", "version", "words", "B", "H", "g", "D", "bs", "general", "grid", "warps", "P",
+                 "n_segs", "n_tasks", "n_zero", "total", "off_wseg", "off_segs", "off_ctask", "off_tasks",
+                 "off_zero", "max_pieces", "max_entries", "off_xrows", "n_xrows")
+        return {n: int(self.host[i]) for i, n in enumerate(names)}
+
+
+def decode_plan_host(seq_lens, num_kv_heads, num_q_heads, head_dim, block_size, bt_stride,
+                     num_entries=None, num_sms=0):
+    """bkv_decode_plan on host arrays -> numpy int32 plan buffer (no device copy).
+    ``num_sms`` = 0 plans for the current device (needs a GPU); > 0 plans for that SM count."""
+    import numpy as np
+    ln = np.ascontiguousarray(np.asarray(seq_lens), dtype=np.int32)
+    ne = None if num_entries is None else np.ascontiguousarray(np.asarray(num_entries), dtype=np.int32)
+    B = ln.shape[0]
+    cap = lib().bkv_decode_plan_bytes(B, int(num_kv_heads), int(num_sms))
+    if cap == 0:
+        raise BkvError("bkv_decode_plan_bytes: " + lib().bkv_last_error().decode())
+    buf = np.zeros((cap + 15) // 4 + 4, dtype=np.int32)
+    off = (-buf.ctypes.data) % 16 // 4            # 16-byte aligned view
+    view = buf[off:off + cap // 4]
+    used = ctypes.c_size_t(0)
+    rc = lib().bkv_decode_plan(ln.ctypes.data, None if ne is None else ne.ctypes.data, B, int(bt_stride),
+                               int(num_kv_heads), int(num_q_heads), int(head_dim), int(block_size),
+                               int(num_sms), view.ctypes.data, view.nbytes, ctypes.byref(used))
+    _check(rc, "bkv_decode_plan")
+    return view[:used.value // 4]   # (a view: keeps the aligned buffer alive)
+
+
+def decode_plan(seq_lens_host, pool_or_geom, num_q_heads, bt_stride, num_entries_host=None, device=None,
+                stream=None):
+    """Build the step's plan on the host and copy it to the device (non_blocking on ``stream``).
+
+    ``pool_or_geom``: a KVPool (geometry taken from it) or a tuple (num_kv_heads, head_dim, block_size)."""
+    if isinstance(pool_or_geom, KVPool):
+        H, d, bs = pool_or_geom.num_kv_heads, pool_or_geom.head_dim, pool_or_geom.block_size
+        device = pool_or_geom.k.device if device is None else device
+    else:
+        H, d, bs = pool_or_geom
+    host = decode_plan_host(seq_lens_host, H, num_q_heads, d, bs, bt_stride, num_entries_host)
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    t = torch.from_numpy(host.view("uint8"))
+    s = torch.cuda.current_stream(dev) if stream is None else stream
+    with torch.cuda.stream(s):
+        d_t = torch.empty(t.numel() + 16, dtype=torch.uint8, device=dev)
+        off = (-d_t.data_ptr()) % 16
+        d_t = d_t[off:off + t.numel()]
+        d_t.copy_(t)     # synchronous-enough: the host buffer is pageable, the copy completes before return
+    return DecodePlan(host, d_t, t.numel())
+
+
+def decode_planned(pool: KVPool, block_tables, dirs, seq_lens, plan: DecodePlan, q, k_new=None, v_new=None,
+                   softmax_scale=None, out=None, peer_outs=(), ws=None, stream=None, pdl=False, fills=None,
+                   num_entries=None, kv_early=False):
+    """bkv_decode_planned: one layer's decode attention (or fused decode step when k_new/v_new
+    are given) with the step's host-built plan, in one kernel launch.  Returns out.
+    ``kv_early`` (with ``pdl``): BKV_FLAG_KV_EARLY -- the preceding kernel does not write this
+    pool's resident KV, so the first KV tiles are requested before the grid wait."""
+    p, m, out, scale, _, ws = _attn_args(pool, block_tables, dirs, seq_lens, q, softmax_scale,
+                                         out, None, ws, stream, fills, num_entries)
+    if plan.dev.device != q.device:
+        raise BkvError("plan was copied to another device")
+    kp = vp = None
+    if (k_new is None) != (v_new is None):
+        raise BkvError("k_new and v_new must both be given or both be None")
+    if k_new is not None:
+        _dev(k_new, "k_new", torch.bfloat16)
+        _dev(v_new, "v_new", torch.bfloat16)
+        shape = (q.shape[0], pool.num_kv_heads, pool.head_dim)
+        if tuple(k_new.shape) != shape or tuple(v_new.shape) != shape:
+            raise BkvError(f"k_new/v_new must be [B][H_kv][d] = {list(shape)}")
+        if not (k_new.is_contiguous() and v_new.is_contiguous()):
+            raise BkvError("k_new/v_new must be contiguous")
+        kp, vp = k_new.data_ptr(), v_new.data_ptr()
+    arr, n = _ptr_array(list(peer_outs))
+    rc = lib().bkv_decode_planned(
+        ctypes.byref(p), ctypes.byref(m), seq_lens.data_ptr(), plan.host.ctypes.data, plan.dev.data_ptr(),
+        kp, vp, q.data_ptr(), q.stride(0), q.stride(1), q.shape[1], float(scale), out.data_ptr(),
+        out.stride(0), out.stride(1), arr if n else None, n, ws.data_ptr(), ws.numel(),
+        (BKV_FLAG_PDL if pdl else 0) | (BKV_FLAG_KV_EARLY if (pdl and kv_early) else 0), _stream_ptr(stream))
+    _check(rc, "bkv_decode_planned")
     return out
 
 

@@ -6,11 +6,98 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <atomic>
+#include <map>
 #include <mutex>
 #include <vector>
 
 #include "../../include/bkv.h"
 #include "bkv_internal.h"
+
+namespace bkv {
+
+namespace {
+std::mutex g_sw_mu;
+DevSwitches g_sw;
+std::atomic<bool> g_sw_loaded{false};
+int env_int(const char *name, int dflt) {
+  const char *s = getenv(name);
+  return (s && *s) ? atoi(s) : dflt;
+}
+void load_switches() {
+  DevSwitches s;
+  s.slots = env_int("BKV_SLOTS", 2);
+  s.warps = env_int("BKV_WARPS", 0);
+  s.ctas_per_sm = env_int("BKV_CTAS_PER_SM", 1);
+  s.units_per_warp = env_int("BKV_UNITS_PER_WARP", 3);
+  s.min_split = env_int("BKV_MIN_SPLIT", -1);
+  s.small_plan = env_int("BKV_SMALL_PLAN", 1);
+  s.streamk = env_int("BKV_STREAMK", 1);
+  s.merge_warps = env_int("BKV_MERGE_WARPS", 8);
+  s.fused_merge = env_int("BKV_FUSED_MERGE", 0);
+  s.kv_combined = env_int("BKV_KV_COMBINED", 1);
+  s.mha_cuda_cores = env_int("BKV_MHA_CUDA_CORES", 0);
+  s.prefill_mma_sync = env_int("BKV_PREFILL_MMA_SYNC", 0);
+  s.prefill_qt = env_int("BKV_PREFILL_QT", 2);
+  s.mixed_overlap = env_int("BKV_MIXED_OVERLAP", 1);
+#ifdef BKV_DEV_TRACE
+  s.debug = env_int("BKV_DEBUG", 0);
+  s.trace = env_int("BKV_TRACE", 0);
+#else
+  s.debug = 0;   // work-skipping probes exist only in the dev trace build
+  s.trace = 0;
+#endif
+  s.planned_slots = env_int("BKV_PLANNED_SLOTS", 2);
+  s.planned_xmerge = env_int("BKV_PLANNED_XMERGE", 1);
+  g_sw = s;
+}
+}  // namespace
+
+const DevSwitches &dev_switches() {
+  if (!g_sw_loaded.load(std::memory_order_acquire)) {
+    std::lock_guard<std::mutex> lk(g_sw_mu);
+    if (!g_sw_loaded.load(std::memory_order_relaxed)) {
+      load_switches();
+      g_sw_loaded.store(true, std::memory_order_release);
+    }
+  }
+  return g_sw;
+}
+
+cudaError_t dev_props(DevProps *out) {
+  static std::mutex mu;
+  static std::map<int, DevProps> cache;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it == cache.end()) {
+    DevProps d;
+    if ((e = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&d.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess)
+      return e;
+    it = cache.emplace(dev, d).first;
+  }
+  *out = it->second;
+  return cudaSuccess;
+}
+
+cudaError_t ensure_dyn_smem(const void *func, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void *, int>, int> granted;   // (kernel, device) -> bytes
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  int &have = granted[std::make_pair(func, dev)];
+  if (bytes <= have) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
+
+}  // namespace bkv
 
 namespace {
 
@@ -108,8 +195,7 @@ bkv_status encode_pool_map(CUtensorMap *m, void *base, const bkv_kv_pool *pool, 
 // tiles of a chunk -- one TMA instruction per chunk instead of two.
 // Returns 0 (not applicable), 1 (K first) or 2 (V first, V below K).
 int encode_pool_map_kv(CUtensorMap *m, const bkv_kv_pool *pool) {
-  const char *e = getenv("BKV_KV_COMBINED");
-  if (e && atoi(e) == 0) return 0;
+  if (bkv::dev_switches().kv_combined == 0) return 0;
   auto fn = encode_fn();
   if (!fn) return 0;
   if (pool->stride_block != (int64_t)pool->num_kv_heads * pool->stride_head) return 0;
@@ -157,8 +243,7 @@ bkv_status ws_layout(int B, int Hq, int H, int D, WsLayout *w, bkv::DecodeLaunch
   w->ml = w->mcnt + up256((size_t)bkv::kMaxSeqs * bkv::kMaxKvHeads * 4);
   w->o = w->ml + up256((size_t)units * g * 2 * 4);
   w->trace = w->o + up256((size_t)units * g * D * 4);
-  const char *tr = getenv("BKV_TRACE");   // dev only: per-warp event log after the partials
-  w->trace_cap = (tr && *tr) ? atoi(tr) : 0;
+  w->trace_cap = bkv::dev_switches().trace;   // dev only (trace build): per-warp event log after the partials
   w->total = w->trace + up256((size_t)cfg->grid * cfg->warps * w->trace_cap * 16);
   return BKV_OK;
 }
@@ -181,7 +266,7 @@ const char *bkv_status_string(bkv_status s) {
 
 const char *bkv_last_error(void) { return g_err; }
 
-int32_t bkv_version(void) { return 200; }
+int32_t bkv_version(void) { return 300; }
 
 static bkv_status append_impl(const bkv_kv_pool *pool, const bkv_block_map *map,
                               const int32_t *seq_lens_before, const int32_t *cu_new_tokens,
@@ -398,8 +483,9 @@ static bkv_status decode_impl(const bkv_kv_pool *pool, const bkv_block_map *map,
   p.part_o = reinterpret_cast<float *>(ws + w.o);
   p.target_units = bkv::decode_target_units(cfg);
   p.min_split = bkv::decode_min_split(g);
-  p.small_plan = getenv("BKV_SMALL_PLAN") ? atoi(getenv("BKV_SMALL_PLAN")) : 1;
-  p.streamk = getenv("BKV_STREAMK") ? atoi(getenv("BKV_STREAMK")) : 1;   // 0 off, 1 auto, 2 always (dev)
+  const bkv::DevSwitches &sw = bkv::dev_switches();
+  p.small_plan = sw.small_plan;
+  p.streamk = sw.streamk;   // 0 off, 1 auto, 2 always (dev)
   p.units_max = w.units_max;
   p.slots = slots;
   p.q_bytes = qb;
@@ -408,8 +494,7 @@ static bkv_status decode_impl(const bkv_kv_pool *pool, const bkv_block_map *map,
   // mixed dispatch: the preceding kernel is our own prefill kernel, which
   // writes only the prefill rows of `out` and was itself launched in stream
   // order -- the decode part may run alongside its tail (no grid wait)
-  const char *ov = getenv("BKV_MIXED_OVERLAP");   // dev: 0 = keep the grid wait
-  p.pdl_nowait = (p.pdl && after_own_prefill && !(ov && atoi(ov) == 0)) ? 1 : 0;
+  p.pdl_nowait = (p.pdl && after_own_prefill && sw.mixed_overlap != 0) ? 1 : 0;   // dev: 0 = keep the grid wait
   p.k_new = static_cast<const uint16_t *>(k_new);
   p.v_new = static_cast<const uint16_t *>(v_new);
   p.k_pool = static_cast<uint16_t *>(pool->k);
@@ -423,7 +508,7 @@ static bkv_status decode_impl(const bkv_kv_pool *pool, const bkv_block_map *map,
   // split merge: separate stream-ordered merge_kernel by default; in-kernel last-arriver merge
   // (opt-in, BKV_FUSED_MERGE=1: measured slower -- the last-arriving warp merges all g rows
   // of a GQA group serially at the tail, e.g. Llama-70B TP1 115 -> 149 us per layer)
-  p.fused_merge = (n_peers == 0 && getenv("BKV_FUSED_MERGE") && atoi(getenv("BKV_FUSED_MERGE"))) ? 1 : 0;
+  p.fused_merge = (n_peers == 0 && sw.fused_merge) ? 1 : 0;
   if (p.fused_merge) p.streamk = 0;   // the in-kernel merge knows only the split plan
   for (int k = 0; k < bkv::kMaxPeers; ++k) {
     p.peer_out[k] = k < n_peers ? static_cast<uint16_t *>(peer_outs[k]) : nullptr;
@@ -431,7 +516,7 @@ static bkv_status decode_impl(const bkv_kv_pool *pool, const bkv_block_map *map,
       return fail(BKV_ERR_INVALID_ARGUMENT, "peer output %d is NULL or not 16-byte aligned", k);
   }
   p.kv_mode = kv_mode;
-  p.debug_flags = getenv("BKV_DEBUG") ? atoi(getenv("BKV_DEBUG")) : 0;
+  p.debug_flags = sw.debug;
   p.trace_cap = w.trace_cap;
   p.trace = w.trace_cap ? reinterpret_cast<unsigned long long *>(ws + w.trace) : nullptr;
   cudaError_t e = bkv::launch_decode(tmK, tmV, p, D, cfg, reinterpret_cast<cudaStream_t>(stream));
@@ -751,6 +836,199 @@ bkv_status bkv_validate_block_map_host(const bkv_block_map *map, const int32_t *
       }
     }
   }
+  return BKV_OK;
+}
+
+// ------------------------------------------------------------ planned decode
+void bkv_reload_dev_switches(void) {
+  std::lock_guard<std::mutex> lk(bkv::g_sw_mu);
+  bkv::load_switches();
+  bkv::g_sw_loaded.store(true, std::memory_order_release);
+}
+
+// SM count a plan is made for: the caller's, or the current device's (0)
+static bkv_status plan_sms(int32_t num_sms, int *sms) {
+  if (num_sms < 0 || num_sms > 4096) return fail(BKV_ERR_INVALID_ARGUMENT, "num_sms %d outside [0, 4096]", num_sms);
+  if (num_sms > 0) {
+    *sms = num_sms;
+    return BKV_OK;
+  }
+  bkv::DevProps dp;
+  cudaError_t e = bkv::dev_props(&dp);
+  if (e != cudaSuccess) return cuda_fail(e, "querying the device (pass num_sms to plan without one)");
+  *sms = dp.sms;
+  return BKV_OK;
+}
+
+size_t bkv_decode_plan_bytes(int32_t num_seqs, int32_t num_kv_heads, int32_t num_sms) {
+  if (num_seqs < 0 || num_kv_heads <= 0) {
+    fail(BKV_ERR_INVALID_ARGUMENT, "num_seqs < 0 or num_kv_heads <= 0");
+    return 0;
+  }
+  int sms = 0;
+  if (plan_sms(num_sms, &sms)) return 0;
+  return 4 * bkv::plan_words_bound(num_seqs, num_kv_heads, sms, bkv::kPlannedWarps);
+}
+
+bkv_status bkv_decode_plan(const int32_t *seq_lens, const int32_t *num_entries, int32_t num_seqs,
+                           int32_t bt_stride, int32_t num_kv_heads, int32_t num_q_heads, int32_t head_dim,
+                           int32_t block_size, int32_t num_sms, void *plan, size_t plan_bytes,
+                           size_t *plan_bytes_used) {
+  if (num_seqs < 0 || (num_seqs > 0 && !seq_lens) || !plan)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "seq_lens/plan is NULL or num_seqs < 0");
+  if (num_seqs > bkv::kMaxSeqs) return fail(BKV_ERR_UNSUPPORTED, "num_seqs %d > %d", num_seqs, bkv::kMaxSeqs);
+  if (num_kv_heads <= 0 || num_kv_heads > bkv::kMaxKvHeads)
+    return fail(BKV_ERR_UNSUPPORTED, "num_kv_heads %d outside [1, %d]", num_kv_heads, bkv::kMaxKvHeads);
+  if (num_q_heads <= 0 || num_q_heads % num_kv_heads)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "num_q_heads %d is not a multiple of num_kv_heads %d", num_q_heads,
+                num_kv_heads);
+  const int g = num_q_heads / num_kv_heads;
+  if (g > bkv::kMaxGroup) return fail(BKV_ERR_UNSUPPORTED, "group %d > %d", g, bkv::kMaxGroup);
+  if (head_dim != 64 && head_dim != 128) return fail(BKV_ERR_UNSUPPORTED, "head_dim %d not in {64, 128}", head_dim);
+  if (block_size != 16 && block_size != 32)
+    return fail(BKV_ERR_UNSUPPORTED, "block_size %d not in {16, 32}", block_size);
+  if (bt_stride <= 0 || bt_stride > bkv::kMaxEntries)
+    return fail(BKV_ERR_UNSUPPORTED, "bt_stride %d outside [1, %d]", bt_stride, bkv::kMaxEntries);
+  if ((reinterpret_cast<uintptr_t>(plan) & 15u) != 0) return fail(BKV_ERR_INVALID_ARGUMENT, "plan must be 16-byte aligned");
+  int sms = 0;
+  bkv_status st = plan_sms(num_sms, &sms);
+  if (st) return st;
+  size_t used = 0;
+  const char *msg = bkv::build_plan(seq_lens, num_entries, num_seqs, num_kv_heads, g, head_dim, block_size,
+                                    bt_stride, sms, bkv::kPlannedWarps, static_cast<int32_t *>(plan),
+                                    plan_bytes / 4, &used);
+  if (plan_bytes_used) *plan_bytes_used = used * 4;
+  if (msg) return fail(strstr(msg, "too small") ? BKV_ERR_WORKSPACE_TOO_SMALL : BKV_ERR_INVALID_ARGUMENT,
+                       "bkv_decode_plan: %s", msg);
+  return BKV_OK;
+}
+
+bkv_status bkv_decode_planned(const bkv_kv_pool *pool, const bkv_block_map *map, const int32_t *seq_lens,
+                              const void *plan_host, const void *plan_dev, const void *k_new,
+                              const void *v_new, const void *q, int64_t q_stride_seq, int64_t q_stride_head,
+                              int32_t num_q_heads, float softmax_scale, void *out, int64_t o_stride_seq,
+                              int64_t o_stride_head, void *const *peer_outs, int32_t n_peers,
+                              void *workspace, size_t workspace_bytes, uint32_t flags, bkv_stream_t stream) {
+  if (flags & ~(BKV_FLAG_PDL | BKV_FLAG_KV_EARLY)) return fail(BKV_ERR_INVALID_ARGUMENT, "unknown flags 0x%x", flags);
+  if ((flags & BKV_FLAG_KV_EARLY) && !(flags & BKV_FLAG_PDL))
+    return fail(BKV_ERR_INVALID_ARGUMENT, "BKV_FLAG_KV_EARLY needs BKV_FLAG_PDL");
+  bkv_status s = check_pool(pool);
+  if (s) return s;
+  if ((s = check_map(map))) return s;
+  if (!plan_host || !plan_dev) return fail(BKV_ERR_INVALID_ARGUMENT, "plan_host/plan_dev is NULL");
+  if ((reinterpret_cast<uintptr_t>(plan_dev) & 15u) != 0)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "plan_dev must be 16-byte aligned");
+  const bkv::PlanHeader *hd = static_cast<const bkv::PlanHeader *>(plan_host);
+  const int B = map->num_seqs, H = pool->num_kv_heads, D = pool->head_dim;
+  if (hd->magic != bkv::kPlanMagic || hd->version != bkv::kPlanVersion)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "plan_host is not a bkv_decode_plan buffer of this library version");
+  if (B == 0) return BKV_OK;
+  if ((k_new == nullptr) != (v_new == nullptr))
+    return fail(BKV_ERR_INVALID_ARGUMENT, "k_new and v_new must both be set or both be NULL");
+  if (k_new && (!aligned16(k_new) || !aligned16(v_new)))
+    return fail(BKV_ERR_INVALID_ARGUMENT, "k_new/v_new must be 16-byte aligned");
+  if (!seq_lens || !q || !out || !workspace)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "seq_lens/q/out/workspace is NULL");
+  if (num_q_heads <= 0 || num_q_heads % H)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "num_q_heads %d is not a multiple of num_kv_heads %d", num_q_heads, H);
+  const int g = num_q_heads / H;
+  bkv::DevProps dp;
+  cudaError_t e = bkv::dev_props(&dp);
+  if (e != cudaSuccess) return cuda_fail(e, "querying the device");
+  if (hd->B != B || hd->H != H || hd->g != g || hd->D != D || hd->bs != pool->block_size ||
+      hd->general != (map->fills ? 1 : 0) || hd->max_entries > map->bt_stride)
+    return fail(BKV_ERR_INVALID_ARGUMENT,
+                "plan built for (B %d, H %d, g %d, d %d, bs %d, general %d, entries %d) does not match the call "
+                "(B %d, H %d, g %d, d %d, bs %d, general %d, bt_stride %d)",
+                hd->B, hd->H, hd->g, hd->D, hd->bs, hd->general, hd->max_entries, B, H, g, D, pool->block_size,
+                map->fills ? 1 : 0, map->bt_stride);
+  if ((int64_t)B * num_q_heads > (int64_t)bkv::kMaxSeqs * bkv::kMaxKvHeads)
+    return fail(BKV_ERR_UNSUPPORTED, "num_seqs x num_q_heads %lld exceeds the workspace's %d row counters",
+                (long long)B * num_q_heads, bkv::kMaxSeqs * bkv::kMaxKvHeads);
+  if (hd->grid != dp.sms || hd->warps != bkv::kPlannedWarps)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "plan built for %d x %d warps, this device runs %d x %d", hd->grid,
+                hd->warps, dp.sms, bkv::kPlannedWarps);
+  if (!aligned16(q) || !aligned16(out) || q_stride_seq % 8 || q_stride_head % 8 || o_stride_seq % 8 ||
+      o_stride_head % 8)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "q/out must be 16-byte aligned with strides multiple of 8");
+  if (!(softmax_scale == softmax_scale) || isinf(softmax_scale))
+    return fail(BKV_ERR_INVALID_ARGUMENT, "softmax_scale must be finite");
+  if ((reinterpret_cast<uintptr_t>(workspace) & 255u) != 0)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+  if (n_peers < 0 || n_peers > bkv::kMaxPeers)
+    return fail(BKV_ERR_UNSUPPORTED, "n_peers %d outside [0, %d]", n_peers, bkv::kMaxPeers);
+  if (n_peers > 0 && !peer_outs) return fail(BKV_ERR_INVALID_ARGUMENT, "peer_outs is NULL");
+  WsLayout w;
+  bkv::DecodeLaunch cfg;
+  int slots0, qb;
+  if ((s = ws_layout(B, num_q_heads, H, D, &w, &cfg, &slots0, &qb))) return s;
+  if (workspace_bytes < w.total)
+    return fail(BKV_ERR_WORKSPACE_TOO_SMALL, "workspace %zu < required %zu bytes", workspace_bytes, w.total);
+  if ((size_t)2 * hd->grid * bkv::planned_piece_floats(g, D) * 4 > w.trace - w.o)
+    return fail(BKV_ERR_WORKSPACE_TOO_SMALL, "workspace partial region too small for the plan");
+  const int S = std::max(1, std::min(4, bkv::dev_switches().planned_slots));
+  const int smem = bkv::planned_smem_bytes(D, g, S);
+  if (smem > dp.smem_optin) return fail(BKV_ERR_UNSUPPORTED, "planned kernel needs %d B of shared memory", smem);
+  CUtensorMap tmK, tmV;
+  if ((s = encode_pool_map(&tmK, pool->k, pool))) return s;
+  if ((s = encode_pool_map(&tmV, pool->v, pool))) return s;
+  CUtensorMap tmKV;
+  const int kv_mode = encode_pool_map_kv(&tmKV, pool);
+  if (kv_mode) tmK = tmKV;
+  uint8_t *ws = static_cast<uint8_t *>(workspace);
+  const int32_t *pw = static_cast<const int32_t *>(plan_dev);
+  bkv::PlannedParams p;
+  p.bt = map->block_tables;
+  p.bt_stride = map->bt_stride;
+  p.dirs = map->dirs;
+  p.dir_rs = map->dir_row_stride;
+  p.dir_cs = map->dir_col_stride;
+  p.seq_lens = seq_lens;
+  p.fills = map->fills;
+  p.fill_rs = map->fill_row_stride;
+  p.nent = map->num_entries;
+  p.B = B;
+  p.H = H;
+  p.bs = pool->block_size;
+  p.g = g;
+  p.q = static_cast<const uint16_t *>(q);
+  p.q_ss = q_stride_seq;
+  p.q_sh = q_stride_head;
+  p.out = static_cast<uint16_t *>(out);
+  p.o_ss = o_stride_seq;
+  p.o_sh = o_stride_head;
+  p.scale_log2 = softmax_scale * 1.4426950408889634f;
+  p.wseg = pw + hd->off_wseg;
+  p.segs = reinterpret_cast<const int4 *>(pw + hd->off_segs);
+  p.ctask = pw + hd->off_ctask;
+  p.tasks = reinterpret_cast<const int4 *>(pw + hd->off_tasks);
+  p.zero = pw + hd->off_zero;
+  p.n_zero = hd->n_zero;
+  p.xrows = reinterpret_cast<const int4 *>(pw + hd->off_xrows);
+  p.n_xrows = hd->n_xrows;
+  p.xmerge = bkv::dev_switches().planned_xmerge;
+  p.cnt = reinterpret_cast<int *>(ws + w.mcnt);
+  p.gpiece = reinterpret_cast<float *>(ws + w.o);
+  p.slots = S;
+  p.pdl = (flags & BKV_FLAG_PDL) ? 1 : 0;
+  p.kv_early = (flags & BKV_FLAG_KV_EARLY) ? 1 : 0;
+  p.kv_mode = kv_mode;
+  p.k_new = static_cast<const uint16_t *>(k_new);
+  p.v_new = static_cast<const uint16_t *>(v_new);
+  p.k_pool = static_cast<uint16_t *>(pool->k);
+  p.v_pool = static_cast<uint16_t *>(pool->v);
+  p.pool_sb = pool->stride_block;
+  p.pool_sh = pool->stride_head;
+  p.pool_ss = pool->stride_slot;
+  p.n_peers = n_peers;
+  for (int k = 0; k < bkv::kMaxPeers; ++k) {
+    p.peer_out[k] = k < n_peers ? static_cast<uint16_t *>(peer_outs[k]) : nullptr;
+    if (k < n_peers && (!peer_outs[k] || !aligned16(peer_outs[k])))
+      return fail(BKV_ERR_INVALID_ARGUMENT, "peer output %d is NULL or not 16-byte aligned", k);
+  }
+  p.trace = w.trace_cap >= 8 ? reinterpret_cast<unsigned long long *>(ws + w.trace) : nullptr;
+  e = bkv::launch_planned(tmK, tmV, p, D, hd->grid, smem, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "planned decode launch");
   return BKV_OK;
 }
 

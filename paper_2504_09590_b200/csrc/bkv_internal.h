@@ -141,6 +141,106 @@ struct PeerBarrierParams {
 cudaError_t launch_peer_barrier(const PeerBarrierParams &p, cudaStream_t s);
 constexpr int kMaxPeers = 8;
 
+// ------------------------------------ planned decode (static split plan)
+// A decode plan is built on the HOST once per step from the scheduler's host
+// seq_lens (bkv_decode_plan, csrc/decode_plan.cu) and reused by every layer's
+// bkv_decode_planned call ("computed on device or host").
+// Buffer = int32 words: PlanHeader, then the arrays at the header's offsets.
+constexpr int32_t kPlanMagic = 0x504b5642;   // "BVKP"
+constexpr int32_t kPlanVersion = 1;
+constexpr int kPlanSplitBit = 30;            // seg.w = e1 | split << 30
+struct PlanHeader {
+  int32_t magic, version, words;             // words = total int32 words of the plan
+  int32_t B, H, g, D, bs, general;           // geometry the plan was built for
+  int32_t grid, warps;                       // launch it was built for (grid = SMs, one CTA each)
+  int32_t P;                                 // blocks per warp range
+  int32_t n_segs, n_tasks, n_zero;
+  int32_t total;                             // N = sum_r nb_r * H (blocks x kv heads)
+  int32_t off_wseg;                          // int32 [grid*warps + 1]: segments of warp w
+  int32_t off_segs;                          // 2 x int4 [n_segs] {r, h, e0, e1 | split << 30}, {L, nb, 0, 0}
+  int32_t off_ctask;                         // int32 [grid + 1]: merge tasks of CTA c
+  int32_t off_tasks;                         // int4  [2 * n_tasks] (see PlanTask)
+  int32_t off_zero;                          // int32 [2 * n_zero] {r, h}: rows with no tokens
+  int32_t max_pieces;                        // largest n of a cross-CTA row
+  int32_t max_entries;                       // bt_stride the plan was checked against
+  int32_t off_xrows, n_xrows;                // int4 [n_xrows] {r, h, c0, n | flag0 << 16}: rows cut across CTAs
+  int32_t reserved[7];
+};
+static_assert(sizeof(PlanHeader) == 32 * 4, "plan header is 32 words");
+// A merge task (two int4) combines the pieces of one (request r, kv head h) row
+// that lie in warps wa..wb of one CTA (piece k in warp wa+k: shared-memory slot
+// wa_slot for k = 0, slot 0 otherwise).  mode 0: the row lies in this CTA only
+// -> bf16 output.  mode 1: the row crosses CTAs c0 .. c0+n-1; this CTA's
+// combined piece goes to global slot gslot and the last CTA to arrive merges
+// the n pieces in CTA order (global slot of piece k: k ? 2(c0+k) : 2 c0 + flag0).
+struct PlanTask {
+  int32_t r, h, warps, mode;   // warps = wa | wb << 8 | wa_slot << 16 (CTA-local warp ids)
+  int32_t c0, n, flag0, gslot;
+};
+size_t plan_words_bound(int B, int H, int grid, int warps);
+const char *build_plan(const int32_t *seq_lens, const int32_t *num_entries, int B, int H, int g, int D,
+                       int bs, int max_entries, int grid, int warps, int32_t *out, size_t out_words,
+                       size_t *used_words);
+constexpr int kPlannedWarps = 8;             // warps per CTA of the planned kernel
+
+struct PlannedParams {
+  const int32_t *bt;
+  int bt_stride;
+  const uint8_t *dirs;
+  int dir_rs, dir_cs;
+  const int32_t *seq_lens;
+  const uint8_t *fills;  // general map (f3) or nullptr
+  int fill_rs;
+  const int32_t *nent;
+  int B, H, bs, g;
+  const uint16_t *q;
+  int64_t q_ss, q_sh;
+  uint16_t *out;
+  int64_t o_ss, o_sh;
+  float scale_log2;
+  // the plan (device copy of the host-built buffer)
+  const int32_t *wseg;   // [W + 1]
+  const int4 *segs;      // 2 per segment: {r, h, e0, e1 | split << 30}, {L_r, entries of r, 0, 0}
+  const int32_t *ctask;  // [grid + 1]
+  const int4 *tasks;     // 2 per task (PlanTask)
+  const int32_t *zero;   // {r, h} pairs
+  int n_zero;
+  const int4 *xrows;     // rows cut across CTAs (merged by planned_xmerge_kernel when xmerge == 1)
+  int n_xrows;
+  int xmerge;            // 0: last-arriver merge inside the kernel; 1: separate stream-ordered merge kernel
+  int *cnt;              // [B*H] cross-CTA arrival counters (self-cleaning, zero at rest)
+  float *gpiece;         // [2*grid][g*(D+2)] cross-CTA pieces
+  int slots, pdl, kv_mode;
+  int kv_early;          // BKV_FLAG_KV_EARLY: first ring tiles requested before the PDL grid wait
+  const uint16_t *k_new, *v_new;   // fused decode step (f2), nullptr otherwise
+  uint16_t *k_pool, *v_pool;
+  int64_t pool_sb, pool_sh, pool_ss;
+  uint16_t *peer_out[8];
+  int n_peers;
+  unsigned long long *trace;   // dev only (trace build, BKV_TRACE >= 4): 8 %globaltimer stamps per warp
+};
+int planned_smem_bytes(int head_dim, int group, int slots);
+int planned_piece_floats(int group, int head_dim);   // floats per cross-CTA piece slot
+cudaError_t launch_planned(const CUtensorMap &tmK, const CUtensorMap &tmV, const PlannedParams &p,
+                           int head_dim, int grid, int smem_bytes, cudaStream_t s);
+// Developer switches (DESIGN.md §7 table), read from the environment ONCE per
+// process and again only on bkv_reload_dev_switches().  BKV_DEBUG (probes that
+// skip work) is honoured only by a BKV_DEV_TRACE build.
+struct DevSwitches {
+  int slots, warps, ctas_per_sm, units_per_warp, min_split /* -1: default */, small_plan, streamk;
+  int merge_warps, fused_merge, kv_combined, mha_cuda_cores, prefill_mma_sync, prefill_qt;
+  int mixed_overlap, debug, trace, planned_slots, planned_xmerge;
+};
+const DevSwitches &dev_switches();
+// Immutable per-device properties (cached per device).
+struct DevProps {
+  int sms, smem_optin;
+};
+cudaError_t dev_props(DevProps *out);
+// Opt a kernel in to `bytes` of dynamic shared memory on the CURRENT device
+// (per device and thread-safe: cudaFuncSetAttribute applies to one device).
+cudaError_t ensure_dyn_smem(const void *func, int bytes);
+
 constexpr int kMaxSeqs = 2048;  // plan arrays live in shared memory
 constexpr int kMaxGroup = 16;   // GQA rows per MMA tile
 constexpr int kMaxKvHeads = 128; // per rank; sizes the fixed counter region of the workspace

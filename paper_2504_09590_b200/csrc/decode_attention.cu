@@ -1256,27 +1256,19 @@ __global__ void __launch_bounds__(256) merge_kernel(const DecodeParams p) {
 }
 
 // ----------------------------------------------------------------- host
-static int env_int(const char *name, int dflt) {
-  const char *s = getenv(name);
-  return (s && *s) ? atoi(s) : dflt;
-}
-
 // g = 1 runs on the tensor-core kernel too (one useful n column of 8, but half
 // the instructions per chunk of the CUDA-core kernel: no bf16 unpacking; measured
 // opt13b TP1 88.8% -> 92.7% of HBM peak).  BKV_MHA_CUDA_CORES=1 (dev) keeps the
 // CUDA-core kernel selectable.
-static bool mha_on_mma() { return env_int("BKV_MHA_CUDA_CORES", 0) == 0; }
+static bool mha_on_mma() { return dev_switches().mha_cuda_cores == 0; }
 
 cudaError_t decode_config(int head_dim, int group, int num_seqs, DecodeLaunch *cfg, int *slots,
                           int *q_bytes) {
-  int dev = 0, sms = 0, smem_optin = 0;
-  cudaError_t e = cudaGetDevice(&dev);
+  DevProps dp;
+  cudaError_t e = dev_props(&dp);
   if (e != cudaSuccess) return e;
-  e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (e != cudaSuccess) return e;
-  e = cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  if (e != cudaSuccess) return e;
-  int S = env_int("BKV_SLOTS", 2);
+  const DevSwitches &sw = dev_switches();
+  int S = sw.slots;
   const int slot_bytes = 2 * (head_dim / 64) * 2048;
   const int qb = 0;   // q is read from global (L2-prefetched), no shared-memory ring
   auto need = [&](int w, int s) {
@@ -1284,11 +1276,11 @@ cudaError_t decode_config(int head_dim, int group, int num_seqs, DecodeLaunch *c
            4 * (num_seqs + 1) * (int)sizeof(int) + 2 * ((num_seqs + 3) & ~3) * 4 + 256;
   };
   const bool mma = group > 1 || mha_on_mma();
-  int W = env_int("BKV_WARPS", mma ? 8 : 12);   // measured best: MMA kernels 8, CUDA-core MHA 12
-  W = std::min(W, mma ? 8 : 12);                 // = the kernels' __launch_bounds__
-  while (W > 4 && need(W, S) > smem_optin - 1024) W -= 4;
-  while (S > 1 && need(W, S) > smem_optin - 1024) --S;
-  cfg->grid = sms * env_int("BKV_CTAS_PER_SM", 1);
+  int W = sw.warps > 0 ? sw.warps : (mma ? 8 : 12);   // measured best: MMA kernels 8, CUDA-core MHA 12
+  W = std::min(W, mma ? 8 : 12);                       // = the kernels' __launch_bounds__
+  while (W > 4 && need(W, S) > dp.smem_optin - 1024) W -= 4;
+  while (S > 1 && need(W, S) > dp.smem_optin - 1024) --S;
+  cfg->grid = dp.sms * sw.ctas_per_sm;
   cfg->warps = W;
   cfg->smem_bytes = need(W, S);
   *slots = S;
@@ -1297,22 +1289,20 @@ cudaError_t decode_config(int head_dim, int group, int num_seqs, DecodeLaunch *c
 }
 
 int decode_target_units(const DecodeLaunch &cfg) {
-  return env_int("BKV_UNITS_PER_WARP", 3) * cfg.grid * cfg.warps;
+  return dev_switches().units_per_warp * cfg.grid * cfg.warps;
 }
 
 int decode_min_split(int group) {
-  return env_int("BKV_MIN_SPLIT", group > 1 || mha_on_mma() ? 16 : 4);
+  const int ms = dev_switches().min_split;
+  return ms >= 0 ? ms : (group > 1 || mha_on_mma() ? 16 : 4);
 }
 
 template <int D, int KIND>
 static cudaError_t launch_t(const CUtensorMap &tmK, const CUtensorMap &tmV, const DecodeParams &p,
                             const DecodeLaunch &cfg, cudaStream_t s) {
-  static int configured = 0;  // max dynamic smem already granted to this instantiation
-  if (cfg.smem_bytes > configured) {
-    cudaError_t e = cudaFuncSetAttribute(decode_kernel<D, KIND>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, cfg.smem_bytes);
+  {
+    cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void *>(decode_kernel<D, KIND>), cfg.smem_bytes);
     if (e != cudaSuccess) return e;
-    configured = cfg.smem_bytes;
   }
   cudaLaunchConfig_t lc = {};
   cudaLaunchAttribute attr[1];
@@ -1334,7 +1324,7 @@ static cudaError_t launch_t(const CUtensorMap &tmK, const CUtensorMap &tmV, cons
   // 114 vs 124 us, TP8 26 vs 45 us per layer)
   const int warps = p.B * p.H * p.g;
   cudaLaunchConfig_t lm = {};
-  const int mw = std::max(1, std::min(8, env_int("BKV_MERGE_WARPS", 8)));   // warps per merge CTA
+  const int mw = std::max(1, std::min(8, dev_switches().merge_warps));   // warps per merge CTA
   lm.gridDim = dim3((p.debug_flags & 2) ? 1 : (warps + mw - 1) / mw);   // dev: 2 = re-arm only (times the merge)
   lm.blockDim = dim3(32 * mw);
   lm.stream = s;

@@ -151,13 +151,10 @@ __global__ void __launch_bounds__(256) kv_append_general_kernel(AppendParams p) 
 
 template <int D>
 static cudaError_t launch_general(const AppendParams &p, cudaStream_t s) {
-  static int configured = 0;   // dynamic smem already granted
   const int smem = 4 * (p.max_entries + 1);
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(kv_append_general_kernel<D>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (smem > 48 * 1024) {
+    cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void *>(kv_append_general_kernel<D>), smem);
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   kv_append_general_kernel<D><<<p.B, 256, smem, s>>>(p);
   return cudaGetLastError();

@@ -347,8 +347,7 @@ __global__ void __launch_bounds__(32 * (kConsumerWarps + 1), 1)
 // prompt prefills 160 vs 140 TF/s for this mma.sync kernel, which stays the
 // head_dim-64 path and is selectable for 128 with BKV_PREFILL_MMA_SYNC=1 (dev A/B).
 bool prefill_uses_tc(int head_dim) {
-  const char *e = getenv("BKV_PREFILL_MMA_SYNC");
-  return head_dim == 128 && !(e && atoi(e) != 0);
+  return head_dim == 128 && dev_switches().prefill_mma_sync == 0;
 }
 
 int prefill_smem_bytes(int head_dim) {
@@ -359,11 +358,9 @@ template <int D>
 static cudaError_t launch_prefill_t(const CUtensorMap &tmK, const CUtensorMap &tmV,
                                     const PrefillParams &p, int max_q_len, cudaStream_t s) {
   const int smem = prefill_smem_bytes(D);
-  static int configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(prefill_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  {
+    cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void *>(prefill_kernel<D>), smem);
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   const long long tiles = (static_cast<long long>(max_q_len) * p.g + kRowsPerTile - 1) / kRowsPerTile;
   dim3 grid(static_cast<unsigned>(tiles), p.H, p.B);

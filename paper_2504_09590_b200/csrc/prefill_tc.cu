@@ -641,18 +641,19 @@ template <int QT>
 static cudaError_t launch_tc(const CUtensorMap &tmK, const CUtensorMap &tmV, const PrefillParams &p,
                              int max_q_len, cudaStream_t s) {
   const int smem = tc_smem_bytes<QT>();
-  static int configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(prefill_tc_kernel<QT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  {
+    cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void *>(prefill_tc_kernel<QT>), smem);
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   const long long tiles = (static_cast<long long>(max_q_len) * p.g + kTcRows - 1) / kTcRows;
   PrefillParams q = p;
   q.tiles_max = static_cast<int>(tiles);
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  DevProps dp;
+  {
+    cudaError_t e = dev_props(&dp);
+    if (e != cudaSuccess) return e;
+  }
+  const int sms = dp.sms;
   const long long items = ((tiles + QT - 1) / QT) * p.H * p.B;
   const int grid = static_cast<int>(items < sms ? items : sms);   // one persistent CTA per SM
   prefill_tc_kernel<QT><<<grid, 32 * (4 * QT + 3), smem, s>>>(tmK, tmV, q);
@@ -663,8 +664,7 @@ cudaError_t launch_prefill_tc(const CUtensorMap &tmK, const CUtensorMap &tmV, co
                               int max_q_len, cudaStream_t s) {
   // default: two ping-pong 128-row query tiles per CTA share every K/V tile (Llama-70B
   // TP1 prefill rows 191 -> 233 TF/s); BKV_PREFILL_QT=1 (dev) runs one tile per CTA
-  const char *e = getenv("BKV_PREFILL_QT");
-  if (e && atoi(e) == 1) return launch_tc<1>(tmK, tmV, p, max_q_len, s);
+  if (dev_switches().prefill_qt == 1) return launch_tc<1>(tmK, tmV, p, max_q_len, s);
   return launch_tc<2>(tmK, tmV, p, max_q_len, s);
 }
 

@@ -21,9 +21,17 @@ def run(cfg, tp=1, layers=8, iters=20, mode="attn"):
     ws = bkv.workspace(lay.batch, Hq, H, d)
     kn = torch.randn(lay.batch, H, d, device=dev).to(torch.bfloat16)
     vn = torch.randn(lay.batch, H, d, device=dev).to(torch.bfloat16)
+    plan = bkv.decode_plan(lay.lens, pools[0], Hq, lay.block_tables.shape[1]) if mode.startswith("planned") else None
     def body():
         for p in pools:
-            if mode == "fused":
+            if mode == "planned":
+                bkv.decode_planned(p, bt, dirs, lens, plan, q, k_new=kn, v_new=vn, out=out, ws=ws, pdl=True)
+            elif mode == "planned_early":
+                bkv.decode_planned(p, bt, dirs, lens, plan, q, k_new=kn, v_new=vn, out=out, ws=ws, pdl=True,
+                                   kv_early=True)
+            elif mode == "planned_attn":
+                bkv.decode_planned(p, bt, dirs, lens, plan, q, out=out, ws=ws, pdl=True)
+            elif mode == "fused":
                 bkv.decode_step(p, bt, dirs, lens, kn, vn, q, out=out, ws=ws, pdl=True)
             else:
                 bkv.paged_decode_attention(p, bt, dirs, lens, q, out=out, ws=ws, pdl=True)

@@ -92,4 +92,4 @@ def test_status_strings_cover_every_code():
     names = [L.bkv_status_string(c).decode() for c in range(6)]
     assert names == ["BKV_OK", "BKV_ERR_INVALID_ARGUMENT", "BKV_ERR_UNSUPPORTED",
                      "BKV_ERR_WORKSPACE_TOO_SMALL", "BKV_ERR_LAYOUT", "BKV_ERR_CUDA"]
-    assert L.bkv_version() == 200
+    assert L.bkv_version() == 300
