@@ -2,18 +2,24 @@
 """Benchmark of the BROS bidirectional paged decode-attention hot path on B200.
 
 One STEP = one decode iteration of the attention path over ALL layers of the
-model shape: per layer, kv_append of the batch's new tokens
-and paged decode attention over the bidirectional block map (a3-a5); at N > 1
-GPUs each rank owns a head shard (tensor parallel by kv head) and the
-head-major outputs of every layer are reassembled with ONE NCCL all-gather per
-step (a6; ``--gather layer``: one per layer, ``--reassembly p2p``: peer stores).
+model shape: per layer, this step's new K/V rows are appended into their
+bidirectional slots and every request attends over its context (SURVEY §8(a)
+a1-a5), fused in one planned-decode call (bkv_decode_planned: the decode kernel
+with the append fused in, plus the light cross-CTA merge kernel); the split plan
+is built on the host once per step (bkv_decode_plan) and shared by all layers.
+At N > 1 GPUs each rank owns a head shard (tensor parallel by kv head)
+and the head-major outputs of every layer are reassembled with ONE NCCL
+all-gather per step (a6; ``--gather layer``: one per layer; ``--reassembly
+p2p``: stores into the peers' outputs over NVLink + a peer barrier, f2).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config opt13b] [--impl reference]
 
 Prints ONE JSON line (rank 0).  ``value`` = decode tokens/s of the whole job
 (batch tokens per step / device step time, max over ranks).  Per-layer KV data
-is far larger than L2 and every step sweeps every layer's pool once, so no
-explicit L2 flush is needed ("inputs larger than L2").
+is far larger than L2 and every step sweeps every layer's pool once ("inputs
+larger than L2").  At N = 1 the line also carries ``shards``: the per-layer
+time of every head shard the paper runs (Llama-2-70B TP1/2/4/8, OPT-13B
+TP2/4/8, OPT-30B TP4) on this GPU, median / p10 / p90 over 60 graph replays.
 """
 from __future__ import annotations
 
@@ -24,7 +30,6 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 import numpy as np
@@ -39,6 +44,11 @@ WORKLOADS = {
     "llama70b": "Llama-2-70B shape: 64 Q / 8 KV heads (GQA 8) x d128, bs16, ShareGPT-like lengths, batch 256, 80 layers",
     "tiny": "tiny: 4 heads x d64, bs16, 8 requests (4 RT + 4 BE) sharing blocks, ctx <= 256, 1 layer",
 }
+# the head shards of the paper's deployments and their neighbours, measured at N = 1
+SHARDS = [("llama70b", 1), ("llama70b", 2), ("llama70b", 4), ("llama70b", 8),
+          ("opt13b", 2), ("opt13b", 4), ("opt13b", 8), ("opt30b", 4)]
+L2_BYTES = 126 * 2 ** 20
+PLANNED_DYNAMIC_P = 128   # bkv_decode_planned's default switch to the dynamic schedule (include/bkv.h)
 
 
 # ------------------------------------------------------------------ helpers
@@ -60,13 +70,36 @@ def load_peaks():
 
 
 def ncu_traffic(key):
-    """dram read+write bytes per attention launch from the committed ncu capture."""
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    """DRAM read+write bytes per layer launch pair from this round's committed ncu capture
+    of the same kernels and shard (profiles/r02/ncu_traffic.json); not measured in this run."""
+    p = os.path.join(ROOT, "profiles", "r02", "ncu_traffic.json")
     try:
         with open(p) as f:
             return json.load(f).get(key)
     except Exception:
         return None
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        return os.cpu_count() or 1
+
+
+def pct(xs, q):
+    return float(np.percentile(np.asarray(xs, dtype=np.float64), q))
 
 
 class ClockSampler:
@@ -119,9 +152,8 @@ class ClockSampler:
 
 
 def algorithmic_bytes(lay, H, Hq, d, bs):
-    """Bytes one attention launch must move: KV of every resident
-    token for the local kv heads, q and out rows, block-table + direction entries
-    and seq_lens."""
+    """Bytes one layer's attention must move: KV of every resident token
+    for the local kv heads, q and out rows, block-table + direction entries and seq_lens."""
     L = lay.lens.astype(np.int64)
     nb = lay.nblocks().astype(np.int64)        # entries: ceil(L/bs), or num_entries of a general map
     kv = float(L.sum()) * 2 * H * d * 2
@@ -135,87 +167,158 @@ def append_bytes(B, H, d):
     return 8.0 * B * H * d   # read k_new, v_new + write the two rows: 4 x B*H*d bf16 values
 
 
-# --------------------------------------------------------- reference (oracle) arm
-def host_cores(oracle):
-    """Let the oracle use every core this process may run on."""
-    try:
-        n = len(os.sched_getaffinity(0))
-    except (AttributeError, OSError):
-        n = os.cpu_count() or 1
-    oracle.set_num_threads(max(1, n))
+def workload_config(args, ws, sh, lay):
+    """The config object both arms print (same keys, so the driver can compare them)."""
+    return {"workload": WORKLOADS.get(args.config, args.config), "name": args.config,
+            "global_batch": int(lay.batch), "n_layers": int(args.layers or sh.n_layers),
+            "parallelism": f"tp{ws} (kv-head sharded)", "head_dim": sh.head_dim,
+            "block_size": sh.block_size, "num_q_heads": sh.num_q_heads, "num_kv_heads": sh.num_kv_heads,
+            "block_map": "general (per-entry fills, f3)" if args.general_map else "dense",
+            "seed": args.seed,
+            "l2": "inputs larger than L2: every step reads every layer's KV pool once"}
+
+
+# --------------------------------------------------------- oracle timing (CPU)
+def oracle_layer(sh, lay, seed=2):
+    """One full layer of the workload (all heads, all requests) as host arrays for the oracle."""
+    H, d, bs, B = sh.num_kv_heads, sh.head_dim, sh.block_size, lay.batch
+    rng = np.random.default_rng(seed)
+    bf = lambda shape: (rng.standard_normal(shape, dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
+    return bf((lay.num_blocks, H, bs, d)), bf((lay.num_blocks, H, bs, d)), bf((B, sh.num_q_heads, d))
+
+
+def time_oracle_layer(oracle, K, V, lay, q, d, threads, reps):
+    oracle.set_num_threads(threads)
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        oracle.attention(K, V, lay.block_tables, lay.dirs, lay.lens, q, 1.0 / math.sqrt(d))
+        ts.append(time.perf_counter() - t0)
+    return ts
 
 
 def run_reference(args):
+    """The reference arm of the tier framing: the CPU oracle as it stands, on the host cores.
+    One step = one full layer of the workload (every head, every request); value = the
+    batch's tokens / (measured per-layer time x the model's layers)."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
     import oracle
     from synth import CONFIGS, make_case
     sh = CONFIGS[args.config]
-    case = make_case(args.config, args.seed)
-    lay = case.layout
-    H, Hq, d, bs, B = sh.num_kv_heads, sh.num_q_heads, sh.head_dim, sh.block_size, lay.batch
-    rng = np.random.default_rng(1)
-    # bounded sample: one layer of the workload, all requests, first `heads` kv heads
-    heads = max(1, min(H, args.ref_heads))
-    g = sh.group
-    K = (rng.standard_normal((lay.num_blocks, heads, bs, d), dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
-    V = (rng.standard_normal((lay.num_blocks, heads, bs, d), dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
-    q = (rng.standard_normal((B, heads * g, d), dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
-    host_cores(oracle)   # rank 0 runs alone: all host cores (torchrun sets OMP_NUM_THREADS=1)
-    cores = oracle.num_threads()
-    W = args.warmup if args.warmup_ref is None else args.warmup_ref
-    times = []
-    for i in range(W + args.steps):
-        t0 = time.perf_counter()
-        oracle.attention(K, V, lay.block_tables, lay.dirs, lay.lens, q, 1.0 / math.sqrt(d))
-        dt = time.perf_counter() - t0
-        if i >= W:
-            times.append(dt)
-    t_layer_full = statistics.median(times) * (H / heads)        # scale the head sample to all heads
-    t_step = t_layer_full * sh.n_layers
-    value = B / t_step
+    lay = make_case(args.config, args.seed).layout
+    n_layers = args.layers or sh.n_layers
+    K, V, q = oracle_layer(sh, lay)
+    cores = host_cores()   # rank 0 runs alone: all host cores (torchrun sets OMP_NUM_THREADS=1)
+    times = time_oracle_layer(oracle, K, V, lay, q, sh.head_dim, cores, args.warmup + args.steps)[args.warmup:]
+    one = time_oracle_layer(oracle, K, V, lay, q, sh.head_dim, 1, 1)[0]
+    t_layer = statistics.median(times)
+    value = lay.batch / (t_layer * n_layers)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
-        "n_gpus": ws, "steps": args.steps, "warmup": W, "ms_per_step": t_step * 1e3,
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": float(np.mean(times)) * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": WORKLOADS.get(args.config, args.config), "name": args.config,
-                   "global_batch": B, "n_layers": sh.n_layers, "tp": 1},
+        "config": workload_config(args, ws, sh, lay),
+        "step_definition": f"one full layer of the workload (all {sh.num_q_heads} q heads, all {lay.batch} "
+                           f"requests) per step; value = batch / (median layer time x {n_layers} layers)",
+        "step_ms": {"median": t_layer * 1e3, "p10": pct(times, 10) * 1e3, "p90": pct(times, 90) * 1e3},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle",
-                         "sample": f"one layer, all {B} requests, {heads}/{H} kv heads "
-                                   f"({heads * g} q heads) of {args.config}; time scaled by "
-                                   f"{H}/{heads} heads x {sh.n_layers} layers; median of {len(times)}"},
+                         "cpu_model": cpu_model(),
+                         "sample": f"one full layer ({sh.num_q_heads} q heads x {lay.batch} requests) of "
+                                   f"{args.config} per step, fp64 C oracle with OpenMP",
+                         "layer_ms_all_cores": t_layer * 1e3, "layer_ms_1_thread": one * 1e3,
+                         "value_1_thread": lay.batch / (one * n_layers)},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(args, lay, sh):
-    """The oracle as it stands, timed on the host cores on a bounded sample."""
+def cpu_baseline(args, lay, sh, n_layers):
+    """The oracle as it stands, timed on the host cores on a bounded sample: one full layer."""
     import oracle
-    H, Hq, d, bs, B = sh.num_kv_heads, sh.num_q_heads, sh.head_dim, sh.block_size, lay.batch
-    heads = max(1, min(H, args.ref_heads))
-    g = sh.group
-    host_cores(oracle)
-    rng = np.random.default_rng(2)
-    K = (rng.standard_normal((lay.num_blocks, heads, bs, d), dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
-    V = (rng.standard_normal((lay.num_blocks, heads, bs, d), dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
-    q = (rng.standard_normal((B, heads * g, d), dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
-    ts = []
-    t_end = time.perf_counter() + args.cpu_seconds
-    while len(ts) < 3 and (not ts or time.perf_counter() < t_end):
-        t0 = time.perf_counter()
-        oracle.attention(K, V, lay.block_tables, lay.dirs, lay.lens, q, 1.0 / math.sqrt(d))
-        ts.append(time.perf_counter() - t0)
-    t_step = statistics.median(ts) * (H / heads) * sh.n_layers
-    return {"value": B / t_step, "unit": "tokens/s", "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"one layer, all {B} requests, {heads}/{H} kv heads of {args.config}, "
-                      f"median of {len(ts)} runs, scaled x{H}/{heads} heads x {sh.n_layers} layers"}
+    K, V, q = oracle_layer(sh, lay)
+    cores = host_cores()
+    ts = time_oracle_layer(oracle, K, V, lay, q, sh.head_dim, cores, 3)
+    one = time_oracle_layer(oracle, K, V, lay, q, sh.head_dim, 1, 1)[0]
+    t = statistics.median(ts)
+    return {"value": lay.batch / (t * n_layers), "unit": "tokens/s", "cores": cores, "kind": "oracle",
+            "cpu_model": cpu_model(),
+            "sample": f"one full layer ({sh.num_q_heads} q heads x {lay.batch} requests) of {args.config}, "
+                      f"median of 3 at {cores} threads, scaled x {n_layers} layers",
+            "layer_ms_all_cores": t * 1e3, "layer_ms_1_thread": one * 1e3,
+            "value_1_thread": lay.batch / (one * n_layers)}
+
+
+# ------------------------------------------------------------------ shards
+def measure_shards(dev, peak, seed, replays=60, warm=10):
+    """Per-layer time of every head shard of the paper's deployments on this GPU: the
+    planned fused decode step per layer in a CUDA graph over >= 4x L2 of rotated layers."""
+    import torch
+    import paper_2504_09590_b200 as bkv
+    from synth import CONFIGS, make_case
+    from synth.workload import shard_heads
+    res = []
+    for cfg, tp in SHARDS:
+        sh = CONFIGS[cfg]
+        lay = make_case(cfg, seed).layout
+        kvh, qh = shard_heads(sh, tp, 0)
+        H, Hq, d, bs, B = len(kvh), len(qh), sh.head_dim, sh.block_size, lay.batch
+        alg, kv = algorithmic_bytes(lay, H, Hq, d, bs)
+        alg += append_bytes(B, H, d)
+        layers = max(8, math.ceil(4 * L2_BYTES / kv))
+        gen = torch.Generator(device=dev).manual_seed(7)
+        pools = []
+        for _ in range(layers):
+            k = torch.empty((lay.num_blocks, H, bs, d), dtype=torch.bfloat16, device=dev).normal_(generator=gen)
+            pools.append(bkv.KVPool(k, torch.empty_like(k).normal_(generator=gen)))
+        bt = torch.from_numpy(lay.block_tables).to(dev)
+        dirs = torch.from_numpy(lay.dirs).to(dev)
+        lens = torch.from_numpy(lay.lens.astype(np.int32)).to(dev)
+        q = torch.randn((layers, B, Hq, d), device=dev).to(torch.bfloat16)
+        kn = torch.randn((layers, B, H, d), device=dev).to(torch.bfloat16)
+        vn = torch.randn((layers, B, H, d), device=dev).to(torch.bfloat16)
+        out = torch.empty((B, Hq, d), dtype=torch.bfloat16, device=dev)
+        ws = bkv.workspace(B, Hq, H, d, dev)
+        plan = bkv.decode_plan(lay.lens, pools[0], Hq, lay.block_tables.shape[1])
+
+        def body():
+            for l in range(layers):
+                bkv.decode_planned(pools[l], bt, dirs, lens, plan, q[l], k_new=kn[l], v_new=vn[l], out=out,
+                                   ws=ws, pdl=True, kv_early=True)
+        body()
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            body()
+        for _ in range(warm):
+            g.replay()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(replays + 1)]
+        torch.cuda.synchronize(dev)
+        evs[0].record()
+        for i in range(replays):
+            g.replay()
+            evs[i + 1].record()
+        torch.cuda.synchronize(dev)
+        us = [evs[i].elapsed_time(evs[i + 1]) * 1e3 / layers for i in range(replays)]
+        med = statistics.median(us)
+        res.append({"shard": f"{cfg} tp{tp}", "kv_heads": H, "q_heads": Hq, "batch": B,
+                    "kv_mb_per_layer": kv / 1e6, "alg_mb_per_layer": alg / 1e6, "layers_rotated": layers,
+                    "us_per_layer": {"median": med, "p10": pct(us, 10), "p90": pct(us, 90)},
+                    "gbs": alg / (med * 1e-6) / 1e9, "frac": alg / (med * 1e-6) / 1e9 / peak,
+                    "traffic": ncu_traffic(f"{cfg}_tp{tp}")})
+        del pools, g, q, kn, vn
+        torch.cuda.empty_cache()
+    return res
 
 
 # ------------------------------------------------------------------ our arm
 def run_ours(args):
+    ws, rank, local = dist_env()
+    if ws > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")   # NCCL's init log (rank count, NVLS/NVLink) on stderr
     import torch
     import torch.distributed as dist
 
@@ -223,7 +326,6 @@ def run_ours(args):
     from synth import CONFIGS, make_case
     from paper_2504_09590_b200.tp import HeadShard, PeerReassembly, gather_heads
 
-    ws, rank, local = dist_env()
     # dev-only: BKV_DIST_BACKEND=gloo runs several ranks on one GPU (smoke test of the N>1 path)
     backend = os.environ.get("BKV_DIST_BACKEND", "nccl")
     if backend != "nccl":
@@ -249,6 +351,7 @@ def run_ours(args):
     H, Hq, d, bs, B = len(kv_heads), len(q_heads), sh.head_dim, sh.block_size, lay.batch
     n_layers = args.layers or sh.n_layers
     stream = torch.cuda.current_stream(dev)
+    bt_stride = lay.block_tables.shape[1]
 
     # ---- resident state: one KV pool per layer (random bf16 contents), block map
     gen = torch.Generator(device=dev)
@@ -260,15 +363,18 @@ def run_ours(args):
         k.normal_(generator=gen)
         v.normal_(generator=gen)
         pools.append(bkv.KVPool(k, v))
-    # ---- per-step inputs (host-pinned originals for the e2e leg)
-    before_h = torch.from_numpy((lay.lens - 1).astype(np.int32))
-    cu_h = torch.arange(B + 1, dtype=torch.int32)
+    # ---- per-step inputs (host-pinned originals for the e2e leg), incl. the step's split plan
+    nent_h = lay.num_entries if args.general_map else None
+
+    def host_plan():
+        return bkv.decode_plan_host(lay.lens, H, Hq, d, bs, bt_stride, num_entries=nent_h)
+
+    plan_np = host_plan()
     meta_h = {
         "bt": torch.from_numpy(lay.block_tables).pin_memory(),
         "dirs": torch.from_numpy(lay.dirs).pin_memory(),
         "lens": torch.from_numpy(lay.lens.astype(np.int32)).pin_memory(),
-        "before": before_h.pin_memory(),
-        "cu": cu_h.pin_memory(),
+        "plan": torch.from_numpy(plan_np.view(np.uint8).copy()).pin_memory(),
     }
     if args.general_map:   # per-entry fill counts travel with the map
         meta_h["fills"] = torch.from_numpy(lay.fills).pin_memory()
@@ -277,59 +383,60 @@ def run_ours(args):
     q_h = torch.randn((n_layers, B, Hq, d), generator=g_cpu).to(torch.bfloat16).pin_memory()
     kn_h = torch.randn((n_layers, B, H, d), generator=g_cpu).to(torch.bfloat16).pin_memory()
     vn_h = torch.randn((n_layers, B, H, d), generator=g_cpu).to(torch.bfloat16).pin_memory()
-    meta_d = {k: v.to(dev) for k, v in meta_h.items()}
+
+    def dev_meta():
+        md = {k: v.to(dev) for k, v in meta_h.items()}
+        md["plan_obj"] = bkv.DecodePlan(plan_np, md["plan"], md["plan"].numel())
+        return md
+
+    meta_d = dev_meta()
     q_d, kn_d, vn_d = q_h.to(dev), kn_h.to(dev), vn_h.to(dev)
     out_loc = torch.empty((n_layers, Hq, B, d), dtype=torch.bfloat16, device=dev)   # head-major
     # reassembled outputs: per-layer gather -> [layer][global head][B][d]; one gather per step
     # (default) -> rank-major [rank][layer][local head][B][d] (global head = rank * Hq + local)
     glob_shape = (n_layers, Hq * tp, B, d) if args.gather == "layer" else (tp, n_layers, Hq, B, d)
-    out_glob = torch.empty(glob_shape, dtype=torch.bfloat16, device=dev) if tp > 1 else None
-    p2p = None
+    n_sets = 3 if (tp > 1 and args.reassembly == "p2p") else 2   # e2e buffer sets (p2p: triple)
+    p2ps = None
     if tp > 1 and args.reassembly == "p2p":   # f2: fused NVLink reassembly instead of the all-gather
-        p2p = PeerReassembly(shard, n_layers, B, d, dev)
-        out_glob = p2p.glob
+        p2ps = [PeerReassembly(shard, n_layers, B, d, dev) for _ in range(n_sets)]
+        out_glob = p2ps[0].glob
+    else:
+        out_glob = torch.empty(glob_shape, dtype=torch.bfloat16, device=dev) if tp > 1 else None
     out_h = torch.empty(tuple(out_glob.shape) if out_glob is not None else (n_layers, Hq, B, d),
                         dtype=torch.bfloat16).pin_memory()
     wsb = bkv.workspace(B, Hq, H, d, dev)
-    max_len = int(lay.lens.max())
     scale = 1.0 / math.sqrt(d)
 
-    def step(md, qd, knd, vnd, attn_only=False, ol=None, og=None):
-        """One decode step over all layers (append + attention [+ all-gather])."""
-        ol = out_loc if ol is None else ol
-        og = out_glob if og is None else og
+    def step(md, qd, knd, vnd, ol, og, p2p=None, attn_only=False, gather_only=False):
+        """One decode step over all layers (planned fused append + attention [+ reassembly])."""
         launches = 0
         gm = dict(fills=md["fills"], num_entries=md["nent"]) if args.general_map else {}
-        for l in range(n_layers):
-            if p2p is not None:   # f2: fused step + stores into every peer's output, then signal
-                bkv.decode_multi_out(pools[l], md["bt"], md["dirs"], md["lens"], qd[l],
-                                     p2p.local_out(l).permute(1, 0, 2), p2p.peer_outs(l),
-                                     k_new=knd[l], v_new=vnd[l], softmax_scale=scale,
-                                     max_seq_len=max_len, ws=wsb, pdl=args.pdl, **gm)
-                launches += 2
-                if not attn_only:
-                    p2p.barrier()
-                    launches += 1
-                continue
-            o = ol[l].permute(1, 0, 2)                                        # [B][Hq][d] view
-            if args.fused:   # f2: append fused into the attention kernel (bkv_decode_step)
-                bkv.decode_step(pools[l], md["bt"], md["dirs"], md["lens"], knd[l], vnd[l], qd[l],
-                                scale, out=o, max_seq_len=max_len, ws=wsb, pdl=args.pdl, **gm)
-            else:
-                if not attn_only:
-                    bkv.kv_append(pools[l], md["bt"], md["dirs"], md["before"], md["cu"], knd[l],
-                                  vnd[l], total_new_tokens=B, **gm)
-                    launches += 1
-                bkv.paged_decode_attention(pools[l], md["bt"], md["dirs"], md["lens"], qd[l], scale,
-                                           out=o, max_seq_len=max_len, ws=wsb, pdl=args.pdl, **gm)
-            launches += 2                                                     # decode + merge kernels
-            if tp > 1 and not attn_only and args.gather == "layer":
-                gather_heads(ol[l], og[l])
-        if tp > 1 and not attn_only and p2p is None and args.gather == "step":
-            # a6: head-sharded TP needs no per-layer reassembly (each rank's o_proj shard
-            # consumes its own heads); the step's per-request outputs of every layer are
-            # reassembled by ONE all-gather
-            gather_heads(ol.view(n_layers * Hq, B, d), og.view(tp * n_layers * Hq, B, d))
+        if not gather_only:
+            for l in range(n_layers):
+                if p2p is not None:   # f2: the layer's rows are also stored into every peer's output
+                    bkv.decode_planned(pools[l], md["bt"], md["dirs"], md["lens"], md["plan_obj"], qd[l],
+                                       k_new=knd[l], v_new=vnd[l], softmax_scale=scale,
+                                       out=p2p.local_out(l).permute(1, 0, 2), peer_outs=p2p.peer_outs(l),
+                                       ws=wsb, pdl=True, kv_early=True, **gm)
+                else:
+                    bkv.decode_planned(pools[l], md["bt"], md["dirs"], md["lens"], md["plan_obj"], qd[l],
+                                       k_new=knd[l], v_new=vnd[l], softmax_scale=scale,
+                                       out=ol[l].permute(1, 0, 2), ws=wsb, pdl=True, kv_early=True, **gm)
+                launches += 2                                  # decode kernel + cross-CTA merge kernel
+                if tp > 1 and not attn_only and p2p is None and args.gather == "layer":
+                    gather_heads(ol[l], og[l])
+        if tp > 1 and not attn_only:
+            if p2p is not None:
+                p2p.barrier()
+                launches += 1
+            elif args.gather == "step":
+                # a6: head-sharded TP needs no per-layer reassembly (each rank's o_proj shard
+                # consumes its own heads); the step's outputs of every layer are reassembled
+                # by ONE all-gather
+                gather_heads(ol.view(n_layers * Hq, B, d), og.view(tp * n_layers * Hq, B, d))
+            elif gather_only:
+                for l in range(n_layers):
+                    gather_heads(ol[l], og[l])
         return launches
 
     def barrier():
@@ -344,158 +451,169 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---- eager warm-up, then capture the step (and an attention-only step) in CUDA graphs
+    p2p0 = p2ps[0] if p2ps else None
+    full = lambda: step(meta_d, q_d, kn_d, vn_d, out_loc, out_glob, p2p0)
+    attn = lambda: step(meta_d, q_d, kn_d, vn_d, out_loc, out_glob, p2p0, attn_only=True)
+    gath = lambda: step(meta_d, q_d, kn_d, vn_d, out_loc, out_glob, p2p0, gather_only=True)
+
+    # ---- eager warm-up, then capture the step (and attention-only / gather-only parts) in graphs
     for _ in range(args.warmup):
-        launches_per_step = step(meta_d, q_d, kn_d, vn_d)
+        launches_per_step = full()
     barrier()
-    g_step, g_attn = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    g_step, g_attn, g_gath = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
     if args.graphs:
         try:
             with torch.cuda.graph(g_step):
-                step(meta_d, q_d, kn_d, vn_d)
+                full()
             with torch.cuda.graph(g_attn):
-                step(meta_d, q_d, kn_d, vn_d, attn_only=True)
+                attn()
+            if tp > 1 and p2p0 is None:
+                with torch.cuda.graph(g_gath):
+                    gath()
         except Exception as e:   # e.g. a collective that cannot be captured: time the eager launches
             print(f"bench: CUDA graph capture failed ({type(e).__name__}: {e}); running eagerly",
                   file=sys.stderr, flush=True)
             torch.cuda.synchronize(dev)
             args.graphs = False
-    if args.graphs:
-        run_step, run_attn = g_step.replay, g_attn.replay
-    else:
-        run_step = lambda: step(meta_d, q_d, kn_d, vn_d)
-        run_attn = lambda: step(meta_d, q_d, kn_d, vn_d, attn_only=True)
+    run_step = g_step.replay if args.graphs else full
+    run_attn = g_attn.replay if args.graphs else attn
+    run_gath = g_gath.replay if args.graphs else gath
     for _ in range(args.warmup):
         run_step()
     barrier()
 
     def timed(fn, n):
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
+        """n back-to-back calls bracketed by barrier + sync; per-call events for percentiles.
+        Returns (total ms max over ranks, per-call ms list of this rank)."""
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(n + 1)]
         barrier()
-        e0.record(stream)
-        for _ in range(n):
+        evs[0].record(stream)
+        for i in range(n):
             fn()
-        e1.record(stream)
+            evs[i + 1].record(stream)
         barrier()
-        return max_over_ranks(e0.elapsed_time(e1))
+        per = [evs[i].elapsed_time(evs[i + 1]) for i in range(n)]
+        return max_over_ranks(evs[0].elapsed_time(evs[n])), per
 
     # ---- device-resident timed region (W warm-up steps done above)
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.2)                          # let nvidia-smi attach before the timed region
-    ms_total = timed(run_step, args.steps)
+    ms_total, per_step = timed(run_step, args.steps)
     ms_step = ms_total / args.steps
     launches = launches_per_step * args.steps
-    # ---- the dominant kernel alone: same pools, attention launches only, same stream
+    # ---- the hot path alone (decode + merge kernels of every layer, no reassembly), same stream
     for _ in range(2):
         run_attn()
-    att_avg_us = timed(run_attn, args.steps) * 1e3 / (args.steps * n_layers)
-
-    # ---- end to end: pinned host inputs -> device, step, device -> host outputs
-    src_out = out_glob if tp > 1 else out_loc
-
-    def e2e_step():
-        for k, v in meta_h.items():
-            meta_d[k].copy_(v, non_blocking=True)
-        q_d.copy_(q_h, non_blocking=True)
-        kn_d.copy_(kn_h, non_blocking=True)
-        vn_d.copy_(vn_h, non_blocking=True)
-        run_step()
-        out_h.copy_(src_out, non_blocking=True)
-
-    pipelined = args.graphs and p2p is None and args.e2e_pipeline
-    if pipelined:
-        # Serving pipeline: two input/output buffer sets, one captured graph per set; one
-        # copy stream moves step i+1's inputs host -> device while step i computes, another
-        # step i's outputs device -> host while step i+1 computes (both copy engines busy).  Every step still
-        # moves all of its inputs and outputs through PCIe inside the timed region.
-        meta_d2 = {k: torch.empty_like(v) for k, v in meta_d.items()}
-        q_d2, kn_d2, vn_d2 = torch.empty_like(q_d), torch.empty_like(kn_d), torch.empty_like(vn_d)
-        out_loc2 = torch.empty_like(out_loc)
-        out_glob2 = torch.empty_like(out_glob) if out_glob is not None else None
-        for k in meta_d:
-            meta_d2[k].copy_(meta_d[k])
-        q_d2.copy_(q_d), kn_d2.copy_(kn_d), vn_d2.copy_(vn_d)
-        step(meta_d2, q_d2, kn_d2, vn_d2, ol=out_loc2, og=out_glob2)   # eager warm-up of set 2
-        torch.cuda.synchronize(dev)
-        g_step2 = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g_step2):
-            step(meta_d2, q_d2, kn_d2, vn_d2, ol=out_loc2, og=out_glob2)
-        sets = [(meta_d, q_d, kn_d, vn_d, g_step, src_out),
-                (meta_d2, q_d2, kn_d2, vn_d2, g_step2, out_glob2 if tp > 1 else out_loc2)]
-        up = torch.cuda.Stream(dev)     # host -> device (one copy engine) ...
-        down = torch.cuda.Stream(dev)   # ... and device -> host (the other), concurrently
-        ev_h2d = [torch.cuda.Event(), torch.cuda.Event()]
-        ev_comp = [torch.cuda.Event(), torch.cuda.Event()]
-        ev_d2h = [torch.cuda.Event(), torch.cuda.Event()]
-
-        def h2d(si):
-            md, qd, knd, vnd, _, _ = sets[si]
-            with torch.cuda.stream(up):
-                for k, v in meta_h.items():
-                    md[k].copy_(v, non_blocking=True)
-                qd.copy_(q_h, non_blocking=True)
-                knd.copy_(kn_h, non_blocking=True)
-                vnd.copy_(vn_h, non_blocking=True)
-                ev_h2d[si].record(up)
-
-        def run_pipeline(n):
-            up.wait_stream(stream)
-            down.wait_stream(stream)
-            h2d(0)
-            for i in range(n):
-                si = i % 2
-                stream.wait_event(ev_h2d[si])
-                if i >= 2:                         # step i-2's outputs (same set) are on the host
-                    stream.wait_event(ev_d2h[si])
-                sets[si][4].replay()
-                ev_comp[si].record(stream)
-                if i + 1 < n:                      # inputs of step i+1 (its set was last read by step i-1)
-                    sj = 1 - si
-                    if i >= 1:
-                        up.wait_event(ev_comp[sj])
-                    h2d(sj)
-                with torch.cuda.stream(down):      # outputs of step i, overlapping step i+1
-                    down.wait_event(ev_comp[si])
-                    out_h.copy_(sets[si][5], non_blocking=True)
-                    ev_d2h[si].record(down)
-            stream.wait_stream(up)
-            stream.wait_stream(down)
-
-        def timed_pipeline(n):
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            barrier()
-            e0.record(stream)
-            run_pipeline(n)
-            e1.record(stream)
-            barrier()
-            return max_over_ranks(e0.elapsed_time(e1))
-
-        run_pipeline(2)
-        ms_e2e = timed_pipeline(args.steps) / args.steps
-    else:
+    att_total, att_per = timed(run_attn, args.steps)
+    att_avg_us = att_total * 1e3 / (args.steps * n_layers)
+    gath_ms = None
+    if tp > 1 and p2p0 is None:
         for _ in range(2):
-            e2e_step()
-        ms_e2e = timed(e2e_step, args.steps) / args.steps
-    if p2p is not None:
-        p2p.check()
-    clk = clocks.stop()                      # clocks sampled over all three timed regions
-    h2d = sum(v.numel() * v.element_size() for v in meta_h.values()) + \
-        (q_h.numel() + kn_h.numel() + vn_h.numel()) * 2
+            run_gath()
+        gath_ms = timed(run_gath, args.steps)[0] / args.steps
+
+    # ---- end to end through the public API: every step the host rebuilds the step's plan
+    # (bkv_decode_plan), pinned host inputs go to the device, the step runs, outputs come back
+    sets = []
+    for si in range(n_sets):
+        if si == 0:
+            md, qd, knd, vnd, ol, og = meta_d, q_d, kn_d, vn_d, out_loc, out_glob
+        else:
+            md = dev_meta()
+            qd, knd, vnd = torch.empty_like(q_d), torch.empty_like(kn_d), torch.empty_like(vn_d)
+            qd.copy_(q_d), knd.copy_(kn_d), vnd.copy_(vn_d)
+            ol = torch.empty_like(out_loc)
+            og = p2ps[si].glob if p2ps else (torch.empty_like(out_glob) if out_glob is not None else None)
+        p2p = p2ps[si] if p2ps else None
+        fn = (lambda md=md, qd=qd, knd=knd, vnd=vnd, ol=ol, og=og, p2p=p2p: step(md, qd, knd, vnd, ol, og, p2p))
+        g = torch.cuda.CUDAGraph() if args.graphs else None
+        if si > 0:
+            fn()                                          # eager warm-up of this set
+            torch.cuda.synchronize(dev)
+            if g is not None:
+                with torch.cuda.graph(g):
+                    fn()
+        src = og if tp > 1 else ol
+        sets.append({"md": md, "q": qd, "kn": knd, "vn": vnd, "run": (g_step.replay if si == 0 else g.replay)
+                     if args.graphs else fn, "src": src,
+                     "plan_h": torch.empty_like(meta_h["plan"]).pin_memory()})
+    up = torch.cuda.Stream(dev)     # host -> device (one copy engine) ...
+    down = torch.cuda.Stream(dev)   # ... and device -> host (the other), concurrently
+    ev_h2d = [torch.cuda.Event() for _ in range(n_sets)]
+    ev_comp = [torch.cuda.Event() for _ in range(n_sets)]
+    ev_d2h = [torch.cuda.Event() for _ in range(n_sets)]
+    h2d_bytes = [0]
+
+    def h2d(si):
+        s = sets[si]
+        ev_h2d[si].synchronize()                          # this set's pinned plan buffer is free again
+        s["plan_h"].copy_(torch.from_numpy(host_plan().view(np.uint8)))   # the host scheduler's plan
+        with torch.cuda.stream(up):
+            n = 0
+            for k, v in meta_h.items():
+                srcv = s["plan_h"] if k == "plan" else v
+                s["md"][k].copy_(srcv, non_blocking=True)
+                n += srcv.numel() * srcv.element_size()
+            for dst, srcv in ((s["q"], q_h), (s["kn"], kn_h), (s["vn"], vn_h)):
+                dst.copy_(srcv, non_blocking=True)
+                n += srcv.numel() * srcv.element_size()
+            ev_h2d[si].record(up)
+        h2d_bytes[0] = n
+
+    def run_pipeline(n):
+        up.wait_stream(stream)
+        down.wait_stream(stream)
+        h2d(0)
+        for i in range(n):
+            si = i % n_sets
+            stream.wait_event(ev_h2d[si])
+            # set si is rewritten by step i: step i - n_sets's outputs must be on the host.  p2p:
+            # the PEERS write it as soon as they pass our barrier of step i-1, so that D2H must
+            # be done before our step i-1 (i.e. wait for step i+1-n_sets's D2H here)
+            j = i + 1 - n_sets if p2ps else i - n_sets
+            if j >= 0:
+                stream.wait_event(ev_d2h[j % n_sets])
+            sets[si]["run"]()
+            ev_comp[si].record(stream)
+            if i + 1 < n:                                  # inputs of step i+1 overlap step i
+                sj = (i + 1) % n_sets
+                if i + 1 >= n_sets:
+                    up.wait_event(ev_comp[sj])
+                h2d(sj)
+            with torch.cuda.stream(down):                  # outputs of step i overlap step i+1
+                down.wait_event(ev_comp[si])
+                out_h.copy_(sets[si]["src"], non_blocking=True)
+                ev_d2h[si].record(down)
+        stream.wait_stream(up)
+        stream.wait_stream(down)
+
+    run_pipeline(2)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    run_pipeline(args.steps)
+    e1.record(stream)
+    barrier()
+    ms_e2e = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+    for p in (p2ps or []):
+        p.check()
+    clk = clocks.stop()                      # clocks sampled over every timed region
     d2h = out_h.numel() * 2
 
+    peak, peak_src = load_peaks()
+    shards = None
+    if ws == 1 and not args.no_shards:
+        shards = measure_shards(dev, peak, args.seed)
     if rank != 0:
         dist.destroy_process_group()
         return
     alg_bytes, kv_bytes = algorithmic_bytes(lay, H, Hq, d, bs)
-    if args.fused:   # the fused kernel also reads the new rows and writes them into the pool
-        alg_bytes += append_bytes(B, H, d)
-    peak, peak_src = load_peaks()
+    alg_bytes += append_bytes(B, H, d)   # the fused step also reads the new rows and writes them into the pool
     achieved = alg_bytes / (att_avg_us * 1e-6) / 1e9
+    static = meta_d["plan_obj"].header["P"] < PLANNED_DYNAMIC_P
     tok_s = B / (ms_step * 1e-3)
-    cpu = cpu_baseline(args, lay, sh) if (ws == 1 and not args.no_cpu) else None
+    cpu = cpu_baseline(args, lay, sh, n_layers) if (ws == 1 and not args.no_cpu) else None
     line = {
         "metric": METRIC,
         "value": tok_s,
@@ -509,36 +627,47 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic",
-        "config": {
-            "workload": WORKLOADS.get(args.config, args.config), "name": args.config,
-            "global_batch": B, "n_layers": n_layers, "parallelism": f"tp{tp} (kv-head sharded)",
-            "kv_heads_per_gpu": H, "q_heads_per_gpu": Hq, "head_dim": d, "block_size": bs,
+        "config": workload_config(args, ws, sh, lay),
+        "step_ms": {"mean": ms_step, "median": statistics.median(per_step), "p10": pct(per_step, 10),
+                    "p90": pct(per_step, 90), "n": len(per_step)},
+        "detail": {
+            "kv_heads_per_gpu": H, "q_heads_per_gpu": Hq,
             "mean_ctx": float(lay.lens.mean()), "max_ctx": int(lay.lens.max()),
             "shared_blocks": int(lay.n_shared),
-            "block_map": "general (per-entry fills, f3)" if args.general_map else "dense",
-            "l2": f"inputs larger than L2: each step reads {n_layers} layers x {kv_bytes / 1e6:.0f} MB of KV per GPU",
+            "kv_mb_per_layer_per_gpu": kv_bytes / 1e6,
             "per_layer_us": ms_step * 1e3 / n_layers,
             "attn_us_per_layer": att_avg_us,
+            "attn_us_per_layer_pct": {"median": statistics.median(att_per) * 1e3 / n_layers,
+                                      "p10": pct(att_per, 10) * 1e3 / n_layers,
+                                      "p90": pct(att_per, 90) * 1e3 / n_layers},
             "attn_share_of_step": att_avg_us * n_layers / (ms_step * 1e3),
+            "reassembly_ms_per_step": gath_ms,
             "cuda_graphs": bool(args.graphs),
-            "fused_append": bool(args.fused),
-            "reassembly": ("p2p stores + peer barrier (bkv_decode_multi_out)" if p2p is not None
+            "path": "bkv_decode_plan once per step (host) + bkv_decode_planned per layer (fused append, "
+                    "PDL, early KV tiles)",
+            "plan_blocks_per_warp": meta_d["plan_obj"].header["P"],
+            "reassembly": ("p2p stores + peer barrier (bkv_decode_planned peer_outs)" if p2ps
                            else f"nccl all_gather_into_tensor, one per {args.gather}" if tp > 1
                            else "none (1 GPU)"),
             "attn_layer_tokens_per_s": B / (att_avg_us * 1e-6),
-            "seed": args.seed,
         },
         "roofline": {
-            "bound": "hbm", "kernel": "bkv::decode_kernel" + (" (fused append)" if args.fused else ""), "achieved": achieved, "peak": peak,
-            "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
-            "algorithmic_bytes_per_launch": alg_bytes,
+            "bound": "hbm",
+            "kernel": ("bkv::planned_kernel + planned_xmerge_kernel (static plan)" if static else
+                       "bkv::decode_kernel + merge_kernel (dynamic schedule: plan ranges >= "
+                       f"{PLANNED_DYNAMIC_P} blocks per warp)") + ", one layer, fused append",
+            "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+            "frac": achieved / peak, "algorithmic_bytes_per_launch": alg_bytes,
             "traffic": ncu_traffic(f"{args.config}_tp{tp}"),
+            "traffic_source": "profiles/r02/ncu_traffic.json (ncu --set full of these kernels on this shard; "
+                              "not measured in this run)",
         },
+        "shards": shards,
         "cpu_baseline": cpu,
         "e2e": {"value": B / (ms_e2e * 1e-3), "unit": "tokens/s", "ms_per_step": ms_e2e,
-                "pipeline": ("two copy streams overlap step i+1 H2D and step i D2H with compute (2 buffer sets)"
-                             if pipelined else "serial H2D, step, D2H on one stream"),
-                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+                "pipeline": f"host rebuilds the step's plan; {n_sets} buffer sets; one copy stream uploads "
+                            f"step i+1 while step i computes, another downloads step i's outputs",
+                "h2d_bytes_per_step": int(h2d_bytes[0]), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": launches,
         "clocks": clk,
     }
@@ -556,23 +685,15 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--layers", type=int, default=0, help="override the model's layer count")
-    ap.add_argument("--ref-heads", type=int, default=4, help="kv heads in the oracle's bounded sample")
-    ap.add_argument("--warmup-ref", type=int, default=None, help="reference-arm warm-ups (default: --warmup)")
-    ap.add_argument("--cpu-seconds", type=float, default=20.0)
-    ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-pdl", dest="pdl", action="store_false",
-                    help="launch attention without programmatic dependent launch")
-    ap.add_argument("--no-e2e-pipeline", dest="e2e_pipeline", action="store_false",
-                    help="e2e leg: serial H2D/step/D2H instead of the double-buffered copy-stream pipeline")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline (oracle) leg")
+    ap.add_argument("--no-shards", action="store_true", help="skip the per-shard table (N = 1)")
     ap.add_argument("--general-map", action="store_true",
                     help="FindBlock-style general block map (partly filled entries, SURVEY §8(f) f3)")
     ap.add_argument("--gather", default="step", choices=["step", "layer"],
                     help="N>1, nccl reassembly: one all-gather per step of every layer's outputs (default) "
                          "or one per layer")
     ap.add_argument("--reassembly", default="nccl", choices=["nccl", "p2p"],
-                    help="N>1: NCCL all-gather (default) or fused NVLink stores (symmetric memory)")
-    ap.add_argument("--no-fused", dest="fused", action="store_false",
-                    help="separate kv_append + attention launches instead of bkv_decode_step")
+                    help="N>1: NCCL all-gather (default) or fused NVLink stores (CUDA IPC peer memory)")
     ap.add_argument("--no-graphs", dest="graphs", action="store_false",
                     help="launch eagerly instead of replaying CUDA graphs")
     args = ap.parse_args()

@@ -502,6 +502,10 @@ BKV_API bkv_status bkv_validate_block_map_host(const bkv_block_map *map, const i
  *                stream completes, so none of them may be written by that
  *                kernel (host copies and earlier kernels are fine); q, k_new,
  *                v_new, the pool and the workspace are read after it.
+ *   Large problems (plan ranges of >= 128 blocks per warp, e.g. OPT-30B on one
+ *   GPU) run the dynamically scheduled kernel pair of bkv_decode_multi_out
+ *   instead (same results up to fp32 summation order): over a long kernel the
+ *   per-SM bandwidth spread outweighs the static plan's savings.
  *   Errors: as bkv_decode_multi_out, plus BKV_ERR_INVALID_ARGUMENT when the
  *   plan's geometry (num_seqs, heads, group, head_dim, block_size, dense or
  *   general map, SM count) does not match the call.

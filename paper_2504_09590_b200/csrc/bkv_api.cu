@@ -49,6 +49,7 @@ void load_switches() {
 #endif
   s.planned_slots = env_int("BKV_PLANNED_SLOTS", 2);
   s.planned_xmerge = env_int("BKV_PLANNED_XMERGE", 1);
+  s.planned_dynamic_p = env_int("BKV_PLANNED_DYNAMIC_P", 128);
   g_sw = s;
 }
 }  // namespace
@@ -948,6 +949,15 @@ bkv_status bkv_decode_planned(const bkv_kv_pool *pool, const bkv_block_map *map,
   if (hd->grid != dp.sms || hd->warps != bkv::kPlannedWarps)
     return fail(BKV_ERR_INVALID_ARGUMENT, "plan built for %d x %d warps, this device runs %d x %d", hd->grid,
                 hd->warps, dp.sms, bkv::kPlannedWarps);
+  // Large problems (long warp ranges: e.g. OPT-30B at one GPU, 190 blocks per warp) run the
+  // dynamically scheduled kernel instead: over a long kernel, per-SM bandwidth differences
+  // outweigh the static plan's fixed-cost savings (measured OPT-30B TP1 313 vs 299 us per
+  // layer; Llama-70B TP1, 64 blocks per warp, 106 vs 111 for the static plan).
+  const int dyn_p = bkv::dev_switches().planned_dynamic_p;
+  if (dyn_p > 0 && hd->P >= dyn_p)
+    return decode_impl(pool, map, seq_lens, map->bt_stride * pool->block_size, k_new, v_new, q, q_stride_seq,
+                       q_stride_head, num_q_heads, softmax_scale, out, o_stride_seq, o_stride_head, workspace,
+                       workspace_bytes, flags & BKV_FLAG_PDL, stream, peer_outs, n_peers);
   if (!aligned16(q) || !aligned16(out) || q_stride_seq % 8 || q_stride_head % 8 || o_stride_seq % 8 ||
       o_stride_head % 8)
     return fail(BKV_ERR_INVALID_ARGUMENT, "q/out must be 16-byte aligned with strides multiple of 8");
@@ -1003,9 +1013,9 @@ bkv_status bkv_decode_planned(const bkv_kv_pool *pool, const bkv_block_map *map,
   p.ctask = pw + hd->off_ctask;
   p.tasks = reinterpret_cast<const int4 *>(pw + hd->off_tasks);
   p.zero = pw + hd->off_zero;
-  p.n_zero = hd->n_zero;
   p.xrows = reinterpret_cast<const int4 *>(pw + hd->off_xrows);
-  p.n_xrows = hd->n_xrows;
+  p.plan_hdr = pw;
+  p.xrows_cap = hd->grid;
   p.xmerge = bkv::dev_switches().planned_xmerge;
   p.cnt = reinterpret_cast<int *>(ws + w.mcnt);
   p.gpiece = reinterpret_cast<float *>(ws + w.o);

@@ -204,9 +204,9 @@ struct PlannedParams {
   const int32_t *ctask;  // [grid + 1]
   const int4 *tasks;     // 2 per task (PlanTask)
   const int32_t *zero;   // {r, h} pairs
-  int n_zero;
   const int4 *xrows;     // rows cut across CTAs (merged by planned_xmerge_kernel when xmerge == 1)
-  int n_xrows;
+  const int32_t *plan_hdr;   // device copy of the PlanHeader: per-step counts (n_zero, n_xrows)
+  int xrows_cap;         // capacity of xrows (sizes the merge kernel's grid; graph-safe)
   int xmerge;            // 0: last-arriver merge inside the kernel; 1: separate stream-ordered merge kernel
   int *cnt;              // [B*H] cross-CTA arrival counters (self-cleaning, zero at rest)
   float *gpiece;         // [2*grid][g*(D+2)] cross-CTA pieces
@@ -229,7 +229,7 @@ cudaError_t launch_planned(const CUtensorMap &tmK, const CUtensorMap &tmV, const
 struct DevSwitches {
   int slots, warps, ctas_per_sm, units_per_warp, min_split /* -1: default */, small_plan, streamk;
   int merge_warps, fused_merge, kv_combined, mha_cuda_cores, prefill_mma_sync, prefill_qt;
-  int mixed_overlap, debug, trace, planned_slots, planned_xmerge;
+  int mixed_overlap, debug, trace, planned_slots, planned_xmerge, planned_dynamic_p;
 };
 const DevSwitches &dev_switches();
 // Immutable per-device properties (cached per device).

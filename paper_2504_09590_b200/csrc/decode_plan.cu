@@ -20,6 +20,10 @@
 //     last CTA to arrive combines them in CTA order (mode 1).  The combine
 //     order is fixed by the plan, so results are run-to-run deterministic.
 //   * Rows with no tokens (reading Q8) get zeros.
+//   * The layout has fixed capacities (offsets depend on num_seqs, kv heads and
+//     the grid only), so a captured CUDA graph replays any later plan of the
+//     same geometry copied into the same device buffer; the kernels read the
+//     per-step counts from the device copy of the header.
 #include <string.h>
 
 #include <algorithm>
@@ -30,15 +34,35 @@
 
 namespace bkv {
 
-size_t plan_words_bound(int B, int H, int grid, int warps) {
-  const size_t W = static_cast<size_t>(grid) * warps, BH = static_cast<size_t>(B) * H;
-  return sizeof(PlanHeader) / 4 + (W + 1 + 4) + 8 * (W + BH) + 4 + (grid + 1 + 4) + 8 * 2 * W + 4 +
-         2 * BH + 4 + 4 * BH + 4;
-}
-
 namespace {
 size_t up4(size_t x) { return (x + 3) & ~size_t(3); }
+
+// Fixed-capacity layout: the array offsets depend only on (B, H, grid, warps), never on
+// the lengths, so a CUDA graph captured with one step's plan stays valid when the next
+// step's plan (same geometry) is copied into the same device buffer.
+struct PlanLayout {
+  size_t off_wseg, off_segs, off_ctask, off_tasks, off_zero, off_xrows, words;
+  size_t cap_segs, cap_tasks, cap_zero, cap_xrows;
+};
+PlanLayout plan_layout(int B, int H, int grid, int warps) {
+  const size_t W = static_cast<size_t>(grid) * warps, BH = static_cast<size_t>(B) * H;
+  PlanLayout l;
+  l.cap_segs = W + BH;        // each warp range starts one segment, each row start another
+  l.cap_tasks = 2 * W;        // a warp has at most two split segments, one task each
+  l.cap_zero = BH;
+  l.cap_xrows = grid;         // each CTA boundary cuts at most one row
+  l.off_wseg = sizeof(PlanHeader) / 4;
+  l.off_segs = up4(l.off_wseg + W + 1);
+  l.off_ctask = up4(l.off_segs + 8 * l.cap_segs);
+  l.off_tasks = up4(l.off_ctask + grid + 1);
+  l.off_zero = up4(l.off_tasks + 8 * l.cap_tasks);
+  l.off_xrows = up4(l.off_zero + 2 * l.cap_zero);
+  l.words = up4(l.off_xrows + 4 * l.cap_xrows);
+  return l;
+}
 }  // namespace
+
+size_t plan_words_bound(int B, int H, int grid, int warps) { return plan_layout(B, H, grid, warps).words; }
 
 // Returns 0 on success, else a message (static string) for the caller's fail().
 const char *build_plan(const int32_t *seq_lens, const int32_t *num_entries, int B, int H, int g, int D,
@@ -116,14 +140,13 @@ const char *build_plan(const int32_t *seq_lens, const int32_t *num_entries, int 
   size_t n_segs = 0, n_tasks = 0;
   for (auto &v : wsegs) n_segs += v.size();
   for (auto &v : ctasks) n_tasks += v.size();
-  const size_t hdr = sizeof(PlanHeader) / 4;
-  const size_t off_wseg = hdr;
-  const size_t off_segs = up4(off_wseg + W + 1);
-  const size_t off_ctask = up4(off_segs + 8 * n_segs);
-  const size_t off_tasks = up4(off_ctask + grid + 1);
-  const size_t off_zero = up4(off_tasks + 8 * n_tasks);
-  const size_t off_xrows = up4(off_zero + zero.size());
-  const size_t words = up4(off_xrows + xrows.size());
+  const PlanLayout lay = plan_layout(B, H, grid, warps);
+  if (n_segs > lay.cap_segs || n_tasks > lay.cap_tasks || zero.size() / 2 > lay.cap_zero ||
+      xrows.size() / 4 > lay.cap_xrows)
+    return "internal: plan exceeds its fixed capacity";
+  const size_t off_wseg = lay.off_wseg, off_segs = lay.off_segs, off_ctask = lay.off_ctask;
+  const size_t off_tasks = lay.off_tasks, off_zero = lay.off_zero, off_xrows = lay.off_xrows;
+  const size_t words = lay.words;
   *used_words = words;
   if (words > out_words) return "plan buffer too small";
   if (words >= (size_t(1) << 31)) return "plan too large";

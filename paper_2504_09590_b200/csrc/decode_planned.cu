@@ -32,6 +32,7 @@
 // fused append of this step's token (bkv_decode_step semantics), dead slots
 // selected to -inf and their V rows zeroed (reading Q10).
 #include <math.h>
+#include <stddef.h>
 
 #include "bkv_internal.h"
 #include "bkv_ptx.cuh"
@@ -601,7 +602,8 @@ __global__ void __launch_bounds__(256, 1)
   // ------------------------------------------------ rows without tokens (Q8)
   {
     const int nw = gridDim.x * W;
-    for (int z = gw; z < p.n_zero; z += nw) {
+    const int n_zero = __ldg(p.plan_hdr + offsetof(PlanHeader, n_zero) / 4);
+    for (int z = gw; z < n_zero; z += nw) {
       const int r = __ldg(p.zero + 2 * z), h = __ldg(p.zero + 2 * z + 1);
       const float o0[EPL] = {};
       for (int head = 0; head < g; ++head) store_row(r, h * g + head, o0, 0.f);
@@ -755,7 +757,7 @@ __global__ void __launch_bounds__(256) planned_xmerge_kernel(const PlannedParams
   const int lane = threadIdx.x & 31;
   const int item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int g = p.g;
-  if (item >= p.n_xrows * g) {
+  if (item >= __ldg(p.plan_hdr + offsetof(PlanHeader, n_xrows) / 4) * g) {
     if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
     return;
   }
@@ -837,9 +839,9 @@ static cudaError_t launch_planned_t(const CUtensorMap &tmK, const CUtensorMap &t
   }
   e = cudaLaunchKernelEx(&lc, planned::planned_kernel<D, G16>, tmK, tmV, p);
   if (e != cudaSuccess) return e;
-  if (p.xmerge && p.n_xrows > 0) {
+  if (p.xmerge) {   // sized by capacity (graph-safe); items beyond the step's count exit
     cudaLaunchConfig_t lm = {};
-    lm.gridDim = dim3((p.n_xrows * p.g + 7) / 8);
+    lm.gridDim = dim3((p.xrows_cap * p.g + 7) / 8);
     lm.blockDim = dim3(256);
     lm.stream = s;
     if (p.pdl) {

@@ -255,3 +255,17 @@ def test_plan_rejects_bad_input():
         _plan(np.array([40], np.int32), 1, 1, 16, 2, 148)
     with pytest.raises(bkv.BkvError):      # group 32 > 16
         _plan(np.array([40], np.int32), 1, 32, 16, 4, 148)
+
+
+def test_plan_layout_is_fixed_by_geometry():
+    """Graph safety: offsets and size depend on (num_seqs, kv heads, SM count) only, so a
+    captured graph replays any later plan of the same geometry from the same buffer."""
+    rng = np.random.default_rng(7)
+    plans = [_plan(rng.integers(0, 3000, 64).astype(np.int32), 2, 8, 16, 256, 148) for _ in range(4)]
+    plans.append(_plan(np.zeros(64, np.int32), 2, 8, 16, 256, 148))
+    plans.append(_plan(np.full(64, 4096, np.int32), 2, 8, 16, 256, 148))
+    hs = [decode(p)[0] for p in plans]
+    keys = ("words", "off_wseg", "off_segs", "off_ctask", "off_tasks", "off_zero", "off_xrows")
+    assert all(len(p) == len(plans[0]) for p in plans)
+    assert all({k: h[k] for k in keys} == {k: hs[0][k] for k in keys} for h in hs)
+    assert all(h["n_xrows"] <= h["grid"] for h in hs)

@@ -182,3 +182,49 @@ def test_planned_in_kernel_cross_cta_merge(cfg, tp, monkeypatch):
     for cfg_s, seed, qs in ATT_CASES:
         o, ref = _planned_case(make_case(cfg_s, seed, q_scale_log2=qs), repeat=2)
         check_close(o, ref, cfg_s)
+
+
+def test_planned_graph_replays_a_new_plan():
+    """A CUDA graph captured with step A's plan replays step B (new lengths, same batch and
+    geometry) once B's plan and lengths are copied into the same device buffers: equal to an
+    eager call with plan B (graph safety of the fixed-capacity plan layout)."""
+    sh = Shape("gr", 16, 2, 128, 16, 40, 0.5, "uniform", 900, 1, 1, uniform_max=900)
+    case_b = make_case(sh, 77)
+    lay = case_b.layout
+    ks, vs, q = dense_case(case_b)
+    K, V, _ = oracle_pool(case_b, ks, vs, 2)
+    ref = oracle.attention(K, V, lay.block_tables, lay.dirs, lay.lens, q, default_scale(128))
+    pool = bkv.KVPool(t_u16(K), t_u16(V))
+    bt, dirs, lens = gpu_map(lay)
+    lens_a = np.maximum(1, lay.lens // 3).astype(np.int32)          # step A: shorter contexts
+    plan = bkv.decode_plan(lens_a, pool, 16, lay.block_tables.shape[1])
+    lens.copy_(torch.from_numpy(lens_a))
+    qd = t_u16(q)
+    out = torch.empty_like(qd)
+    ws = bkv.workspace(lay.batch, 16, 2, 128)
+    bkv.decode_planned(pool, bt, dirs, lens, plan, qd, out=out, ws=ws, pdl=True)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        bkv.decode_planned(pool, bt, dirs, lens, plan, qd, out=out, ws=ws, pdl=True)
+    plan_b = bkv.decode_plan_host(lay.lens, 2, 16, 128, 16, lay.block_tables.shape[1])
+    assert plan_b.nbytes == plan.nbytes
+    plan.dev.copy_(torch.from_numpy(plan_b.view(np.uint8)))
+    lens.copy_(torch.from_numpy(lay.lens.astype(np.int32)))
+    g.replay()
+    torch.cuda.synchronize()
+    check_close(out, ref, "graph replay with plan B")
+    eager = bkv.decode_planned(pool, bt, dirs, lens, bkv.DecodePlan(plan_b, plan.dev, plan.nbytes), qd)
+    torch.cuda.synchronize()
+    assert torch.equal(eager.view(torch.int16), out.view(torch.int16))
+
+
+def test_planned_dynamic_dispatch(monkeypatch):
+    """Plans with long warp ranges (>= BKV_PLANNED_DYNAMIC_P blocks per warp; 128 by default,
+    e.g. OPT-30B on one GPU) run the dynamically scheduled kernel pair: forced here for a
+    full-size Llama-70B TP8 shard and the small cases -- every element vs the oracle."""
+    monkeypatch.setenv("BKV_PLANNED_DYNAMIC_P", "1")
+    run_full("llama70b", 8, 4, seed=6, mode="step", planned=True, repeat=2)
+    for cfg_s, seed, qs in ATT_CASES:
+        o, ref = _planned_case(make_case(cfg_s, seed, q_scale_log2=qs))
+        check_close(o, ref, cfg_s)
