@@ -282,7 +282,7 @@ def measure_shards(dev, peak, seed, replays=60, warm=10):
         vn = torch.randn((layers, B, H, d), device=dev).to(torch.bfloat16)
         out = torch.empty((B, Hq, d), dtype=torch.bfloat16, device=dev)
         ws = bkv.workspace(B, Hq, H, d, dev)
-        plan = bkv.decode_plan(lay.lens, pools[0], Hq, lay.block_tables.shape[1])
+        plan = bkv.decode_plan(lay.lens, lay.block_tables, lay.dirs, pools[0], Hq)
 
         def body():
             for l in range(layers):
@@ -366,8 +366,9 @@ def run_ours(args):
     # ---- per-step inputs (host-pinned originals for the e2e leg), incl. the step's split plan
     nent_h = lay.num_entries if args.general_map else None
 
-    def host_plan():
-        return bkv.decode_plan_host(lay.lens, H, Hq, d, bs, bt_stride, num_entries=nent_h)
+    def host_plan():   # the host scheduler's plan of the step: lengths + block map -> flattened work list
+        return bkv.decode_plan_host(lay.lens, lay.block_tables, lay.dirs, H, Hq, d, bs,
+                                    fills=lay.fills if args.general_map else None, num_entries=nent_h)
 
     plan_np = host_plan()
     meta_h = {
@@ -548,13 +549,18 @@ def run_ours(args):
     def h2d(si):
         s = sets[si]
         ev_h2d[si].synchronize()                          # this set's pinned plan buffer is free again
-        s["plan_h"].copy_(torch.from_numpy(host_plan().view(np.uint8)))   # the host scheduler's plan
+        hp = host_plan()                                  # the host scheduler's plan of this step
+        used = bkv.plan_used_bytes(hp)
+        s["plan_h"][:used].copy_(torch.from_numpy(hp.view(np.uint8)[:used]))
         with torch.cuda.stream(up):
             n = 0
             for k, v in meta_h.items():
-                srcv = s["plan_h"] if k == "plan" else v
-                s["md"][k].copy_(srcv, non_blocking=True)
-                n += srcv.numel() * srcv.element_size()
+                if k == "plan":                           # the plan's used bytes (fixed layout, entries last)
+                    s["md"][k][:used].copy_(s["plan_h"][:used], non_blocking=True)
+                    n += used
+                    continue
+                s["md"][k].copy_(v, non_blocking=True)
+                n += v.numel() * v.element_size()
             for dst, srcv in ((s["q"], q_h), (s["kn"], kn_h), (s["vn"], vn_h)):
                 dst.copy_(srcv, non_blocking=True)
                 n += srcv.numel() * srcv.element_size()

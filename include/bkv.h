@@ -463,28 +463,37 @@ BKV_API bkv_status bkv_validate_block_map_host(const bkv_block_map *map, const i
  * depends only on the lengths (and entry counts) and on the device's SM
  * count: identical on every rank of a head-sharded TP group.
  *
- * bkv_decode_plan_bytes -- an upper bound on the plan size (bytes) for
- *   num_seqs requests and num_kv_heads local kv heads on a device with num_sms
- *   SMs (0: the CURRENT device).  Returns 0 on an invalid argument (see
- *   bkv_last_error).
+ * bkv_decode_plan_bytes -- the plan capacity (bytes) for num_seqs requests,
+ *   num_kv_heads local kv heads and block tables of bt_stride entries per
+ *   request, on a device with num_sms SMs (0: the CURRENT device).  The layout
+ *   depends on nothing else, so one buffer of this size serves every step.
+ *   Returns 0 on an invalid argument (see bkv_last_error).
  *
  * bkv_decode_plan -- host only; no CUDA call unless num_sms = 0 (then one
  *   cached query of the current device's SM count).
  *   seq_lens     HOST int32 [num_seqs]: resident lengths the layer calls will
  *                receive (after this step's append), >= 0
- *   num_entries  HOST int32 [num_seqs] for a general map (f3), else NULL
- *   bt_stride    the block map's bt_stride (bounds the entries per request)
+ *   map          the step's block map with HOST pointers (block_tables,
+ *                dirs, and fills/num_entries for a general map, f3) -- the
+ *                plan carries it flattened in warp order, packed per entry
+ *                (block id < 2^25, direction, live tokens, last-entry bit),
+ *                so the layer kernels read no block table
  *   num_kv_heads, num_q_heads, head_dim, block_size: the layer geometry
  *   num_sms      SM count of the device that will run it (0: current device);
  *                bkv_decode_planned rejects a plan made for another count
  *   plan         HOST buffer, 16-byte aligned, plan_bytes long, written
- *   *plan_bytes_used (optional) bytes of the plan (also on
- *                BKV_ERR_WORKSPACE_TOO_SMALL: the size needed)
- *   The caller copies plan[0, *plan_bytes_used) to device memory (one H2D
- *   with the step's other metadata) and passes both copies to every layer.
- *   Errors: BKV_ERR_INVALID_ARGUMENT (negative length, entries > bt_stride,
- *   problem >= 2^30 blocks x heads), BKV_ERR_UNSUPPORTED (geometry outside
- *   the built set), BKV_ERR_WORKSPACE_TOO_SMALL (plan_bytes too small).
+ *   *plan_bytes_used (optional) bytes of the plan the step must upload (the
+ *                layout is fixed; the used bytes end with the step's entries)
+ *   The caller copies plan[0, *plan_bytes_used) to a device buffer of
+ *   bkv_decode_plan_bytes (one H2D with the step's other metadata) and passes
+ *   both copies to every layer.  Fixed layout: a CUDA graph captured with one
+ *   step's plan replays any later plan of the same geometry copied into the
+ *   same device buffer.
+ *   Errors: BKV_ERR_INVALID_ARGUMENT (negative length, entries > bt_stride, a
+ *   block id >= 2^25, a direction not 0/1, a fill outside [1, block_size] or
+ *   fills not summing to the length, problem >= 2^30 blocks x heads),
+ *   BKV_ERR_UNSUPPORTED (geometry outside the built set),
+ *   BKV_ERR_WORKSPACE_TOO_SMALL (plan_bytes below the capacity).
  *
  * bkv_decode_planned -- one layer: decode attention (k_new = v_new = NULL,
  *   semantics of bkv_paged_decode_attention_ex) or the fused decode step
@@ -493,6 +502,8 @@ BKV_API bkv_status bkv_validate_block_map_host(const bkv_block_map *map, const i
  *   none).  ONE kernel launch.
  *   plan_host    the buffer bkv_decode_plan wrote (only its header is read)
  *   plan_dev     device copy of it, 16-byte aligned
+ *   map          the step's block map (device pointers): the plan already holds
+ *                it flattened; read by the dynamically scheduled path below
  *   seq_lens     device int32 [num_seqs], the lengths the plan was built from
  *   workspace    as bkv_paged_decode_attention (bkv_decode_workspace_size;
  *                zero-initialised once: the kernel leaves its counters zero)
@@ -510,11 +521,11 @@ BKV_API bkv_status bkv_validate_block_map_host(const bkv_block_map *map, const i
  *   plan's geometry (num_seqs, heads, group, head_dim, block_size, dense or
  *   general map, SM count) does not match the call.
  */
-BKV_API size_t bkv_decode_plan_bytes(int32_t num_seqs, int32_t num_kv_heads, int32_t num_sms);
-BKV_API bkv_status bkv_decode_plan(const int32_t *seq_lens, const int32_t *num_entries, int32_t num_seqs,
-                                   int32_t bt_stride, int32_t num_kv_heads, int32_t num_q_heads,
-                                   int32_t head_dim, int32_t block_size, int32_t num_sms, void *plan,
-                                   size_t plan_bytes, size_t *plan_bytes_used);
+BKV_API size_t bkv_decode_plan_bytes(int32_t num_seqs, int32_t num_kv_heads, int32_t bt_stride,
+                                     int32_t num_sms);
+BKV_API bkv_status bkv_decode_plan(const int32_t *seq_lens, const bkv_block_map *map, int32_t num_kv_heads,
+                                   int32_t num_q_heads, int32_t head_dim, int32_t block_size, int32_t num_sms,
+                                   void *plan, size_t plan_bytes, size_t *plan_bytes_used);
 BKV_API bkv_status bkv_decode_planned(const bkv_kv_pool *pool, const bkv_block_map *map,
                                       const int32_t *seq_lens, const void *plan_host, const void *plan_dev,
                                       const void *k_new, const void *v_new, const void *q,

@@ -12,6 +12,7 @@ import os
 import threading
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -105,9 +106,9 @@ def lib():
                 L.bkv_kv_checkpoint.restype = ctypes.c_int
                 L.bkv_kv_restore.argtypes = [ctypes.POINTER(_Pool), P, i32, P, P, P]
                 L.bkv_kv_restore.restype = ctypes.c_int
-                L.bkv_decode_plan_bytes.argtypes = [i32, i32, i32]
+                L.bkv_decode_plan_bytes.argtypes = [i32, i32, i32, i32]
                 L.bkv_decode_plan_bytes.restype = ctypes.c_size_t
-                L.bkv_decode_plan.argtypes = [P, P, i32, i32, i32, i32, i32, i32, i32, P, ctypes.c_size_t,
+                L.bkv_decode_plan.argtypes = [P, ctypes.POINTER(_Map), i32, i32, i32, i32, i32, P, ctypes.c_size_t,
                                               ctypes.POINTER(ctypes.c_size_t)]
                 L.bkv_decode_plan.restype = ctypes.c_int
                 L.bkv_decode_planned.argtypes = [
@@ -501,47 +502,74 @@ def reload_dev_switches():
 class DecodePlan:
     """A host-built split plan of one decode step (bkv_decode_plan) and its device copy.
 
-    Built from the scheduler's HOST lengths once per step; every layer's
+    Built from the scheduler's HOST lengths and block map once per step; every layer's
     :func:`decode_planned` call reuses it."""
 
     def __init__(self, host, dev, nbytes):
         self.host = host          # numpy int32 buffer (the header is read by each call)
-        self.dev = dev            # torch uint8 device tensor holding the same bytes
-        self.nbytes = nbytes
+        self.dev = dev            # torch uint8 device tensor holding the same bytes (capacity-sized)
+        self.nbytes = nbytes      # bytes a step uploads (the layout is fixed; the tail is the entry list)
 
     @property
     def header(self):
         names = ("magic", "version", "words", "B", "H", "g", "D", "bs", "general", "grid", "warps", "P",
                  "n_segs", "n_tasks", "n_zero", "total", "off_wseg", "off_segs", "off_ctask", "off_tasks",
-                 "off_zero", "max_pieces", "max_entries", "off_xrows", "n_xrows")
+                 "off_zero", "max_pieces", "max_entries", "off_xrows", "n_xrows", "off_ent", "n_ent")
         return {n: int(self.host[i]) for i, n in enumerate(names)}
 
+    def upload(self, host, stream=None):
+        """Copy a later step's plan (same geometry) into this plan's device buffer."""
+        t = torch.from_numpy(np.asarray(host).view(np.uint8))
+        self.dev[:t.numel()].copy_(t, non_blocking=False)
+        self.host = host
 
-def decode_plan_host(seq_lens, num_kv_heads, num_q_heads, head_dim, block_size, bt_stride,
-                     num_entries=None, num_sms=0):
-    """bkv_decode_plan on host arrays -> numpy int32 plan buffer (no device copy).
-    ``num_sms`` = 0 plans for the current device (needs a GPU); > 0 plans for that SM count."""
-    import numpy as np
+
+def _host_map(block_tables, dirs, fills=None, num_entries=None):
+    bt = np.ascontiguousarray(np.asarray(block_tables), dtype=np.int32)
+    dd = np.ascontiguousarray(np.asarray(dirs), dtype=np.uint8)
+    rs, cs = (1, 0) if dd.ndim == 1 else (dd.shape[1], 1)
+    keep = [bt, dd]
+    if fills is None:
+        m = _Map(bt.ctypes.data, bt.shape[1], dd.ctypes.data, rs, cs, bt.shape[0], None, 0, None)
+    else:
+        f = np.ascontiguousarray(np.asarray(fills), dtype=np.uint8)
+        ne = np.ascontiguousarray(np.asarray(num_entries), dtype=np.int32)
+        keep += [f, ne]
+        m = _Map(bt.ctypes.data, bt.shape[1], dd.ctypes.data, rs, cs, bt.shape[0], f.ctypes.data, f.shape[1],
+                 ne.ctypes.data)
+    return m, keep
+
+
+def decode_plan_host(seq_lens, block_tables, dirs, num_kv_heads, num_q_heads, head_dim, block_size,
+                     fills=None, num_entries=None, num_sms=0):
+    """bkv_decode_plan on host arrays (lengths and the step's block map) -> numpy int32 plan
+    (capacity-sized view; the first ``nbytes`` bytes are the step's upload, see .nbytes of
+    :class:`DecodePlan`).  ``num_sms`` = 0 plans for the current device (needs a GPU)."""
     ln = np.ascontiguousarray(np.asarray(seq_lens), dtype=np.int32)
-    ne = None if num_entries is None else np.ascontiguousarray(np.asarray(num_entries), dtype=np.int32)
-    B = ln.shape[0]
-    cap = lib().bkv_decode_plan_bytes(B, int(num_kv_heads), int(num_sms))
+    m, keep = _host_map(block_tables, dirs, fills, num_entries)
+    cap = lib().bkv_decode_plan_bytes(m.num_seqs, int(num_kv_heads), m.bt_stride, int(num_sms))
     if cap == 0:
         raise BkvError("bkv_decode_plan_bytes: " + lib().bkv_last_error().decode())
     buf = np.zeros((cap + 15) // 4 + 4, dtype=np.int32)
     off = (-buf.ctypes.data) % 16 // 4            # 16-byte aligned view
     view = buf[off:off + cap // 4]
     used = ctypes.c_size_t(0)
-    rc = lib().bkv_decode_plan(ln.ctypes.data, None if ne is None else ne.ctypes.data, B, int(bt_stride),
-                               int(num_kv_heads), int(num_q_heads), int(head_dim), int(block_size),
-                               int(num_sms), view.ctypes.data, view.nbytes, ctypes.byref(used))
+    rc = lib().bkv_decode_plan(ln.ctypes.data, ctypes.byref(m), int(num_kv_heads), int(num_q_heads),
+                               int(head_dim), int(block_size), int(num_sms), view.ctypes.data, view.nbytes,
+                               ctypes.byref(used))
+    del keep
     _check(rc, "bkv_decode_plan")
-    return view[:used.value // 4]   # (a view: keeps the aligned buffer alive)
+    return view   # (a view: keeps the aligned buffer alive)
 
 
-def decode_plan(seq_lens_host, pool_or_geom, num_q_heads, bt_stride, num_entries_host=None, device=None,
-                stream=None):
-    """Build the step's plan on the host and copy it to the device (non_blocking on ``stream``).
+def plan_used_bytes(host):
+    """Bytes of a host plan a step must upload (header words: off_ent + n_ent entries)."""
+    return 4 * (int(host[25]) + int(host[26]))
+
+
+def decode_plan(seq_lens_host, block_tables_host, dirs_host, pool_or_geom, num_q_heads, fills_host=None,
+                num_entries_host=None, device=None, stream=None):
+    """Build the step's plan on the host and copy it to a device buffer of the plan capacity.
 
     ``pool_or_geom``: a KVPool (geometry taken from it) or a tuple (num_kv_heads, head_dim, block_size)."""
     if isinstance(pool_or_geom, KVPool):
@@ -549,16 +577,18 @@ def decode_plan(seq_lens_host, pool_or_geom, num_q_heads, bt_stride, num_entries
         device = pool_or_geom.k.device if device is None else device
     else:
         H, d, bs = pool_or_geom
-    host = decode_plan_host(seq_lens_host, H, num_q_heads, d, bs, bt_stride, num_entries_host)
+    host = decode_plan_host(seq_lens_host, block_tables_host, dirs_host, H, num_q_heads, d, bs, fills_host,
+                            num_entries_host)
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-    t = torch.from_numpy(host.view("uint8"))
+    t = torch.from_numpy(host.view(np.uint8))
     s = torch.cuda.current_stream(dev) if stream is None else stream
     with torch.cuda.stream(s):
         d_t = torch.empty(t.numel() + 16, dtype=torch.uint8, device=dev)
         off = (-d_t.data_ptr()) % 16
         d_t = d_t[off:off + t.numel()]
-        d_t.copy_(t)     # synchronous-enough: the host buffer is pageable, the copy completes before return
-    return DecodePlan(host, d_t, t.numel())
+        n = plan_used_bytes(host)
+        d_t[:n].copy_(t[:n])   # pageable source: complete on return
+    return DecodePlan(host, d_t, n)
 
 
 def decode_planned(pool: KVPool, block_tables, dirs, seq_lens, plan: DecodePlan, q, k_new=None, v_new=None,
@@ -596,7 +626,6 @@ def decode_planned(pool: KVPool, block_tables, dirs, seq_lens, plan: DecodePlan,
 
 def validate_layout_host(block_tables, dirs, seq_lens, num_blocks, block_size, require_nonempty=True):
     """Host validator (I1-I4) on CPU tensors / numpy arrays.  Returns (ok, info[5])."""
-    import numpy as np
     bt = np.ascontiguousarray(np.asarray(block_tables), dtype=np.int32)
     dd = np.ascontiguousarray(np.asarray(dirs), dtype=np.uint8)
     ln = np.ascontiguousarray(np.asarray(seq_lens), dtype=np.int32)
@@ -614,7 +643,6 @@ def validate_block_map_host(block_tables, dirs, seq_lens, num_blocks, block_size
                             num_entries=None, require_nonempty=True):
     """bkv_validate_block_map_host on host arrays (dense, or general with fills/num_entries).
     Returns (ok, info[5])."""
-    import numpy as np
     bt = np.ascontiguousarray(np.asarray(block_tables), dtype=np.int32)
     dd = np.ascontiguousarray(np.asarray(dirs), dtype=np.uint8)
     ln = np.ascontiguousarray(np.asarray(seq_lens), dtype=np.int32)

@@ -861,22 +861,23 @@ static bkv_status plan_sms(int32_t num_sms, int *sms) {
   return BKV_OK;
 }
 
-size_t bkv_decode_plan_bytes(int32_t num_seqs, int32_t num_kv_heads, int32_t num_sms) {
-  if (num_seqs < 0 || num_kv_heads <= 0) {
-    fail(BKV_ERR_INVALID_ARGUMENT, "num_seqs < 0 or num_kv_heads <= 0");
+size_t bkv_decode_plan_bytes(int32_t num_seqs, int32_t num_kv_heads, int32_t bt_stride, int32_t num_sms) {
+  if (num_seqs < 0 || num_kv_heads <= 0 || bt_stride <= 0) {
+    fail(BKV_ERR_INVALID_ARGUMENT, "num_seqs < 0, num_kv_heads <= 0 or bt_stride <= 0");
     return 0;
   }
   int sms = 0;
   if (plan_sms(num_sms, &sms)) return 0;
-  return 4 * bkv::plan_words_bound(num_seqs, num_kv_heads, sms, bkv::kPlannedWarps);
+  return 4 * bkv::plan_words_bound(num_seqs, num_kv_heads, bt_stride, sms, bkv::kPlannedWarps);
 }
 
-bkv_status bkv_decode_plan(const int32_t *seq_lens, const int32_t *num_entries, int32_t num_seqs,
-                           int32_t bt_stride, int32_t num_kv_heads, int32_t num_q_heads, int32_t head_dim,
-                           int32_t block_size, int32_t num_sms, void *plan, size_t plan_bytes,
-                           size_t *plan_bytes_used) {
-  if (num_seqs < 0 || (num_seqs > 0 && !seq_lens) || !plan)
-    return fail(BKV_ERR_INVALID_ARGUMENT, "seq_lens/plan is NULL or num_seqs < 0");
+bkv_status bkv_decode_plan(const int32_t *seq_lens, const bkv_block_map *map, int32_t num_kv_heads,
+                           int32_t num_q_heads, int32_t head_dim, int32_t block_size, int32_t num_sms, void *plan,
+                           size_t plan_bytes, size_t *plan_bytes_used) {
+  bkv_status st = check_map(map);
+  if (st) return st;
+  const int num_seqs = map->num_seqs, bt_stride = map->bt_stride;
+  if ((num_seqs > 0 && !seq_lens) || !plan) return fail(BKV_ERR_INVALID_ARGUMENT, "seq_lens/plan is NULL");
   if (num_seqs > bkv::kMaxSeqs) return fail(BKV_ERR_UNSUPPORTED, "num_seqs %d > %d", num_seqs, bkv::kMaxSeqs);
   if (num_kv_heads <= 0 || num_kv_heads > bkv::kMaxKvHeads)
     return fail(BKV_ERR_UNSUPPORTED, "num_kv_heads %d outside [1, %d]", num_kv_heads, bkv::kMaxKvHeads);
@@ -888,16 +889,23 @@ bkv_status bkv_decode_plan(const int32_t *seq_lens, const int32_t *num_entries, 
   if (head_dim != 64 && head_dim != 128) return fail(BKV_ERR_UNSUPPORTED, "head_dim %d not in {64, 128}", head_dim);
   if (block_size != 16 && block_size != 32)
     return fail(BKV_ERR_UNSUPPORTED, "block_size %d not in {16, 32}", block_size);
-  if (bt_stride <= 0 || bt_stride > bkv::kMaxEntries)
+  if (bt_stride > bkv::kMaxEntries)
     return fail(BKV_ERR_UNSUPPORTED, "bt_stride %d outside [1, %d]", bt_stride, bkv::kMaxEntries);
   if ((reinterpret_cast<uintptr_t>(plan) & 15u) != 0) return fail(BKV_ERR_INVALID_ARGUMENT, "plan must be 16-byte aligned");
   int sms = 0;
-  bkv_status st = plan_sms(num_sms, &sms);
-  if (st) return st;
+  if ((st = plan_sms(num_sms, &sms))) return st;
+  bkv::HostMap hm;
+  hm.bt = map->block_tables;
+  hm.bt_stride = bt_stride;
+  hm.dirs = map->dirs;
+  hm.dir_rs = map->dir_row_stride;
+  hm.dir_cs = map->dir_col_stride;
+  hm.fills = map->fills;
+  hm.fill_rs = map->fill_row_stride;
+  hm.nent = map->num_entries;
   size_t used = 0;
-  const char *msg = bkv::build_plan(seq_lens, num_entries, num_seqs, num_kv_heads, g, head_dim, block_size,
-                                    bt_stride, sms, bkv::kPlannedWarps, static_cast<int32_t *>(plan),
-                                    plan_bytes / 4, &used);
+  const char *msg = bkv::build_plan(seq_lens, hm, num_seqs, num_kv_heads, g, head_dim, block_size, sms,
+                                    bkv::kPlannedWarps, static_cast<int32_t *>(plan), plan_bytes / 4, &used);
   if (plan_bytes_used) *plan_bytes_used = used * 4;
   if (msg) return fail(strstr(msg, "too small") ? BKV_ERR_WORKSPACE_TOO_SMALL : BKV_ERR_INVALID_ARGUMENT,
                        "bkv_decode_plan: %s", msg);
@@ -1015,6 +1023,7 @@ bkv_status bkv_decode_planned(const bkv_kv_pool *pool, const bkv_block_map *map,
   p.zero = pw + hd->off_zero;
   p.xrows = reinterpret_cast<const int4 *>(pw + hd->off_xrows);
   p.plan_hdr = pw;
+  p.ent = reinterpret_cast<const uint32_t *>(pw + hd->off_ent);
   p.xrows_cap = hd->grid;
   p.xmerge = bkv::dev_switches().planned_xmerge;
   p.cnt = reinterpret_cast<int *>(ws + w.mcnt);

@@ -164,8 +164,12 @@ struct PlanHeader {
   int32_t max_pieces;                        // largest n of a cross-CTA row
   int32_t max_entries;                       // bt_stride the plan was checked against
   int32_t off_xrows, n_xrows;                // int4 [n_xrows] {r, h, c0, n | flag0 << 16}: rows cut across CTAs
-  int32_t reserved[7];
+  int32_t off_ent, n_ent;                    // uint32 [total]: the step's entries in flattened (r, h, e) order
+  int32_t reserved[5];
 };
+// packed flattened entry: block id | direction << 25 | (live tokens - 1) << 26 | last entry of the row << 31
+constexpr uint32_t kEntBlockMask = (1u << 25) - 1;
+constexpr int kEntDirShift = 25, kEntFillShift = 26, kEntLastShift = 31;
 static_assert(sizeof(PlanHeader) == 32 * 4, "plan header is 32 words");
 // A merge task (two int4) combines the pieces of one (request r, kv head h) row
 // that lie in warps wa..wb of one CTA (piece k in warp wa+k: shared-memory slot
@@ -177,10 +181,18 @@ struct PlanTask {
   int32_t r, h, warps, mode;   // warps = wa | wb << 8 | wa_slot << 16 (CTA-local warp ids)
   int32_t c0, n, flag0, gslot;
 };
-size_t plan_words_bound(int B, int H, int grid, int warps);
-const char *build_plan(const int32_t *seq_lens, const int32_t *num_entries, int B, int H, int g, int D,
-                       int bs, int max_entries, int grid, int warps, int32_t *out, size_t out_words,
-                       size_t *used_words);
+size_t plan_words_bound(int B, int H, int bt_stride, int grid, int warps);
+struct HostMap {   // the host copy of a step's block map (bkv_block_map with host pointers)
+  const int32_t *bt;
+  int bt_stride;
+  const uint8_t *dirs;
+  int dir_rs, dir_cs;
+  const uint8_t *fills;   // general map or nullptr
+  int fill_rs;
+  const int32_t *nent;
+};
+const char *build_plan(const int32_t *seq_lens, const HostMap &map, int B, int H, int g, int D, int bs, int grid,
+                       int warps, int32_t *out, size_t out_words, size_t *used_words);
 constexpr int kPlannedWarps = 8;             // warps per CTA of the planned kernel
 
 struct PlannedParams {
@@ -205,7 +217,8 @@ struct PlannedParams {
   const int4 *tasks;     // 2 per task (PlanTask)
   const int32_t *zero;   // {r, h} pairs
   const int4 *xrows;     // rows cut across CTAs (merged by planned_xmerge_kernel when xmerge == 1)
-  const int32_t *plan_hdr;   // device copy of the PlanHeader: per-step counts (n_zero, n_xrows)
+  const int32_t *plan_hdr;   // device copy of the PlanHeader: per-step values (P, n_zero, n_xrows)
+  const uint32_t *ent;       // packed flattened entries (block, dir, fill, last) in warp order
   int xrows_cap;         // capacity of xrows (sizes the merge kernel's grid; graph-safe)
   int xmerge;            // 0: last-arriver merge inside the kernel; 1: separate stream-ordered merge kernel
   int *cnt;              // [B*H] cross-CTA arrival counters (self-cleaning, zero at rest)

@@ -19,6 +19,10 @@
 //     cut across CTAs has one combined piece per CTA in the workspace; the
 //     last CTA to arrive combines them in CTA order (mode 1).  The combine
 //     order is fixed by the plan, so results are run-to-run deterministic.
+//   * The step's block map travels inside the plan, flattened in the same order
+//     and packed (block id, direction, live tokens, last-entry bit): a warp's
+//     blocks are a contiguous slice of that list, so the kernel reads no block
+//     table and its first tile needs one dependent load.
 //   * Rows with no tokens (reading Q8) get zeros.
 //   * The layout has fixed capacities (offsets depend on num_seqs, kv heads and
 //     the grid only), so a captured CUDA graph replays any later plan of the
@@ -41,10 +45,10 @@ size_t up4(size_t x) { return (x + 3) & ~size_t(3); }
 // the lengths, so a CUDA graph captured with one step's plan stays valid when the next
 // step's plan (same geometry) is copied into the same device buffer.
 struct PlanLayout {
-  size_t off_wseg, off_segs, off_ctask, off_tasks, off_zero, off_xrows, words;
-  size_t cap_segs, cap_tasks, cap_zero, cap_xrows;
+  size_t off_wseg, off_segs, off_ctask, off_tasks, off_zero, off_xrows, off_ent, words;
+  size_t cap_segs, cap_tasks, cap_zero, cap_xrows, cap_ent;
 };
-PlanLayout plan_layout(int B, int H, int grid, int warps) {
+PlanLayout plan_layout(int B, int H, int bt_stride, int grid, int warps) {
   const size_t W = static_cast<size_t>(grid) * warps, BH = static_cast<size_t>(B) * H;
   PlanLayout l;
   l.cap_segs = W + BH;        // each warp range starts one segment, each row start another
@@ -57,18 +61,23 @@ PlanLayout plan_layout(int B, int H, int grid, int warps) {
   l.off_tasks = up4(l.off_ctask + grid + 1);
   l.off_zero = up4(l.off_tasks + 8 * l.cap_tasks);
   l.off_xrows = up4(l.off_zero + 2 * l.cap_zero);
-  l.words = up4(l.off_xrows + 4 * l.cap_xrows);
+  l.cap_ent = BH * static_cast<size_t>(bt_stride);   // last: the bytes a step uploads end with its entries
+  l.off_ent = up4(l.off_xrows + 4 * l.cap_xrows);
+  l.words = up4(l.off_ent + l.cap_ent);
   return l;
 }
 }  // namespace
 
-size_t plan_words_bound(int B, int H, int grid, int warps) { return plan_layout(B, H, grid, warps).words; }
+size_t plan_words_bound(int B, int H, int bt_stride, int grid, int warps) {
+  return plan_layout(B, H, bt_stride, grid, warps).words;
+}
 
 // Returns 0 on success, else a message (static string) for the caller's fail().
-const char *build_plan(const int32_t *seq_lens, const int32_t *num_entries, int B, int H, int g, int D,
-                       int bs, int max_entries, int grid, int warps, int32_t *out, size_t out_words,
-                       size_t *used_words) {
+const char *build_plan(const int32_t *seq_lens, const HostMap &map, int B, int H, int g, int D, int bs, int grid,
+                       int warps, int32_t *out, size_t out_words, size_t *used_words) {
   const int W = grid * warps;
+  const int32_t *num_entries = map.fills ? map.nent : nullptr;
+  const int max_entries = map.bt_stride;
   std::vector<int64_t> pre(B + 1, 0);
   for (int r = 0; r < B; ++r) {
     const int32_t L = seq_lens[r];
@@ -140,17 +149,43 @@ const char *build_plan(const int32_t *seq_lens, const int32_t *num_entries, int 
   size_t n_segs = 0, n_tasks = 0;
   for (auto &v : wsegs) n_segs += v.size();
   for (auto &v : ctasks) n_tasks += v.size();
-  const PlanLayout lay = plan_layout(B, H, grid, warps);
+  const PlanLayout lay = plan_layout(B, H, max_entries, grid, warps);
   if (n_segs > lay.cap_segs || n_tasks > lay.cap_tasks || zero.size() / 2 > lay.cap_zero ||
       xrows.size() / 4 > lay.cap_xrows)
     return "internal: plan exceeds its fixed capacity";
   const size_t off_wseg = lay.off_wseg, off_segs = lay.off_segs, off_ctask = lay.off_ctask;
   const size_t off_tasks = lay.off_tasks, off_zero = lay.off_zero, off_xrows = lay.off_xrows;
-  const size_t words = lay.words;
+  const size_t off_ent = lay.off_ent;
+  const size_t words = off_ent + static_cast<size_t>(N);   // used bytes (the capacity is lay.words)
   *used_words = words;
-  if (words > out_words) return "plan buffer too small";
-  if (words >= (size_t(1) << 31)) return "plan too large";
-  memset(out, 0, words * 4);
+  if (lay.words > out_words) return "plan buffer too small";
+  if (lay.words >= (size_t(1) << 31)) return "plan too large";
+  // the step's entries in flattened (r, h, e) order, packed: block | dir << 25 | (n - 1) << 26 | last << 31
+  // (dense map: every entry but the last holds bs tokens; general map: the entry's fill, f3)
+  std::vector<uint32_t> row_ent;
+  uint32_t *ent = reinterpret_cast<uint32_t *>(out + off_ent);
+  size_t pos = 0;
+  for (int r = 0; r < B; ++r) {
+    const int nb = static_cast<int>(pre[r + 1] - pre[r]);
+    row_ent.resize(nb);
+    int64_t sum = 0;
+    for (int e = 0; e < nb; ++e) {
+      const int64_t blk = map.bt[static_cast<int64_t>(r) * map.bt_stride + e];
+      const int dir = map.dirs[static_cast<int64_t>(r) * map.dir_rs + static_cast<int64_t>(e) * map.dir_cs];
+      const int n = map.fills ? map.fills[static_cast<int64_t>(r) * map.fill_rs + e]
+                              : static_cast<int>(std::min<int64_t>(bs, seq_lens[r] - static_cast<int64_t>(e) * bs));
+      if (blk < 0 || blk > static_cast<int64_t>(kEntBlockMask)) return "a block id is negative or >= 2^25";
+      if (dir < 0 || dir > 1) return "a direction flag is not 0 or 1";
+      if (n < 1 || n > bs) return "an entry holds no token or more than block_size (fills)";
+      sum += n;
+      row_ent[e] = static_cast<uint32_t>(blk) | (static_cast<uint32_t>(dir) << kEntDirShift) |
+                   (static_cast<uint32_t>(n - 1) << kEntFillShift) | (e == nb - 1 ? 1u << kEntLastShift : 0u);
+    }
+    if (map.fills && sum != seq_lens[r]) return "seq_lens[r] differs from the sum of its fills";
+    for (int h = 0; h < H; ++h)
+      for (int e = 0; e < nb; ++e) ent[pos++] = row_ent[e];
+  }
+  memset(out, 0, off_ent * 4);
   PlanHeader *hd = reinterpret_cast<PlanHeader *>(out);
   hd->magic = kPlanMagic;
   hd->version = kPlanVersion;
@@ -177,6 +212,8 @@ const char *build_plan(const int32_t *seq_lens, const int32_t *num_entries, int 
   hd->max_entries = max_entries;
   hd->off_xrows = static_cast<int32_t>(off_xrows);
   hd->n_xrows = static_cast<int32_t>(xrows.size() / 4);
+  hd->off_ent = static_cast<int32_t>(off_ent);
+  hd->n_ent = N;
   int32_t *wseg = out + off_wseg, *segs = out + off_segs, *ctask = out + off_ctask, *tasks = out + off_tasks;
   size_t k = 0;
   for (int w = 0; w < W; ++w) {
@@ -186,7 +223,7 @@ const char *build_plan(const int32_t *seq_lens, const int32_t *num_entries, int 
       segs[8 * k + 1] = s.h;
       segs[8 * k + 2] = s.e0;
       segs[8 * k + 3] = s.e1 | (s.split << kPlanSplitBit);
-      segs[8 * k + 4] = seq_lens[s.r];                                // L of the row
+      segs[8 * k + 4] = seq_lens[s.r];                                // L of the row (informational)
       segs[8 * k + 5] = static_cast<int32_t>(pre[s.r + 1] - pre[s.r]); // its entries
       ++k;
     }

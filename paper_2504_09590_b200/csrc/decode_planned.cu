@@ -168,26 +168,32 @@ __global__ void __launch_bounds__(256, 1)
   if (p.pdl) asm volatile("griddepcontrol.launch_dependents;");
 
   // ---------------------------------------------------------- pre-wait reads
-  // The plan, seq_lens and the block map are step metadata (BKV_FLAG_PDL
-  // contract: not written by the immediately preceding kernel), so they are
-  // read while that kernel drains.  Lane i holds segment s0 + i.
+  // The plan is step metadata (BKV_FLAG_PDL contract: not written by the
+  // immediately preceding kernel), so it is read while that kernel drains.  It
+  // carries the step's block map already flattened in warp order: warp w's
+  // blocks are entries [w P, w P + n) of the packed entry list (block id,
+  // direction, live tokens, last-entry bit), so the first TMA needs ONE
+  // dependent load, issued together with the segment descriptors.
+  const int P = __ldg(p.plan_hdr + offsetof(PlanHeader, P) / 4);
   const int s0 = __ldg(p.wseg + gw), s1 = __ldg(p.wseg + gw + 1);
+  const int ent0 = gw * P;                          // the warp's first flattened entry
   int4 sg_l = make_int4(0, 0, 0, 0);
-  int L_l = 0, nb_l = 0;
   auto load_segs = [&](int first) {
     const int si = first + lane;
-    if (si < s1) {   // (the plan carries each row's length and entry count)
-      sg_l = __ldg(p.segs + 2 * si);
-      const int4 ln = __ldg(p.segs + 2 * si + 1);
-      L_l = ln.x;
-      nb_l = ln.y;
-    }
+    if (si < s1) sg_l = __ldg(p.segs + 2 * si);
   };
   int seg_base = s0;
   load_segs(seg_base);
+  uint32_t ent_w = 0;                               // lane i: packed entry ent0 + ent_base + i
+  int ent_base = 0;
+  auto load_ents = [&](int first) {
+    ent_base = first;
+    if (first + lane < P) ent_w = __ldg(p.ent + ent0 + first + lane);
+  };
+  load_ents(0);
 
   struct SegInfo {
-    int si, r, h, L, nb, e0, e1, split;
+    int si, r, h, e0, e1, split;
   };
   auto seg_info = [&](int si) -> SegInfo {
     SegInfo x;
@@ -204,32 +210,16 @@ __global__ void __launch_bounds__(256, 1)
     const int w4 = __shfl_sync(FULL, sg_l.w, j);
     x.e1 = w4 & 0xffff;
     x.split = (w4 >> kPlanSplitBit) & 1;
-    x.L = __shfl_sync(FULL, L_l, j);
-    x.nb = __shfl_sync(FULL, nb_l, j);
     return x;
-  };
-  // window of 32 block-table/direction(/fill) entries starting at entry wb
-  auto load_window = [&](const SegInfo &x, int wb, int &btv, int &dirv, int &filv) {
-    const int ew = wb + lane;
-    btv = 0;
-    dirv = 0;
-    filv = 0;
-    if (x.si < s1 && ew < x.e1) {
-      btv = __ldg(p.bt + static_cast<int64_t>(x.r) * p.bt_stride + ew);
-      dirv = __ldg(p.dirs + static_cast<int64_t>(x.r) * p.dir_rs + static_cast<int64_t>(ew) * p.dir_cs);
-      if (p.fills) filv = __ldg(p.fills + static_cast<int64_t>(x.r) * p.fill_rs + ew);
-    }
   };
   // this CTA's merge tasks (<= 2 per warp: a warp has at most two split segments)
   __shared__ int4 task_s[2 * 2 * kPlannedWarps];
   const int t_beg = __ldg(p.ctask + blockIdx.x), t_end = __ldg(p.ctask + blockIdx.x + 1);
   if (threadIdx.x < 2 * (t_end - t_beg)) task_s[threadIdx.x] = __ldg(p.tasks + 2 * t_beg + threadIdx.x);
   SegInfo cur{}, nxt = seg_info(s0);
-  int nx_bt = 0, nx_dir = 0, nx_fil = 0;
-  load_window(nxt, nxt.e0, nx_bt, nx_dir, nx_fil);
 
   if (kTrace) {   // (the stamp needs the loads to have landed)
-    volatile int sink = nx_bt + nxt.L;
+    volatile int sink = static_cast<int>(ent_w) + nxt.r;
     (void)sink;
     stamp(1);
   }
@@ -254,7 +244,7 @@ __global__ void __launch_bounds__(256, 1)
   if (!p.kv_early) grid_wait();
 
   bool is_active = false, is_done = false, is_first = false;
-  int is_ci = 0, is_nc = 0, is_wb = 0, bt_w = 0, dir_w = 0, fil_w = 0;
+  int is_ci = 0, is_nc = 0, ent_pos = 0;
   // next chunk of the warp's stream: 16 slots (sub-chunk ci % cpb) of entry e0 + ci / cpb
   auto next_chunk = [&](SlotMeta &m, int &blk, int &csub) -> bool {
     if (!is_active) {
@@ -263,12 +253,7 @@ __global__ void __launch_bounds__(256, 1)
         return false;
       }
       cur = nxt;
-      bt_w = nx_bt;
-      dir_w = nx_dir;
-      fil_w = nx_fil;
-      is_wb = cur.e0;
       nxt = seg_info(cur.si + 1);
-      load_window(nxt, nxt.e0, nx_bt, nx_dir, nx_fil);
       if (lane < g) {   // the segment's q rows into L2 (read by the consumer later)
         const uint16_t *qrow = p.q + static_cast<int64_t>(cur.r) * p.q_ss +
                                static_cast<int64_t>(cur.h * g + lane) * p.q_sh;
@@ -280,22 +265,18 @@ __global__ void __launch_bounds__(256, 1)
       is_first = true;
       is_active = true;
     }
-    const int e = cur.e0 + (chunks_per_block == 1 ? is_ci : (is_ci >> 1));
+    const int k = ent_pos + (chunks_per_block == 1 ? is_ci : (is_ci >> 1));   // entry within the warp range
     const int c = chunks_per_block == 1 ? 0 : (is_ci & 1);
-    if (e - is_wb >= 32) {
-      is_wb = e;
-      load_window(cur, e, bt_w, dir_w, fil_w);
-    }
-    const int idx = e - is_wb;
-    const int b = __shfl_sync(FULL, bt_w, idx);
-    const int dr = __shfl_sync(FULL, dir_w, idx);
-    const int fl = __shfl_sync(FULL, fil_w, idx);
-    const int ne = p.fills ? fl : min(bs, cur.L - e * bs);   // live tokens of the entry
-    const int lo_s = dr ? bs - ne : 0;                       // RT from the left,
-    const int hi_s = dr ? bs : ne;                           //        BE from the right
+    if (k - ent_base >= 32) load_ents(k);
+    const uint32_t en = __shfl_sync(FULL, ent_w, k - ent_base);
+    const int b = static_cast<int>(en & kEntBlockMask);
+    const int dr = (en >> kEntDirShift) & 1;
+    const int ne = static_cast<int>((en >> kEntFillShift) & 31u) + 1;   // live tokens of the entry
+    const int lo_s = dr ? bs - ne : 0;                                 // RT from the left,
+    const int hi_s = dr ? bs : ne;                                     //        BE from the right
     const int lo = max(lo_s - c * 16, 0), hi = min(hi_s - c * 16, 16);
     int flags = (is_first ? F_FIRST : 0) | (lo >= hi ? F_NOKV : 0);
-    if (p.k_new != nullptr && e == cur.nb - 1) {   // fused step: token L-1 lives in the last entry
+    if (p.k_new != nullptr && (en >> kEntLastShift)) {   // fused step: token L-1 lives in the last entry
       const int j = ne - 1;
       const int slot_new = dr ? bs - 1 - j : j;
       if ((slot_new >> 4) == c) flags |= F_NEW | (slot_new << 8);
@@ -307,6 +288,7 @@ __global__ void __launch_bounds__(256, 1)
     if (is_ci >= is_nc) {
       flags |= F_LAST;
       is_active = false;
+      ent_pos += cur.e1 - cur.e0;
     }
     m = SlotMeta{cur.si, cur.r, cur.h, cur.split, lo, hi, flags, b};
     return true;

@@ -16,7 +16,7 @@ bt = torch.from_numpy(lay.block_tables).cuda(); dirs = torch.from_numpy(lay.dirs
 lens = torch.from_numpy(lay.lens).cuda(); q = torch.randn(B, Hq, d, device="cuda").to(torch.bfloat16)
 kn = torch.randn(B, H, d, device="cuda").to(torch.bfloat16)
 vn = torch.randn(B, H, d, device="cuda").to(torch.bfloat16)
-plan = bkv.decode_plan(lay.lens, pool, Hq, lay.block_tables.shape[1])
+plan = bkv.decode_plan(lay.lens, lay.block_tables, lay.dirs, pool, Hq)
 for _ in range(n):
     bkv.decode_planned(pool, bt, dirs, lens, plan, q, k_new=kn, v_new=vn, pdl=True, kv_early=True)
 torch.cuda.synchronize()

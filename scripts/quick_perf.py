@@ -21,7 +21,7 @@ def run(cfg, tp=1, layers=8, iters=20, mode="attn"):
     ws = bkv.workspace(lay.batch, Hq, H, d)
     kn = torch.randn(lay.batch, H, d, device=dev).to(torch.bfloat16)
     vn = torch.randn(lay.batch, H, d, device=dev).to(torch.bfloat16)
-    plan = bkv.decode_plan(lay.lens, pools[0], Hq, lay.block_tables.shape[1]) if mode.startswith("planned") else None
+    plan = bkv.decode_plan(lay.lens, lay.block_tables, lay.dirs, pools[0], Hq) if mode.startswith("planned") else None
     def body():
         for p in pools:
             if mode == "planned":

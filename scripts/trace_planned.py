@@ -37,7 +37,7 @@ vn = torch.randn(lay.batch, H, d, device=dev).to(torch.bfloat16)
 out = torch.empty_like(q)
 need = bkv.decode_workspace_size(lay.batch, Hq, H, d)
 wss = [torch.zeros(need, dtype=torch.uint8, device=dev) for _ in range(nl)]
-plan = bkv.decode_plan(lay.lens, pools[0], Hq, lay.block_tables.shape[1])
+plan = bkv.decode_plan(lay.lens, lay.block_tables, lay.dirs, pools[0], Hq)
 hd = plan.header
 W = hd["grid"] * hd["warps"]
 tr_bytes = W * 16 * 8

@@ -65,7 +65,8 @@ def run_full(cfg, tp=1, rank=0, seed=0, mode="step", pdl=True, planned=False, sp
     scale = 1.0 / math.sqrt(d)
     plan = None
     if planned:
-        plan = bkv.decode_plan(lay.lens, pool, len(q_heads), lay.block_tables.shape[1],
+        plan = bkv.decode_plan(lay.lens, lay.block_tables, lay.dirs, pool, len(q_heads),
+                               fills_host=lay.fills if general else None,
                                num_entries_host=lay.num_entries if general else None)
     outs = []
     for it in range(repeat):   # (a repeated fused step re-writes the same token: idempotent)

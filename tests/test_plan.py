@@ -18,7 +18,7 @@ from synth import make_case
 
 HDR = ("magic", "version", "words", "B", "H", "g", "D", "bs", "general", "grid", "warps", "P",
        "n_segs", "n_tasks", "n_zero", "total", "off_wseg", "off_segs", "off_ctask", "off_tasks",
-       "off_zero", "max_pieces", "max_entries", "off_xrows", "n_xrows")
+       "off_zero", "max_pieces", "max_entries", "off_xrows", "n_xrows", "off_ent", "n_ent")
 
 
 def decode(plan):
@@ -181,8 +181,35 @@ def dense_attention(lens, H, g, q, K, V):
     return out
 
 
-def _plan(lens, H, g, bs, bt_stride, sms, nent=None, d=128):
-    return bkv.decode_plan_host(lens, H, H * g, d, bs, bt_stride, num_entries=nent, num_sms=sms)
+def synth_map(lens, bt_stride, seed=0):
+    """A block map for bare lengths: distinct random block ids, random per-entry directions."""
+    B = len(lens)
+    rng = np.random.default_rng(seed)
+    ids = rng.permutation(max(1, B * bt_stride)).astype(np.int32)[:B * bt_stride].reshape(B, bt_stride)
+    return ids, rng.integers(0, 2, size=(B, bt_stride)).astype(np.uint8)
+
+
+def _plan(lens, H, g, bs, bt_stride, sms, nent=None, fills=None, d=128, bt=None, dirs=None):
+    if bt is None:
+        bt, dirs = synth_map(lens, bt_stride)
+    return bkv.decode_plan_host(lens, bt, dirs, H, H * g, d, bs, fills=fills, num_entries=nent, num_sms=sms)
+
+
+def check_entries(plan, lens, H, bs, bt, dirs, nent=None, fills=None):
+    """The plan's flattened entry list: every (r, h, e) in flattened order, packed
+    block | dir << 25 | (live tokens - 1) << 26 | last << 31."""
+    h = decode(plan)[0]
+    ent = plan[h["off_ent"]:h["off_ent"] + h["n_ent"]].view(np.uint32)
+    nb = entries(lens, bs, nent)
+    exp = []
+    for r in range(len(lens)):
+        row = []
+        for e in range(int(nb[r])):
+            n = int(fills[r][e]) if fills is not None else min(bs, int(lens[r]) - e * bs)
+            dr = int(dirs[r][e]) if np.asarray(dirs).ndim == 2 else int(dirs[r])
+            row.append(int(bt[r][e]) | dr << 25 | (n - 1) << 26 | (int(e == nb[r] - 1) << 31))
+        exp += row * H
+    assert h["n_ent"] == len(exp) and np.array_equal(ent, np.array(exp, dtype=np.uint64).astype(np.uint32))
 
 
 CASES = [("tiny", 1, 148), ("tiny", 1, 3), ("tiny_gqa", 1, 5), ("opt13b", 8, 148), ("opt13b", 1, 148),
@@ -194,8 +221,10 @@ def test_plan_structure(cfg, tp, sms):
     case = make_case(cfg, 0)
     sh, lay = case.shape, case.layout
     H = sh.num_kv_heads // tp
-    plan = _plan(lay.lens, H, sh.group, sh.block_size, lay.block_tables.shape[1], sms)
+    plan = _plan(lay.lens, H, sh.group, sh.block_size, lay.block_tables.shape[1], sms, bt=lay.block_tables,
+                 dirs=lay.dirs)
     h = check_structure(plan, lay.lens, H, sh.block_size)
+    check_entries(plan, lay.lens, H, sh.block_size, lay.block_tables, lay.dirs)
     assert h["grid"] == sms and h["warps"] == 8
 
 
@@ -204,14 +233,19 @@ def test_plan_structure_general_and_edge(seed):
     rng = np.random.default_rng(seed)
     case = make_case("tiny_gqa", seed, general=True, share_prob=0.8)
     lay, sh = case.layout, case.shape
-    check_structure(_plan(lay.lens, 2, 4, 16, lay.block_tables.shape[1], 7, nent=lay.num_entries), lay.lens, 2,
-                    16, nent=lay.num_entries)
+    gp = _plan(lay.lens, 2, 4, 16, lay.block_tables.shape[1], 7, nent=lay.num_entries, fills=lay.fills,
+               bt=lay.block_tables, dirs=lay.dirs)
+    check_structure(gp, lay.lens, 2, 16, nent=lay.num_entries)
+    check_entries(gp, lay.lens, 2, 16, lay.block_tables, lay.dirs, nent=lay.num_entries, fills=lay.fills)
     # empty requests, one very long request, single warp ranges of one block
     lens = rng.integers(0, 300, size=40).astype(np.int32)
     lens[rng.integers(0, 40, size=6)] = 0
     lens[3] = 8192
+    bt, dirs = synth_map(lens, 512)
     for sms in (1, 2, 148):
-        check_structure(_plan(lens, 3, 1, 16, 512, sms), lens, 3, 16)
+        p = _plan(lens, 3, 1, 16, 512, sms)
+        check_structure(p, lens, 3, 16)
+        check_entries(p, lens, 3, 16, bt, dirs)
     check_structure(_plan(np.zeros(5, np.int32), 2, 1, 16, 4, 148), np.zeros(5, np.int32), 2, 16)
 
 
@@ -240,7 +274,7 @@ def test_plan_execution_model_matches_dense_attention(sms, H, g, bs, general):
     V = [rng.standard_normal((int(L), H, d)) for L in lens]
     q = rng.standard_normal((B, H * g, d))
     bt_stride = int(max(entries(lens, bs, nent).max(), 1))
-    plan = _plan(lens, H, g, bs, bt_stride, sms, nent=nent, d=64)
+    plan = _plan(lens, H, g, bs, bt_stride, sms, nent=nent, fills=fills, d=64)
     check_structure(plan, lens, H, bs, nent)
     sim = simulate(plan, lens, H, g, bs, q, K, V, nent, fills)
     ref = dense_attention(lens, H, g, q, K, V)
@@ -251,6 +285,14 @@ def test_plan_execution_model_matches_dense_attention(sms, H, g, bs, general):
 def test_plan_rejects_bad_input():
     with pytest.raises(bkv.BkvError):
         _plan(np.array([10, -1], np.int32), 1, 1, 16, 4, 148)
+    bt, dirs = synth_map([40], 4)
+    with pytest.raises(bkv.BkvError, match="block id"):
+        _plan(np.array([40], np.int32), 1, 1, 16, 4, 148, bt=bt - 10 ** 6, dirs=dirs)
+    with pytest.raises(bkv.BkvError, match="direction"):
+        _plan(np.array([40], np.int32), 1, 1, 16, 4, 148, bt=bt, dirs=dirs + 2)
+    with pytest.raises(bkv.BkvError, match="fills"):   # fills summing to 33, not 40
+        _plan(np.array([40], np.int32), 1, 1, 16, 4, 148, bt=bt, dirs=dirs,
+              fills=np.array([[16, 16, 1, 0]], np.uint8), nent=np.array([3], np.int32))
     with pytest.raises(bkv.BkvError):      # needs 3 entries > bt_stride 2
         _plan(np.array([40], np.int32), 1, 1, 16, 2, 148)
     with pytest.raises(bkv.BkvError):      # group 32 > 16
@@ -265,7 +307,7 @@ def test_plan_layout_is_fixed_by_geometry():
     plans.append(_plan(np.zeros(64, np.int32), 2, 8, 16, 256, 148))
     plans.append(_plan(np.full(64, 4096, np.int32), 2, 8, 16, 256, 148))
     hs = [decode(p)[0] for p in plans]
-    keys = ("words", "off_wseg", "off_segs", "off_ctask", "off_tasks", "off_zero", "off_xrows")
+    keys = ("off_wseg", "off_segs", "off_ctask", "off_tasks", "off_zero", "off_xrows", "off_ent")
     assert all(len(p) == len(plans[0]) for p in plans)
     assert all({k: h[k] for k in keys} == {k: hs[0][k] for k in keys} for h in hs)
     assert all(h["n_xrows"] <= h["grid"] for h in hs)

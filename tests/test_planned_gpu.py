@@ -38,7 +38,8 @@ def _planned_case(case, per_request=False, fill=BF16_NAN, out=None, general=Fals
                       t_u16(V if fill == BF16_NAN else np.where(V == BF16_NAN, np.uint16(fill), V)))
     bt, dirs, lens = gpu_map(lay, per_request)
     gm = {k: torch.from_numpy(v).to(DEV) for k, v in gmn.items()}
-    plan = bkv.decode_plan(lay.lens, pool, sh.num_q_heads, lay.block_tables.shape[1],
+    plan = bkv.decode_plan(lay.lens, lay.block_tables, dirs_np, pool, sh.num_q_heads,
+                           fills_host=lay.fills if general else None,
                            num_entries_host=lay.num_entries if general else None)
     peer_bufs = [torch.full((lay.batch, sh.num_q_heads, sh.head_dim), float("nan"), dtype=torch.bfloat16,
                             device=DEV) for _ in range(peers)]
@@ -125,7 +126,7 @@ def test_planned_fused_step_bitwise_pool():
     oracle.append(Kp, Vp, lay.block_tables, lay.dirs, before, cud, kd, vd)
     ref = oracle.attention(Kp, Vp, lay.block_tables, lay.dirs, lay.lens, q, default_scale(128))
     bt, dirs, lens = gpu_map(lay)
-    plan = bkv.decode_plan(lay.lens, pool, 16, lay.block_tables.shape[1])
+    plan = bkv.decode_plan(lay.lens, lay.block_tables, lay.dirs, pool, 16)
     o = bkv.decode_planned(pool, bt, dirs, lens, plan, t_u16(q), k_new=t_u16(kd), v_new=t_u16(vd), pdl=True)
     torch.cuda.synchronize()
     assert np.array_equal(u16(pool.k), Kp) and np.array_equal(u16(pool.v), Vp)
@@ -161,12 +162,12 @@ def test_planned_rejects_mismatched_plan():
     pool = bkv.KVPool.empty(lay.num_blocks, sh.num_kv_heads, sh.block_size, sh.head_dim, DEV)
     bt, dirs, lens = gpu_map(lay)
     q = torch.zeros((lay.batch, sh.num_q_heads, sh.head_dim), dtype=torch.bfloat16, device=DEV)
-    plan = bkv.decode_plan(lay.lens, (sh.num_kv_heads * 2, sh.head_dim, sh.block_size), sh.num_q_heads * 2,
-                           lay.block_tables.shape[1])
+    plan = bkv.decode_plan(lay.lens, lay.block_tables, lay.dirs, (sh.num_kv_heads * 2, sh.head_dim, sh.block_size),
+                           sh.num_q_heads * 2)
     with pytest.raises(bkv.BkvError, match="does not match"):
         bkv.decode_planned(pool, bt, dirs, lens, plan, q)
-    other = bkv.decode_plan_host(lay.lens, sh.num_kv_heads, sh.num_q_heads, sh.head_dim, sh.block_size,
-                                 lay.block_tables.shape[1], num_sms=7)
+    other = bkv.decode_plan_host(lay.lens, lay.block_tables, lay.dirs, sh.num_kv_heads, sh.num_q_heads,
+                                 sh.head_dim, sh.block_size, num_sms=7)
     bad = bkv.DecodePlan(other, plan.dev, plan.nbytes)
     with pytest.raises(bkv.BkvError, match="warps"):
         bkv.decode_planned(pool, bt, dirs, lens, bad, q)
@@ -197,7 +198,7 @@ def test_planned_graph_replays_a_new_plan():
     pool = bkv.KVPool(t_u16(K), t_u16(V))
     bt, dirs, lens = gpu_map(lay)
     lens_a = np.maximum(1, lay.lens // 3).astype(np.int32)          # step A: shorter contexts
-    plan = bkv.decode_plan(lens_a, pool, 16, lay.block_tables.shape[1])
+    plan = bkv.decode_plan(lens_a, lay.block_tables, lay.dirs, pool, 16)
     lens.copy_(torch.from_numpy(lens_a))
     qd = t_u16(q)
     out = torch.empty_like(qd)
@@ -207,14 +208,14 @@ def test_planned_graph_replays_a_new_plan():
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
         bkv.decode_planned(pool, bt, dirs, lens, plan, qd, out=out, ws=ws, pdl=True)
-    plan_b = bkv.decode_plan_host(lay.lens, 2, 16, 128, 16, lay.block_tables.shape[1])
-    assert plan_b.nbytes == plan.nbytes
-    plan.dev.copy_(torch.from_numpy(plan_b.view(np.uint8)))
+    plan_b = bkv.decode_plan_host(lay.lens, lay.block_tables, lay.dirs, 2, 16, 128, 16)
+    assert plan_b.nbytes == plan.host.nbytes
+    plan.upload(plan_b)
     lens.copy_(torch.from_numpy(lay.lens.astype(np.int32)))
     g.replay()
     torch.cuda.synchronize()
     check_close(out, ref, "graph replay with plan B")
-    eager = bkv.decode_planned(pool, bt, dirs, lens, bkv.DecodePlan(plan_b, plan.dev, plan.nbytes), qd)
+    eager = bkv.decode_planned(pool, bt, dirs, lens, plan, qd)
     torch.cuda.synchronize()
     assert torch.equal(eager.view(torch.int16), out.view(torch.int16))
 
