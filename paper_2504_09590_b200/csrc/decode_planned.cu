@@ -177,6 +177,7 @@ __global__ void __launch_bounds__(256, 1)
   const int P = __ldg(p.plan_hdr + offsetof(PlanHeader, P) / 4);
   const int s0 = __ldg(p.wseg + gw), s1 = __ldg(p.wseg + gw + 1);
   const int ent0 = gw * P;                          // the warp's first flattened entry
+  const int n_mine = min(P, __ldg(p.plan_hdr + offsetof(PlanHeader, total) / 4) - ent0);   // its entries
   int4 sg_l = make_int4(0, 0, 0, 0);
   auto load_segs = [&](int first) {
     const int si = first + lane;
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(256, 1)
   int ent_base = 0;
   auto load_ents = [&](int first) {
     ent_base = first;
-    if (first + lane < P) ent_w = __ldg(p.ent + ent0 + first + lane);
+    if (first + lane < n_mine) ent_w = __ldg(p.ent + ent0 + first + lane);
   };
   load_ents(0);
 

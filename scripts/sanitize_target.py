@@ -29,8 +29,10 @@ for sh in (Shape("s1", 4, 4, 64, 16, 8, 0.5, "uniform", 300, 1, 1, uniform_max=3
     for pdl in (False, True):
         out = bkv.paged_decode_attention(pool, bt, dirs, torch.from_numpy(lay.lens).cuda(), g(q), pdl=pdl)
     os.environ["BKV_STREAMK"] = "2"   # stream-K plan (rows cut across warp ranges) on the same case
+    bkv.reload_dev_switches()
     out = bkv.paged_decode_attention(pool, bt, dirs, torch.from_numpy(lay.lens).cuda(), g(q), pdl=True)
     os.environ["BKV_STREAMK"] = "1"
+    bkv.reload_dev_switches()
     ck, cv = bkv.kv_checkpoint(pool, sm[:17])
     bkv.kv_restore(pool, sm[:17], ck, cv)
     torch.cuda.synchronize()
@@ -71,3 +73,28 @@ for sh in (Shape("g1", 4, 4, 64, 16, 8, 0.5, "uniform", 300, 1, 1, uniform_max=3
                              ev, ckk, ckv, fills=fills, num_entries=nent)
     torch.cuda.synchronize()
     print(sh.name, "general ok", float(out.float().abs().mean()), float(op.float().abs().mean()))
+
+# round r02: the planned decode (host plan, one decode kernel + cross-CTA merge kernel per layer),
+# both cross-CTA merge modes, fused step, early KV tiles, peers, on small and TP-shard shapes
+from synth import CONFIGS
+from synth.workload import shard_heads
+for cfg, tp in (("tiny_gqa", 1), ("llama70b", 8), ("opt13b", 8)):
+    sh = CONFIGS[cfg]
+    lay = make_case(cfg, 3).layout
+    kvh, qh = shard_heads(sh, tp, 0)
+    H, Hq, d = len(kvh), len(qh), sh.head_dim
+    pool = bkv.KVPool(torch.randn(lay.num_blocks, H, sh.block_size, d, device="cuda").to(torch.bfloat16),
+                      torch.randn(lay.num_blocks, H, sh.block_size, d, device="cuda").to(torch.bfloat16))
+    bt = torch.from_numpy(lay.block_tables).cuda(); dirs = torch.from_numpy(lay.dirs).cuda()
+    lens = torch.from_numpy(lay.lens).cuda()
+    qd = torch.randn(lay.batch, Hq, d, device="cuda").to(torch.bfloat16)
+    kd = torch.randn(lay.batch, H, d, device="cuda").to(torch.bfloat16)
+    plan = bkv.decode_plan(lay.lens, lay.block_tables, lay.dirs, pool, Hq)
+    peer = torch.empty_like(qd)
+    for xm in ("1", "0"):
+        os.environ["BKV_PLANNED_XMERGE"] = xm
+        bkv.reload_dev_switches()
+        o1 = bkv.decode_planned(pool, bt, dirs, lens, plan, qd, k_new=kd, v_new=kd, pdl=True, kv_early=True)
+        o2 = bkv.decode_planned(pool, bt, dirs, lens, plan, qd, peer_outs=[peer])
+    torch.cuda.synchronize()
+    print(cfg, tp, "planned ok", float(o1.float().abs().mean()), float(o2.float().abs().mean()))

@@ -1,9 +1,11 @@
 #!/usr/bin/env python
 """BASELINE.json configs[4]: RT:BE ratio and context-length sweep (512-8K, block 16/32) on
 the Llama-2-70B shape, per-layer decode attention (fused decode step, CUDA graph over
-rotated layers > L2, CUDA events) at the TP1 and TP8 head shards.  One JSON line per point.
+rotated layers > L2, CUDA events) at the TP1/2/4/8 head shards, through the planned decode
+(bkv_decode_plan once, bkv_decode_planned per layer; its large problems take the dynamic
+kernel pair).  One JSON line per point: median, p10 and p90 over the replays.
 
-    python scripts/sweep_bench.py [--tp 1 8] [--L0 512 2048 8192] [--bs 16 32] [--rt 1 0.5 0]
+    python scripts/sweep_bench.py [--tp 1 2 4 8] [--L0 512 2048 8192] [--bs 16 32] [--rt 1 0.5 0]
 """
 import argparse
 import json
@@ -19,11 +21,11 @@ sys.path.insert(0, ROOT)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--tp", type=int, nargs="+", default=[1, 8])
+    ap.add_argument("--tp", type=int, nargs="+", default=[1, 2, 4, 8])
     ap.add_argument("--L0", type=int, nargs="+", default=[512, 1024, 2048, 4096, 8192])
     ap.add_argument("--bs", type=int, nargs="+", default=[16, 32])
     ap.add_argument("--rt", type=float, nargs="+", default=[1.0, 0.5, 0.0])
-    ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--iters", type=int, default=30)
     a = ap.parse_args()
     import torch
     import paper_2504_09590_b200 as bkv
@@ -55,11 +57,12 @@ def main():
                     vn = torch.randn_like(kn)
                     out = torch.empty_like(q)
                     ws = bkv.workspace(lay.batch, Hq, H, d, dev)
-                    ml = int(lay.lens.max())
+                    plan = bkv.decode_plan(lay.lens, lay.block_tables, lay.dirs, pools[0], Hq)
 
                     def body():
                         for pl in pools:
-                            bkv.decode_step(pl, bt, dirs, lens, kn, vn, q, out=out, max_seq_len=ml, ws=ws, pdl=True)
+                            bkv.decode_planned(pl, bt, dirs, lens, plan, q, k_new=kn, v_new=vn, out=out, ws=ws,
+                                               pdl=True, kv_early=True)
                     body()
                     torch.cuda.synchronize()
                     g = torch.cuda.CUDAGraph()
@@ -77,11 +80,15 @@ def main():
                         torch.cuda.synchronize()
                         ts.append(e0.elapsed_time(e1) * 1e3 / layers)
                     us = float(np.median(ts))
-                    alg = kv_bytes + 4.0 * lay.batch * Hq * d + 4.0 * lay.batch * H * d
+                    nb = lay.nblocks().astype(np.int64)   # bench.py's algorithmic bytes (+ the fused append)
+                    alg = kv_bytes + 4.0 * lay.batch * Hq * d + 8.0 * lay.batch * H * d + nb.sum() * 5 + 4 * lay.batch
                     print(json.dumps({"config": "sweep (BASELINE configs[4])", "tp": tp, "block_size": bs, "L0": L0,
                                       "rt_fraction": rt, "batch": lay.batch, "kv_heads": H, "q_heads": Hq,
                                       "mean_ctx": float(lay.lens.mean()), "shared_blocks": int(lay.n_shared),
-                                      "us_per_layer": us, "decode_tokens_per_s_per_layer": lay.batch / (us * 1e-6),
+                                      "us_per_layer": us, "us_p10": float(np.percentile(ts, 10)),
+                                      "us_p90": float(np.percentile(ts, 90)),
+                                      "plan_blocks_per_warp": plan.header["P"],
+                                      "decode_tokens_per_s_per_layer": lay.batch / (us * 1e-6),
                                       "achieved_gbs": alg / (us * 1e-6) / 1e9, "frac": alg / (us * 1e-6) / 1e9 / peak,
                                       "peak_gbs": peak, "peak_source": src}), flush=True)
                     del pools, g

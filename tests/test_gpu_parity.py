@@ -17,6 +17,7 @@ from synth import CONFIGS, make_case, build_layout, dense_kv_torch, q_torch
 from synth.values import BF16_NAN
 from synth.workload import Shape, shard_heads
 from tests._cases import dense_case, oracle_pool, ragged, default_scale
+from tests._full import run_full
 
 pytestmark = pytest.mark.gpu
 
@@ -248,9 +249,52 @@ def test_gqa_equals_mha_with_repeated_kv_heads():
     assert (o.float() - o2.float()).abs().max().item() <= 2 * MAX_ABS
 
 
-# --------------------------------------- full-size configs, sampled requests
-def _full_size(cfg, tp=1, rank=0, sample=6, seed=0, mode="attn", pdl=False, spare_blocks=3):
-    """Full BASELINE-size batch on the GPU; the oracle checks a sample of requests one by one.
+# --------------------------------------- full-size configs, every element
+def _full_size(cfg, tp=1, rank=0, seed=0, mode="attn", pdl=False, spare_blocks=3, repeat=1, **_):
+    """Full BASELINE-size batch on the GPU through the dynamically scheduled kernel pair
+    (bkv_paged_decode_attention / bkv_decode_step); every output element -- and for the
+    fused step every pool byte -- against the oracle (tests/_full.py)."""
+    got, ref, per_req = run_full(cfg, tp, rank, seed=seed, mode=mode, pdl=pdl, planned=False,
+                                 spare_blocks=spare_blocks, repeat=repeat)
+    return torch.from_numpy(got)
+
+
+@pytest.mark.parametrize("cfg,tp,rank", [("opt13b", 1, 0), ("opt30b", 4, 2), ("llama70b", 1, 0), ("llama70b", 8, 7)])
+def test_full_size_parity(cfg, tp, rank):
+    _full_size(cfg, tp, rank)
+
+
+@pytest.mark.parametrize("cfg,tp", [("opt13b", 1), ("llama70b", 8), ("opt30b", 2)])
+def test_full_size_fused_step(cfg, tp):
+    """The fused decode step with PDL at the full BASELINE batch, seed 0 (bench.py's seed), twice
+    (bitwise repeat); bkv_decode_planned's large-problem path (OPT-30B at one GPU) runs this pair."""
+    _full_size(cfg, tp, 0, mode="step", pdl=True, seed=0, repeat=2)
+
+
+@pytest.mark.parametrize("cfg,tp", [("llama70b", 8), ("opt13b", 4)])
+def test_fused_merge_opt_in(cfg, tp, monkeypatch):
+    """BKV_FUSED_MERGE=1, the opt-in in-kernel last-arriver merge (group merge for GQA, row
+    merge for MHA): sampled oracle parity, twice on one workspace (the arrival counters and
+    the unit counter must be re-armed by the kernel itself), and the same result as the
+    default split merge up to fp32 summation order."""
+    monkeypatch.setenv("BKV_FUSED_MERGE", "1")
+    o1 = _full_size(cfg, tp, 0, mode="step", pdl=True, seed=3, repeat=2)
+    monkeypatch.setenv("BKV_FUSED_MERGE", "0")
+    o0 = _full_size(cfg, tp, 0, mode="step", pdl=True, seed=3)
+    assert (o0.float() - o1.float()).abs().max().item() <= 2e-2
+
+
+@pytest.mark.parametrize("L0,bs,rt", [(8192, 32, 0.25), (8192, 16, 1.0), (512, 16, 0.0), (2048, 32, 0.75)])
+def test_sweep_config_sampled_parity(L0, bs, rt):
+    """BASELINE configs[4]: Llama-2-70B shape, context sweep 512-8K, block 16/32, RT:BE mix
+    (TP8 shard: 1 kv head / 8 q heads), full batch 256, sampled requests vs the oracle."""
+    from synth.workload import sweep_shape
+    _full_size(sweep_shape(L0, bs, rt), tp=8, rank=3, seed=2, mode="step", pdl=True)
+
+
+def _sampled_full_size(cfg, tp=1, rank=0, sample=6, seed=0, mode="attn", pdl=False, spare_blocks=3):
+    """Kept for the one case whose host oracle pool would not fit (> 2^31-element pools): a
+    full-size batch on the GPU, the oracle checks a sample of requests one by one.
     mode "attn": bkv_paged_decode_attention over the resident context; mode "step": the
     bench's launch configuration -- the fused decode step (bkv_decode_step, PDL) appending
     token L-1 of every request and attending over all L."""
@@ -301,40 +345,6 @@ def _full_size(cfg, tp=1, rank=0, sample=6, seed=0, mode="attn", pdl=False, spar
     return o
 
 
-@pytest.mark.parametrize("cfg,tp,rank", [("opt13b", 1, 0), ("opt30b", 4, 2), ("llama70b", 1, 0), ("llama70b", 8, 7)])
-def test_full_size_sampled_parity(cfg, tp, rank):
-    _full_size(cfg, tp, rank)
-
-
-@pytest.mark.parametrize("cfg,tp", [("opt13b", 1), ("llama70b", 8), ("opt30b", 1)])
-def test_full_size_bench_launch_config(cfg, tp):
-    """What bench.py times: the fused decode step with PDL at the full BASELINE batch."""
-    _full_size(cfg, tp, 0, mode="step", pdl=True, seed=1)
-
-
-@pytest.mark.parametrize("cfg,tp", [("llama70b", 8), ("opt13b", 4)])
-def test_fused_merge_opt_in(cfg, tp, monkeypatch):
-    """BKV_FUSED_MERGE=1, the opt-in in-kernel last-arriver merge (group merge for GQA, row
-    merge for MHA): sampled oracle parity, twice on one workspace (the arrival counters and
-    the unit counter must be re-armed by the kernel itself), and the same result as the
-    default split merge up to fp32 summation order."""
-    monkeypatch.setenv("BKV_FUSED_MERGE", "1")
-    o1 = _full_size(cfg, tp, 0, mode="step", pdl=True, seed=3)
-    o2 = _full_size(cfg, tp, 0, mode="step", pdl=True, seed=3)
-    assert torch.equal(o1, o2)
-    monkeypatch.setenv("BKV_FUSED_MERGE", "0")
-    o0 = _full_size(cfg, tp, 0, mode="step", pdl=True, seed=3, sample=2)
-    assert (o0.float() - o1.float()).abs().max().item() <= 2e-2
-
-
-@pytest.mark.parametrize("L0,bs,rt", [(8192, 32, 0.25), (8192, 16, 1.0), (512, 16, 0.0), (2048, 32, 0.75)])
-def test_sweep_config_sampled_parity(L0, bs, rt):
-    """BASELINE configs[4]: Llama-2-70B shape, context sweep 512-8K, block 16/32, RT:BE mix
-    (TP8 shard: 1 kv head / 8 q heads), full batch 256, sampled requests vs the oracle."""
-    from synth.workload import sweep_shape
-    _full_size(sweep_shape(L0, bs, rt), tp=8, rank=3, sample=4, seed=2, mode="step", pdl=True)
-
-
 def test_int64_offsets_tp1_8k_pool():
     """Llama-70B TP1 at 8K contexts: the pool holds > 2^31 elements per tensor, so every
     kernel's block/head/slot offsets must be 64-bit (sampled requests vs the oracle)."""
@@ -342,14 +352,14 @@ def test_int64_offsets_tp1_8k_pool():
     sh = sweep_shape(8192, 16, 0.5)
     lay = make_case(sh, 5, spare_blocks=4000).layout
     assert int(lay.block_tables.max()) * sh.num_kv_heads * sh.block_size * sh.head_dim > 2 ** 31
-    _full_size(sh, tp=1, rank=0, sample=3, seed=5, mode="step", pdl=True, spare_blocks=4000)
+    _sampled_full_size(sh, tp=1, rank=0, sample=3, seed=5, mode="step", pdl=True, spare_blocks=4000)
 
 
 def test_max_batch_2048():
     """num_seqs at the ABI maximum (2048): the in-kernel plan arrays are full."""
     sh = Shape("maxb", 4, 2, 64, 16, 2048, 0.5, "uniform", 96, 1, 1, uniform_max=96)
-    _full_size(sh, 1, 0, sample=8, seed=3, mode="step")
-    _full_size(sh, 1, 0, sample=8, seed=4, mode="attn")
+    _full_size(sh, 1, 0, seed=3, mode="step")
+    _full_size(sh, 1, 0, seed=4, mode="attn")
 
 
 # ---------------------------------------------------------------- ABI errors
