@@ -271,8 +271,9 @@ BKV_API bkv_status bkv_kv_append_checkpoint(const bkv_kv_pool *pool, const bkv_b
  * token except the ones this call appends) is not written by the immediately
  * preceding kernel either -- true when that kernel is e.g. the layer's QKV
  * projection or another layer's decode call -- so the first tiles of every
- * warp's ring are requested before the grid wait; q, k_new, v_new and the
- * workspace are still read after it. */
+ * warp's ring are requested, and its next few blocks prefetched into L2,
+ * before the grid wait; q, k_new, v_new and the workspace are still read
+ * after it. */
 #define BKV_FLAG_KV_EARLY 2u
 BKV_API bkv_status bkv_paged_decode_attention_ex(const bkv_kv_pool *pool, const bkv_block_map *map,
                                                  const int32_t *seq_lens, int32_t max_seq_len,
@@ -457,9 +458,10 @@ BKV_API bkv_status bkv_validate_block_map_host(const bkv_block_map *map, const i
  * layer of the step reuses it.  The plan cuts the flattened sequence of
  * (request r, kv head h, block e) -- r-major, then h, then e -- into equal
  * contiguous ranges, one per warp of a persistent grid (one CTA per SM);
- * rows cut across warps are merged inside the kernel (shared memory within a
- * CTA, a last-arriver merge of one piece per CTA across CTAs) in an order
- * fixed by the plan, so results are run-to-run bitwise identical.  The plan
+ * rows cut across warps are merged in shared memory inside the kernel, rows
+ * cut across CTAs by a small stream-ordered merge kernel (one combined piece
+ * per CTA), in an order fixed by the plan, so results are run-to-run bitwise
+ * identical.  The plan
  * depends only on the lengths (and entry counts) and on the device's SM
  * count: identical on every rank of a head-sharded TP group.
  *
@@ -499,7 +501,7 @@ BKV_API bkv_status bkv_validate_block_map_host(const bkv_block_map *map, const i
  *   semantics of bkv_paged_decode_attention_ex) or the fused decode step
  *   (both set, semantics of bkv_decode_step), with optional peer outputs
  *   (semantics of bkv_decode_multi_out; n_peers = 0, peer_outs = NULL for
- *   none).  ONE kernel launch.
+ *   none).  Two launches (the decode kernel and the cross-CTA merge kernel).
  *   plan_host    the buffer bkv_decode_plan wrote (only its header is read)
  *   plan_dev     device copy of it, 16-byte aligned
  *   map          the step's block map (device pointers): the plan already holds

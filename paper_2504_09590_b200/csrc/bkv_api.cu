@@ -48,8 +48,8 @@ void load_switches() {
   s.trace = 0;
 #endif
   s.planned_slots = env_int("BKV_PLANNED_SLOTS", 2);
-  s.planned_xmerge = env_int("BKV_PLANNED_XMERGE", 1);
   s.planned_dynamic_p = env_int("BKV_PLANNED_DYNAMIC_P", 128);
+  s.planned_pf = env_int("BKV_PLANNED_PF", 4);
   g_sw = s;
 }
 }  // namespace
@@ -985,7 +985,7 @@ bkv_status bkv_decode_planned(const bkv_kv_pool *pool, const bkv_block_map *map,
   if ((size_t)2 * hd->grid * bkv::planned_piece_floats(g, D) * 4 > w.trace - w.o)
     return fail(BKV_ERR_WORKSPACE_TOO_SMALL, "workspace partial region too small for the plan");
   const int S = std::max(1, std::min(4, bkv::dev_switches().planned_slots));
-  const int smem = bkv::planned_smem_bytes(D, g, S);
+  const int smem = bkv::planned_smem_bytes(D, g, S, hd->warps);
   if (smem > dp.smem_optin) return fail(BKV_ERR_UNSUPPORTED, "planned kernel needs %d B of shared memory", smem);
   CUtensorMap tmK, tmV;
   if ((s = encode_pool_map(&tmK, pool->k, pool))) return s;
@@ -1025,12 +1025,11 @@ bkv_status bkv_decode_planned(const bkv_kv_pool *pool, const bkv_block_map *map,
   p.plan_hdr = pw;
   p.ent = reinterpret_cast<const uint32_t *>(pw + hd->off_ent);
   p.xrows_cap = hd->grid;
-  p.xmerge = bkv::dev_switches().planned_xmerge;
-  p.cnt = reinterpret_cast<int *>(ws + w.mcnt);
   p.gpiece = reinterpret_cast<float *>(ws + w.o);
   p.slots = S;
   p.pdl = (flags & BKV_FLAG_PDL) ? 1 : 0;
   p.kv_early = (flags & BKV_FLAG_KV_EARLY) ? 1 : 0;
+  p.pf = std::max(0, std::min(32, bkv::dev_switches().planned_pf));
   p.kv_mode = kv_mode;
   p.k_new = static_cast<const uint16_t *>(k_new);
   p.v_new = static_cast<const uint16_t *>(v_new);
@@ -1046,7 +1045,7 @@ bkv_status bkv_decode_planned(const bkv_kv_pool *pool, const bkv_block_map *map,
       return fail(BKV_ERR_INVALID_ARGUMENT, "peer output %d is NULL or not 16-byte aligned", k);
   }
   p.trace = w.trace_cap >= 8 ? reinterpret_cast<unsigned long long *>(ws + w.trace) : nullptr;
-  e = bkv::launch_planned(tmK, tmV, p, D, hd->grid, smem, reinterpret_cast<cudaStream_t>(stream));
+  e = bkv::launch_planned(tmK, tmV, p, D, hd->grid, hd->warps, smem, reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "planned decode launch");
   return BKV_OK;
 }

@@ -195,7 +195,7 @@ const char *build_plan(const int32_t *seq_lens, const HostMap &map, int B, int H
                        int warps, int32_t *out, size_t out_words, size_t *used_words);
 constexpr int kPlannedWarps = 8;             // warps per CTA of the planned kernel
 
-struct PlannedParams {
+struct __align__(16) PlannedParams {
   const int32_t *bt;
   int bt_stride;
   const uint8_t *dirs;
@@ -216,15 +216,14 @@ struct PlannedParams {
   const int32_t *ctask;  // [grid + 1]
   const int4 *tasks;     // 2 per task (PlanTask)
   const int32_t *zero;   // {r, h} pairs
-  const int4 *xrows;     // rows cut across CTAs (merged by planned_xmerge_kernel when xmerge == 1)
+  const int4 *xrows;     // rows cut across CTAs (merged by planned_xmerge_kernel)
   const int32_t *plan_hdr;   // device copy of the PlanHeader: per-step values (P, n_zero, n_xrows)
   const uint32_t *ent;       // packed flattened entries (block, dir, fill, last) in warp order
   int xrows_cap;         // capacity of xrows (sizes the merge kernel's grid; graph-safe)
-  int xmerge;            // 0: last-arriver merge inside the kernel; 1: separate stream-ordered merge kernel
-  int *cnt;              // [B*H] cross-CTA arrival counters (self-cleaning, zero at rest)
   float *gpiece;         // [2*grid][g*(D+2)] cross-CTA pieces
   int slots, pdl, kv_mode;
   int kv_early;          // BKV_FLAG_KV_EARLY: first ring tiles requested before the PDL grid wait
+  int pf;                // kv_early: the warp's first pf entries are also prefetched into L2 before the wait
   const uint16_t *k_new, *v_new;   // fused decode step (f2), nullptr otherwise
   uint16_t *k_pool, *v_pool;
   int64_t pool_sb, pool_sh, pool_ss;
@@ -232,17 +231,17 @@ struct PlannedParams {
   int n_peers;
   unsigned long long *trace;   // dev only (trace build, BKV_TRACE >= 4): 8 %globaltimer stamps per warp
 };
-int planned_smem_bytes(int head_dim, int group, int slots);
+int planned_smem_bytes(int head_dim, int group, int slots, int warps);
 int planned_piece_floats(int group, int head_dim);   // floats per cross-CTA piece slot
 cudaError_t launch_planned(const CUtensorMap &tmK, const CUtensorMap &tmV, const PlannedParams &p,
-                           int head_dim, int grid, int smem_bytes, cudaStream_t s);
+                           int head_dim, int grid, int warps, int smem_bytes, cudaStream_t s);
 // Developer switches (DESIGN.md §7 table), read from the environment ONCE per
 // process and again only on bkv_reload_dev_switches().  BKV_DEBUG (probes that
 // skip work) is honoured only by a BKV_DEV_TRACE build.
 struct DevSwitches {
   int slots, warps, ctas_per_sm, units_per_warp, min_split /* -1: default */, small_plan, streamk;
   int merge_warps, fused_merge, kv_combined, mha_cuda_cores, prefill_mma_sync, prefill_qt;
-  int mixed_overlap, debug, trace, planned_slots, planned_xmerge, planned_dynamic_p;
+  int mixed_overlap, debug, trace, planned_slots, planned_dynamic_p, planned_pf;
 };
 const DevSwitches &dev_switches();
 // Immutable per-device properties (cached per device).

@@ -21,10 +21,14 @@
 //    block) sequence, so all warps finish together;
 //  * the plan, lengths and block-table windows are read before the PDL grid
 //    wait, so a layer starts streaming as soon as the previous one completes;
+//  * the resident KV of the warp's first entries is requested (ring tiles) or
+//    prefetched into L2 before the PDL grid wait, while the previous kernel
+//    drains (BKV_FLAG_KV_EARLY);
 //  * rows cut across the warps of a CTA are merged from shared memory after
-//    the CTA's last block; rows cut across CTAs through one combined piece per
-//    CTA in the workspace and a last-arriver merge (no thread ever waits for
-//    another, so the kernel cannot deadlock whatever the residency).
+//    the CTA's last block; rows cut across CTAs leave one combined piece per
+//    CTA in the workspace, merged by planned_xmerge_kernel, the next kernel on
+//    the stream (no thread ever waits for another CTA: no deadlock whatever
+//    the residency).
 // The streaming core is the one of decode_kernel: per-warp 2-deep rings of
 // 128B-swizzled smem slots filled by ONE 5-D TMA box per 16-slot chunk (K and
 // V of one (block, kv head)), mbarrier completion, S^T = K.Q^T and
@@ -87,15 +91,12 @@ __host__ __device__ inline WarpSmem warp_smem(int D, int gmax, int S) {
   return w;
 }
 
-// Online merge of one piece into a running (M, L, O) row state (log2 domain).
-__device__ __forceinline__ void merge_in(float &M, float &L, float *O, int EPL, float m, float l,
-                                         const float *o) {
-  if (!(l > 0.f)) return;                       // empty piece: nothing to add
-  const float Mn = fmaxf(M, m);
-  const float a = ex2(M - Mn), b = ex2(m - Mn); // M = -inf first: a = 0
-  L = L * a + l * b;
-  for (int e = 0; e < EPL; ++e) O[e] = O[e] * a + o[e] * b;
-  M = Mn;
+// 1/x for a softmax denominator (x >= 1 whenever a token is live: the maximum
+// contributes ex2(0)), 0 for an empty row; MUFU reciprocal, no IEEE slow path.
+__device__ __forceinline__ float rcp_pos(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return x > 0.f ? r : 0.f;
 }
 
 // Merge a batch of up to NB pieces (m, l, o; l = 0 marks an empty slot) into
@@ -213,11 +214,42 @@ __global__ void __launch_bounds__(256, 1)
     x.split = (w4 >> kPlanSplitBit) & 1;
     return x;
   };
+  const int n_zero = __ldg(p.plan_hdr + offsetof(PlanHeader, n_zero) / 4);   // plan data: pre-wait
   // this CTA's merge tasks (<= 2 per warp: a warp has at most two split segments)
   __shared__ int4 task_s[2 * 2 * kPlannedWarps];
   const int t_beg = __ldg(p.ctask + blockIdx.x), t_end = __ldg(p.ctask + blockIdx.x + 1);
   if (threadIdx.x < 2 * (t_end - t_beg)) task_s[threadIdx.x] = __ldg(p.tasks + 2 * t_beg + threadIdx.x);
   SegInfo cur{}, nxt = seg_info(s0);
+
+  // L2 prefetch of the warp's next entries (BKV_FLAG_KV_EARLY contract: the
+  // resident KV is not written by the preceding kernel).  The ring's own first
+  // tiles are requested below; lane k hints entry k < pf of the range, so the
+  // HBM, idle while the previous kernel drains, already streams this layer.
+  if (p.kv_early && p.pf > 0) {
+    const int npf = min(p.pf, n_mine), skip = S / chunks_per_block;
+    int my_h = 0;
+    for (int j = 0, k0 = 0; k0 < npf && s0 + j < s1 && j < 32; ++j) {   // head of entry `lane`
+      const int h = __shfl_sync(FULL, sg_l.y, j);
+      const int len = (__shfl_sync(FULL, sg_l.w, j) & 0xffff) - __shfl_sync(FULL, sg_l.z, j);
+      if (lane >= k0 && lane < k0 + len) my_h = h;
+      k0 += len;
+    }
+    if (lane >= skip && lane < npf) {
+      const int b = static_cast<int>(ent_w & kEntBlockMask);
+      const int dr = (ent_w >> kEntDirShift) & 1;
+      const int ne = static_cast<int>((ent_w >> kEntFillShift) & 31u) + 1;
+      const int lo_s = dr ? bs - ne : 0, hi_s = dr ? bs : ne;
+      for (int c = 0; c < chunks_per_block; ++c) {
+        if (min(hi_s - c * 16, 16) <= max(lo_s - c * 16, 0)) continue;   // no live slot in this chunk
+        if (p.kv_mode) {
+          tma_prefetch_5d(&tmK, 0, c * 16, 0, 0, b * H + my_h);
+        } else {
+          tma_prefetch_5d(&tmK, 0, c * 16, 0, my_h, b);
+          tma_prefetch_5d(&tmV, 0, c * 16, 0, my_h, b);
+        }
+      }
+    }
+  }
 
   if (kTrace) {   // (the stamp needs the loads to have landed)
     volatile int sink = static_cast<int>(ent_w) + nxt.r;
@@ -477,7 +509,7 @@ __global__ void __launch_bounds__(256, 1)
         for (int j = 0; j < 2; ++j) {
           const int head = n * 8 + (lane & 3) * 2 + j;
           if (head >= g) continue;
-          const float inv = lsum[n][j] > 0.f ? 1.f / lsum[n][j] : 0.f;
+          const float inv = rcp_pos(lsum[n][j]);
           uint16_t *o = p.out + static_cast<int64_t>(m.r) * p.o_ss + static_cast<int64_t>(m.h * g + head) * p.o_sh;
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt) {
@@ -585,7 +617,6 @@ __global__ void __launch_bounds__(256, 1)
   // ------------------------------------------------ rows without tokens (Q8)
   {
     const int nw = gridDim.x * W;
-    const int n_zero = __ldg(p.plan_hdr + offsetof(PlanHeader, n_zero) / 4);
     for (int z = gw; z < n_zero; z += nw) {
       const int r = __ldg(p.zero + 2 * z), h = __ldg(p.zero + 2 * z + 1);
       const float o0[EPL] = {};
@@ -594,21 +625,18 @@ __global__ void __launch_bounds__(256, 1)
   }
 
   // ------------------------------------------------------ split merges (a5)
-  // Every (task, q head) pair is one warp-sized item: lane owns elements
-  // [lane*EPL, lane*EPL + EPL) of one head.  A warp merges its items' warp
-  // pieces from shared memory (all loads first, then the weights: no serial
-  // chain), stores bf16 rows (mode 0) or its CTA piece of a cross-CTA row
-  // (mode 1); then ONE fence, one arrival per mode-1 item on that row head's
-  // counter, and the items it closes (it arrived last) are merged from the
-  // global pieces -- no CTA barrier after the first, nothing ever waits.
-  // Pieces are combined in plan order (warp order, then CTA order).
-  __syncthreads();   // every warp's pieces (and the task descriptors) are in shared memory
+  // Items = (merge task, q head) pairs, dealt round-robin to the warps; lane
+  // owns elements [lane*EPL, lane*EPL + EPL) of the item's head.  An item loads
+  // all its warp pieces from shared memory at once and combines them against
+  // one common maximum, in warp order (deterministic).  A row wholly inside the
+  // CTA is normalised and stored (mode 0); a row cut across CTAs leaves its CTA
+  // piece in the workspace for planned_xmerge_kernel, next on the stream
+  // (mode 1).
+  __syncthreads();   // every warp's pieces are in shared memory
   stamp(5);
   const int PS = piece_stride(g, D);   // floats per global piece slot
   const int n_items = (t_end - t_beg) * g;
-  const int Hq = H * g;
-  uint32_t mode1 = 0;
-  for (int it = warp, k = 0; it < n_items; it += W, ++k) {
+  for (int it = warp; it < n_items; it += W) {
     const int i = it / g, j = it - i * g;
     const int4 ta = task_s[2 * i], tb = task_s[2 * i + 1];
     const int wa = ta.z & 0xff, wb = (ta.z >> 8) & 0xff, wa_slot = (ta.z >> 16) & 1;
@@ -640,13 +668,8 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
     for (int e = 0; e < EPL; ++e) O[e] = 0.f;
     merge_batch<EPL, kPlannedWarps>(m, l, o, M, Lr, O);
-    if (kTrace && k == 0) {
-      volatile float sink = O[0];
-      (void)sink;
-      stamp(9);
-    }
     if (ta.w == 0) {
-      store_row(ta.x, ta.y * g + j, O, Lr > 0.f ? 1.f / Lr : 0.f);
+      store_row(ta.x, ta.y * g + j, O, rcp_pos(Lr));
     } else {
       float *gp = p.gpiece + static_cast<int64_t>(tb.w) * PS;
       if constexpr (EPL == 4)
@@ -654,80 +677,12 @@ __global__ void __launch_bounds__(256, 1)
       else
         *reinterpret_cast<float2 *>(gp + j * D + lane * EPL) = make_float2(O[0], O[1]);
       if (lane == 0) *reinterpret_cast<float2 *>(gp + g * D + 2 * j) = make_float2(M, Lr);
-      mode1 |= 1u << k;
     }
-  }
-  stamp(7);
-  if (mode1 == 0 || p.xmerge) {   // (xmerge: planned_xmerge_kernel, next on the stream, merges them)
-    stamp(6);
-    return;
-  }
-  // release this warp's CTA pieces (one fence), then one arrival per (cross-CTA
-  // row, q head): lane k takes the warp's k-th item, relaxed atomics all in
-  // flight at once; the acquire fence below orders the closing loads
-  fence_acq_rel_gpu();
-  __syncwarp();
-  bool close = false;
-  if ((mode1 >> lane) & 1) {
-    const int it = warp + lane * W;
-    const int i = it / g, j = it - i * g;
-    const int4 ta = task_s[2 * i], tb = task_s[2 * i + 1];
-    int *c = p.cnt + ta.x * Hq + ta.y * g + j;
-    int old;
-    asm volatile("atom.relaxed.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(c) : "memory");
-    if (old == tb.y - 1) {
-      close = true;
-      asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(c), "r"(0) : "memory");   // self-cleaning
-    }
-  }
-  const uint32_t closes = __ballot_sync(FULL, close);
-  stamp(8);
-  if (closes == 0) {
-    stamp(6);
-    return;
-  }
-  fence_acq_rel_gpu();
-  for (int it = warp, k = 0; it < n_items; it += W, ++k) {
-    if (!((closes >> k) & 1)) continue;
-    const int i = it / g, j = it - i * g;
-    const int4 ta = task_s[2 * i], tb = task_s[2 * i + 1];
-    const int c0 = tb.x, n = tb.y, flag0 = tb.z;
-    float M = -INFINITY, Lr = 0.f, O[EPL];
-#pragma unroll
-    for (int e = 0; e < EPL; ++e) O[e] = 0.f;
-    for (int k0 = 0; k0 < n; k0 += 8) {   // the row's CTA pieces, CTA order, 8 loads in flight
-      float m[8], l[8], o[8][EPL];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        l[u] = 0.f;
-        m[u] = -INFINITY;
-        if (k0 + u < n) {
-          const int kk = k0 + u;
-          const float *q = p.gpiece + static_cast<int64_t>(kk == 0 ? 2 * c0 + flag0 : 2 * (c0 + kk)) * PS;
-          if constexpr (EPL == 4) {
-            const float4 v = __ldcg(reinterpret_cast<const float4 *>(q + j * D + lane * EPL));
-            o[u][0] = v.x;
-            o[u][1] = v.y;
-            o[u][2] = v.z;
-            o[u][3] = v.w;
-          } else {
-            const float2 v = __ldcg(reinterpret_cast<const float2 *>(q + j * D + lane * EPL));
-            o[u][0] = v.x;
-            o[u][1] = v.y;
-          }
-          const float2 v = __ldcg(reinterpret_cast<const float2 *>(q + g * D + 2 * j));
-          m[u] = v.x;
-          l[u] = v.y;
-        }
-      }
-      merge_batch<EPL, 8>(m, l, o, M, Lr, O);
-    }
-    store_row(ta.x, ta.y * g + j, O, Lr > 0.f ? 1.f / Lr : 0.f);
   }
   stamp(6);
 }
 
-// Cross-CTA merge as a second, stream-ordered kernel (xmerge = 1, the default):
+// Cross-CTA merge as a second, stream-ordered kernel:
 // one warp per (row cut across CTAs, q head) loads the row's n CTA pieces at once
 // and combines them in CTA order.  It needs no atomics or fences -- the decode
 // grid has completed -- and its CTAs hold no shared memory, so they co-reside
@@ -779,7 +734,7 @@ __global__ void __launch_bounds__(256) planned_xmerge_kernel(const PlannedParams
     }
     merge_batch<EPL, 8>(m, l, o, M, Lr, O);
   }
-  const float inv = Lr > 0.f ? 1.f / Lr : 0.f;
+  const float inv = rcp_pos(Lr);
   const int64_t off = static_cast<int64_t>(r) * p.o_ss + static_cast<int64_t>(h * g + j) * p.o_sh + lane * EPL;
   if constexpr (EPL == 4) {
     uint2 w;
@@ -798,20 +753,20 @@ __global__ void __launch_bounds__(256) planned_xmerge_kernel(const PlannedParams
 
 int planned_piece_floats(int group, int head_dim) { return planned::piece_stride(group, head_dim); }
 
-int planned_smem_bytes(int head_dim, int group, int slots) {
+int planned_smem_bytes(int head_dim, int group, int slots, int warps) {
   const int gmax = group > 8 ? 16 : 8;
-  return 1024 + kPlannedWarps * planned::warp_smem(head_dim, gmax, slots).total;
+  return 1024 + warps * planned::warp_smem(head_dim, gmax, slots).total;
 }
 
 template <int D, bool G16>
 static cudaError_t launch_planned_t(const CUtensorMap &tmK, const CUtensorMap &tmV, const PlannedParams &p,
-                                   int grid, int smem, cudaStream_t s) {
+                                   int grid, int warps, int smem, cudaStream_t s) {
   cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void *>(planned::planned_kernel<D, G16>), smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t lc = {};
   cudaLaunchAttribute attr[1];
   lc.gridDim = dim3(grid);
-  lc.blockDim = dim3(kPlannedWarps * 32);
+  lc.blockDim = dim3(warps * 32);
   lc.dynamicSmemBytes = smem;
   lc.stream = s;
   if (p.pdl) {
@@ -822,7 +777,7 @@ static cudaError_t launch_planned_t(const CUtensorMap &tmK, const CUtensorMap &t
   }
   e = cudaLaunchKernelEx(&lc, planned::planned_kernel<D, G16>, tmK, tmV, p);
   if (e != cudaSuccess) return e;
-  if (p.xmerge) {   // sized by capacity (graph-safe); items beyond the step's count exit
+  {   // cross-CTA merge kernel, sized by capacity (graph-safe); items beyond the step's count exit
     cudaLaunchConfig_t lm = {};
     lm.gridDim = dim3((p.xrows_cap * p.g + 7) / 8);
     lm.blockDim = dim3(256);
@@ -838,13 +793,13 @@ static cudaError_t launch_planned_t(const CUtensorMap &tmK, const CUtensorMap &t
 }
 
 cudaError_t launch_planned(const CUtensorMap &tmK, const CUtensorMap &tmV, const PlannedParams &p,
-                           int head_dim, int grid, int smem, cudaStream_t s) {
+                           int head_dim, int grid, int warps, int smem, cudaStream_t s) {
   const bool g16 = p.g > 8;
   if (head_dim == 128)
-    return g16 ? launch_planned_t<128, true>(tmK, tmV, p, grid, smem, s)
-               : launch_planned_t<128, false>(tmK, tmV, p, grid, smem, s);
-  return g16 ? launch_planned_t<64, true>(tmK, tmV, p, grid, smem, s)
-             : launch_planned_t<64, false>(tmK, tmV, p, grid, smem, s);
+    return g16 ? launch_planned_t<128, true>(tmK, tmV, p, grid, warps, smem, s)
+               : launch_planned_t<128, false>(tmK, tmV, p, grid, warps, smem, s);
+  return g16 ? launch_planned_t<64, true>(tmK, tmV, p, grid, warps, smem, s)
+             : launch_planned_t<64, false>(tmK, tmV, p, grid, warps, smem, s);
 }
 
 }  // namespace bkv

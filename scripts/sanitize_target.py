@@ -91,10 +91,7 @@ for cfg, tp in (("tiny_gqa", 1), ("llama70b", 8), ("opt13b", 8)):
     kd = torch.randn(lay.batch, H, d, device="cuda").to(torch.bfloat16)
     plan = bkv.decode_plan(lay.lens, lay.block_tables, lay.dirs, pool, Hq)
     peer = torch.empty_like(qd)
-    for xm in ("1", "0"):
-        os.environ["BKV_PLANNED_XMERGE"] = xm
-        bkv.reload_dev_switches()
-        o1 = bkv.decode_planned(pool, bt, dirs, lens, plan, qd, k_new=kd, v_new=kd, pdl=True, kv_early=True)
-        o2 = bkv.decode_planned(pool, bt, dirs, lens, plan, qd, peer_outs=[peer])
+    o1 = bkv.decode_planned(pool, bt, dirs, lens, plan, qd, k_new=kd, v_new=kd, pdl=True, kv_early=True)
+    o2 = bkv.decode_planned(pool, bt, dirs, lens, plan, qd, peer_outs=[peer])
     torch.cuda.synchronize()
     print(cfg, tp, "planned ok", float(o1.float().abs().mean()), float(o2.float().abs().mean()))

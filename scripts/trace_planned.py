@@ -74,8 +74,7 @@ print(f"{cfg} tp{tp} {mode}: graph of {nl} layers {e0.elapsed_time(e1) * 1e3 / n
 T = np.stack([w[start:start + tr_bytes].view(torch.int64).cpu().numpy().reshape(W, 16) for w in wss])   # [layer][warp][k]
 t0 = T[0, :, 0][T[0, :, 0] > 0].min()
 T = np.where(T > 0, T - t0, -1) / 1e3    # us
-names = ["entry", "prewait", "gridwait", "first", "stream_end", "barrier", "merged", "phaseA",
-         "arrived", "item0", "unused"]
+names = ["entry", "prewait", "gridwait", "first", "stream_end", "barrier", "merged"]
 for l in range(nl):
     row = []
     for k, n in enumerate(names):
@@ -89,7 +88,7 @@ s = T[l, :, 4] - T[l, :, 3]
 print(f"  L{l} per-warp streaming (first tile -> done): p10 {np.percentile(s, 10):.2f} p50 {np.median(s):.2f} "
       f"p90 {np.percentile(s, 90):.2f} max {s.max():.2f} us; merges (barrier -> merged) max "
       f"{(T[l, :, 6] - T[l, :, 5]).max():.2f} us; first tile after wait p50 {np.median(T[l, :, 3] - T[l, :, 2]):.2f}")
-for a, b in ((5, 9), (9, 7), (7, 8), (8, 6)):
+for a, b in ((4, 5), (5, 6)):
     ok = (T[l, :, a] >= 0) & (T[l, :, b] >= 0)
     dd = T[l, ok, b] - T[l, ok, a]
     if dd.size:

@@ -173,18 +173,6 @@ def test_planned_rejects_mismatched_plan():
         bkv.decode_planned(pool, bt, dirs, lens, bad, q)
 
 
-@pytest.mark.parametrize("cfg,tp", [("llama70b", 8), ("opt13b", 4)])
-def test_planned_in_kernel_cross_cta_merge(cfg, tp, monkeypatch):
-    """BKV_PLANNED_XMERGE=0: rows cut across CTAs merged inside the decode kernel by the
-    last CTA to arrive (relaxed per-head counters after one release fence) instead of the
-    separate merge kernel -- every element vs the oracle, repeat bitwise, counters reset."""
-    monkeypatch.setenv("BKV_PLANNED_XMERGE", "0")
-    run_full(cfg, tp, 1, seed=5, mode="step", planned=True, repeat=3)
-    for cfg_s, seed, qs in ATT_CASES:
-        o, ref = _planned_case(make_case(cfg_s, seed, q_scale_log2=qs), repeat=2)
-        check_close(o, ref, cfg_s)
-
-
 def test_planned_graph_replays_a_new_plan():
     """A CUDA graph captured with step A's plan replays step B (new lengths, same batch and
     geometry) once B's plan and lengths are copied into the same device buffers: equal to an
