@@ -95,3 +95,4 @@ for a, b in ((4, 5), (5, 6)):
         print(f"  {names[a]} -> {names[b]}: n {dd.size} p50 {np.median(dd):.2f} p90 {np.percentile(dd, 90):.2f} max {dd.max():.2f} us")
 out_dir = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
 np.savez(os.path.join(out_dir, f"trace_{cfg}_tp{tp}_{mode}.npz"), T=T, warps=hd["warps"], grid=hd["grid"])
+
