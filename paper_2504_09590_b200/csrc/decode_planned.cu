@@ -99,33 +99,6 @@ __device__ __forceinline__ float rcp_pos(float x) {
   return x > 0.f ? r : 0.f;
 }
 
-// Merge a batch of up to NB pieces (m, l, o; l = 0 marks an empty slot) into
-// the running row state (M, L, O), log2 domain: all weights of the batch come
-// from one common maximum, so the loads need not wait for each other.
-template <int EPL, int NB>
-__device__ __forceinline__ void merge_batch(const float (&m)[NB], const float (&l)[NB], const float (&o)[NB][EPL],
-                                            float &M, float &L, float (&O)[EPL]) {
-  float Mb = M;
-#pragma unroll
-  for (int k = 0; k < NB; ++k)
-    if (l[k] > 0.f) Mb = fmaxf(Mb, m[k]);
-  if (Mb == -INFINITY) return;   // nothing live yet
-  const float a = ex2(M - Mb);   // M = -inf: a = 0
-  L *= a;
-#pragma unroll
-  for (int e = 0; e < EPL; ++e) O[e] *= a;
-#pragma unroll
-  for (int k = 0; k < NB; ++k) {
-    if (l[k] > 0.f) {
-      const float w = ex2(m[k] - Mb);
-      L = fmaf(l[k], w, L);
-#pragma unroll
-      for (int e = 0; e < EPL; ++e) O[e] = fmaf(o[k][e], w, O[e]);
-    }
-  }
-  M = Mb;
-}
-
 template <int D, bool G16>
 __global__ void __launch_bounds__(256, 1)
     planned_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
@@ -729,35 +702,53 @@ __global__ void __launch_bounds__(256) planned_xmerge_kernel(const PlannedParams
   if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
   const int r = x.x, h = x.y, c0 = x.z, n = x.w & 0xffff, flag0 = x.w >> 16;
   const int PS = piece_stride(g, D);
-  float M = -INFINITY, Lr = 0.f, O[EPL];
+  // the row's CTA pieces in CTA order, 8 loads in flight per batch, branch-free
+  // (predicated loads, empty slots weigh nothing), rescaled across batches
+  float M = -1e30f, Lr = 0.f, O[EPL];
 #pragma unroll
   for (int e = 0; e < EPL; ++e) O[e] = 0.f;
   for (int k0 = 0; k0 < n; k0 += 8) {
     float m[8], l[8], o[8][EPL];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      l[u] = 0.f;
-      m[u] = -INFINITY;
-      if (k0 + u < n) {
-        const int kk = k0 + u;
-        const float *q = p.gpiece + static_cast<int64_t>(kk == 0 ? 2 * c0 + flag0 : 2 * (c0 + kk)) * PS;
+      const int kk = k0 + u;
+      const float *q = p.gpiece + static_cast<int64_t>(kk == 0 ? 2 * c0 + flag0 : 2 * (c0 + kk)) * PS;
+      float2 ml = make_float2(-INFINITY, 0.f);
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (kk < n) {
+        ml = __ldg(reinterpret_cast<const float2 *>(q + g * D + 2 * j));
         if constexpr (EPL == 4) {
-          const float4 v = __ldg(reinterpret_cast<const float4 *>(q + j * D + lane * EPL));
-          o[u][0] = v.x;
-          o[u][1] = v.y;
-          o[u][2] = v.z;
-          o[u][3] = v.w;
+          v = __ldg(reinterpret_cast<const float4 *>(q + j * D + lane * EPL));
         } else {
-          const float2 v = __ldg(reinterpret_cast<const float2 *>(q + j * D + lane * EPL));
-          o[u][0] = v.x;
-          o[u][1] = v.y;
+          const float2 v2 = __ldg(reinterpret_cast<const float2 *>(q + j * D + lane * EPL));
+          v.x = v2.x;
+          v.y = v2.y;
         }
-        const float2 v = __ldg(reinterpret_cast<const float2 *>(q + g * D + 2 * j));
-        m[u] = v.x;
-        l[u] = v.y;
+      }
+      m[u] = ml.x;
+      l[u] = ml.y;
+      o[u][0] = v.x;
+      o[u][1] = v.y;
+      if constexpr (EPL == 4) {
+        o[u][2] = v.z;
+        o[u][3] = v.w;
       }
     }
-    merge_batch<EPL, 8>(m, l, o, M, Lr, O);
+    float Mb = M;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) Mb = fmaxf(Mb, m[u]);
+    const float a = ex2(M - Mb);
+    Lr *= a;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) O[e] *= a;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const float w = ex2(m[u] - Mb);
+      Lr = fmaf(l[u], w, Lr);
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) O[e] = fmaf(o[u][e], w, O[e]);
+    }
+    M = Mb;
   }
   const float inv = rcp_pos(Lr);
   const int64_t off = static_cast<int64_t>(r) * p.o_ss + static_cast<int64_t>(h * g + j) * p.o_sh + lane * EPL;

@@ -4,6 +4,3 @@ python paper_2504_09590_b200/build.py > /dev/null 2>&1
 timeout 900 python -m pytest tests/test_planned_gpu.py -x -q 2>&1 | tail -3 | tee gpurun_out/dev/planned_tests.txt
 SH="llama70b:8:planned_early opt13b:8:planned_early llama70b:4:planned_early opt13b:4:planned_early llama70b:2:planned_early opt13b:2:planned_early llama70b:1:planned_early opt13b:1:planned_early opt30b:4:planned_early"
 timeout 600 python scripts/quick_perf.py $SH 2>&1 | tee gpurun_out/dev/perf.txt
-BKV_BUILD_TRACE=1 python paper_2504_09590_b200/build.py --force > /dev/null 2>&1
-for s in "llama70b 8 6 early"; do BKV_TRACE=8 timeout 300 python scripts/trace_planned.py $s; done 2>&1 | tee gpurun_out/dev/trace_cyc.txt
-python paper_2504_09590_b200/build.py --force > /dev/null 2>&1
