@@ -324,7 +324,7 @@ def run_ours(args):
 
     import paper_2504_09590_b200 as bkv
     from synth import CONFIGS, make_case
-    from paper_2504_09590_b200.tp import HeadShard, PeerReassembly, gather_heads
+    from paper_2504_09590_b200.tp import HeadShard, MulticastReassembly, PeerReassembly, gather_heads
 
     # dev-only: BKV_DIST_BACKEND=gloo runs several ranks on one GPU (smoke test of the N>1 path)
     backend = os.environ.get("BKV_DIST_BACKEND", "nccl")
@@ -396,10 +396,12 @@ def run_ours(args):
     # reassembled outputs: per-layer gather -> [layer][global head][B][d]; one gather per step
     # (default) -> rank-major [rank][layer][local head][B][d] (global head = rank * Hq + local)
     glob_shape = (n_layers, Hq * tp, B, d) if args.gather == "layer" else (tp, n_layers, Hq, B, d)
-    n_sets = 3 if (tp > 1 and args.reassembly == "p2p") else 2   # e2e buffer sets (p2p: triple)
+    fused = tp > 1 and args.reassembly in ("p2p", "nvls")
+    n_sets = 3 if fused else 2   # e2e buffer sets (fused reassembly: triple)
     p2ps = None
-    if tp > 1 and args.reassembly == "p2p":   # f2: fused NVLink reassembly instead of the all-gather
-        p2ps = [PeerReassembly(shard, n_layers, B, d, dev) for _ in range(n_sets)]
+    if fused:   # f2: fused NVLink reassembly (peer stores, or NVLS multicast stores) instead of the all-gather
+        R = MulticastReassembly if args.reassembly == "nvls" else PeerReassembly
+        p2ps = [R(shard, n_layers, B, d, dev) for _ in range(n_sets)]
         out_glob = p2ps[0].glob
     else:
         out_glob = torch.empty(glob_shape, dtype=torch.bfloat16, device=dev) if tp > 1 else None
@@ -418,7 +420,8 @@ def run_ours(args):
                     bkv.decode_planned(pools[l], md["bt"], md["dirs"], md["lens"], md["plan_obj"], qd[l],
                                        k_new=knd[l], v_new=vnd[l], softmax_scale=scale,
                                        out=p2p.local_out(l).permute(1, 0, 2), peer_outs=p2p.peer_outs(l),
-                                       ws=wsb, pdl=True, kv_early=True, **gm)
+                                       ws=wsb, pdl=True, kv_early=True,
+                                       multicast=getattr(p2p, "multicast", False), **gm)
                 else:
                     bkv.decode_planned(pools[l], md["bt"], md["dirs"], md["lens"], md["plan_obj"], qd[l],
                                        k_new=knd[l], v_new=vnd[l], softmax_scale=scale,
@@ -652,7 +655,9 @@ def run_ours(args):
             "path": "bkv_decode_plan once per step (host) + bkv_decode_planned per layer (fused append, "
                     "PDL, early KV tiles)",
             "plan_blocks_per_warp": meta_d["plan_obj"].header["P"],
-            "reassembly": ("p2p stores + peer barrier (bkv_decode_planned peer_outs)" if p2ps
+            "reassembly": ("nvls multicast stores + peer barrier (bkv_decode_planned, BKV_FLAG_PEER_MULTICAST)"
+                           if p2ps and args.reassembly == "nvls"
+                           else "p2p stores + peer barrier (bkv_decode_planned peer_outs)" if p2ps
                            else f"nccl all_gather_into_tensor, one per {args.gather}" if tp > 1
                            else "none (1 GPU)"),
             "attn_layer_tokens_per_s": B / (att_avg_us * 1e-6),
@@ -698,8 +703,9 @@ def main():
     ap.add_argument("--gather", default="step", choices=["step", "layer"],
                     help="N>1, nccl reassembly: one all-gather per step of every layer's outputs (default) "
                          "or one per layer")
-    ap.add_argument("--reassembly", default="nccl", choices=["nccl", "p2p"],
-                    help="N>1: NCCL all-gather (default) or fused NVLink stores (CUDA IPC peer memory)")
+    ap.add_argument("--reassembly", default="nccl", choices=["nccl", "p2p", "nvls"],
+                    help="N>1: NCCL all-gather (default), fused NVLink stores (CUDA IPC peer memory) or "
+                         "fused NVLS multicast stores (torch symmetric memory's multicast mapping)")
     ap.add_argument("--no-graphs", dest="graphs", action="store_false",
                     help="launch eagerly instead of replaying CUDA graphs")
     args = ap.parse_args()

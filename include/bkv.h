@@ -275,6 +275,14 @@ BKV_API bkv_status bkv_kv_append_checkpoint(const bkv_kv_pool *pool, const bkv_b
  * before the grid wait; q, k_new, v_new and the workspace are still read
  * after it. */
 #define BKV_FLAG_KV_EARLY 2u
+/* bkv_decode_multi_out and bkv_decode_planned: peer_outs[0] (n_peers must be 1)
+ * is an NVLS MULTICAST address (cuMulticastCreate / torch symmetric memory's
+ * multicast_ptr) that maps every rank's global output: each output row slice
+ * is stored ONCE with multimem.st and the NVSwitch replicates it to every rank
+ * bound to the object (PAPER.md P:759 moves these outputs
+ * with NCCL).  Same offsets as the per-peer form; completion still needs
+ * bkv_peer_barrier (which orders the multicast alias before its release). */
+#define BKV_FLAG_PEER_MULTICAST 4u
 BKV_API bkv_status bkv_paged_decode_attention_ex(const bkv_kv_pool *pool, const bkv_block_map *map,
                                                  const int32_t *seq_lens, int32_t max_seq_len,
                                                  const void *q, int64_t q_stride_seq,

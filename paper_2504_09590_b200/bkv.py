@@ -53,6 +53,7 @@ EXPORTS = ("bkv_kv_append", "bkv_paged_decode_attention", "bkv_decode_workspace_
            "bkv_paged_mixed_attention")
 BKV_FLAG_PDL = 1   # include/bkv.h: programmatic dependent launch (seq_lens not written by the previous kernel)
 BKV_FLAG_KV_EARLY = 2   # planned decode: resident KV not written by the previous kernel either
+BKV_FLAG_PEER_MULTICAST = 4   # peer_outs = [one NVLS multicast address] (multimem stores)
 
 
 def lib():
@@ -430,11 +431,12 @@ def _ptr_array(ptrs):
 
 def decode_multi_out(pool: KVPool, block_tables, dirs, seq_lens, q, out, peer_outs, k_new=None,
                      v_new=None, softmax_scale=None, max_seq_len=None, ws=None, stream=None, pdl=False,
-                     fills=None, num_entries=None):
+                     fills=None, num_entries=None, multicast=False):
     """bkv_decode_multi_out (fused reassembly): decode attention (or the fused
     decode step when k_new/v_new are given) whose output rows are also stored into every
     pointer of ``peer_outs`` (ints = device-accessible peer addresses, or tensors), with
-    ``out``'s strides.  Returns out."""
+    ``out``'s strides.  ``multicast``: peer_outs is ONE NVLS multicast address and each row
+    is stored once with multimem.st (BKV_FLAG_PEER_MULTICAST).  Returns out."""
     p, m, out, scale, msl, ws = _attn_args(pool, block_tables, dirs, seq_lens, q, softmax_scale,
                                            out, max_seq_len, ws, stream, fills, num_entries)
     arr, n = _ptr_array(peer_outs)
@@ -446,7 +448,8 @@ def decode_multi_out(pool: KVPool, block_tables, dirs, seq_lens, q, out, peer_ou
     rc = lib().bkv_decode_multi_out(
         ctypes.byref(p), ctypes.byref(m), seq_lens.data_ptr(), int(msl), kp, vp, q.data_ptr(),
         q.stride(0), q.stride(1), q.shape[1], float(scale), out.data_ptr(), arr, n, out.stride(0),
-        out.stride(1), ws.data_ptr(), ws.numel(), BKV_FLAG_PDL if pdl else 0, _stream_ptr(stream))
+        out.stride(1), ws.data_ptr(), ws.numel(),
+        (BKV_FLAG_PDL if pdl else 0) | (BKV_FLAG_PEER_MULTICAST if multicast else 0), _stream_ptr(stream))
     _check(rc, "bkv_decode_multi_out")
     return out
 
@@ -593,11 +596,13 @@ def decode_plan(seq_lens_host, block_tables_host, dirs_host, pool_or_geom, num_q
 
 def decode_planned(pool: KVPool, block_tables, dirs, seq_lens, plan: DecodePlan, q, k_new=None, v_new=None,
                    softmax_scale=None, out=None, peer_outs=(), ws=None, stream=None, pdl=False, fills=None,
-                   num_entries=None, kv_early=False):
+                   num_entries=None, kv_early=False, multicast=False):
     """bkv_decode_planned: one layer's decode attention (or fused decode step when k_new/v_new
-    are given) with the step's host-built plan, in one kernel launch.  Returns out.
-    ``kv_early`` (with ``pdl``): BKV_FLAG_KV_EARLY -- the preceding kernel does not write this
-    pool's resident KV, so the first KV tiles are requested before the grid wait."""
+    are given) with the step's host-built plan (the decode kernel + the cross-CTA merge
+    kernel).  Returns out.  ``kv_early`` (with ``pdl``): BKV_FLAG_KV_EARLY -- the preceding
+    kernel does not write this pool's resident KV, so the first KV tiles are requested (and
+    the next few prefetched into L2) before the grid wait.  ``multicast``: ``peer_outs`` is
+    ONE NVLS multicast address (BKV_FLAG_PEER_MULTICAST)."""
     p, m, out, scale, _, ws = _attn_args(pool, block_tables, dirs, seq_lens, q, softmax_scale,
                                          out, None, ws, stream, fills, num_entries)
     if plan.dev.device != q.device:
@@ -619,7 +624,8 @@ def decode_planned(pool: KVPool, block_tables, dirs, seq_lens, plan: DecodePlan,
         ctypes.byref(p), ctypes.byref(m), seq_lens.data_ptr(), plan.host.ctypes.data, plan.dev.data_ptr(),
         kp, vp, q.data_ptr(), q.stride(0), q.stride(1), q.shape[1], float(scale), out.data_ptr(),
         out.stride(0), out.stride(1), arr if n else None, n, ws.data_ptr(), ws.numel(),
-        (BKV_FLAG_PDL if pdl else 0) | (BKV_FLAG_KV_EARLY if (pdl and kv_early) else 0), _stream_ptr(stream))
+        (BKV_FLAG_PDL if pdl else 0) | (BKV_FLAG_KV_EARLY if (pdl and kv_early) else 0)
+        | (BKV_FLAG_PEER_MULTICAST if multicast else 0), _stream_ptr(stream))
     _check(rc, "bkv_decode_planned")
     return out
 

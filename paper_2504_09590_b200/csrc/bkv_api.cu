@@ -417,7 +417,10 @@ static bkv_status decode_impl(const bkv_kv_pool *pool, const bkv_block_map *map,
                               void *workspace, size_t workspace_bytes, uint32_t flags,
                               bkv_stream_t stream, void *const *peer_outs = nullptr,
                               int32_t n_peers = 0, bool after_own_prefill = false) {
-  if (flags & ~BKV_FLAG_PDL) return fail(BKV_ERR_INVALID_ARGUMENT, "unknown flags 0x%x", flags);
+  if (flags & ~(BKV_FLAG_PDL | BKV_FLAG_PEER_MULTICAST))
+    return fail(BKV_ERR_INVALID_ARGUMENT, "unknown flags 0x%x", flags);
+  if ((flags & BKV_FLAG_PEER_MULTICAST) && n_peers != 1)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "BKV_FLAG_PEER_MULTICAST needs exactly one peer output (the multicast address)");
   bkv_status s = check_pool(pool);
   if (s) return s;
   if ((s = check_map(map))) return s;
@@ -506,6 +509,7 @@ static bkv_status decode_impl(const bkv_kv_pool *pool, const bkv_block_map *map,
   if (n_peers < 0 || n_peers > bkv::kMaxPeers)
     return fail(BKV_ERR_UNSUPPORTED, "n_peers %d outside [0, %d]", n_peers, bkv::kMaxPeers);
   p.n_peers = n_peers;
+  p.peer_mc = (flags & BKV_FLAG_PEER_MULTICAST) ? 1 : 0;
   // split merge: separate stream-ordered merge_kernel by default; in-kernel last-arriver merge
   // (opt-in, BKV_FUSED_MERGE=1: measured slower -- the last-arriving warp merges all g rows
   // of a GQA group serially at the tail, e.g. Llama-70B TP1 115 -> 149 us per layer)
@@ -918,7 +922,10 @@ bkv_status bkv_decode_planned(const bkv_kv_pool *pool, const bkv_block_map *map,
                               int32_t num_q_heads, float softmax_scale, void *out, int64_t o_stride_seq,
                               int64_t o_stride_head, void *const *peer_outs, int32_t n_peers,
                               void *workspace, size_t workspace_bytes, uint32_t flags, bkv_stream_t stream) {
-  if (flags & ~(BKV_FLAG_PDL | BKV_FLAG_KV_EARLY)) return fail(BKV_ERR_INVALID_ARGUMENT, "unknown flags 0x%x", flags);
+  if (flags & ~(BKV_FLAG_PDL | BKV_FLAG_KV_EARLY | BKV_FLAG_PEER_MULTICAST))
+    return fail(BKV_ERR_INVALID_ARGUMENT, "unknown flags 0x%x", flags);
+  if ((flags & BKV_FLAG_PEER_MULTICAST) && n_peers != 1)
+    return fail(BKV_ERR_INVALID_ARGUMENT, "BKV_FLAG_PEER_MULTICAST needs exactly one peer output (the multicast address)");
   if ((flags & BKV_FLAG_KV_EARLY) && !(flags & BKV_FLAG_PDL))
     return fail(BKV_ERR_INVALID_ARGUMENT, "BKV_FLAG_KV_EARLY needs BKV_FLAG_PDL");
   bkv_status s = check_pool(pool);
@@ -965,7 +972,8 @@ bkv_status bkv_decode_planned(const bkv_kv_pool *pool, const bkv_block_map *map,
   if (dyn_p > 0 && hd->P >= dyn_p)
     return decode_impl(pool, map, seq_lens, map->bt_stride * pool->block_size, k_new, v_new, q, q_stride_seq,
                        q_stride_head, num_q_heads, softmax_scale, out, o_stride_seq, o_stride_head, workspace,
-                       workspace_bytes, flags & BKV_FLAG_PDL, stream, peer_outs, n_peers);
+                       workspace_bytes, flags & (BKV_FLAG_PDL | BKV_FLAG_PEER_MULTICAST), stream, peer_outs,
+                       n_peers);
   if (!aligned16(q) || !aligned16(out) || q_stride_seq % 8 || q_stride_head % 8 || o_stride_seq % 8 ||
       o_stride_head % 8)
     return fail(BKV_ERR_INVALID_ARGUMENT, "q/out must be 16-byte aligned with strides multiple of 8");
@@ -1039,6 +1047,7 @@ bkv_status bkv_decode_planned(const bkv_kv_pool *pool, const bkv_block_map *map,
   p.pool_sh = pool->stride_head;
   p.pool_ss = pool->stride_slot;
   p.n_peers = n_peers;
+  p.peer_mc = (flags & BKV_FLAG_PEER_MULTICAST) ? 1 : 0;
   for (int k = 0; k < bkv::kMaxPeers; ++k) {
     p.peer_out[k] = k < n_peers ? static_cast<uint16_t *>(peer_outs[k]) : nullptr;
     if (k < n_peers && (!peer_outs[k] || !aligned16(peer_outs[k])))

@@ -87,6 +87,7 @@ struct DecodeParams {
   // these device-accessible outputs (peers' buffers over NVLink), same strides
   uint16_t *peer_out[8];
   int n_peers;
+  int peer_mc;   // peer_out[0] is an NVLS multicast address (one multimem store reaches every rank)
   int debug_flags;       // dev only: 1 = skip the math (data-movement skeleton), 2 = merge re-arm only, 4 = CTA-major first units, 8 = exit after the plan, 16 = exit at entry, 32 = no early PDL trigger
   unsigned long long *trace;  // dev only (BKV_TRACE): per-warp event log, else nullptr
   int trace_cap;         // events per warp
@@ -229,6 +230,7 @@ struct __align__(16) PlannedParams {
   int64_t pool_sb, pool_sh, pool_ss;
   uint16_t *peer_out[8];
   int n_peers;
+  int peer_mc;   // peer_out[0] is an NVLS multicast address (one multimem store reaches every rank)
   unsigned long long *trace;   // dev only (trace build, BKV_TRACE >= 4): 8 %globaltimer stamps per warp
 };
 int planned_smem_bytes(int head_dim, int group, int slots, int warps);

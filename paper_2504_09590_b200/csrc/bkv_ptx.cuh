@@ -99,6 +99,35 @@ __device__ __forceinline__ void tma_prefetch_5d(const CUtensorMap *m, int c0, in
                "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
                : "memory");
 }
+// NVLS multicast stores (fused reassembly, f2): ONE store to a multicast address
+// reaches the same offset of every buffer bound to the multicast object (every
+// rank's global output), through the NVSwitch.
+__device__ __forceinline__ void mc_store8(void *mc, uint2 w) {
+  const unsigned long long v = static_cast<unsigned long long>(w.x) | (static_cast<unsigned long long>(w.y) << 32);
+  asm volatile("multimem.st.relaxed.sys.global.b64 [%0], %1;" ::"l"(mc), "l"(v) : "memory");
+}
+__device__ __forceinline__ void mc_store4(void *mc, uint32_t w) {
+  asm volatile("multimem.st.relaxed.sys.global.b32 [%0], %1;" ::"l"(mc), "r"(w) : "memory");
+}
+// the output row slice of this lane also goes to the peers: n_peers plain stores
+// (CUDA-IPC / P2P mappings) or, peer_mc set, one multicast store via peer_out[0]
+template <class P>
+__device__ __forceinline__ void peer_put8(const P &p, int64_t off, uint2 w) {
+  if (p.peer_mc) {
+    mc_store8(p.peer_out[0] + off, w);
+  } else {
+    for (int k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint2 *>(p.peer_out[k] + off) = w;
+  }
+}
+template <class P>
+__device__ __forceinline__ void peer_put4(const P &p, int64_t off, uint32_t w) {
+  if (p.peer_mc) {
+    mc_store4(p.peer_out[0] + off, w);
+  } else {
+    for (int k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint32_t *>(p.peer_out[k] + off) = w;
+  }
+}
+
 // 1-D bulk copy global -> shared (16-byte aligned, size multiple of 16).
 __device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_t bytes,
                                           uint32_t bar) {

@@ -391,11 +391,11 @@ __device__ __forceinline__ void merge_row(const DecodeParams &p, int u0, int ns,
     w.x = pack_bf16(acc[0] * inv, acc[1] * inv);
     w.y = pack_bf16(acc[2] * inv, acc[3] * inv);
     *reinterpret_cast<uint2 *>(p.out + off) = w;
-    for (int k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint2 *>(p.peer_out[k] + off) = w;
+    peer_put8(p, off, w);
   } else {
     const uint32_t w = pack_bf16(acc[0] * inv, acc[1] * inv);
     *reinterpret_cast<uint32_t *>(p.out + off) = w;
-    for (int k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint32_t *>(p.peer_out[k] + off) = w;
+    peer_put4(p, off, w);
   }
 }
 
@@ -1217,10 +1217,10 @@ __global__ void __launch_bounds__(256) merge_kernel(const DecodeParams p) {
     if (nb == 0) {   // empty context (reading Q8): zeros; no range ever touched the row
       if constexpr (EPL == 4) {
         *reinterpret_cast<uint2 *>(p.out + off) = make_uint2(0u, 0u);
-        for (int k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint2 *>(p.peer_out[k] + off) = make_uint2(0u, 0u);
+        peer_put8(p, off, make_uint2(0u, 0u));
       } else {
         *reinterpret_cast<uint32_t *>(p.out + off) = 0u;
-        for (int k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint32_t *>(p.peer_out[k] + off) = 0u;
+        peer_put4(p, off, 0u);
       }
       return;
     }
@@ -1244,10 +1244,10 @@ __global__ void __launch_bounds__(256) merge_kernel(const DecodeParams p) {
     if (p.n_peers > 0) {
       if constexpr (EPL == 4) {
         const uint2 w = *reinterpret_cast<const uint2 *>(p.out + off);
-        for (int k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint2 *>(p.peer_out[k] + off) = w;
+        peer_put8(p, off, w);
       } else {
         const uint32_t w = *reinterpret_cast<const uint32_t *>(p.out + off);
-        for (int k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint32_t *>(p.peer_out[k] + off) = w;
+        peer_put4(p, off, w);
       }
     }
     return;
@@ -1354,6 +1354,9 @@ __global__ void peer_barrier_kernel(PeerBarrierParams p) {
   const uint32_t epoch = epoch_s;
   const int k = threadIdx.x;
   if (k >= p.n) return;
+  // outputs may have been stored through a multicast alias (BKV_FLAG_PEER_MULTICAST):
+  // order those with the unicast accesses that follow, then publish system-wide
+  asm volatile("fence.proxy.alias;" ::: "memory");
   asm volatile("fence.acq_rel.sys;" ::: "memory");
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.pads[k] + p.rank), "r"(epoch) : "memory");
   unsigned long long t0;

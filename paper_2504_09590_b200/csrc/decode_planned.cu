@@ -453,11 +453,11 @@ __global__ void __launch_bounds__(256, 1)
       w.x = pack_bf16(o[0] * inv, o[1] * inv);
       w.y = pack_bf16(o[2] * inv, o[3] * inv);
       *reinterpret_cast<uint2 *>(p.out + off) = w;
-      for (int k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint2 *>(p.peer_out[k] + off) = w;
+      peer_put8(p, off, w);
     } else {
       const uint32_t w = pack_bf16(o[0] * inv, o[1] * inv);
       *reinterpret_cast<uint32_t *>(p.out + off) = w;
-      for (int k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint32_t *>(p.peer_out[k] + off) = w;
+      peer_put4(p, off, w);
     }
   };
 
@@ -499,10 +499,10 @@ __global__ void __launch_bounds__(256, 1)
                               lane * EPL;
           if constexpr (EPL == 4) {
             const uint2 w = __ldcg(reinterpret_cast<const uint2 *>(p.out + off));
-            for (int k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint2 *>(p.peer_out[k] + off) = w;
+            peer_put8(p, off, w);
           } else {
             const uint32_t w = __ldcg(reinterpret_cast<const unsigned int *>(p.out + off));
-            for (int k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint32_t *>(p.peer_out[k] + off) = w;
+            peer_put4(p, off, w);
           }
         }
       }
@@ -757,11 +757,11 @@ __global__ void __launch_bounds__(256) planned_xmerge_kernel(const PlannedParams
     w.x = pack_bf16(O[0] * inv, O[1] * inv);
     w.y = pack_bf16(O[2] * inv, O[3] * inv);
     *reinterpret_cast<uint2 *>(p.out + off) = w;
-    for (int k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint2 *>(p.peer_out[k] + off) = w;
+    peer_put8(p, off, w);
   } else {
     const uint32_t w = pack_bf16(O[0] * inv, O[1] * inv);
     *reinterpret_cast<uint32_t *>(p.out + off) = w;
-    for (int k = 0; k < p.n_peers; ++k) *reinterpret_cast<uint32_t *>(p.peer_out[k] + off) = w;
+    peer_put4(p, off, w);
   }
 }
 

@@ -151,3 +151,49 @@ class PeerReassembly:
         """Raise if a peer barrier timed out (call outside timed regions)."""
         if int(self.err.item()) != 0:
             raise RuntimeError("bkv_peer_barrier timed out: a peer rank did not arrive")
+
+
+class MulticastReassembly(PeerReassembly):
+    """Fused reassembly through an NVLS multicast object (BKV_FLAG_PEER_MULTICAST):
+    every rank's global output [n_layers][H_q][B][d] is bound to one multicast object, and
+    the decode kernels store each row slice ONCE to the multicast address; the NVSwitch writes
+    it into every rank's buffer (instead of n_peers separate NVLink stores).  Completion: the
+    same peer barrier (its alias fence orders the multicast stores before the release).
+
+    Plumbing only, through torch symmetric memory (allocation, handle exchange, multicast
+    mapping): needs a CUDA process group on GPUs joined by NVSwitch with multicast support;
+    raises if the runtime offers no multicast address.  Same interface as PeerReassembly,
+    ``multicast = True`` tells the caller to pass BKV_FLAG_PEER_MULTICAST."""
+
+    multicast = True
+
+    def __init__(self, shard: HeadShard, n_layers: int, batch: int, head_dim: int, device, group=None):
+        import torch.distributed._symmetric_memory as symm_mem
+        self.shard = shard
+        hq, hl = shard.num_q_heads, len(shard.q_heads)
+        grp = group if group is not None else dist.group.WORLD
+        gname = grp.group_name
+        if hasattr(symm_mem, "enable_symm_mem_for_group"):
+            symm_mem.enable_symm_mem_for_group(gname)
+        self.glob = symm_mem.empty((n_layers, hq, batch, head_dim), dtype=torch.bfloat16, device=device)
+        self.glob.zero_()
+        self._hdl = symm_mem.rendezvous(self.glob, gname)
+        mc = int(getattr(self._hdl, "multicast_ptr", 0) or 0)
+        if mc == 0:
+            raise RuntimeError("no NVLS multicast address for this group (needs NVSwitch multicast support)")
+        self.pads = symm_mem.empty((shard.tp,), dtype=torch.int32, device=device)
+        self.pads.zero_()
+        self._hdl_pads = symm_mem.rendezvous(self.pads, gname)
+        self.pad_ptrs = [int(x) for x in self._hdl_pads.buffer_ptrs]
+        esz = self.glob.element_size()
+        self.layer_bytes = hq * batch * head_dim * esz
+        self.slice_off = shard.rank * hl * batch * head_dim * esz
+        self.mc_base = mc
+        self.counter = torch.zeros(1, dtype=torch.int32, device=device)
+        self.err = torch.zeros(1, dtype=torch.int32, device=device)
+        torch.cuda.synchronize(device)
+        dist.barrier(grp)
+
+    def peer_outs(self, layer: int):
+        """ONE pointer: this rank's slice of layer `layer` in the multicast mapping."""
+        return [self.mc_base + layer * self.layer_bytes + self.slice_off]

@@ -40,7 +40,9 @@ def test_decode_argument_errors():
     assert decode(pool(), bmap(), q=FAKE + 2) == INVALID and "aligned" in err()
     assert decode(pool(), bmap(), scale=float("nan")) == INVALID and "scale" in err()
     assert decode(pool(), bmap(), max_len=8 * 16 + 1) == INVALID and "max_seq_len" in err()
-    assert decode(pool(), bmap(), flags=4) == INVALID and "flags" in err()
+    assert decode(pool(), bmap(), flags=8) == INVALID and "flags" in err()
+    # BKV_FLAG_PEER_MULTICAST without exactly one peer output (the plain call has none)
+    assert decode(pool(), bmap(), flags=4) == INVALID and "MULTICAST" in err()
     p = pool()
     p.k = None
     assert decode(p, bmap()) == INVALID
