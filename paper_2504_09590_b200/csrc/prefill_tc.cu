@@ -15,20 +15,21 @@
 //              causal by token index; a mask-free path for whole
 //              tiles), online softmax in the log2 domain with a lazy rescale
 //              (the running max moves only when it grows by > 8, so O in TMEM
-//              is rarely touched), writes P (bf16) to shared memory, zeroes
-//              dead V rows (group 0), runs the epilogue;
+//              is rarely touched), writes P (bf16 pairs) back into the TMEM
+//              columns of the S buffer it just read, zeroes dead V rows
+//              (group 0), runs the epilogue;
 //   warp 8     K producer: walks the request's entries in logical order and
 //              publishes each 64-key tile's chunk metadata through named
 //              barriers, then TMA-streams the K tile (four 16-slot chunks as
 //              rows of one 128B-swizzled operand) into a 3-stage ring;
 //   warp 9     MMA issuer (one lane) + TMEM owner: per key tile, for each
 //              query tile S = Q.K^T (M 128, N <= 64, K 128) into one of two
-//              TMEM S buffers, then O += P.V (M 128, N 128, K 16 per chunk)
-//              into that tile's TMEM O accumulator; tcgen05.commit releases
-//              S/P buffers and stages;
+//              TMEM S buffers, then O += P.V (M 128, N 128, K 16 per chunk,
+//              A = P straight from TMEM: the "TS" form) into that tile's TMEM
+//              O accumulator; tcgen05.commit releases S/P buffers and stages;
 //   warp 10    V producer (same walk, V tiles).
-// Operands: Q, K and P are K-major 128B-swizzled, V is MN-major 128B-swizzled
-// -- exactly the layout the TMA boxes of the pool land in.
+// Operands: Q and K are K-major 128B-swizzled, V is MN-major 128B-swizzled
+// -- exactly the layout the TMA boxes of the pool land in; P never leaves TMEM.
 #include <math.h>
 
 #include "bkv_internal.h"
@@ -67,6 +68,16 @@ __device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, ui
       "l"(a), "l"(b), "r"(id), "r"(acc)
       : "memory");
 }
+// the "TS" form: A (M x K, here P) read from TMEM -- row i = lane i, bf16 pairs packed per
+// 32-bit column (element k in column k/2, even k in the low half); validated by
+// scripts/umma_probe.cu against a host GEMM
+__device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(id), "r"(acc)
+      : "memory");
+}
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                : "memory");
@@ -91,6 +102,11 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float *v) {
       "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
       "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
       : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t *w) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(w[0]),
+               "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+               : "memory");
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
@@ -206,8 +222,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
   uint8_t *gb = smem_raw + (base - raw);
   const uint32_t sQ = base;                                  // QT x (2 halves x 128 rows x 128 B)
   const uint32_t sStage = sQ + QT * 2 * kTcRows * 128;       // NS key tiles (K | V)
-  const uint32_t sP = sStage + NS * STAGE;                   // QT x 2 x 128 rows x 128 B (64 keys)
-  int4 *metas = reinterpret_cast<int4 *>(gb + (sP - base) + QT * 2 * kTcRows * 128);   // [stage][chunk]
+  int4 *metas = reinterpret_cast<int4 *>(gb + (sStage + NS * STAGE - base));   // [stage][chunk]
   int *tcount = reinterpret_cast<int *>(metas + NS * kTcChunks);                 // chunks | last flag
   uint64_t *bars = reinterpret_cast<uint64_t *>(tcount + ((NS + 1) & ~1));   // 8-byte aligned
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * NS + 8 * QT + 1);
@@ -365,10 +380,9 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
       for (int q = 0; q < QT; ++q) {
         mbar_wait(grp0 + 64 * q + 32 + 8 * pb, (gt >> 1) & 1);
         tc_fence_after();
-        for (int j = 0; j < nch; ++j) {
-          const uint64_t a = sdesc(sP + (q * 2 + pb) * (kTcRows * 128) + j * 32, 16, 1024);
+        for (int j = 0; j < nch; ++j) {   // A = P of chunk j: 8 TMEM columns of the S buffer pb
           const uint64_t b = sdesc(sStage + st * STAGE + TILE + j * 2048, HALF, 1024);
-          umma(tmem + 256 * q + 128, a, b, idO, first_pv[q] ? 0u : 1u);
+          umma_ts(tmem + 256 * q + 128, tmem + 256 * q + pb * 64 + 8 * j, b, idO, first_pv[q] ? 0u : 1u);
           first_pv[q] = false;
         }
         umma_commit(grp0 + 64 * q + 48 + 8 * pb);
@@ -486,9 +500,6 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
       for (int j = 0; j < kTcChunks; ++j)
         if (j < nch) tmem_ld16(tq + lane_addr + sb * 64 + 16 * j, s + 16 * j);
       tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(s_free0 + 8 * sb);
       // per chunk, the live slots of this row form one interval [clo, chi): the
       // entry's live range intersected with the causal bound (forward: token
       // tb + c <= pos -> c <= pos - tb; reversed: tb - c <= pos -> c >= tb - pos)
@@ -553,11 +564,12 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
       }
       if (grow) m_ref = mx;
       const float base_m = m_ref == -INFINITY ? 0.f : m_ref;
-      // P -> shared memory buffer sb (K-major, 128B swizzle)
+      // P -> TMEM over the S buffer sb just read (bf16 pairs, columns 8j .. 8j + 7 per
+      // 16-key chunk): the P.V MMA takes it as its A operand from TMEM (no shared-memory
+      // round trip, no proxy fence).  S(t + 2) reuses the buffer: it is issued after
+      // s_free below and after P.V(t) (tcgen05 MMAs of one thread execute in order).
       prof(4);
-      if (t >= 2) mbar_wait(p_free0 + 8 * sb, ((t - 2) >> 1) & 1);
       prof(5);
-      const uint32_t prow = sP + (qg * 2 + sb) * (kTcRows * 128);
       float l4[4] = {0.f, 0.f, 0.f, 0.f};   // independent row-sum chains, folded into l below
 #pragma unroll
       for (int j = 0; j < kTcChunks; ++j) {
@@ -571,13 +583,17 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
           l4[(c >> 1) & 3] += p0 + p1;
           pw[c >> 1] = pack_bf16(p0, p1);
         }
-        st_shared_v4(prow + tswz(row, 2 * j), make_uint4(pw[0], pw[1], pw[2], pw[3]));
-        st_shared_v4(prow + tswz(row, 2 * j + 1), make_uint4(pw[4], pw[5], pw[6], pw[7]));
+        tmem_st8(tq + lane_addr + sb * 64 + 8 * j, pw);
       }
       l += (l4[0] + l4[1]) + (l4[2] + l4[3]);
-      fence_proxy_async_smem();
+      tmem_wait_st();
+      fence_proxy_async_smem();   // (group 0's zeroed V rows: generic writes the MMA reads)
+      tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full0 + 8 * sb);
+      if (lane == 0) {
+        mbar_arrive(s_free0 + 8 * sb);
+        mbar_arrive(p_full0 + 8 * sb);
+      }
       prof(6);
       if (kTcProf && threadIdx.x == 0 && blockIdx.x < 148) atomicAdd(&g_tc_prof[(blockIdx.x * 3 + 0) * kProfSlots + 7], 1ull);
       if (tc & kTcLastFlag) {
@@ -631,7 +647,7 @@ namespace bkv {
 template <int QT>
 static int tc_smem_bytes() {
   constexpr int NS = QT == 1 ? kTcStages : 3;
-  return 1024 + QT * 2 * kTcRows * 128 + NS * 4 * kTcKeys * 128 + QT * 2 * kTcRows * 128 +
+  return 1024 + QT * 2 * kTcRows * 128 + NS * 4 * kTcKeys * 128 +
          NS * kTcChunks * 16 + ((NS + 1) & ~1) * 4 + (2 * NS + 8 * QT + 1) * 8 + 16;   // + metadata, barriers, TMEM slot
 }
 

@@ -4,6 +4,9 @@
 //                                   B = K K-major SW128 ([half][16 slots][128B], as TMA lands it)
 //   O = P.V     M=128, N=128, K=16: A = P K-major SW128 (128B rows, first 32B used),
 //                                   B = V MN-major SW128 ([half][16 slots][128B])
+//   O2 = P.V    the same product with A = P in TMEM (the "TS" form): row i = lane i,
+//               bf16 pairs packed per 32-bit column (element k in column k/2, even
+//               k in the low half), written by tcgen05.st from the row's thread
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o umma_probe scripts/umma_probe.cu
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -40,6 +43,12 @@ __device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t a, uint64_t b, uin
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(id), "r"(acc));
 }
+__device__ __forceinline__ void mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(id), "r"(acc));
+}
 __device__ __forceinline__ void commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                : "memory");
@@ -63,7 +72,7 @@ __device__ __forceinline__ void ld16(uint32_t taddr, float *v) {
 
 __global__ void __launch_bounds__(128, 1) probe(const __nv_bfloat16 *Q, const __nv_bfloat16 *K,
                                                 const __nv_bfloat16 *V, const __nv_bfloat16 *P,
-                                                float *S_out, float *O_out) {
+                                                float *S_out, float *O_out, float *O2_out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sQ = sm;                 // 2 halves x 128 rows x 128B = 32KB
@@ -97,14 +106,28 @@ __global__ void __launch_bounds__(128, 1) probe(const __nv_bfloat16 *Q, const __
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tslot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tslot;
-  const uint32_t tS = tmem, tO = tmem + 128;   // columns
+  const uint32_t tS = tmem, tO = tmem + 128, tP = tmem + 64, tO2 = tmem + 256;   // columns
+  {   // P row tid -> TMEM lane tid, columns tP .. tP + 7 (bf16 pairs)
+    uint32_t w[8];
+    for (int c = 0; c < 8; ++c) {
+      const __nv_bfloat162 pr = *reinterpret_cast<const __nv_bfloat162 *>(P + tid * 16 + 2 * c);
+      w[c] = *reinterpret_cast<const uint32_t *>(&pr);
+    }
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(tP + lane_base),
+                 "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]) : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
   if (tid == 0) {
     const uint32_t idS = idesc(128, 16, 0, 0), idO = idesc(128, 128, 0, 1);
     for (int k = 0; k < 8; ++k) {
@@ -116,6 +139,7 @@ __global__ void __launch_bounds__(128, 1) probe(const __nv_bfloat16 *Q, const __
     const uint64_t a = sdesc(smem_u32(sP), 16, 1024);
     const uint64_t b = sdesc(smem_u32(sV), 2048, 1024);
     mma(tO, a, b, idO, 0);
+    mma_ts(tO2, tP, b, idO, 0);
     commit(smem_u32(bar));
   }
   mbar_wait(smem_u32(bar), 0);
@@ -128,10 +152,12 @@ __global__ void __launch_bounds__(128, 1) probe(const __nv_bfloat16 *Q, const __
   for (int c = 0; c < 128; c += 16) {
     ld16(tO + lane_base + c, v);
     for (int i = 0; i < 16; ++i) O_out[row * 128 + c + i] = v[i];
+    ld16(tO2 + lane_base + c, v);
+    for (int i = 0; i < 16; ++i) O2_out[row * 128 + c + i] = v[i];
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 int main() {
@@ -144,19 +170,20 @@ int main() {
   for (int i = 0; i < NK; ++i) hK[i] = __float2bfloat16(rnd()), hV[i] = __float2bfloat16(rnd());
   for (int i = 0; i < NP; ++i) hP[i] = __float2bfloat16(rnd());
   __nv_bfloat16 *dQ, *dK, *dV, *dP;
-  float *dS, *dO;
+  float *dS, *dO, *dO2;
   cudaMalloc(&dQ, NQ * 2); cudaMalloc(&dK, NK * 2); cudaMalloc(&dV, NK * 2); cudaMalloc(&dP, NP * 2);
-  cudaMalloc(&dS, 128 * 16 * 4); cudaMalloc(&dO, 128 * 128 * 4);
+  cudaMalloc(&dS, 128 * 16 * 4); cudaMalloc(&dO, 128 * 128 * 4); cudaMalloc(&dO2, 128 * 128 * 4);
   cudaMemcpy(dQ, hQ, NQ * 2, cudaMemcpyHostToDevice); cudaMemcpy(dK, hK, NK * 2, cudaMemcpyHostToDevice);
   cudaMemcpy(dV, hV, NK * 2, cudaMemcpyHostToDevice); cudaMemcpy(dP, hP, NP * 2, cudaMemcpyHostToDevice);
   const int smem = 1024 + 32768 + 4096 + 4096 + 16384 + 64;
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  probe<<<1, 128, smem>>>(dQ, dK, dV, dP, dS, dO);
+  probe<<<1, 128, smem>>>(dQ, dK, dV, dP, dS, dO, dO2);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { printf("CUDA error %s\n", cudaGetErrorString(e)); return 1; }
-  float *S = (float *)malloc(128 * 16 * 4), *O = (float *)malloc(128 * 128 * 4);
+  float *S = (float *)malloc(128 * 16 * 4), *O = (float *)malloc(128 * 128 * 4), *O2 = (float *)malloc(128 * 128 * 4);
+  cudaMemcpy(O2, dO2, 128 * 128 * 4, cudaMemcpyDeviceToHost);
   cudaMemcpy(S, dS, 128 * 16 * 4, cudaMemcpyDeviceToHost); cudaMemcpy(O, dO, 128 * 128 * 4, cudaMemcpyDeviceToHost);
-  double es = 0, eo = 0;
+  double es = 0, eo = 0, eo2 = 0;
   for (int r = 0; r < 128; ++r)
     for (int c = 0; c < 16; ++c) {
       double ref = 0;
@@ -168,8 +195,10 @@ int main() {
       double ref = 0;
       for (int k = 0; k < 16; ++k) ref += (double)__bfloat162float(hP[r * 16 + k]) * __bfloat162float(hV[k * 128 + c]);
       eo = fmax(eo, fabs(ref - O[r * 128 + c]));
+      eo2 = fmax(eo2, fabs(ref - O2[r * 128 + c]));
     }
-  printf("S max err %.3e (S[0][0]=%f)  O max err %.3e (O[0][0]=%f)\n", es, S[0], eo, O[0]);
-  printf("%s\n", (es < 1e-2 && eo < 1e-2) ? "UMMA PROBE OK" : "UMMA PROBE MISMATCH");
+  printf("S max err %.3e (S[0][0]=%f)  O max err %.3e (O[0][0]=%f)  O(TS, P in TMEM) max err %.3e (O2[0][0]=%f)\n",
+         es, S[0], eo, O[0], eo2, O2[0]);
+  printf("%s\n", (es < 1e-2 && eo < 1e-2 && eo2 < 1e-2) ? "UMMA PROBE OK" : "UMMA PROBE MISMATCH");
   return 0;
 }
