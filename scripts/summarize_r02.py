@@ -112,12 +112,17 @@ for fn in sorted(os.listdir(SRC)) if os.path.isdir(SRC) else []:
         cfg, tp = name.split("_", 1)[1].rsplit("_tp", 1)
         tp = int(tp)
         alg = alg_bytes(cfg, tp) / 1e6
-        dur = sum(r["dur_us"] for r in rows)
-        dram = sum(r["dram_mb"] for r in rows)
-        main = rows[0]
-        layer.append((f"{cfg} tp{tp}", name.split("_")[0], main["dur_us"], dur, dram, alg,
-                      alg / dur * 1e3 / PEAK))
-        traffic[f"{cfg}_tp{tp}"] = dram * 1e6
+        # one layer = one launch of each kernel; captures hold several layers: mean per kernel
+        per = defaultdict(list)
+        for r in rows:
+            per[r["kernel"]].append(r)
+        mean = lambda k, f: sum(x[f] for x in per[k]) / len(per[k])
+        dur = sum(mean(k, "dur_us") for k in per)
+        dram = sum(mean(k, "dram_mb") for k in per)
+        main_k = rows[0]["kernel"]
+        layer.append((f"{cfg} tp{tp}", name.split("_")[0], mean(main_k, "dur_us"), dur, dram, alg,
+                      alg / dur * 1e3 / PEAK, len(per[main_k])))
+        traffic[f"{cfg}_tp{tp}"] = dram * 1e6   # per layer (mean over the captured layers)
     if name.startswith("prefill_") and rows:
         cfg = name[len("prefill_"):].rsplit("_tp", 1)[0]
         sh = CONFIGS[cfg]
@@ -131,10 +136,10 @@ for fn in sorted(os.listdir(SRC)) if os.path.isdir(SRC) else []:
         prefill.append(f"| {name} | {r['dur_us']:.1f} | {flops / 1e9:.1f} | "
                        f"{flops / (r['dur_us'] * 1e-6) / 1e12:.1f} | {r['tensor_pct']} |")
 md += ["", "## Per-layer roofline from ncu (kernels timed alone)", "",
-       "| shard | path | decode kernel us | layer us (decode + merge) | dram MB | alg MB | dram/alg | frac of measured peak |",
-       "|---|---|---|---|---|---|---|---|"]
-for s, path, dk, dur, dram, alg, frac in layer:
-    md.append(f"| {s} | {path} | {dk:.1f} | {dur:.1f} | {dram:.1f} | {alg:.1f} | {dram / alg:.3f} | {frac:.3f} |")
+       "| shard | path | layers | decode kernel us | layer us (decode + merge) | dram MB | alg MB | dram/alg | frac of measured peak |",
+       "|---|---|---|---|---|---|---|---|---|"]
+for s, path, dk, dur, dram, alg, frac, nl in layer:
+    md.append(f"| {s} | {path} | {nl} | {dk:.1f} | {dur:.1f} | {dram:.1f} | {alg:.1f} | {dram / alg:.3f} | {frac:.3f} |")
 if prefill:
     md += ["", "## Prefill kernel (tensor-bound; causal flops of the 16 whole-prompt prefills)", "",
            "| capture | dur us | GFLOP | TFLOP/s | tensor pipe % |", "|---|---|---|---|---|"] + prefill
