@@ -78,6 +78,16 @@ def test_planned_edge_lengths_and_empty(direction):
         assert (u16(o)[[i for i, L in enumerate(lens) if L == 0]] == 0).all(), "empty context -> zeros (Q8)"
 
 
+@pytest.mark.parametrize("L,hq,hkv,bs", [(8192, 8, 1, 16), (30000, 8, 1, 32), (4096, 4, 4, 16)])
+def test_planned_one_long_request_spans_every_cta(L, hq, hkv, bs):
+    """One request: its row(s) are cut across every warp of the grid (P = 1-2 blocks per
+    warp), so the cross-CTA merge combines up to 148 CTA pieces in batches of 8."""
+    sh = Shape("long", hq, hkv, 128, bs, 1, 0.5, "uniform", L, 1, 1)
+    case = make_case(sh, 9, lens=[L], is_be=[True])
+    o, ref = _planned_case(case, repeat=2)
+    check_close(o, ref, f"long L={L} g={hq // hkv} bs={bs}")
+
+
 def test_planned_single_token_is_exact_v0():
     for hq, hkv, d in ((4, 4, 64), (8, 1, 128), (16, 2, 128)):
         sh = Shape("one", hq, hkv, d, 16, 6, 0.5, "uniform", 16, 1, 1)
