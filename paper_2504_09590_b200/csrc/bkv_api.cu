@@ -49,7 +49,7 @@ void load_switches() {
 #endif
   s.planned_slots = env_int("BKV_PLANNED_SLOTS", 2);
   s.planned_dynamic_p = env_int("BKV_PLANNED_DYNAMIC_P", 128);
-  s.planned_pf = env_int("BKV_PLANNED_PF", 4);
+  s.planned_pf = env_int("BKV_PLANNED_PF", 3);
   g_sw = s;
 }
 }  // namespace
