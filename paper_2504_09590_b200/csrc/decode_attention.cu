@@ -917,44 +917,35 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
       release();
       const int t0 = lane >> 2, t1 = t0 + 8;
       const bool ok0 = t0 >= lo && t0 < hi, ok1 = t1 >= lo && t1 < hi;
-      float alpha[NT][2];
+      // Lazy reference maximum (log2 domain), as in the planned kernel: the common chunk
+      // exponentiates against the running reference (p <= 2^8); the cross-lane max, the
+      // correction exponential and the O rescale run only when a live score passes the
+      // reference by more than 8 (a segment's first chunk, rarely after).
+      float sv0[NT][2], sv1[NT][2];
+      bool need = false;
 #pragma unroll
-      for (int n = 0; n < NT; ++n) {
+      for (int n = 0; n < NT; ++n)
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          const float s0 = ok0 ? (sa[n][j] + sb[n][j]) * p.scale_log2 : -INFINITY;
-          const float s1 = ok1 ? (sa[n][2 + j] + sb[n][2 + j]) * p.scale_log2 : -INFINITY;
-          float mx = fmaxf(s0, s1);
-          mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, 4));
-          mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, 8));
-          mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, 16));
-          const float mnew = fmaxf(mrun[n][j], mx);
-          alpha[n][j] = ex2(mrun[n][j] - mnew);
-          const float p0 = ex2(s0 - mnew), p1 = ex2(s1 - mnew);
-          lrun[n][j] = lrun[n][j] * alpha[n][j] + (p0 + p1);
-          mrun[n][j] = mnew;
-          // P^T -> scratch as P[head][token] (row stride 48 B: conflict-free ldmatrix)
-          const int head = n * 8 + (lane & 3) * 2 + j;
-          st_shared_bf16(my_scr + head * 48 + t0 * 2, p0);
-          st_shared_bf16(my_scr + head * 48 + t1 * 2, p1);
+          sv0[n][j] = ok0 ? (sa[n][j] + sb[n][j]) * p.scale_log2 : -INFINITY;
+          sv1[n][j] = ok1 ? (sa[n][2 + j] + sb[n][2 + j]) * p.scale_log2 : -INFINITY;
+          need |= fmaxf(sv0[n][j], sv1[n][j]) > mrun[n][j] + 8.f;
         }
-      }
-      __syncwarp();
-      // B = P^T (k = token, n = head): ldmatrix of P rows (heads) x 8 tokens
-      uint32_t pb[NT][2];
-      if constexpr (NT == 1) {
-        const int r8 = lane & 7, hi8 = (lane >> 3) & 1;
-        ldsm_x2(my_scr + r8 * 48 + hi8 * 16, pb[0][0], pb[0][1]);
-      } else {
-        const int r8 = lane & 7, hi8 = (lane >> 3) & 1, nn = lane >> 4;
-        ldsm_x4(my_scr + (nn * 8 + r8) * 48 + hi8 * 16, pb[0][0], pb[0][1], pb[1][0], pb[1][1]);
-      }
-      // ---- O^T = alpha * O^T + V^T . P^T  (the rescale is skipped, warp-uniformly,
-      // once no running max moved -- the common case after the first chunks)
-      bool moved = false;
+      if (__any_sync(FULL, need)) {
+        float alpha[NT][2];
 #pragma unroll
-      for (int n = 0; n < NT; ++n) moved |= (alpha[n][0] != 1.f) | (alpha[n][1] != 1.f);
-      if (__any_sync(FULL, moved)) {
+        for (int n = 0; n < NT; ++n)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            float mx = fmaxf(sv0[n][j], sv1[n][j]);
+            mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, 4));
+            mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, 8));
+            mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, 16));
+            const float mnew = fmaxf(mrun[n][j], mx);
+            alpha[n][j] = mnew == -INFINITY ? 1.f : ex2(mrun[n][j] - mnew);   // mrun = -inf: 0
+            lrun[n][j] *= alpha[n][j];
+            mrun[n][j] = mnew;
+          }
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -968,6 +959,29 @@ __global__ void __launch_bounds__(KIND == 0 ? 384 : 256, 1)
             oacc[mt][n][3] = hi2.y;
           }
       }
+#pragma unroll
+      for (int n = 0; n < NT; ++n)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const float base_m = mrun[n][j] == -INFINITY ? 0.f : mrun[n][j];   // no live token yet: p = 0
+          const float p0 = ex2(sv0[n][j] - base_m), p1 = ex2(sv1[n][j] - base_m);
+          lrun[n][j] += p0 + p1;
+          // P^T -> scratch as P[head][token] (row stride 48 B: conflict-free ldmatrix)
+          const int head = n * 8 + (lane & 3) * 2 + j;
+          st_shared_bf16(my_scr + head * 48 + t0 * 2, p0);
+          st_shared_bf16(my_scr + head * 48 + t1 * 2, p1);
+        }
+      __syncwarp();
+      // B = P^T (k = token, n = head): ldmatrix of P rows (heads) x 8 tokens
+      uint32_t pb[NT][2];
+      if constexpr (NT == 1) {
+        const int r8 = lane & 7, hi8 = (lane >> 3) & 1;
+        ldsm_x2(my_scr + r8 * 48 + hi8 * 16, pb[0][0], pb[0][1]);
+      } else {
+        const int r8 = lane & 7, hi8 = (lane >> 3) & 1, nn = lane >> 4;
+        ldsm_x4(my_scr + (nn * 8 + r8) * 48 + hi8 * 16, pb[0][0], pb[0][1], pb[1][0], pb[1][1]);
+      }
+      // ---- O^T += V^T . P^T
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
