@@ -1,6 +1,5 @@
 #!/bin/bash
 cd ${GRAFT_REPO_ROOT:-.}; mkdir -p gpurun_out/dev
 python paper_2504_09590_b200/build.py > /dev/null 2>&1
-timeout 900 python -m pytest tests/test_planned_gpu.py -x -q 2>&1 | tail -3 | tee gpurun_out/dev/planned_tests.txt
-SH="llama70b:8:planned_early opt13b:8:planned_early llama70b:4:planned_early opt13b:4:planned_early llama70b:2:planned_early opt13b:2:planned_early llama70b:1:planned_early opt13b:1:planned_early opt30b:4:planned_early"
-for PF in 4 3; do BKV_PLANNED_PF=$PF timeout 600 python scripts/quick_perf.py $SH 2>&1 | sed "s/^/pf$PF /"; done | tee gpurun_out/dev/perf.txt
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_fused_step.py tests/test_general_map_gpu.py tests/test_streams_graphs_gpu.py tests/test_reassembly_gpu.py -x -q 2>&1 | tail -3 | tee gpurun_out/dev/dyn_tests.txt
+timeout 600 python scripts/quick_perf.py opt30b:1:fused llama70b:1:fused opt13b:1:fused llama70b:8:fused 2>&1 | tee gpurun_out/dev/perf_dyn.txt

@@ -3,7 +3,7 @@
 #   pytest_gpu.txt  smoke.txt  bench_*.json (opt13b default with shards, llama70b, opt30b,
 #   general maps, reference arm)  sweep.jsonl (BASELINE configs[4], TP1/2/4/8)
 #   prefill_*.json  sanitizer.txt  n2_gloo_smoke.txt, and the ncu captures (profile_r02.sh).
-# Then, here: python scripts/summarize_r02.py && cp the files to profiles/r02/.
+# ncu reports are summarised on the box into gpurun_out/r02_summary/ (copy to profiles/r02/ here).
 set -u
 cd ${GRAFT_REPO_ROOT:-.}
 O=gpurun_out/r02
@@ -40,5 +40,9 @@ if [ $step = all ] || [ $step = sanitize ]; then
 fi
 if [ $step = all ] || [ $step = ncu ]; then
   timeout 2400 bash scripts/profile_r02.sh > $O/profile.log 2>&1
+  # summarise on the box (gpurun copies back <= 64 MiB): the .ncu-rep files stay there
+  mkdir -p gpurun_out/r02_summary
+  BKV_SUMMARY_DST=gpurun_out/r02_summary python scripts/summarize_r02.py > $O/summarize.log 2>&1
+  rm -f gpurun_out/prof_r02/*.ncu-rep
 fi
 ls -la $O

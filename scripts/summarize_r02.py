@@ -14,7 +14,7 @@ from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SRC = os.path.join(ROOT, "gpurun_out", "prof_r02")
-DST = os.path.join(ROOT, "profiles", "r02")
+DST = os.environ.get("BKV_SUMMARY_DST", os.path.join(ROOT, "profiles", "r02"))
 os.makedirs(DST, exist_ok=True)
 sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
