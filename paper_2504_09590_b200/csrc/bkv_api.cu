@@ -39,6 +39,8 @@ void load_switches() {
   s.mha_cuda_cores = env_int("BKV_MHA_CUDA_CORES", 0);
   s.prefill_mma_sync = env_int("BKV_PREFILL_MMA_SYNC", 0);
   s.prefill_qt = env_int("BKV_PREFILL_QT", 2);
+  s.prefill_q_ldg = env_int("BKV_PREFILL_Q_LDG", 0);
+  s.prefill_o_stg = env_int("BKV_PREFILL_O_STG", 0);
   s.mixed_overlap = env_int("BKV_MIXED_OVERLAP", 1);
 #ifdef BKV_DEV_TRACE
   s.debug = env_int("BKV_DEBUG", 0);
@@ -187,6 +189,27 @@ bkv_status encode_pool_map(CUtensorMap *m, void *base, const bkv_kv_pool *pool, 
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(BKV_ERR_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)r);
+  return BKV_OK;
+}
+
+// 4-D view (64 d, d-half, q head, token) of the query (or output) rows of the
+// prefill kernel: one box {64, 1, g, rows/g} is one 64-d half of `rows` rows
+// (rows = (token, head of the group) pairs), 128B-swizzled.  The token extent is
+// open-ended (the caller passes no row count): the kernel's tiles end at a
+// request's last row, so a box never starts past a token the caller owns, reads
+// before token 0 zero-fill, and output boxes hold only the request's own rows.
+bkv_status encode_rows_map(CUtensorMap *m, const void *q, int head_dim, int num_q_heads, int64_t st_tok,
+                           int64_t st_head, int g, int rows) {
+  auto fn = encode_fn();
+  if (!fn) return fail(BKV_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+  cuuint64_t dims[4] = {64, (cuuint64_t)(head_dim / 64), (cuuint64_t)num_q_heads, (cuuint64_t)1 << 31};
+  cuuint64_t strides[3] = {128, (cuuint64_t)st_head * 2, (cuuint64_t)st_tok * 2};
+  cuuint32_t box[4] = {64, 1, (cuuint32_t)g, (cuuint32_t)(rows / g)};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(q), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(BKV_ERR_CUDA, "cuTensorMapEncodeTiled (queries) failed (CUresult %d)", (int)r);
   return BKV_OK;
 }
 
@@ -713,7 +736,19 @@ bkv_status bkv_paged_prefill_attention(const bkv_kv_pool *pool, const bkv_block_
   p.o_st = o_stride_tok;
   p.o_sh = o_stride_head;
   p.scale_log2 = softmax_scale * 1.4426950408889634f;
-  cudaError_t e = bkv::launch_prefill(tmK, tmV, p, pool->head_dim, max_q_len,
+  p.tiles_max = 0;
+  p.q_tma = 0;
+  // tcgen05 kernel: Q tiles by TMA when a 128-row tile is whole tokens (g | 128)
+  // and output rows by TMA store when a warp's 32 rows are whole tokens (g | 32)
+  CUtensorMap tmQ, tmO;
+  const bool q_tma = tc && 128 % p.g == 0 && bkv::dev_switches().prefill_q_ldg == 0;
+  const bool o_tma = tc && 32 % p.g == 0 && bkv::dev_switches().prefill_o_stg == 0;
+  if (q_tma && (s = encode_rows_map(&tmQ, q, pool->head_dim, num_q_heads, q_stride_tok, q_stride_head, p.g, 128)))
+    return s;
+  if (o_tma && (s = encode_rows_map(&tmO, out, pool->head_dim, num_q_heads, o_stride_tok, o_stride_head, p.g, 32)))
+    return s;
+  cudaError_t e = bkv::launch_prefill(tmK, tmV, q_tma ? &tmQ : nullptr, o_tma ? &tmO : nullptr, p, pool->head_dim,
+                                      max_q_len,
                                       reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "prefill attention launch");
   return BKV_OK;

@@ -123,13 +123,15 @@ struct PrefillParams {
   int64_t o_st, o_sh;
   float scale_log2;
   int tiles_max;          // 128-row query tiles of the longest request (persistent kernels)
+  int q_tma;              // tcgen05 kernel: Q tiles arrive by TMA (tmQ; needs g | 128)
+  int o_tma;              // tcgen05 kernel: whole-warp output rows leave by TMA store (tmO; g | 32)
 };
 int prefill_smem_bytes(int head_dim);
 bool prefill_uses_tc(int head_dim);   // tcgen05 kernel (wants 1-half TMA boxes)
-cudaError_t launch_prefill(const CUtensorMap &tmK, const CUtensorMap &tmV, const PrefillParams &p,
-                           int head_dim, int max_q_len, cudaStream_t s);
-cudaError_t launch_prefill_tc(const CUtensorMap &tmK, const CUtensorMap &tmV, const PrefillParams &p,
-                              int max_q_len, cudaStream_t s);
+cudaError_t launch_prefill(const CUtensorMap &tmK, const CUtensorMap &tmV, const CUtensorMap *tmQ,
+                           const CUtensorMap *tmO, const PrefillParams &p, int head_dim, int max_q_len, cudaStream_t s);
+cudaError_t launch_prefill_tc(const CUtensorMap &tmK, const CUtensorMap &tmV, const CUtensorMap *tmQ,
+                              const CUtensorMap *tmO, const PrefillParams &p, int max_q_len, cudaStream_t s);
 
 // cross-rank completion signal of the fused reassembly (f2)
 struct PeerBarrierParams {
@@ -242,7 +244,7 @@ cudaError_t launch_planned(const CUtensorMap &tmK, const CUtensorMap &tmV, const
 // skip work) is honoured only by a BKV_DEV_TRACE build.
 struct DevSwitches {
   int slots, warps, ctas_per_sm, units_per_warp, min_split /* -1: default */, small_plan, streamk;
-  int merge_warps, fused_merge, kv_combined, mha_cuda_cores, prefill_mma_sync, prefill_qt;
+  int merge_warps, fused_merge, kv_combined, mha_cuda_cores, prefill_mma_sync, prefill_qt, prefill_q_ldg, prefill_o_stg;
   int mixed_overlap, debug, trace, planned_slots, planned_dynamic_p, planned_pf;
 };
 const DevSwitches &dev_switches();

@@ -368,11 +368,11 @@ static cudaError_t launch_prefill_t(const CUtensorMap &tmK, const CUtensorMap &t
   return cudaGetLastError();
 }
 
-cudaError_t launch_prefill(const CUtensorMap &tmK, const CUtensorMap &tmV, const PrefillParams &p,
-                           int head_dim, int max_q_len, cudaStream_t s) {
+cudaError_t launch_prefill(const CUtensorMap &tmK, const CUtensorMap &tmV, const CUtensorMap *tmQ,
+                           const CUtensorMap *tmO, const PrefillParams &p, int head_dim, int max_q_len, cudaStream_t s) {
   if (p.B <= 0 || max_q_len <= 0) return cudaSuccess;
   // head_dim 128: the tcgen05 / TMEM kernel (prefill_tc.cu; tensor maps with one 64-d half per box)
-  if (prefill_uses_tc(head_dim)) return launch_prefill_tc(tmK, tmV, p, max_q_len, s);
+  if (prefill_uses_tc(head_dim)) return launch_prefill_tc(tmK, tmV, tmQ, tmO, p, max_q_len, s);
   return head_dim == 128 ? launch_prefill_t<128>(tmK, tmV, p, max_q_len, s)
                          : launch_prefill_t<64>(tmK, tmV, p, max_q_len, s);
 }

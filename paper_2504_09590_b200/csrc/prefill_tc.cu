@@ -78,6 +78,72 @@ __device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64
       "r"(tmem_a), "l"(b), "r"(id), "r"(acc)
       : "memory");
 }
+// Warp-collective forms: the whole (converged) warp executes them and one
+// elected lane issues -- the descriptors stay warp-uniform (uniform registers),
+// with no per-instruction single-lane divergence loop around the issue.
+__device__ __forceinline__ void umma_w(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(id), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void umma_ts_w(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(id), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_w(uint32_t bar) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(bar)
+      : "memory");
+}
+// S = Q.K^T of one 64-key tile: eight K=16 steps issued from one asm block under one
+// elect; step k's operands sit at fixed byte offsets from the tile bases (the
+// descriptors' start-address field counts 16-byte units and cannot carry):
+//   A (Q, two 64-d halves of 128 rows x 128 B): (k >> 2) * 16384 + (k & 3) * 32
+//   B (K, two halves of 64 keys x 128 B):       (k >> 2) * 8192  + (k & 3) * 32
+__device__ __forceinline__ void umma_s8_w(uint32_t tmem_d, uint64_t a0, uint64_t b0, uint32_t id) {
+  asm volatile(
+      "{\n.reg .pred e;\n.reg .b64 a<8>, b<8>;\n"
+      "mov.b64 a0, %1;\nadd.s64 a1, %1, 2;\nadd.s64 a2, %1, 4;\nadd.s64 a3, %1, 6;\n"
+      "add.s64 a4, %1, 1024;\nadd.s64 a5, %1, 1026;\nadd.s64 a6, %1, 1028;\nadd.s64 a7, %1, 1030;\n"
+      "mov.b64 b0, %2;\nadd.s64 b1, %2, 2;\nadd.s64 b2, %2, 4;\nadd.s64 b3, %2, 6;\n"
+      "add.s64 b4, %2, 512;\nadd.s64 b5, %2, 514;\nadd.s64 b6, %2, 516;\nadd.s64 b7, %2, 518;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a0, b0, %3, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a4, b4, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a5, b5, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a6, b6, %3, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a7, b7, %3, 1;\n}\n" ::"r"(tmem_d),
+      "l"(a0), "l"(b0), "r"(id)
+      : "memory");
+}
+// O += P.V of one key tile: up to four 16-key chunks j < nch, A = P chunk j in TMEM
+// (8 columns from a_tmem), B = V chunk j (MN-major, 2048 B apart); the first step
+// accumulates iff acc0
+__device__ __forceinline__ void umma_pv4_w(uint32_t tmem_d, uint32_t a_tmem, uint64_t b0, uint32_t id, int nch,
+                                           uint32_t acc0) {
+  asm volatile(
+      "{\n.reg .pred e, p0, p1, p2, p3, q0, pa;\n.reg .b64 b<4>;\n.reg .b32 t<4>;\n"
+      "mov.b64 b0, %2;\nadd.s64 b1, %2, 128;\nadd.s64 b2, %2, 256;\nadd.s64 b3, %2, 384;\n"
+      "mov.b32 t0, %1;\nadd.s32 t1, %1, 8;\nadd.s32 t2, %1, 16;\nadd.s32 t3, %1, 24;\n"
+      "setp.ne.b32 pa, %5, 0;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.gt.and.s32 p1, %4, 1, e;\nsetp.gt.and.s32 p2, %4, 2, e;\nsetp.gt.and.s32 p3, %4, 3, e;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t0], b0, %3, pa;\n"
+      "@p1 tcgen05.mma.cta_group::1.kind::f16 [%0], [t1], b1, %3, 1;\n"
+      "@p2 tcgen05.mma.cta_group::1.kind::f16 [%0], [t2], b2, %3, 1;\n"
+      "@p3 tcgen05.mma.cta_group::1.kind::f16 [%0], [t3], b3, %3, 1;\n}\n" ::"r"(tmem_d),
+      "r"(a_tmem), "l"(b0), "r"(id), "r"(nch), "r"(acc0)
+      : "memory");
+}
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                : "memory");
@@ -110,6 +176,24 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t *w) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// packed two-lane FP32 (sm_100 FFMA2 / FADD2)
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n.reg .b64 ra, rb, rc, rd;\nmov.b64 ra, {%2, %3};\nmov.b64 rb, {%4, %5};\nmov.b64 rc, {%6, %7};\n"
+      "fma.rn.f32x2 rd, ra, rb, rc;\nmov.b64 {%0, %1}, rd;\n}\n"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n.reg .b64 ra, rb, rd;\nmov.b64 ra, {%2, %3};\nmov.b64 rb, {%4, %5};\n"
+      "add.rn.f32x2 rd, ra, rb;\nmov.b64 {%0, %1}, rd;\n}\n"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
 
 // the chunk walk (see prefill_attention.cu): entries in logical order, 32 at a
 // time in a lane-distributed window
@@ -197,12 +281,32 @@ constexpr bool kTcProf = false;
 #endif
 constexpr int kProfSlots = 8;
 __device__ unsigned long long g_tc_prof[148 * 3 * kProfSlots];
+// event timeline of CTA 0 (trace builds): per warp, {clock64, tile << 16 | warp << 8 | event};
+// each warp's lane 0 appends to its own region (no atomics on the traced path)
+constexpr int kTraceWarps = 12, kTracePerWarp = 2048;
+__device__ unsigned long long g_tc_trace[2 * kTraceWarps * kTracePerWarp];
+__device__ unsigned int g_tc_tn[kTraceWarps];
+__shared__ unsigned int s_tc_tn[kTraceWarps];   // per-warp event counts (shared: cheap to bump)
+__device__ __forceinline__ void tc_event(int ev, int gt = 0) {
+  if (kTcProf && blockIdx.x == 0 && (threadIdx.x & 31) == 0) {
+    const int w = threadIdx.x >> 5;
+    volatile unsigned int *cnt = s_tc_tn + w;
+    const unsigned i = *cnt;
+    if (i < kTracePerWarp) {
+      unsigned long long *e = g_tc_trace + 2 * (w * kTracePerWarp + i);
+      e[0] = clock64();
+      e[1] = (static_cast<unsigned long long>(gt) << 16) | w << 8 | ev;
+      *cnt = i + 1;
+    }
+  }
+}
 
 // QT = query tiles of 128 rows per CTA (1, or 2 "ping-pong" groups sharing every
 // K/V tile: two softmax warpgroups, twice the MMA work per streamed byte).
 template <int QT>
 __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
     prefill_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                      const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmO,
                       const PrefillParams p) {
   constexpr int D = 128;
   constexpr int NS = QT == 1 ? kTcStages : 3;   // key-tile stages (shared memory budget)
@@ -222,10 +326,13 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
   uint8_t *gb = smem_raw + (base - raw);
   const uint32_t sQ = base;                                  // QT x (2 halves x 128 rows x 128 B)
   const uint32_t sStage = sQ + QT * 2 * kTcRows * 128;       // NS key tiles (K | V)
-  int4 *metas = reinterpret_cast<int4 *>(gb + (sStage + NS * STAGE - base));   // [stage][chunk]
+  // output staging (o_tma): per query group, per softmax warp, per 64-d half: 32 rows x 128 B
+  const uint32_t sO = sStage + NS * STAGE;
+  const int n_ostage = p.o_tma ? QT : 0;
+  int4 *metas = reinterpret_cast<int4 *>(gb + (sO + n_ostage * 2 * kTcRows * 128 - base));   // [stage][chunk]
   int *tcount = reinterpret_cast<int *>(metas + NS * kTcChunks);                 // chunks | last flag
   uint64_t *bars = reinterpret_cast<uint64_t *>(tcount + ((NS + 1) & ~1));   // 8-byte aligned
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * NS + 8 * QT + 1);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * NS + 8 * QT + 2);
   const uint32_t bar0 = smem_u32(bars);
   const uint32_t full0 = bar0, empty0 = bar0 + 8 * NS;
   // per query group q: s_full/s_free (S buffer handoff) and p_full/p_free (P
@@ -233,6 +340,8 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
   // O"), two buffers each; q_full: Q staged
   const uint32_t grp0 = bar0 + 16 * NS;   // group q: + 64 q; s_full +0, s_free +16, p_full +32, p_free +48
   const uint32_t q_full = grp0 + 64 * QT;
+  const uint32_t q_free = q_full + 8;     // every S of the item's query tiles is done: Q may be replaced
+  const bool q_tma = p.q_tma != 0;        // the K producer TMA-loads Q (else the softmax warps stage it)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   auto init_barriers = [&]() {
@@ -247,12 +356,16 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
         mbar_init(grp0 + 64 * q + 32 + 8 * b, 4);   // p_full
         mbar_init(grp0 + 64 * q + 48 + 8 * b, 1);   // p_free
       }
-    mbar_init(q_full, SMW);
+    mbar_init(q_full, q_tma ? 1 : SMW);
+    mbar_init(q_free, 1);
     fence_mbar_init();
   };
+  if (kTcProf && threadIdx.x < kTraceWarps) s_tc_tn[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmK);
     prefetch_tmap(&tmV);
+    if (q_tma) prefetch_tmap(&tmQ);
+    if (p.o_tma) prefetch_tmap(&tmO);
     init_barriers();
   }
   if (warp == WMMA) {   // TMEM per group q: S buffers at 256q + [0, 64) / [64, 128), O at 256q + [128, 256)
@@ -294,7 +407,19 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
     }
     return n_items;
   };
+  // item-level accounting (trace builds): role 2 slots 0 kernel cycles, 1 items,
+  // 2 item start -> first tile metadata, 3 epilogue, 4 next-item search
+  const long long k_t0 = kTcProf ? clock64() : 0;
+  long long it_t = k_t0;
+  auto iprof = [&](int slot, long long &t) {
+    if (kTcProf && threadIdx.x == 0 && blockIdx.x < 148) {
+      const long long c = clock64();
+      atomicAdd(&g_tc_prof[(blockIdx.x * 3 + 2) * kProfSlots + slot], static_cast<unsigned long long>(c - t));
+      t = c;
+    }
+  };
   for (int item = next_item(blockIdx.x); item < n_items; item = next_item(item + G)) {
+  iprof(4, it_t);
   const int x = item / (p.H * p.B), hr = item - x * (p.H * p.B);
   const int r = hr / p.H, h = hr - r * p.H;
   const int q0 = __ldg(p.cu_q + r);
@@ -304,8 +429,11 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
   const int tile_last = ntiles - 1 - QT * x;      // this item: tiles tile_last - QT + 1 .. tile_last
   if (tile_last < 0) continue;
   const int L = __ldg(p.seq_lens + r);
-  const int row0 = (tile_last - QT + 1) * kTcRows;   // may be negative: that group has no rows
-  const int row_end = min(rows, (tile_last + 1) * kTcRows);
+  // query tiles are aligned to the END of the request's rows: the latest rows fill
+  // whole tiles, a partial tile holds the earliest rows (and its dead rows lie
+  // before the request: the TMA Q box never reads past the request's last token)
+  const int row_end = rows - QT * kTcRows * x;
+  const int row0 = row_end - QT * kTcRows;   // may be negative: those rows (a whole group) are dead
   const int pos_max = L - n + (row_end - 1) / g;
 
   // Tile metadata: the producer walks the request's chunks (one tile of
@@ -317,6 +445,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
   auto bar_mma = [](int st) { return 1 + st; };                  // producer + MMA warp: 64 threads
   auto bar_sm = [](int st) { return 1 + NS + st; };              // producer + softmax: 32 + 32 SMW threads
 
+  long long ep_t = 0;
   if (warp == WK || warp == WV) {
     // ------------------------------------------------------------ producers
     // A key tile = up to four 16-slot chunks of the walk, each landing as rows
@@ -325,16 +454,35 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
     // Warp 4 streams K and publishes the tile metadata (before its copies, so
     // the consumers can prepare), warp 6 streams V: 8 boxes per warp per tile.
     const bool is_k = warp == WK;
+    tc_event(0);
     TcWalk walk;
     tc_walk_init(p, r, L, walk);
     TcChunk ch[kTcChunks], nx[kTcChunks];
     const uint64_t pol = policy_evict_last();   // every query tile of the request re-reads these
     int nch = tc_tile(p, r, L, pos_max, walk, ch);
+    tc_event(1);
+    if (is_k && q_tma && lane == 0) {
+      // Q of the item's QT query tiles: one box {64 d, 1 half, g heads, 128/g tokens}
+      // per 64-d half lands as 128 rows (token, head) x 128 B, 128B-swizzled -- the
+      // K-major operand layout.  Rows before the request read earlier tokens (or
+      // zero-fill below token 0); they are dead rows, masked by the softmax.
+      if (items_done > 0) mbar_wait(q_free, (items_done - 1) & 1);
+      mbar_arrive_expect_tx(q_full, QT * 2 * kTcRows * 128);
+      const uint64_t pq = policy_evict_first();
+#pragma unroll
+      for (int q = 0; q < QT; ++q)
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf)
+          tma_load_4d(sQ + q * (2 * kTcRows * 128) + hf * (kTcRows * 128), &tmQ, 0, hf, h * g,
+                      q0 + (row0 + q * kTcRows) / g, q_full, pq);
+    }
+    if (is_k) tc_event(2);
     for (int t = 0; nch > 0; ++t) {
       const int nnx = tc_tile(p, r, L, pos_max, walk, nx);   // lookahead: is this tile the last?
       const int gt = gt0 + t, st = gt % NS, round = gt / NS;
       if (lane == 0) {
         if (round > 0) mbar_wait(empty0 + 8 * st, (round - 1) & 1);
+        tc_event(3, gt);
         if (is_k) {
           for (int j = 0; j < nch; ++j) metas[st * kTcChunks + j] = make_int4(ch[j].lo, ch[j].hi, ch[j].tb, ch[j].dir);
           tcount[st] = nch | (nnx == 0 ? kTcLastFlag : 0);
@@ -365,11 +513,10 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
     }
   } else if (warp == WMMA) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      mbar_wait(q_full, items_done & 1);
-      tc_fence_after();
-    }
-    __syncwarp();
+    // The whole warp walks the loop (waits, descriptors); one elected lane issues
+    // each tcgen05.mma / commit (umma_w and friends).
+    mbar_wait(q_full, items_done & 1);
+    tc_fence_after();
     bool first_pv[QT];
 #pragma unroll
     for (int q = 0; q < QT; ++q) first_pv[q] = true;
@@ -379,15 +526,15 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
 #pragma unroll
       for (int q = 0; q < QT; ++q) {
         mbar_wait(grp0 + 64 * q + 32 + 8 * pb, (gt >> 1) & 1);
+        tc_event(17 + q, gt);
         tc_fence_after();
-        for (int j = 0; j < nch; ++j) {   // A = P of chunk j: 8 TMEM columns of the S buffer pb
-          const uint64_t b = sdesc(sStage + st * STAGE + TILE + j * 2048, HALF, 1024);
-          umma_ts(tmem + 256 * q + 128, tmem + 256 * q + pb * 64 + 8 * j, b, idO, first_pv[q] ? 0u : 1u);
-          first_pv[q] = false;
-        }
-        umma_commit(grp0 + 64 * q + 48 + 8 * pb);
+        // A = P of chunk j: 8 TMEM columns of the S buffer pb
+        umma_pv4_w(tmem + 256 * q + 128, tmem + 256 * q + pb * 64, sdesc(sStage + st * STAGE + TILE, HALF, 1024), idO,
+                   nch, first_pv[q] ? 0u : 1u);
+        first_pv[q] = false;
+        umma_commit_w(grp0 + 64 * q + 48 + 8 * pb);
       }
-      umma_commit(empty0 + 8 * st);
+      umma_commit_w(empty0 + 8 * st);
     };
     int prev_nch = 0;
     for (int t = 0;; ++t) {
@@ -401,32 +548,34 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
         }
       };
       named_bar_sync(bar_mma(st), 64);
+      tc_event(10, gt);
       prof(0);
       const int tc = tcount[st];
       const int nch = tc & 0xff;
-      if (lane == 0) {
-        mbar_wait(full0 + 8 * st, (gt / NS) & 1);
-        prof(1);
-        const uint32_t idS = idesc(128, 16 * nch, 0, 0);
-        const uint32_t sk = sStage + st * STAGE;
+      mbar_wait(full0 + 8 * st, (gt / NS) & 1);
+      tc_event(11, gt);
+      prof(1);
+      const uint32_t idS = idesc(128, 16 * nch, 0, 0);
+      const uint32_t sk = sStage + st * STAGE;
 #pragma unroll
-        for (int q = 0; q < QT; ++q) {
-          if (gt >= 2) mbar_wait(grp0 + 64 * q + 16 + 8 * sb, ((gt - 2) >> 1) & 1);
-          tc_fence_after();
-#pragma unroll
-          for (int k = 0; k < D / 16; ++k) {
-            const uint64_t a = sdesc(sQ + q * (2 * kTcRows * 128) + (k >> 2) * (kTcRows * 128) + (k & 3) * 32, 16, 1024);
-            const uint64_t b = sdesc(sk + (k >> 2) * HALF + (k & 3) * 32, 16, 1024);
-            umma(tmem + 256 * q + sb * 64, a, b, idS, k > 0);
-          }
-          umma_commit(grp0 + 64 * q + 8 * sb);
-        }
-        prof(3);
-        if (t >= 1) issue_pv(gt - 1, prev_nch);   // P.V of the previous tile overlaps S of this one
-        prof(4);
-        if (tc & kTcLastFlag) issue_pv(gt, nch);
+      for (int q = 0; q < QT; ++q) {
+        if (gt >= 2) mbar_wait(grp0 + 64 * q + 16 + 8 * sb, ((gt - 2) >> 1) & 1);
+        tc_event(15 + q, gt);
+        tc_fence_after();
+        static_assert(D == 128 && HALF == 8192 && kTcRows * 128 == 16384, "umma_s8_w operand offsets");
+        umma_s8_w(tmem + 256 * q + sb * 64, sdesc(sQ + q * (2 * kTcRows * 128), 16, 1024), sdesc(sk, 16, 1024), idS);
+        umma_commit_w(grp0 + 64 * q + 8 * sb);
       }
-      __syncwarp();
+      if (tc & kTcLastFlag) umma_commit_w(q_free);   // the item's last S: Q may be replaced
+      tc_event(12, gt);
+      prof(3);
+      if (t >= 1) issue_pv(gt - 1, prev_nch);   // P.V of the previous tile overlaps S of this one
+      tc_event(13, gt);
+      prof(4);
+      if (tc & kTcLastFlag) {
+        issue_pv(gt, nch);
+        tc_event(14, gt);
+      }
       prev_nch = nch;
       if (tc & kTcLastFlag) {
         gt0 += t + 1;
@@ -444,7 +593,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
     const uint32_t tq = tmem + 256 * qg;       // this group's TMEM columns
     const int tok = ok ? grow / g : 0, jh = ok ? grow - tok * g : 0;
     const int pos = ok ? L - n + tok : -1;
-    {   // Q row -> shared memory (K-major, 128B swizzle, two 64-d halves)
+    if (!q_tma) {   // Q row -> shared memory (K-major, 128B swizzle, two 64-d halves)
       const uint4 *qs = reinterpret_cast<const uint4 *>(p.q + static_cast<int64_t>(q0 + tok) * p.q_st +
                                                         static_cast<int64_t>(h * g + jh) * p.q_sh);
 #pragma unroll
@@ -469,16 +618,23 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
           pc0 = c;
         }
       };
+      if ((warp & 3) == 0) tc_event(20, t);
       named_bar_sync(bar_sm(st), 32 + 32 * SMW);
+      if ((warp & 3) == 0) tc_event(21, t);
+      if (ntile == 0) iprof(2, it_t);
       prof(0);
       const int tc = tcount[st];
       const int nch = tc & 0xff;
       int4 meta[kTcChunks];
 #pragma unroll
       for (int j = 0; j < kTcChunks; ++j) meta[j] = j < nch ? metas[st * kTcChunks + j] : make_int4(0, 0, 0, 0);
-      mbar_wait(full0 + 8 * st, (t / NS) & 1);   // the tile's K/V landed (V rows get patched below)
+      // dead V rows of partly live chunks -> zero (P = 0 must never meet NaN, reading Q10);
+      // only then does the softmax wait for the tile's copies itself (S implies K landed)
+      bool patch = false;
+#pragma unroll
+      for (int j = 0; j < kTcChunks; ++j) patch = patch || (j < nch && (meta[j].x > 0 || meta[j].y < 16));
+      if (qg == 0 && patch) mbar_wait(full0 + 8 * st, (t / NS) & 1);   // the tile's K/V landed
       prof(1);
-      // dead V rows of partly live chunks -> zero (P = 0 must never meet NaN, reading Q10)
 #pragma unroll
       for (int j = 0; j < kTcChunks; ++j) {   // unrolled: meta[] stays in registers
         if (qg == 0 && j < nch && (meta[j].x > 0 || meta[j].y < 16)) {   // group 0 patches for all
@@ -493,12 +649,13 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
       // S tile -> registers
       prof(2);
       mbar_wait(s_full0 + 8 * sb, (t >> 1) & 1);
+      tc_event(22, t);
       prof(3);
       tc_fence_after();
       float s[kTcChunks * 16];
 #pragma unroll
-      for (int j = 0; j < kTcChunks; ++j)
-        if (j < nch) tmem_ld16(tq + lane_addr + sb * 64 + 16 * j, s + 16 * j);
+      for (int j = 0; j < kTcChunks; ++j)   // (columns of chunks >= nch: stale, masked below)
+        tmem_ld16(tq + lane_addr + sb * 64 + 16 * j, s + 16 * j);
       tmem_wait_ld();
       // per chunk, the live slots of this row form one interval [clo, chi): the
       // entry's live range intersected with the causal bound (forward: token
@@ -570,6 +727,26 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
       // s_free below and after P.V(t) (tcgen05 MMAs of one thread execute in order).
       prof(4);
       prof(5);
+      if (fold) {
+        // branch-free over the four chunks (chunks >= nch hold -inf: p = 0, stored into
+        // P columns no P.V reads); scale-and-shift and the row sums on the packed
+        // two-lane FP32 pipe (FFMA2 / FADD2)
+        const float2 sc = make_float2(p.scale_log2, p.scale_log2), nb = make_float2(-base_m, -base_m);
+        float2 l2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int j = 0; j < kTcChunks; ++j) {
+          uint32_t pw[8];
+#pragma unroll
+          for (int c = 0; c < 16; c += 2) {
+            const float2 x = ffma2(make_float2(s[16 * j + c], s[16 * j + c + 1]), sc, nb);
+            const float p0 = ex2(x.x), p1 = ex2(x.y);
+            l2[(c >> 1) & 1] = fadd2(l2[(c >> 1) & 1], make_float2(p0, p1));
+            pw[c >> 1] = pack_bf16(p0, p1);
+          }
+          tmem_st8(tq + lane_addr + sb * 64 + 8 * j, pw);
+        }
+        l += (l2[0].x + l2[1].x) + (l2[0].y + l2[1].y);
+      } else {
       float l4[4] = {0.f, 0.f, 0.f, 0.f};   // independent row-sum chains, folded into l below
 #pragma unroll
       for (int j = 0; j < kTcChunks; ++j) {
@@ -586,6 +763,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
         tmem_st8(tq + lane_addr + sb * 64 + 8 * j, pw);
       }
       l += (l4[0] + l4[1]) + (l4[2] + l4[3]);
+      }
       tmem_wait_st();
       fence_proxy_async_smem();   // (group 0's zeroed V rows: generic writes the MMA reads)
       tc_fence_before();
@@ -594,6 +772,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
         mbar_arrive(s_free0 + 8 * sb);
         mbar_arrive(p_full0 + 8 * sb);
       }
+      tc_event(23, t);
       prof(6);
       if (kTcProf && threadIdx.x == 0 && blockIdx.x < 148) atomicAdd(&g_tc_prof[(blockIdx.x * 3 + 0) * kProfSlots + 7], 1ull);
       if (tc & kTcLastFlag) {
@@ -602,28 +781,65 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
       }
     }
     // ---- epilogue: O / l -> bf16 rows, once the last P.V landed
+    if (kTcProf) ep_t = clock64();
+    if ((warp & 3) == 0) tc_event(24);
     gt0 += ntile;
     mbar_wait(p_free0 + 8 * ((gt0 - 1) & 1), ((gt0 - 1) >> 1) & 1);
     tc_fence_after();
+    if ((warp & 3) == 0) tc_event(25);
     const float inv = l > 0.f ? 1.f / l : 0.f;
+    // whole warps of live rows stage their 32 rows in shared memory (128B-swizzled,
+    // conflict-free) and one lane TMA-stores them: coalesced 128-byte lines instead
+    // of 32 row-strided 16-byte stores per instruction.  Warps with dead rows (a
+    // request's first item) store their live rows directly.
+    const bool o_tma = p.o_tma && __all_sync(FULL, ok);
+    const uint32_t so = sO + qg * (2 * kTcRows * 128) + (warp & 3) * (2 * 32 * 128);   // [half][32 rows][128 B]
+    if (o_tma) {
+      if (lane == 0) bulk_wait_read_all();   // this warp's previous store has left the staging buffer
+      __syncwarp();
+    }
     uint4 *orow = reinterpret_cast<uint4 *>(p.out + static_cast<int64_t>(q0 + tok) * p.o_st +
                                             static_cast<int64_t>(h * g + jh) * p.o_sh);
 #pragma unroll 1
-    for (int c = 0; c < D; c += 16) {
-      float o[16];
-      tmem_ld16(tq + lane_addr + 128 + c, o);
+    for (int c0 = 0; c0 < D; c0 += 32) {   // 32 columns per TMEM round trip
+      float o[32];
+#pragma unroll
+      for (int c = 0; c < 32; c += 16) tmem_ld16(tq + lane_addr + 128 + c0 + c, o + c);
       tmem_wait_ld();
-      if (ok) {
-        orow[c / 8] = make_uint4(pack_bf16(o[0] * inv, o[1] * inv), pack_bf16(o[2] * inv, o[3] * inv),
-                                 pack_bf16(o[4] * inv, o[5] * inv), pack_bf16(o[6] * inv, o[7] * inv));
-        orow[c / 8 + 1] = make_uint4(pack_bf16(o[8] * inv, o[9] * inv), pack_bf16(o[10] * inv, o[11] * inv),
-                                     pack_bf16(o[12] * inv, o[13] * inv), pack_bf16(o[14] * inv, o[15] * inv));
+#pragma unroll
+      for (int c = 0; c < 32; c += 8) {
+        const uint4 w = make_uint4(pack_bf16(o[c] * inv, o[c + 1] * inv), pack_bf16(o[c + 2] * inv, o[c + 3] * inv),
+                                   pack_bf16(o[c + 4] * inv, o[c + 5] * inv), pack_bf16(o[c + 6] * inv, o[c + 7] * inv));
+        const int k = (c0 + c) / 8;   // 16-byte chunk of the row: half k / 8, chunk k % 8
+        if (o_tma) st_shared_v4(so + (k >> 3) * (32 * 128) + tswz(lane, k & 7), w);
+        else if (ok) orow[k] = w;
+      }
+    }
+    if (o_tma) {
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        const int tok0 = q0 + (row0 + qg * kTcRows + (warp & 3) * 32) / g;
+        tma_store_4d(&tmO, so, 0, 0, h * g, tok0);
+        tma_store_4d(&tmO, so + 32 * 128, 0, 1, h * g, tok0);
+        bulk_commit();
       }
     }
     tc_fence_before();
   }
+  if (warp < SMW) {
+    if ((warp & 3) == 0) tc_event(26);
+    iprof(3, ep_t);
+    if (kTcProf && threadIdx.x == 0 && blockIdx.x < 148) atomicAdd(&g_tc_prof[(blockIdx.x * 3 + 2) * kProfSlots + 1], 1ull);
+    it_t = kTcProf ? clock64() : 0;
+  }
   ++items_done;
   }   // work items
+  {
+    long long t0 = k_t0;
+    iprof(0, t0);
+  }
+  if (p.o_tma && warp < SMW && lane == 0) bulk_wait_all();   // staged output stores complete
   __syncthreads();
   if (warp == WMMA) {   // the allocating warp frees the TMEM columns
     tc_fence_after();
@@ -632,6 +848,17 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
 }
 
 }  // namespace bkv
+
+extern "C" __attribute__((visibility("default"))) int bkv_dev_prefill_trace(unsigned long long *host, int reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(host, bkv::g_tc_trace, sizeof(bkv::g_tc_trace));
+  if (reset) {
+    static unsigned z[bkv::kTraceWarps] = {};
+    static unsigned long long zz[2 * bkv::kTraceWarps * bkv::kTracePerWarp] = {};
+    cudaMemcpyToSymbol(bkv::g_tc_tn, z, sizeof(z));
+    cudaMemcpyToSymbol(bkv::g_tc_trace, zz, sizeof(zz));
+  }
+  return e == cudaSuccess ? bkv::kTraceWarps * bkv::kTracePerWarp : -1;
+}
 
 extern "C" __attribute__((visibility("default"))) int bkv_dev_prefill_prof(unsigned long long *host, int reset) {
   cudaError_t e = cudaMemcpyFromSymbol(host, bkv::g_tc_prof, sizeof(bkv::g_tc_prof));
@@ -645,18 +872,18 @@ extern "C" __attribute__((visibility("default"))) int bkv_dev_prefill_prof(unsig
 namespace bkv {
 
 template <int QT>
-static int tc_smem_bytes() {
+static int tc_smem_bytes(bool o_tma) {
   constexpr int NS = QT == 1 ? kTcStages : 3;
-  return 1024 + QT * 2 * kTcRows * 128 + NS * 4 * kTcKeys * 128 +
-         NS * kTcChunks * 16 + ((NS + 1) & ~1) * 4 + (2 * NS + 8 * QT + 1) * 8 + 16;   // + metadata, barriers, TMEM slot
+  return 1024 + QT * 2 * kTcRows * 128 * (o_tma ? 2 : 1) + NS * 4 * kTcKeys * 128 +
+         NS * kTcChunks * 16 + ((NS + 1) & ~1) * 4 + (2 * NS + 8 * QT + 2) * 8 + 16;   // + metadata, barriers, TMEM slot
 }
 
-int prefill_tc_smem_bytes() { return tc_smem_bytes<1>(); }
+int prefill_tc_smem_bytes() { return tc_smem_bytes<1>(false); }
 
 template <int QT>
-static cudaError_t launch_tc(const CUtensorMap &tmK, const CUtensorMap &tmV, const PrefillParams &p,
-                             int max_q_len, cudaStream_t s) {
-  const int smem = tc_smem_bytes<QT>();
+static cudaError_t launch_tc(const CUtensorMap &tmK, const CUtensorMap &tmV, const CUtensorMap *tmQ,
+                             const CUtensorMap *tmO, const PrefillParams &p, int max_q_len, cudaStream_t s) {
+  const int smem = tc_smem_bytes<QT>(tmO != nullptr);
   {
     cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void *>(prefill_tc_kernel<QT>), smem);
     if (e != cudaSuccess) return e;
@@ -664,6 +891,8 @@ static cudaError_t launch_tc(const CUtensorMap &tmK, const CUtensorMap &tmV, con
   const long long tiles = (static_cast<long long>(max_q_len) * p.g + kTcRows - 1) / kTcRows;
   PrefillParams q = p;
   q.tiles_max = static_cast<int>(tiles);
+  q.q_tma = tmQ != nullptr;
+  q.o_tma = tmO != nullptr;
   DevProps dp;
   {
     cudaError_t e = dev_props(&dp);
@@ -672,16 +901,16 @@ static cudaError_t launch_tc(const CUtensorMap &tmK, const CUtensorMap &tmV, con
   const int sms = dp.sms;
   const long long items = ((tiles + QT - 1) / QT) * p.H * p.B;
   const int grid = static_cast<int>(items < sms ? items : sms);   // one persistent CTA per SM
-  prefill_tc_kernel<QT><<<grid, 32 * (4 * QT + 3), smem, s>>>(tmK, tmV, q);
+  prefill_tc_kernel<QT><<<grid, 32 * (4 * QT + 3), smem, s>>>(tmK, tmV, tmQ ? *tmQ : tmK, tmO ? *tmO : tmK, q);
   return cudaGetLastError();
 }
 
-cudaError_t launch_prefill_tc(const CUtensorMap &tmK, const CUtensorMap &tmV, const PrefillParams &p,
-                              int max_q_len, cudaStream_t s) {
+cudaError_t launch_prefill_tc(const CUtensorMap &tmK, const CUtensorMap &tmV, const CUtensorMap *tmQ,
+                              const CUtensorMap *tmO, const PrefillParams &p, int max_q_len, cudaStream_t s) {
   // default: two ping-pong 128-row query tiles per CTA share every K/V tile (Llama-70B
   // TP1 prefill rows 191 -> 233 TF/s); BKV_PREFILL_QT=1 (dev) runs one tile per CTA
-  if (dev_switches().prefill_qt == 1) return launch_tc<1>(tmK, tmV, p, max_q_len, s);
-  return launch_tc<2>(tmK, tmV, p, max_q_len, s);
+  if (dev_switches().prefill_qt == 1) return launch_tc<1>(tmK, tmV, tmQ, tmO, p, max_q_len, s);
+  return launch_tc<2>(tmK, tmV, tmQ, tmO, p, max_q_len, s);
 }
 
 }  // namespace bkv

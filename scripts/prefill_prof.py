@@ -28,6 +28,10 @@ tiles = b[:, 0, 7].sum()
 print(f"rc {rc}  key tiles (2 layers) {tiles:.0f}")
 names = {0: ["meta bar", "full", "zero+walk", "s_full wait", "ld+mask+max+resc", "p_free wait", "exp+P store", "tiles"],
          1: ["meta bar", "full wait", "s_free wait", "S issue", "PV (p_full wait+issue)", "-", "-", "-"]}
+it = b[:, 2, :].sum(0)
+print(f"items {it[1]:.0f}  per CTA: kernel cycles {b[:, 2, 0].mean():.0f} (max {b[:, 2, 0].max():.0f}), tiles {tiles / 148:.1f}, items {it[1] / 148:.1f}")
+print(f"softmax thread 0 per item: start->first tile {it[2] / max(it[1], 1):.0f}, epilogue {it[3] / max(it[1], 1):.0f}, "
+      f"next-item search {it[4] / max(it[1], 1):.0f} cycles")
 for role in (0, 1):
     tot = b[:, role, :7].sum(0)
     print(["softmax warp 0", "MMA lane"][role] + ": " + ", ".join(
