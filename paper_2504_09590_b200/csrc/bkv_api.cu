@@ -41,6 +41,7 @@ void load_switches() {
   s.prefill_qt = env_int("BKV_PREFILL_QT", 2);
   s.prefill_q_ldg = env_int("BKV_PREFILL_Q_LDG", 0);
   s.prefill_o_stg = env_int("BKV_PREFILL_O_STG", 0);
+  s.prefill_probe = env_int("BKV_PREFILL_PROBE", 0);
   s.mixed_overlap = env_int("BKV_MIXED_OVERLAP", 1);
 #ifdef BKV_DEV_TRACE
   s.debug = env_int("BKV_DEBUG", 0);
@@ -738,6 +739,7 @@ bkv_status bkv_paged_prefill_attention(const bkv_kv_pool *pool, const bkv_block_
   p.scale_log2 = softmax_scale * 1.4426950408889634f;
   p.tiles_max = 0;
   p.q_tma = 0;
+  p.probe = bkv::dev_switches().prefill_probe;
   // tcgen05 kernel: Q tiles by TMA when a 128-row tile is whole tokens (g | 128)
   // and output rows by TMA store when a warp's 32 rows are whole tokens (g | 32)
   CUtensorMap tmQ, tmO;

@@ -125,6 +125,8 @@ struct PrefillParams {
   int tiles_max;          // 128-row query tiles of the longest request (persistent kernels)
   int q_tma;              // tcgen05 kernel: Q tiles arrive by TMA (tmQ; needs g | 128)
   int o_tma;              // tcgen05 kernel: whole-warp output rows leave by TMA store (tmO; g | 32)
+  int probe;              // dev what-if timing probes (BKV_PREFILL_PROBE; results are wrong): 1 no exp,
+                          // 2 no S MMAs, 4 no P.V MMAs
 };
 int prefill_smem_bytes(int head_dim);
 bool prefill_uses_tc(int head_dim);   // tcgen05 kernel (wants 1-half TMA boxes)
@@ -244,7 +246,7 @@ cudaError_t launch_planned(const CUtensorMap &tmK, const CUtensorMap &tmV, const
 // skip work) is honoured only by a BKV_DEV_TRACE build.
 struct DevSwitches {
   int slots, warps, ctas_per_sm, units_per_warp, min_split /* -1: default */, small_plan, streamk;
-  int merge_warps, fused_merge, kv_combined, mha_cuda_cores, prefill_mma_sync, prefill_qt, prefill_q_ldg, prefill_o_stg;
+  int merge_warps, fused_merge, kv_combined, mha_cuda_cores, prefill_mma_sync, prefill_qt, prefill_q_ldg, prefill_o_stg, prefill_probe;
   int mixed_overlap, debug, trace, planned_slots, planned_dynamic_p, planned_pf;
 };
 const DevSwitches &dev_switches();

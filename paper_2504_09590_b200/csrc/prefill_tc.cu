@@ -270,6 +270,77 @@ __device__ __forceinline__ void tc_walk_init(const PrefillParams &p, int r, int 
   tc_window(p, r, L, w, 0);
 }
 
+// Lane-parallel chunk walk of the producers: a window of entries is loaded one per
+// lane (two lanes per entry for 32-slot blocks), the entries' token offsets come
+// from a warp prefix sum of the fill counts, the live chunks (live slot range,
+// first token <= pos_max) are compacted into lanes 0 .. n-1 -- no per-chunk
+// serial loop.  Same chunks, same order as tc_next.
+struct PWalk {
+  int wb, F, E, n, i;            // next entry to load, its first token; entries; window chunks, consumed
+  int lo, hi, tb, dir, blk, c;   // this lane's compacted window chunk
+};
+__device__ __forceinline__ void pw_load(const PrefillParams &p, int r, int L, int pos_max, PWalk &w) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const int lane = static_cast<int>(threadIdx.x & 31);
+  const int cpe = p.bs >> 4, epw = 32 / cpe;   // chunks per entry (1 or 2), entries per window
+  w.n = 0;
+  w.i = 0;
+  while (w.wb < w.E && w.F <= pos_max) {
+    const int e = w.wb + lane / cpe, c = lane - (lane / cpe) * cpe;
+    const bool in = lane < epw * cpe && e < w.E;
+    int blk = 0, dir = 0, fill = 0;
+    if (in) {
+      blk = __ldg(p.bt + static_cast<int64_t>(r) * p.bt_stride + e);
+      dir = __ldg(p.dirs + static_cast<int64_t>(r) * p.dir_rs + static_cast<int64_t>(e) * p.dir_cs);
+      fill = p.fills ? static_cast<int>(__ldg(p.fills + static_cast<int64_t>(r) * p.fill_rs + e))
+                     : min(p.bs, L - e * p.bs);
+    }
+    int incl = c == 0 ? fill : 0;   // inclusive prefix sum of the entries' fills
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int Fe = w.F + incl - fill;   // first token of the entry
+    const int lo_s = dir ? p.bs - fill : 0, hi_s = dir ? p.bs : fill;
+    const int lo = max(lo_s - 16 * c, 0), hi = min(hi_s - 16 * c, 16);
+    const int tb = dir ? Fe + p.bs - 1 - 16 * c : Fe + 16 * c;
+    const int first = dir ? tb - (hi - 1) : tb + lo;
+    const bool live = in && lo < hi && Fe <= pos_max && first <= pos_max;
+    const unsigned mask = __ballot_sync(FULL, live);
+    w.wb += epw;
+    w.F += __shfl_sync(FULL, incl, 31);
+    w.n = __popc(mask);
+    const int src = lane < w.n ? static_cast<int>(__fns(mask, 0, lane + 1)) : 0;
+    w.lo = __shfl_sync(FULL, lo, src);
+    w.hi = __shfl_sync(FULL, hi, src);
+    w.tb = __shfl_sync(FULL, tb, src);
+    w.dir = __shfl_sync(FULL, dir, src);
+    w.blk = __shfl_sync(FULL, blk, src);
+    w.c = __shfl_sync(FULL, c, src);
+    if (w.n > 0) return;
+  }
+}
+// next key tile (up to kTcChunks chunks): lane j < count receives chunk j
+__device__ __forceinline__ int pw_tile(const PrefillParams &p, int r, int L, int pos_max, PWalk &w, TcChunk &mine) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const int lane = static_cast<int>(threadIdx.x & 31);
+  int nch = 0;
+#pragma unroll
+  for (int j = 0; j < kTcChunks; ++j) {
+    if (w.i == w.n) {
+      pw_load(p, r, L, pos_max, w);
+      if (w.n == 0) break;
+    }
+    const int i = w.i++;
+    const int lo = __shfl_sync(FULL, w.lo, i), hi = __shfl_sync(FULL, w.hi, i), tb = __shfl_sync(FULL, w.tb, i);
+    const int dir = __shfl_sync(FULL, w.dir, i), blk = __shfl_sync(FULL, w.blk, i), c = __shfl_sync(FULL, w.c, i);
+    if (lane == j) mine = TcChunk{lo, hi, tb, dir, blk, c};
+    ++nch;
+  }
+  return nch;
+}
+
 }  // namespace
 
 // Dev-only cycle accounting (trace builds, -DBKV_DEV_TRACE): per CTA and role,
@@ -310,6 +381,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
                       const PrefillParams p) {
   constexpr int D = 128;
   constexpr int NS = QT == 1 ? kTcStages : 3;   // key-tile stages (shared memory budget)
+  constexpr int MS = NS + 2;                     // tile metadata slots (named barrier pairs 1 .. 2 MS)
   constexpr int SMW = 4 * QT;                    // softmax warps
   constexpr int WK = SMW, WMMA = SMW + 1, WV = SMW + 2;   // K producer, MMA issuer, V producer
   constexpr int HALF = kTcKeys * 128;          // one 64-d half of a key tile: 64 rows x 128 B
@@ -329,16 +401,20 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
   // output staging (o_tma): per query group, per softmax warp, per 64-d half: 32 rows x 128 B
   const uint32_t sO = sStage + NS * STAGE;
   const int n_ostage = p.o_tma ? QT : 0;
-  int4 *metas = reinterpret_cast<int4 *>(gb + (sO + n_ostage * 2 * kTcRows * 128 - base));   // [stage][chunk]
-  int *tcount = reinterpret_cast<int *>(metas + NS * kTcChunks);                 // chunks | last flag
-  uint64_t *bars = reinterpret_cast<uint64_t *>(tcount + ((NS + 1) & ~1));   // 8-byte aligned
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * NS + 8 * QT + 2);
+  // tile metadata ring (MS slots; see the producer): [slot][chunk], chunk count | last flag
+  int4 *metas = reinterpret_cast<int4 *>(gb + (sO + n_ostage * 2 * kTcRows * 128 - base));
+  int *tcount = reinterpret_cast<int *>(metas + MS * kTcChunks);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(tcount + ((MS + 1) & ~1));   // 8-byte aligned
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 4 * NS + 8 * QT + 2);
   const uint32_t bar0 = smem_u32(bars);
-  const uint32_t full0 = bar0, empty0 = bar0 + 8 * NS;
+  // K and V stages are handed over separately: a K stage frees as soon as the S
+  // MMAs that read it complete (about two tiles before its V stage), so the K
+  // stream runs further ahead of the MMA than a shared K|V ring allows
+  const uint32_t fullK0 = bar0, fullV0 = bar0 + 8 * NS, emptyK0 = bar0 + 16 * NS, emptyV0 = bar0 + 24 * NS;
   // per query group q: s_full/s_free (S buffer handoff) and p_full/p_free (P
   // buffer handoff; p_free also marks "every P.V up to this tile has landed in
   // O"), two buffers each; q_full: Q staged
-  const uint32_t grp0 = bar0 + 16 * NS;   // group q: + 64 q; s_full +0, s_free +16, p_full +32, p_free +48
+  const uint32_t grp0 = bar0 + 32 * NS;   // group q: + 64 q; s_full +0, s_free +16, p_full +32, p_free +48
   const uint32_t q_full = grp0 + 64 * QT;
   const uint32_t q_free = q_full + 8;     // every S of the item's query tiles is done: Q may be replaced
   const bool q_tma = p.q_tma != 0;        // the K producer TMA-loads Q (else the softmax warps stage it)
@@ -346,8 +422,10 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
 
   auto init_barriers = [&]() {
     for (int i = 0; i < NS; ++i) {
-      mbar_init(full0 + 8 * i, 2);   // the K and the V producer each arm their bytes
-      mbar_init(empty0 + 8 * i, 1);
+      mbar_init(fullK0 + 8 * i, 1);   // the K (V) producer arms its bytes
+      mbar_init(fullV0 + 8 * i, 1);
+      mbar_init(emptyK0 + 8 * i, 1);
+      mbar_init(emptyV0 + 8 * i, 1);
     }
     for (int q = 0; q < QT; ++q)
       for (int b = 0; b < 2; ++b) {
@@ -442,8 +520,8 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
   // barriers per stage (producer bar.arrive; the MMA warp resp. the softmax
   // warpgroup bar.sync: CTA-scope release/acquire) -- the consumers never walk.
   // The tiles themselves are handed over by the mbarriers.
-  auto bar_mma = [](int st) { return 1 + st; };                  // producer + MMA warp: 64 threads
-  auto bar_sm = [](int st) { return 1 + NS + st; };              // producer + softmax: 32 + 32 SMW threads
+  auto bar_mma = [](int m) { return 1 + m; };                  // producer + MMA warp: 64 threads
+  auto bar_sm = [](int m) { return 1 + MS + m; };              // producer + softmax: 32 + 32 SMW threads
 
   long long ep_t = 0;
   if (warp == WK || warp == WV) {
@@ -455,11 +533,14 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
     // the consumers can prepare), warp 6 streams V: 8 boxes per warp per tile.
     const bool is_k = warp == WK;
     tc_event(0);
-    TcWalk walk;
-    tc_walk_init(p, r, L, walk);
-    TcChunk ch[kTcChunks], nx[kTcChunks];
+    PWalk walk;
+    walk.wb = 0;
+    walk.F = 0;
+    walk.E = p.fills ? __ldg(p.nent + r) : (L + p.bs - 1) / p.bs;
+    walk.n = walk.i = 0;
+    TcChunk ch{0, 0, 0, 0, 0, 0}, nx{0, 0, 0, 0, 0, 0};   // lane j: chunk j of the tile
     const uint64_t pol = policy_evict_last();   // every query tile of the request re-reads these
-    int nch = tc_tile(p, r, L, pos_max, walk, ch);
+    int nch = pw_tile(p, r, L, pos_max, walk, ch);
     tc_event(1);
     if (is_k && q_tma && lane == 0) {
       // Q of the item's QT query tiles: one box {64 d, 1 half, g heads, 128/g tokens}
@@ -478,29 +559,30 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
     }
     if (is_k) tc_event(2);
     for (int t = 0; nch > 0; ++t) {
-      const int nnx = tc_tile(p, r, L, pos_max, walk, nx);   // lookahead: is this tile the last?
-      const int gt = gt0 + t, st = gt % NS, round = gt / NS;
-      if (lane == 0) {
-        if (round > 0) mbar_wait(empty0 + 8 * st, (round - 1) & 1);
-        tc_event(3, gt);
-        if (is_k) {
-          for (int j = 0; j < nch; ++j) metas[st * kTcChunks + j] = make_int4(ch[j].lo, ch[j].hi, ch[j].tb, ch[j].dir);
-          tcount[st] = nch | (nnx == 0 ? kTcLastFlag : 0);
-        }
-      }
+      const int nnx = pw_tile(p, r, L, pos_max, walk, nx);   // lookahead: is this tile the last?
+      // metadata slot m of tile gt is rewritten for tile gt + MS only after K stage st
+      // freed (S(gt + MS - NS) done), which follows s_free(gt + MS - NS - 2) = the
+      // softmax finished that tile: with MS = NS + 2 every consumer has read slot m
+      // (and passed its named barriers) by then
+      const int gt = gt0 + t, st = gt % NS, round = gt / NS, m = gt % MS;
+      if (lane == 0 && round > 0) mbar_wait((is_k ? emptyK0 : emptyV0) + 8 * st, (round - 1) & 1);
+      tc_event(3, gt);
       __syncwarp();
       if (is_k) {
-        named_bar_arrive(bar_mma(st), 64);
-        named_bar_arrive(bar_sm(st), 32 + 32 * SMW);
+        if (lane < nch) metas[m * kTcChunks + lane] = make_int4(ch.lo, ch.hi, ch.tb, ch.dir);
+        if (lane == 0) tcount[m] = nch | (nnx == 0 ? kTcLastFlag : 0);
+        __syncwarp();
+        named_bar_arrive(bar_mma(m), 64);
+        named_bar_arrive(bar_sm(m), 32 + 32 * SMW);
       }
-      if (lane == 0) {
-        const uint32_t fb = full0 + 8 * st;
-        mbar_arrive_expect_tx(fb, nch * 2 * 2048);
+      const uint32_t fb = (is_k ? fullK0 : fullV0) + 8 * st;
+      if (lane == 0) mbar_arrive_expect_tx(fb, nch * 2 * 2048);   // two 64-d half boxes per chunk
+      __syncwarp();
+      {   // lane 2j + hf copies half hf of chunk j
+        const int j = (lane >> 1) & (kTcChunks - 1), hf = lane & 1;
+        const int cj = __shfl_sync(FULL, ch.c, j), bj = __shfl_sync(FULL, ch.blk, j);
         const uint32_t dst = sStage + st * STAGE + (is_k ? 0 : TILE);
-        const CUtensorMap *tm = is_k ? &tmK : &tmV;
-        for (int j = 0; j < nch; ++j)
-#pragma unroll
-          for (int hf = 0; hf < 2; ++hf) tma_load_5d(dst + hf * HALF + j * 2048, tm, 0, 16 * ch[j].c, hf, h, ch[j].blk, fb, pol);
+        if (lane < 2 * nch) tma_load_5d(dst + hf * HALF + j * 2048, is_k ? &tmK : &tmV, 0, 16 * cj, hf, h, bj, fb, pol);
       }
       __syncwarp();
       if (nnx == 0) {
@@ -508,8 +590,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
         break;
       }
       nch = nnx;
-#pragma unroll
-      for (int j = 0; j < kTcChunks; ++j) ch[j] = nx[j];
+      ch = nx;
     }
   } else if (warp == WMMA) {
     // ------------------------------------------------------------ MMA issuer
@@ -520,25 +601,26 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
     bool first_pv[QT];
 #pragma unroll
     for (int q = 0; q < QT; ++q) first_pv[q] = true;
-    auto issue_pv = [&](int gt, int nch) {   // P.V of key tile gt for every group, then free the stage
+    auto issue_pv = [&](int gt, int nch) {   // P.V of key tile gt for every group, then free the V stage
       const int pb = gt & 1, st = gt % NS;
       const uint32_t idO = idesc(128, 128, 0, 1);
+      mbar_wait(fullV0 + 8 * st, (gt / NS) & 1);   // V landed (and, patched, reached the softmax's p_full)
 #pragma unroll
       for (int q = 0; q < QT; ++q) {
         mbar_wait(grp0 + 64 * q + 32 + 8 * pb, (gt >> 1) & 1);
         tc_event(17 + q, gt);
         tc_fence_after();
         // A = P of chunk j: 8 TMEM columns of the S buffer pb
-        umma_pv4_w(tmem + 256 * q + 128, tmem + 256 * q + pb * 64, sdesc(sStage + st * STAGE + TILE, HALF, 1024), idO,
+        if (!(p.probe & 4)) umma_pv4_w(tmem + 256 * q + 128, tmem + 256 * q + pb * 64, sdesc(sStage + st * STAGE + TILE, HALF, 1024), idO,
                    nch, first_pv[q] ? 0u : 1u);
         first_pv[q] = false;
         umma_commit_w(grp0 + 64 * q + 48 + 8 * pb);
       }
-      umma_commit_w(empty0 + 8 * st);
+      umma_commit_w(emptyV0 + 8 * st);
     };
     int prev_nch = 0;
     for (int t = 0;; ++t) {
-      const int gt = gt0 + t, sb = gt & 1, st = gt % NS;
+      const int gt = gt0 + t, sb = gt & 1, st = gt % NS, m = gt % MS;
       long long pc0 = kTcProf ? clock64() : 0;
       auto prof = [&](int slot) {
         if (kTcProf && lane == 0 && blockIdx.x < 148) {
@@ -547,12 +629,12 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
           pc0 = c;
         }
       };
-      named_bar_sync(bar_mma(st), 64);
+      named_bar_sync(bar_mma(m), 64);
       tc_event(10, gt);
       prof(0);
-      const int tc = tcount[st];
+      const int tc = tcount[m];
       const int nch = tc & 0xff;
-      mbar_wait(full0 + 8 * st, (gt / NS) & 1);
+      mbar_wait(fullK0 + 8 * st, (gt / NS) & 1);
       tc_event(11, gt);
       prof(1);
       const uint32_t idS = idesc(128, 16 * nch, 0, 0);
@@ -563,9 +645,10 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
         tc_event(15 + q, gt);
         tc_fence_after();
         static_assert(D == 128 && HALF == 8192 && kTcRows * 128 == 16384, "umma_s8_w operand offsets");
-        umma_s8_w(tmem + 256 * q + sb * 64, sdesc(sQ + q * (2 * kTcRows * 128), 16, 1024), sdesc(sk, 16, 1024), idS);
+        if (!(p.probe & 2)) umma_s8_w(tmem + 256 * q + sb * 64, sdesc(sQ + q * (2 * kTcRows * 128), 16, 1024), sdesc(sk, 16, 1024), idS);
         umma_commit_w(grp0 + 64 * q + 8 * sb);
       }
+      umma_commit_w(emptyK0 + 8 * st);               // K stage free once these S are done
       if (tc & kTcLastFlag) umma_commit_w(q_free);   // the item's last S: Q may be replaced
       tc_event(12, gt);
       prof(3);
@@ -609,7 +692,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
     float m_ref = -INFINITY, l = 0.f;
     int ntile = 0;
     for (;; ++ntile) {
-      const int t = gt0 + ntile, sb = t & 1, st = t % NS;   // CTA-global key tile number
+      const int t = gt0 + ntile, sb = t & 1, st = t % NS, m = t % MS;   // CTA-global key tile number
       long long pc0 = kTcProf ? clock64() : 0;
       auto prof = [&](int slot) {
         if (kTcProf && threadIdx.x == 0 && blockIdx.x < 148) {
@@ -619,21 +702,21 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
         }
       };
       if ((warp & 3) == 0) tc_event(20, t);
-      named_bar_sync(bar_sm(st), 32 + 32 * SMW);
+      named_bar_sync(bar_sm(m), 32 + 32 * SMW);
       if ((warp & 3) == 0) tc_event(21, t);
       if (ntile == 0) iprof(2, it_t);
       prof(0);
-      const int tc = tcount[st];
+      const int tc = tcount[m];
       const int nch = tc & 0xff;
       int4 meta[kTcChunks];
 #pragma unroll
-      for (int j = 0; j < kTcChunks; ++j) meta[j] = j < nch ? metas[st * kTcChunks + j] : make_int4(0, 0, 0, 0);
+      for (int j = 0; j < kTcChunks; ++j) meta[j] = j < nch ? metas[m * kTcChunks + j] : make_int4(0, 0, 0, 0);
       // dead V rows of partly live chunks -> zero (P = 0 must never meet NaN, reading Q10);
       // only then does the softmax wait for the tile's copies itself (S implies K landed)
       bool patch = false;
 #pragma unroll
       for (int j = 0; j < kTcChunks; ++j) patch = patch || (j < nch && (meta[j].x > 0 || meta[j].y < 16));
-      if (qg == 0 && patch) mbar_wait(full0 + 8 * st, (t / NS) & 1);   // the tile's K/V landed
+      if (qg == 0 && patch) mbar_wait(fullV0 + 8 * st, (t / NS) & 1);   // the tile's V landed
       prof(1);
 #pragma unroll
       for (int j = 0; j < kTcChunks; ++j) {   // unrolled: meta[] stays in registers
@@ -675,25 +758,69 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
         if (j >= nch) chi[j] = 0;
         whole = whole && clo[j] == 0 && chi[j] == 16;
       }
-      // eight independent max chains (a single running max is a 64-deep
-      // dependency chain on one thread)
-      float mx8[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) mx8[i] = -INFINITY;
-      if (fold && __all_sync(FULL, whole)) {
-#pragma unroll
-        for (int c = 0; c < kTcChunks * 16; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], s[c]);
-      } else {
+      // masks (unless every row of the warp sees the whole tile): dead slots -> -inf;
+      // without the fold the scores are scaled here
+      if (!(fold && __all_sync(FULL, whole))) {
 #pragma unroll
         for (int j = 0; j < kTcChunks; ++j) {
 #pragma unroll
           for (int c = 0; c < 16; ++c) {
             const float v = fold ? s[16 * j + c] : s[16 * j + c] * p.scale_log2;
             s[16 * j + c] = (c >= clo[j] && c < chi[j]) ? v : -INFINITY;
-            mx8[c & 7] = fmaxf(mx8[c & 7], s[16 * j + c]);
           }
         }
       }
+      // P = 2^(s * scale - base) into TMEM over the S buffer sb just read (bf16 pairs,
+      // columns 8j .. 8j + 7 per 16-key chunk), branch-free over the four chunks
+      // (chunks >= nch hold -inf: p = 0, in P columns no P.V reads); scale-and-shift
+      // and the row sums on the packed two-lane FP32 pipe (FFMA2 / FADD2).  Returns
+      // the row sum; xmax = the largest exponent.  S(t + 2) reuses the buffer: it is
+      // issued after s_free below and after P.V(t) (one thread's MMAs run in order).
+      auto exp_store = [&](float base, float &xmax) -> float {
+        const float2 sc = make_float2(p.scale_log2, p.scale_log2), nb = make_float2(-base, -base);
+        float2 l2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        float xm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int j = 0; j < kTcChunks; ++j) {
+          uint32_t pw[8];
+#pragma unroll
+          for (int c = 0; c < 16; c += 2) {
+            const float2 x = ffma2(make_float2(s[16 * j + c], s[16 * j + c + 1]), sc, nb);
+            xm[(c >> 1) & 3] = fmaxf(xm[(c >> 1) & 3], fmaxf(x.x, x.y));
+            const float p0 = ex2(x.x), p1 = ex2(x.y);
+            l2[(c >> 1) & 1] = fadd2(l2[(c >> 1) & 1], make_float2(p0, p1));
+            pw[c >> 1] = pack_bf16(p0, p1);
+          }
+          tmem_st8(tq + lane_addr + sb * 64 + 8 * j, pw);
+        }
+        xmax = fmaxf(fmaxf(xm[0], xm[1]), fmaxf(xm[2], xm[3]));
+        return (l2[0].x + l2[1].x) + (l2[0].y + l2[1].y);
+      };
+      // Speculative pass: exponentiate against the running reference straight away
+      // (no max -> exponent dependency); it stands unless a row has no reference yet or
+      // a live score passes it by more than 8 (p > 2^8) -- then the exact pass below
+      // (row max, lazy rescale) recomputes and overwrites P.  Warp-uniform decision.
+      bool redo = true;
+      if (p.probe & 1) {   // dev what-if: no exponentials (P = 0 stored)
+        const uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int j = 0; j < kTcChunks; ++j) tmem_st8(tq + lane_addr + sb * 64 + 8 * j, z);
+        redo = false;
+      } else if (fold) {
+        float xmax;
+        const float ls = exp_store(m_ref, xmax);
+        redo = __any_sync(FULL, !(m_ref > -INFINITY) || xmax > 8.f);
+        if (!redo) l += ls;
+      }
+      if (redo) {
+      if (fold) tmem_wait_st();   // the speculative P stores land before their overwrite
+      // eight independent max chains (a single running max is a 64-deep
+      // dependency chain on one thread)
+      float mx8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mx8[i] = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < kTcChunks * 16; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], s[c]);
       float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                        fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
       if (fold) mx *= p.scale_log2;   // (-inf stays -inf)
@@ -721,31 +848,9 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
       }
       if (grow) m_ref = mx;
       const float base_m = m_ref == -INFINITY ? 0.f : m_ref;
-      // P -> TMEM over the S buffer sb just read (bf16 pairs, columns 8j .. 8j + 7 per
-      // 16-key chunk): the P.V MMA takes it as its A operand from TMEM (no shared-memory
-      // round trip, no proxy fence).  S(t + 2) reuses the buffer: it is issued after
-      // s_free below and after P.V(t) (tcgen05 MMAs of one thread execute in order).
-      prof(4);
-      prof(5);
       if (fold) {
-        // branch-free over the four chunks (chunks >= nch hold -inf: p = 0, stored into
-        // P columns no P.V reads); scale-and-shift and the row sums on the packed
-        // two-lane FP32 pipe (FFMA2 / FADD2)
-        const float2 sc = make_float2(p.scale_log2, p.scale_log2), nb = make_float2(-base_m, -base_m);
-        float2 l2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-        for (int j = 0; j < kTcChunks; ++j) {
-          uint32_t pw[8];
-#pragma unroll
-          for (int c = 0; c < 16; c += 2) {
-            const float2 x = ffma2(make_float2(s[16 * j + c], s[16 * j + c + 1]), sc, nb);
-            const float p0 = ex2(x.x), p1 = ex2(x.y);
-            l2[(c >> 1) & 1] = fadd2(l2[(c >> 1) & 1], make_float2(p0, p1));
-            pw[c >> 1] = pack_bf16(p0, p1);
-          }
-          tmem_st8(tq + lane_addr + sb * 64 + 8 * j, pw);
-        }
-        l += (l2[0].x + l2[1].x) + (l2[0].y + l2[1].y);
+        float xmax;
+        l += exp_store(base_m, xmax);
       } else {
       float l4[4] = {0.f, 0.f, 0.f, 0.f};   // independent row-sum chains, folded into l below
 #pragma unroll
@@ -764,6 +869,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
       }
       l += (l4[0] + l4[1]) + (l4[2] + l4[3]);
       }
+      }   // redo
       tmem_wait_st();
       fence_proxy_async_smem();   // (group 0's zeroed V rows: generic writes the MMA reads)
       tc_fence_before();
@@ -874,8 +980,9 @@ namespace bkv {
 template <int QT>
 static int tc_smem_bytes(bool o_tma) {
   constexpr int NS = QT == 1 ? kTcStages : 3;
+  constexpr int MS = NS + 2;
   return 1024 + QT * 2 * kTcRows * 128 * (o_tma ? 2 : 1) + NS * 4 * kTcKeys * 128 +
-         NS * kTcChunks * 16 + ((NS + 1) & ~1) * 4 + (2 * NS + 8 * QT + 2) * 8 + 16;   // + metadata, barriers, TMEM slot
+         MS * kTcChunks * 16 + ((MS + 1) & ~1) * 4 + (4 * NS + 8 * QT + 2) * 8 + 16;   // + metadata, barriers, TMEM slot
 }
 
 int prefill_tc_smem_bytes() { return tc_smem_bytes<1>(false); }
