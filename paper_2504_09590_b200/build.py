@@ -24,6 +24,7 @@ NVCC_FLAGS = [
 
 if os.environ.get("BKV_BUILD_TRACE") == "1":   # dev: compile the decode-kernel timeline tracing in
     NVCC_FLAGS += ["-DBKV_DEV_TRACE"]
+NVCC_FLAGS += os.environ.get("BKV_BUILD_DEFINES", "").split()   # dev A/B builds, e.g. -DBKV_POLY_PAIRS=0
 
 
 def sources():

@@ -542,20 +542,24 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
     const uint64_t pol = policy_evict_last();   // every query tile of the request re-reads these
     int nch = pw_tile(p, r, L, pos_max, walk, ch);
     tc_event(1);
-    if (is_k && q_tma && lane == 0) {
+    if (is_k && q_tma) {
       // Q of the item's QT query tiles: one box {64 d, 1 half, g heads, 128/g tokens}
       // per 64-d half lands as 128 rows (token, head) x 128 B, 128B-swizzled -- the
       // K-major operand layout.  Rows before the request read earlier tokens (or
-      // zero-fill below token 0); they are dead rows, masked by the softmax.
+      // zero-fill below token 0); they are dead rows, masked by the softmax.  (The
+      // whole warp waits: a lone spinning lane stalls the converged walk for long.)
       if (items_done > 0) mbar_wait(q_free, (items_done - 1) & 1);
-      mbar_arrive_expect_tx(q_full, QT * 2 * kTcRows * 128);
-      const uint64_t pq = policy_evict_first();
+      if (lane == 0) {
+        mbar_arrive_expect_tx(q_full, QT * 2 * kTcRows * 128);
+        const uint64_t pq = policy_evict_first();
 #pragma unroll
-      for (int q = 0; q < QT; ++q)
+        for (int q = 0; q < QT; ++q)
 #pragma unroll
-        for (int hf = 0; hf < 2; ++hf)
-          tma_load_4d(sQ + q * (2 * kTcRows * 128) + hf * (kTcRows * 128), &tmQ, 0, hf, h * g,
-                      q0 + (row0 + q * kTcRows) / g, q_full, pq);
+          for (int hf = 0; hf < 2; ++hf)
+            tma_load_4d(sQ + q * (2 * kTcRows * 128) + hf * (kTcRows * 128), &tmQ, 0, hf, h * g,
+                        q0 + (row0 + q * kTcRows) / g, q_full, pq);
+      }
+      __syncwarp();
     }
     if (is_k) tc_event(2);
     for (int t = 0; nch > 0; ++t) {
@@ -565,7 +569,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
       // softmax finished that tile: with MS = NS + 2 every consumer has read slot m
       // (and passed its named barriers) by then
       const int gt = gt0 + t, st = gt % NS, round = gt / NS, m = gt % MS;
-      if (lane == 0 && round > 0) mbar_wait((is_k ? emptyK0 : emptyV0) + 8 * st, (round - 1) & 1);
+      if (round > 0) mbar_wait((is_k ? emptyK0 : emptyV0) + 8 * st, (round - 1) & 1);   // whole warp
       tc_event(3, gt);
       __syncwarp();
       if (is_k) {
