@@ -41,7 +41,11 @@ void load_switches() {
   s.prefill_qt = env_int("BKV_PREFILL_QT", 2);
   s.prefill_q_ldg = env_int("BKV_PREFILL_Q_LDG", 0);
   s.prefill_o_stg = env_int("BKV_PREFILL_O_STG", 0);
-  s.prefill_probe = env_int("BKV_PREFILL_PROBE", 0);
+#if defined(BKV_DEV_TRACE) || defined(BKV_DEV_PROBES)
+  s.prefill_probe = env_int("BKV_PREFILL_PROBE", 0);   // work-skipping what-if probes: dev builds only
+#else
+  s.prefill_probe = 0;
+#endif
   s.mixed_overlap = env_int("BKV_MIXED_OVERLAP", 1);
 #ifdef BKV_DEV_TRACE
   s.debug = env_int("BKV_DEBUG", 0);

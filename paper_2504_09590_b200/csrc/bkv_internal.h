@@ -125,7 +125,8 @@ struct PrefillParams {
   int tiles_max;          // 128-row query tiles of the longest request (persistent kernels)
   int q_tma;              // tcgen05 kernel: Q tiles arrive by TMA (tmQ; needs g | 128)
   int o_tma;              // tcgen05 kernel: whole-warp output rows leave by TMA store (tmO; g | 32)
-  int probe;              // dev what-if timing probes (BKV_PREFILL_PROBE; results are wrong): 1 no exp,
+  int probe;              // dev what-if timing probes (BKV_PREFILL_PROBE, only in builds with
+                          // -DBKV_DEV_PROBES or the trace build; results are wrong): 1 no exp,
                           // 2 no S MMAs, 4 no P.V MMAs
 };
 int prefill_smem_bytes(int head_dim);

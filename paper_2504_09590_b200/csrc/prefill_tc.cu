@@ -44,7 +44,6 @@ constexpr int kTcChunks = 4;       // chunks (16 keys each) per key tile
 constexpr int kTcKeys = 16 * kTcChunks;
 constexpr int kTcLastFlag = 1 << 8;   // tile metadata: the item's last key tile
 constexpr int kTcRows = 128;       // query rows per CTA = TMEM lanes
-constexpr int kTcThreads = 224;   // softmax 0-3, K producer 4, MMA 5, V producer 6
 
 __device__ __forceinline__ uint32_t tswz(int row, int c) {
   return static_cast<uint32_t>(row * 128 + ((c ^ (row & 7)) << 4));
@@ -61,40 +60,9 @@ __host__ __device__ constexpr uint32_t idesc(int M, int N, int a_mn, int b_mn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
-__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(id), "r"(acc)
-      : "memory");
-}
-// the "TS" form: A (M x K, here P) read from TMEM -- row i = lane i, bf16 pairs packed per
-// 32-bit column (element k in column k/2, even k in the low half); validated by
-// scripts/umma_probe.cu against a host GEMM
-__device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t id, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(b), "r"(id), "r"(acc)
-      : "memory");
-}
 // Warp-collective forms: the whole (converged) warp executes them and one
 // elected lane issues -- the descriptors stay warp-uniform (uniform registers),
 // with no per-instruction single-lane divergence loop around the issue.
-__device__ __forceinline__ void umma_w(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(id), "r"(acc)
-      : "memory");
-}
-__device__ __forceinline__ void umma_ts_w(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t id, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(b), "r"(id), "r"(acc)
-      : "memory");
-}
 __device__ __forceinline__ void umma_commit_w(uint32_t bar) {
   asm volatile(
       "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
@@ -144,10 +112,6 @@ __device__ __forceinline__ void umma_pv4_w(uint32_t tmem_d, uint32_t a_tmem, uin
       "r"(a_tmem), "l"(b0), "r"(id), "r"(nch), "r"(acc0)
       : "memory");
 }
-__device__ __forceinline__ void umma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-               : "memory");
-}
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *v) {
@@ -195,86 +159,16 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
   return d;
 }
 
-// the chunk walk (see prefill_attention.cu): entries in logical order, 32 at a
-// time in a lane-distributed window
-struct TcWalk {
-  int e, c, F, E, wb;
-  int wblk, wdir, wfill;
-  int blk, dir, fill;
-  bool have;
-};
-__device__ __forceinline__ void tc_window(const PrefillParams &p, int r, int L, TcWalk &w, int wb) {
-  const int e = wb + static_cast<int>(threadIdx.x & 31);
-  w.wb = wb;
-  w.wblk = w.wdir = w.wfill = 0;
-  if (e < w.E) {
-    w.wblk = __ldg(p.bt + static_cast<int64_t>(r) * p.bt_stride + e);
-    w.wdir = __ldg(p.dirs + static_cast<int64_t>(r) * p.dir_rs + static_cast<int64_t>(e) * p.dir_cs);
-    w.wfill = p.fills ? static_cast<int>(__ldg(p.fills + static_cast<int64_t>(r) * p.fill_rs + e))
-                      : min(p.bs, L - e * p.bs);
-  }
-}
-__device__ __forceinline__ bool tc_next(const PrefillParams &p, int r, int L, int pos_max, TcWalk &w,
-                                        int &lo, int &hi, int &tb) {
-  constexpr unsigned FULL = 0xffffffffu;
-  const int bs = p.bs;
-  while (w.e < w.E && w.F <= pos_max) {
-    if (!w.have) {
-      if (w.e - w.wb >= 32) tc_window(p, r, L, w, w.e);
-      const int idx = w.e - w.wb;
-      w.blk = __shfl_sync(FULL, w.wblk, idx);
-      w.dir = __shfl_sync(FULL, w.wdir, idx);
-      w.fill = __shfl_sync(FULL, w.wfill, idx);
-      w.c = 0;
-      w.have = true;
-    }
-    const int lo_s = w.dir ? bs - w.fill : 0, hi_s = w.dir ? bs : w.fill;
-    while (w.c < bs / 16) {
-      const int c = w.c++;
-      lo = max(lo_s - 16 * c, 0);
-      hi = min(hi_s - 16 * c, 16);
-      if (lo >= hi) continue;
-      tb = w.dir ? w.F + bs - 1 - 16 * c : w.F + 16 * c;
-      const int first_tok = w.dir ? tb - (hi - 1) : tb + lo;
-      if (first_tok > pos_max) continue;
-      return true;
-    }
-    w.F += w.fill;
-    ++w.e;
-    w.have = false;
-  }
-  return false;
-}
-
 struct TcChunk {
   int lo, hi, tb, dir, blk, c;
 };
-
-// next key tile (up to kTcChunks chunks) of a warp's own walk; returns the count
-__device__ __forceinline__ int tc_tile(const PrefillParams &p, int r, int L, int pos_max, TcWalk &w,
-                                       TcChunk (&ch)[kTcChunks]) {
-  int nch = 0;
-  int lo, hi, tb;
-  while (nch < kTcChunks && tc_next(p, r, L, pos_max, w, lo, hi, tb)) {
-    ch[nch] = TcChunk{lo, hi, tb, w.dir, w.blk, w.c - 1};
-    ++nch;
-  }
-  return nch;
-}
-
-__device__ __forceinline__ void tc_walk_init(const PrefillParams &p, int r, int L, TcWalk &w) {
-  w.e = 0;
-  w.F = 0;
-  w.E = p.fills ? __ldg(p.nent + r) : (L + p.bs - 1) / p.bs;
-  w.have = false;
-  tc_window(p, r, L, w, 0);
-}
 
 // Lane-parallel chunk walk of the producers: a window of entries is loaded one per
 // lane (two lanes per entry for 32-slot blocks), the entries' token offsets come
 // from a warp prefix sum of the fill counts, the live chunks (live slot range,
 // first token <= pos_max) are compacted into lanes 0 .. n-1 -- no per-chunk
-// serial loop.  Same chunks, same order as tc_next.
+// serial loop.  Same chunks, in the same logical order, as the serial walk of
+// prefill_attention.cu (entries in logical order, P:711 live slot ranges).
 struct PWalk {
   int wb, F, E, n, i;            // next entry to load, its first token; entries; window chunks, consumed
   int lo, hi, tb, dir, blk, c;   // this lane's compacted window chunk
