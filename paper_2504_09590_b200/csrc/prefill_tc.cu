@@ -6,30 +6,32 @@
 // head_dim 128 (see prefill_uses_tc() in prefill_attention.cu).
 //
 // Persistent CTAs (one per SM) walk work items = QT consecutive 128-row query
-// tiles of one (request, kv head), latest rows first; QT = 2 by default
-// ("ping-pong": both tiles share every streamed K/V tile).  Roles, for
-// QT = 2 (352 threads):
+// tiles of one (request, kv head), latest rows first (tiles aligned to the end
+// of the request's rows); QT = 2 by default ("ping-pong": both tiles share every
+// streamed K/V tile).  Roles, for QT = 2 (352 threads):
 //   warps 0-3, 4-7  one softmax warpgroup per query tile: thread t owns row t
 //              of its tile and TMEM lane t (tcgen05.ld 32x32b gives a whole
-//              row to one thread: no shuffles); loads Q, masks (direction +
-//              causal by token index; a mask-free path for whole
-//              tiles), online softmax in the log2 domain with a lazy rescale
-//              (the running max moves only when it grows by > 8, so O in TMEM
-//              is rarely touched), writes P (bf16 pairs) back into the TMEM
-//              columns of the S buffer it just read, zeroes dead V rows
-//              (group 0), runs the epilogue;
-//   warp 8     K producer: walks the request's entries in logical order and
-//              publishes each 64-key tile's chunk metadata through named
-//              barriers, then TMA-streams the K tile (four 16-slot chunks as
-//              rows of one 128B-swizzled operand) into a 3-stage ring;
-//   warp 9     MMA issuer (one lane) + TMEM owner: per key tile, for each
-//              query tile S = Q.K^T (M 128, N <= 64, K 128) into one of two
-//              TMEM S buffers, then O += P.V (M 128, N 128, K 16 per chunk,
-//              A = P straight from TMEM: the "TS" form) into that tile's TMEM
-//              O accumulator; tcgen05.commit releases S/P buffers and stages;
-//   warp 10    V producer (same walk, V tiles).
+//              row to one thread: no shuffles); masks (direction + causal by
+//              token index; a mask-free path for whole tiles), online
+//              softmax in the log2 domain -- a speculative pass against the
+//              running reference, the exact pass (row max, lazy O rescale: the
+//              reference moves only when a score passes it by > 8) only when
+//              needed -- writes P (bf16 pairs) back into the TMEM columns of the
+//              S buffer it just read, zeroes dead V rows (group 0), runs the
+//              epilogue (shared-memory staging + TMA store);
+//   warp 8     K producer: walks the request's entries lane-parallel, TMA-loads
+//              the item's Q, publishes each 64-key tile's chunk metadata
+//              (5-slot ring, named barriers) and TMA-streams the K tile (four
+//              16-slot chunks as rows of one 128B-swizzled operand) into a
+//              3-stage K ring freed by the S MMAs;
+//   warp 9     MMA warp + TMEM owner (one elected lane issues): per key tile,
+//              for each query tile S = Q.K^T (M 128, N <= 64, K 128) into one
+//              of two TMEM S buffers, then O += P.V (M 128, N 128, K 16 per
+//              chunk, A = P straight from TMEM: the "TS" form) into that tile's
+//              TMEM O accumulator; tcgen05.commit releases buffers and stages;
+//   warp 10    V producer (same walk, V tiles, a 3-stage V ring freed by P.V).
 // Operands: Q and K are K-major 128B-swizzled, V is MN-major 128B-swizzled
-// -- exactly the layout the TMA boxes of the pool land in; P never leaves TMEM.
+// -- exactly the layout the TMA boxes land in; P never leaves TMEM.
 #include <math.h>
 
 #include "bkv_internal.h"
@@ -44,6 +46,10 @@ constexpr int kTcChunks = 4;       // chunks (16 keys each) per key tile
 constexpr int kTcKeys = 16 * kTcChunks;
 constexpr int kTcLastFlag = 1 << 8;   // tile metadata: the item's last key tile
 constexpr int kTcRows = 128;       // query rows per CTA = TMEM lanes
+#ifndef BKV_PINGPONG
+#define BKV_PINGPONG 0
+#endif
+constexpr bool kPingPong = BKV_PINGPONG != 0;   // dev A/B: alternate the two groups' exponent phases
 
 __device__ __forceinline__ uint32_t tswz(int row, int c) {
   return static_cast<uint32_t>(row * 128 + ((c ^ (row & 7)) << 4));
@@ -390,6 +396,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
       t = c;
     }
   };
+  if (kPingPong && QT == 2 && warp >= 4 && warp < 8) named_bar_arrive(11, 256);   // group 0 goes first
   for (int item = next_item(blockIdx.x); item < n_items; item = next_item(item + G)) {
   iprof(4, it_t);
   const int x = item / (p.H * p.B), hr = item - x * (p.H * p.B);
@@ -698,6 +705,9 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
       // (no max -> exponent dependency); it stands unless a row has no reference yet or
       // a live score passes it by more than 8 (p > 2^8) -- then the exact pass below
       // (row max, lazy rescale) recomputes and overwrites P.  Warp-uniform decision.
+      // ping-pong (dev A/B): the two groups' exponent phases alternate (group 0 tile t, group 1
+      // tile t, group 0 tile t + 1, ...) so each runs with its SM sub-partitions to itself
+      if (kPingPong && QT == 2) named_bar_sync(qg == 0 ? 11 : 12, 256);
       bool redo = true;
       if (p.probe & 1) {   // dev what-if: no exponentials (P = 0 stored)
         const uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -768,6 +778,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
       l += (l4[0] + l4[1]) + (l4[2] + l4[3]);
       }
       }   // redo
+      if (kPingPong && QT == 2) named_bar_arrive(qg == 0 ? 12 : 11, 256);
       tmem_wait_st();
       fence_proxy_async_smem();   // (group 0's zeroed V rows: generic writes the MMA reads)
       tc_fence_before();
@@ -839,6 +850,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
   }
   ++items_done;
   }   // work items
+  if (kPingPong && QT == 2 && warp < 4) named_bar_sync(11, 256);   // group 1's last hand-back
   {
     long long t0 = k_t0;
     iprof(0, t0);

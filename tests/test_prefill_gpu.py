@@ -204,3 +204,28 @@ def test_prefill_random_geometry_fuzz(seed, monkeypatch):
     n = query_counts(case.layout.lens, rng, full=bool(rng.random() < 0.3))
     o, ref = _run(case, general, n, qs=int(rng.integers(0, 3)))
     check_close(o, ref, f"pfuzz{seed} g{g} hkv{hkv} d{d} bs{bs} B{B} general{general}")
+
+
+@pytest.mark.parametrize("q_ldg,o_stg", [(1, 0), (0, 1), (1, 1)])
+def test_prefill_tcgen05_q_and_output_fallbacks(q_ldg, o_stg, monkeypatch):
+    """The tcgen05 kernel's load/store fallbacks forced at g = 8: Q staged by the softmax warps
+    (BKV_PREFILL_Q_LDG=1, the path of group sizes not dividing 128) and output rows stored
+    directly (BKV_PREFILL_O_STG=1, the path of group sizes not dividing 32)."""
+    monkeypatch.setenv("BKV_PREFILL_Q_LDG", str(q_ldg))
+    monkeypatch.setenv("BKV_PREFILL_O_STG", str(o_stg))
+    for general in (False, True):
+        case = make_case("tiny_gqa", 41 + q_ldg + 2 * o_stg, general=general)
+        n = query_counts(case.layout.lens, np.random.default_rng(41), full=general)
+        o, ref = _run(case, general, n)
+        check_close(o, ref, f"tiny_gqa q_ldg{q_ldg} o_stg{o_stg} general{general}")
+
+
+@pytest.mark.parametrize("hq,hkv", [(6, 2), (10, 2), (12, 2)])
+def test_prefill_tcgen05_group_sizes_not_dividing_tiles(hq, hkv):
+    """Group sizes 3, 5, 6: a 128-row query tile (and a warp's 32 rows) starts mid-token, so
+    the kernel takes its load-staged Q and direct-store output paths (no TMA row boxes)."""
+    sh = Shape(f"g{hq // hkv}", hq, hkv, 128, 16, 6, 0.5, "uniform", 700, 1, 1, uniform_max=700)
+    case = make_case(sh, hq, general=True)
+    n = query_counts(case.layout.lens, np.random.default_rng(hq), decode_frac=0.3)
+    o, ref = _run(case, True, n)
+    check_close(o, ref, f"g{hq // hkv}")
