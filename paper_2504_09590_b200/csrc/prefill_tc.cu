@@ -46,10 +46,6 @@ constexpr int kTcChunks = 4;       // chunks (16 keys each) per key tile
 constexpr int kTcKeys = 16 * kTcChunks;
 constexpr int kTcLastFlag = 1 << 8;   // tile metadata: the item's last key tile
 constexpr int kTcRows = 128;       // query rows per CTA = TMEM lanes
-#ifndef BKV_PINGPONG
-#define BKV_PINGPONG 0
-#endif
-constexpr bool kPingPong = BKV_PINGPONG != 0;   // dev A/B: alternate the two groups' exponent phases
 
 __device__ __forceinline__ uint32_t tswz(int row, int c) {
   return static_cast<uint32_t>(row * 128 + ((c ^ (row & 7)) << 4));
@@ -396,7 +392,6 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
       t = c;
     }
   };
-  if (kPingPong && QT == 2 && warp >= 4 && warp < 8) named_bar_arrive(11, 256);   // group 0 goes first
   for (int item = next_item(blockIdx.x); item < n_items; item = next_item(item + G)) {
   iprof(4, it_t);
   const int x = item / (p.H * p.B), hr = item - x * (p.H * p.B);
@@ -705,9 +700,6 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
       // (no max -> exponent dependency); it stands unless a row has no reference yet or
       // a live score passes it by more than 8 (p > 2^8) -- then the exact pass below
       // (row max, lazy rescale) recomputes and overwrites P.  Warp-uniform decision.
-      // ping-pong (dev A/B): the two groups' exponent phases alternate (group 0 tile t, group 1
-      // tile t, group 0 tile t + 1, ...) so each runs with its SM sub-partitions to itself
-      if (kPingPong && QT == 2) named_bar_sync(qg == 0 ? 11 : 12, 256);
       bool redo = true;
       if (p.probe & 1) {   // dev what-if: no exponentials (P = 0 stored)
         const uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -778,7 +770,6 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
       l += (l4[0] + l4[1]) + (l4[2] + l4[3]);
       }
       }   // redo
-      if (kPingPong && QT == 2) named_bar_arrive(qg == 0 ? 12 : 11, 256);
       tmem_wait_st();
       fence_proxy_async_smem();   // (group 0's zeroed V rows: generic writes the MMA reads)
       tc_fence_before();
@@ -850,7 +841,6 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
   }
   ++items_done;
   }   // work items
-  if (kPingPong && QT == 2 && warp < 4) named_bar_sync(11, 256);   // group 1's last hand-back
   {
     long long t0 = k_t0;
     iprof(0, t0);

@@ -229,3 +229,46 @@ def test_prefill_tcgen05_group_sizes_not_dividing_tiles(hq, hkv):
     n = query_counts(case.layout.lens, np.random.default_rng(hq), decode_frac=0.3)
     o, ref = _run(case, True, n)
     check_close(o, ref, f"g{hq // hkv}")
+
+
+@pytest.mark.parametrize("hkv,dispatch", [(1, False), (1, True), (8, True)])
+def test_prefill_bench_workload_every_element(hkv, dispatch):
+    """bench_prefill.py's mixed batch at the Llama-70B TP8 (1 kv head, 8 q heads) and TP1
+    (8 kv heads, 64 q heads: the headline prefill measurement) shard shapes:
+    the llama70b seed-0 layout (batch 256), 16 BE requests prefilling their whole prompt
+    (rng seed 1, as the bench picks them) and every other request decoding one token; every
+    output element vs the oracle.  dispatch: the bench's default path -- prefill requests
+    moved first, bkv_paged_mixed_attention (prefill kernel + split-K decode kernel) --
+    else one bkv_paged_prefill_attention over the batch in layout order."""
+    from dataclasses import replace
+    from synth.workload import Case
+    base = make_case("llama70b", 0)
+    lay = base.layout
+    rng = np.random.default_rng(1)
+    be = np.flatnonzero(lay.is_be)
+    pre = rng.choice(be, size=min(16, be.size), replace=False)
+    n = np.ones(lay.batch, np.int32)
+    n[pre] = lay.lens[pre]
+    if dispatch:
+        perm = np.concatenate([pre, np.setdiff1d(np.arange(lay.batch), pre)])
+        lay = replace(lay, lens=lay.lens[perm], is_be=lay.is_be[perm], block_tables=lay.block_tables[perm],
+                      dirs=lay.dirs[perm])
+        n = n[perm]
+    sh = Shape("l70bench", 8 * hkv, hkv, 128, 16, lay.batch, 0.5, "sharegpt", 4096, 1, 8 // hkv)
+    case = Case(sh, lay, 0)
+    ks, vs, K, V = pools(case, False)
+    q, cu = make_q(case, n, 8 * hkv)
+    ref = run_oracle(case, K, V, cu, q, False)
+    pool, _ = gpu_pool_from_dense(case, ks, vs, hkv)
+    bt, dirs, lens = gpu_map(lay)
+    cu_d = torch.from_numpy(cu).to(DEV)
+    if dispatch:
+        P = len(pre)
+        o = bkv.paged_mixed_attention(pool, bt, dirs, lens, cu_d, t_u16(q), P, int(cu[P]),
+                                      max_q_len=int(n[:P].max()), max_seq_len=int(lay.lens.max()),
+                                      softmax_scale=default_scale(128), pdl=True)
+    else:
+        o = bkv.paged_prefill_attention(pool, bt, dirs, lens, cu_d, t_u16(q), max_q_len=int(n.max()),
+                                        softmax_scale=default_scale(128))
+    torch.cuda.synchronize()
+    check_close(o, ref, f"bench workload hkv={hkv} dispatch={dispatch}")
