@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
                       const PrefillParams p) {
   constexpr int D = 128;
   constexpr int NS = QT == 1 ? kTcStages : 3;   // key-tile stages (shared memory budget)
-  constexpr int MS = NS + 2;                     // tile metadata slots (named barrier pairs 1 .. 2 MS)
+  constexpr int MS = NS + 2;                     // tile metadata slots (one mbarrier each)
   constexpr int SMW = 4 * QT;                    // softmax warps
   constexpr int WK = SMW, WMMA = SMW + 1, WV = SMW + 2;   // K producer, MMA issuer, V producer
   constexpr int HALF = kTcKeys * 128;          // one 64-d half of a key tile: 64 rows x 128 B
@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
   int4 *metas = reinterpret_cast<int4 *>(gb + (sO + n_ostage * 2 * kTcRows * 128 - base));
   int *tcount = reinterpret_cast<int *>(metas + MS * kTcChunks);
   uint64_t *bars = reinterpret_cast<uint64_t *>(tcount + ((MS + 1) & ~1));   // 8-byte aligned
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 4 * NS + 8 * QT + 2);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 4 * NS + 8 * QT + 2 + MS);
   const uint32_t bar0 = smem_u32(bars);
   // K and V stages are handed over separately: a K stage frees as soon as the S
   // MMAs that read it complete (about two tiles before its V stage), so the K
@@ -313,6 +313,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
   const uint32_t grp0 = bar0 + 32 * NS;   // group q: + 64 q; s_full +0, s_free +16, p_full +32, p_free +48
   const uint32_t q_full = grp0 + 64 * QT;
   const uint32_t q_free = q_full + 8;     // every S of the item's query tiles is done: Q may be replaced
+  const uint32_t meta0 = q_free + 8;      // [MS]: tile metadata slot m published (all 32 K-producer lanes arrive)
   const bool q_tma = p.q_tma != 0;        // the K producer TMA-loads Q (else the softmax warps stage it)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -332,6 +333,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
       }
     mbar_init(q_full, q_tma ? 1 : SMW);
     mbar_init(q_free, 1);
+    for (int i = 0; i < MS; ++i) mbar_init(meta0 + 8 * i, 32);
     fence_mbar_init();
   };
   if (kTcProf && threadIdx.x < kTraceWarps) s_tc_tn[threadIdx.x] = 0;
@@ -411,13 +413,12 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
   const int pos_max = L - n + (row_end - 1) / g;
 
   // Tile metadata: the producer walks the request's chunks (one tile of
-  // lookahead, so each tile carries a "last" flag) and publishes per stage the
-  // chunk count and (lo, hi, tb, dir) per chunk, handed over by two named
-  // barriers per stage (producer bar.arrive; the MMA warp resp. the softmax
-  // warpgroup bar.sync: CTA-scope release/acquire) -- the consumers never walk.
-  // The tiles themselves are handed over by the mbarriers.
-  auto bar_mma = [](int m) { return 1 + m; };                  // producer + MMA warp: 64 threads
-  auto bar_sm = [](int m) { return 1 + MS + m; };              // producer + softmax: 32 + 32 SMW threads
+  // lookahead, so each tile carries a "last" flag) and publishes per slot the
+  // chunk count and (lo, hi, tb, dir) per chunk; every producer lane arrives on
+  // the slot's mbarrier (release: each lane's own stores) and the MMA warp and
+  // the softmax warps wait on its phase (acquire) -- independently: a named
+  // barrier here made the eight softmax warps wait for the slowest every tile.
+  // The tiles themselves are handed over by the stage mbarriers.
 
   long long ep_t = 0;
   if (warp == WK || warp == WV) {
@@ -463,7 +464,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
       // metadata slot m of tile gt is rewritten for tile gt + MS only after K stage st
       // freed (S(gt + MS - NS) done), which follows s_free(gt + MS - NS - 2) = the
       // softmax finished that tile: with MS = NS + 2 every consumer has read slot m
-      // (and passed its named barriers) by then
+      // (and waited on the phase of its mbarrier) by then
       const int gt = gt0 + t, st = gt % NS, round = gt / NS, m = gt % MS;
       if (round > 0) mbar_wait((is_k ? emptyK0 : emptyV0) + 8 * st, (round - 1) & 1);   // whole warp
       tc_event(3, gt);
@@ -471,9 +472,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
       if (is_k) {
         if (lane < nch) metas[m * kTcChunks + lane] = make_int4(ch.lo, ch.hi, ch.tb, ch.dir);
         if (lane == 0) tcount[m] = nch | (nnx == 0 ? kTcLastFlag : 0);
-        __syncwarp();
-        named_bar_arrive(bar_mma(m), 64);
-        named_bar_arrive(bar_sm(m), 32 + 32 * SMW);
+        mbar_arrive(meta0 + 8 * m);   // (each lane: release of its own metadata stores)
       }
       const uint32_t fb = (is_k ? fullK0 : fullV0) + 8 * st;
       if (lane == 0) mbar_arrive_expect_tx(fb, nch * 2 * 2048);   // two 64-d half boxes per chunk
@@ -529,7 +528,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
           pc0 = c;
         }
       };
-      named_bar_sync(bar_mma(m), 64);
+      mbar_wait(meta0 + 8 * m, (gt / MS) & 1);
       tc_event(10, gt);
       prof(0);
       const int tc = tcount[m];
@@ -602,7 +601,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
         }
       };
       if ((warp & 3) == 0) tc_event(20, t);
-      named_bar_sync(bar_sm(m), 32 + 32 * SMW);
+      mbar_wait(meta0 + 8 * m, (t / MS) & 1);
       if ((warp & 3) == 0) tc_event(21, t);
       if (ntile == 0) iprof(2, it_t);
       prof(0);
@@ -882,7 +881,7 @@ static int tc_smem_bytes(bool o_tma) {
   constexpr int NS = QT == 1 ? kTcStages : 3;
   constexpr int MS = NS + 2;
   return 1024 + QT * 2 * kTcRows * 128 * (o_tma ? 2 : 1) + NS * 4 * kTcKeys * 128 +
-         MS * kTcChunks * 16 + ((MS + 1) & ~1) * 4 + (4 * NS + 8 * QT + 2) * 8 + 16;   // + metadata, barriers, TMEM slot
+         MS * kTcChunks * 16 + ((MS + 1) & ~1) * 4 + (4 * NS + 8 * QT + 2 + MS) * 8 + 16;   // + metadata, barriers, TMEM slot
 }
 
 int prefill_tc_smem_bytes() { return tc_smem_bytes<1>(false); }
