@@ -45,6 +45,7 @@ constexpr int kTcStages = 4;       // key-tile ring (K | V of up to 64 keys per 
 constexpr int kTcChunks = 4;       // chunks (16 keys each) per key tile
 constexpr int kTcKeys = 16 * kTcChunks;
 constexpr int kTcLastFlag = 1 << 8;   // tile metadata: the item's last key tile
+constexpr int kTcPatchFlag = 1 << 9;  // tile metadata: some chunk is partly live (dead V rows to zero)
 constexpr int kTcRows = 128;       // query rows per CTA = TMEM lanes
 
 __device__ __forceinline__ uint32_t tswz(int row, int c) {
@@ -299,8 +300,8 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
   const int n_ostage = p.o_tma ? QT : 0;
   // tile metadata ring (MS slots; see the producer): [slot][chunk], chunk count | last flag
   int4 *metas = reinterpret_cast<int4 *>(gb + (sO + n_ostage * 2 * kTcRows * 128 - base));
-  int *tcount = reinterpret_cast<int *>(metas + MS * kTcChunks);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(tcount + ((MS + 1) & ~1));   // 8-byte aligned
+  int2 *tinfo = reinterpret_cast<int2 *>(metas + MS * kTcChunks);   // {chunks | flags, last token}
+  uint64_t *bars = reinterpret_cast<uint64_t *>(tinfo + MS);
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 4 * NS + 8 * QT + 2 + MS);
   const uint32_t bar0 = smem_u32(bars);
   // K and V stages are handed over separately: a K stage frees as soon as the S
@@ -471,7 +472,13 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
       __syncwarp();
       if (is_k) {
         if (lane < nch) metas[m * kTcChunks + lane] = make_int4(ch.lo, ch.hi, ch.tb, ch.dir);
-        if (lane == 0) tcount[m] = nch | (nnx == 0 ? kTcLastFlag : 0);
+        // tile summary: the patch flag and the tile's largest live token (a row at
+        // pos >= it with four whole chunks sees the whole tile: no masks)
+        const bool part = lane < nch && (ch.lo > 0 || ch.hi < 16);
+        const int last_tok = lane < nch ? (ch.dir ? ch.tb - ch.lo : ch.tb + ch.hi - 1) : -1;
+        const unsigned pm = __ballot_sync(FULL, part);
+        const int tmax = __reduce_max_sync(FULL, last_tok);
+        if (lane == 0) tinfo[m] = make_int2(nch | (nnx == 0 ? kTcLastFlag : 0) | (pm ? kTcPatchFlag : 0), tmax);
         mbar_arrive(meta0 + 8 * m);   // (each lane: release of its own metadata stores)
       }
       const uint32_t fb = (is_k ? fullK0 : fullV0) + 8 * st;
@@ -531,7 +538,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
       mbar_wait(meta0 + 8 * m, (gt / MS) & 1);
       tc_event(10, gt);
       prof(0);
-      const int tc = tcount[m];
+      const int tc = tinfo[m].x;
       const int nch = tc & 0xff;
       mbar_wait(fullK0 + 8 * st, (gt / NS) & 1);
       tc_event(11, gt);
@@ -605,29 +612,32 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
       if ((warp & 3) == 0) tc_event(21, t);
       if (ntile == 0) iprof(2, it_t);
       prof(0);
-      const int tc = tcount[m];
+      const int2 ti = tinfo[m];
+      const int tc = ti.x;
       const int nch = tc & 0xff;
-      int4 meta[kTcChunks];
+      auto load_meta = [&](int4 (&meta)[kTcChunks]) {
 #pragma unroll
-      for (int j = 0; j < kTcChunks; ++j) meta[j] = j < nch ? metas[m * kTcChunks + j] : make_int4(0, 0, 0, 0);
+        for (int j = 0; j < kTcChunks; ++j) meta[j] = j < nch ? metas[m * kTcChunks + j] : make_int4(0, 0, 0, 0);
+      };
       // dead V rows of partly live chunks -> zero (P = 0 must never meet NaN, reading Q10);
       // only then does the softmax wait for the tile's copies itself (S implies K landed)
-      bool patch = false;
+      if (qg == 0 && (tc & kTcPatchFlag)) {   // group 0 patches for all
+        int4 meta[kTcChunks];
+        load_meta(meta);
+        mbar_wait(fullV0 + 8 * st, (t / NS) & 1);   // the tile's V landed
 #pragma unroll
-      for (int j = 0; j < kTcChunks; ++j) patch = patch || (j < nch && (meta[j].x > 0 || meta[j].y < 16));
-      if (qg == 0 && patch) mbar_wait(fullV0 + 8 * st, (t / NS) & 1);   // the tile's V landed
-      prof(1);
+        for (int j = 0; j < kTcChunks; ++j) {   // unrolled: meta[] stays in registers
+          if (j < nch && (meta[j].x > 0 || meta[j].y < 16)) {
+            const uint32_t sv = sStage + st * STAGE + TILE + j * 2048;
 #pragma unroll
-      for (int j = 0; j < kTcChunks; ++j) {   // unrolled: meta[] stays in registers
-        if (qg == 0 && j < nch && (meta[j].x > 0 || meta[j].y < 16)) {   // group 0 patches for all
-          const uint32_t sv = sStage + st * STAGE + TILE + j * 2048;
-#pragma unroll
-          for (int q = 0; q < 256; q += kTcRows) {   // 16 slots x 2 halves x 8 pieces
-            const int slot = (q + row) >> 4, rest = (q + row) & 15;
-            if (slot < meta[j].x || slot >= meta[j].y) sts128_zero(sv + (rest >> 3) * HALF + slot * 128 + (rest & 7) * 16);
+            for (int q = 0; q < 256; q += kTcRows) {   // 16 slots x 2 halves x 8 pieces
+              const int slot = (q + row) >> 4, rest = (q + row) & 15;
+              if (slot < meta[j].x || slot >= meta[j].y) sts128_zero(sv + (rest >> 3) * HALF + slot * 128 + (rest & 7) * 16);
+            }
           }
         }
       }
+      prof(1);
       // S tile -> registers
       prof(2);
       mbar_wait(s_full0 + 8 * sb, (t >> 1) & 1);
@@ -646,20 +656,21 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
       // folded into the exponent (p = 2^(s*scale - m)); a tile every row of the
       // warp sees whole (four full chunks before its first query) skips the masks.
       const bool fold = p.scale_log2 > 0.f;
-      bool whole = nch == kTcChunks;
-      int clo[kTcChunks], chi[kTcChunks];
-#pragma unroll
-      for (int j = 0; j < kTcChunks; ++j) {
-        clo[j] = meta[j].x;
-        chi[j] = meta[j].y;
-        if (meta[j].w) clo[j] = max(clo[j], meta[j].z - pos);
-        else chi[j] = min(chi[j], pos - meta[j].z + 1);
-        if (j >= nch) chi[j] = 0;
-        whole = whole && clo[j] == 0 && chi[j] == 16;
-      }
+      const bool whole = nch == kTcChunks && !(tc & kTcPatchFlag) && pos >= ti.y;
       // masks (unless every row of the warp sees the whole tile): dead slots -> -inf;
       // without the fold the scores are scaled here
       if (!(fold && __all_sync(FULL, whole))) {
+        int4 meta[kTcChunks];
+        load_meta(meta);
+        int clo[kTcChunks], chi[kTcChunks];
+#pragma unroll
+        for (int j = 0; j < kTcChunks; ++j) {
+          clo[j] = meta[j].x;
+          chi[j] = meta[j].y;
+          if (meta[j].w) clo[j] = max(clo[j], meta[j].z - pos);
+          else chi[j] = min(chi[j], pos - meta[j].z + 1);
+          if (j >= nch) chi[j] = 0;
+        }
 #pragma unroll
         for (int j = 0; j < kTcChunks; ++j) {
 #pragma unroll
@@ -881,7 +892,7 @@ static int tc_smem_bytes(bool o_tma) {
   constexpr int NS = QT == 1 ? kTcStages : 3;
   constexpr int MS = NS + 2;
   return 1024 + QT * 2 * kTcRows * 128 * (o_tma ? 2 : 1) + NS * 4 * kTcKeys * 128 +
-         MS * kTcChunks * 16 + ((MS + 1) & ~1) * 4 + (4 * NS + 8 * QT + 2 + MS) * 8 + 16;   // + metadata, barriers, TMEM slot
+         MS * kTcChunks * 16 + MS * 8 + (4 * NS + 8 * QT + 2 + MS) * 8 + 16;   // + metadata, barriers, TMEM slot
 }
 
 int prefill_tc_smem_bytes() { return tc_smem_bytes<1>(false); }
