@@ -30,6 +30,12 @@ if [ $step = all ] || [ $step = prefill ]; then
   timeout 900 python scripts/bench_prefill.py --config llama70b --tp 1 > $O/prefill_llama70b_tp1.json 2>> $O/prefill_err.txt
   timeout 900 python scripts/bench_prefill.py --config llama70b --tp 1 --no-decodes > $O/prefill_llama70b_tp1_prefill_only.json 2>> $O/prefill_err.txt
   timeout 900 python scripts/bench_prefill.py --config llama70b --tp 8 > $O/prefill_llama70b_tp8.json 2>> $O/prefill_err.txt
+  # ncu of the prefill kernel alone; key metrics extracted on the box -> prefill_ncu.txt
+  timeout 600 ncu --set full --clock-control none -k regex:prefill_tc -s 2 -c 1 -o $O/prefill_ncu \
+      python scripts/bench_prefill.py --config llama70b --tp 1 --no-decodes --steps 1 > $O/prefill_ncu.log 2>&1
+  ncu -i $O/prefill_ncu.ncu-rep --page raw --csv > $O/prefill_raw.csv 2>> $O/prefill_err.txt && \
+      python scripts/ncu_prefill_metrics.py $O/prefill_raw.csv > $O/prefill_ncu.txt 2>> $O/prefill_err.txt
+  rm -f $O/prefill_ncu.ncu-rep $O/prefill_raw.csv
 fi
 if [ $step = all ] || [ $step = sanitize ]; then
   for tool in memcheck racecheck initcheck synccheck; do
