@@ -308,10 +308,10 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
   // MMAs that read it complete (about two tiles before its V stage), so the K
   // stream runs further ahead of the MMA than a shared K|V ring allows
   const uint32_t fullK0 = bar0, fullV0 = bar0 + 8 * NS, emptyK0 = bar0 + 16 * NS, emptyV0 = bar0 + 24 * NS;
-  // per query group q: s_full/s_free (S buffer handoff) and p_full/p_free (P
-  // buffer handoff; p_free also marks "every P.V up to this tile has landed in
-  // O"), two buffers each; q_full: Q staged
-  const uint32_t grp0 = bar0 + 32 * NS;   // group q: + 64 q; s_full +0, s_free +16, p_full +32, p_free +48
+  // per query group q: s_full (S landed) and p_full/p_free (P written -- which
+  // also frees the S buffer -- and P.V landed; p_free also marks "every P.V up
+  // to this tile has landed in O"), two buffers each; q_full: Q staged
+  const uint32_t grp0 = bar0 + 32 * NS;   // group q: + 64 q; s_full +0, (+16 unused), p_full +32, p_free +48
   const uint32_t q_full = grp0 + 64 * QT;
   const uint32_t q_free = q_full + 8;     // every S of the item's query tiles is done: Q may be replaced
   const uint32_t meta0 = q_free + 8;      // [MS]: tile metadata slot m published (all 32 K-producer lanes arrive)
@@ -328,7 +328,6 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
     for (int q = 0; q < QT; ++q)
       for (int b = 0; b < 2; ++b) {
         mbar_init(grp0 + 64 * q + 8 * b, 1);        // s_full
-        mbar_init(grp0 + 64 * q + 16 + 8 * b, 4);   // s_free
         mbar_init(grp0 + 64 * q + 32 + 8 * b, 4);   // p_full
         mbar_init(grp0 + 64 * q + 48 + 8 * b, 1);   // p_free
       }
@@ -463,7 +462,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
     for (int t = 0; nch > 0; ++t) {
       const int nnx = pw_tile(p, r, L, pos_max, walk, nx);   // lookahead: is this tile the last?
       // metadata slot m of tile gt is rewritten for tile gt + MS only after K stage st
-      // freed (S(gt + MS - NS) done), which follows s_free(gt + MS - NS - 2) = the
+      // freed (S(gt + MS - NS) done), which follows p_full(gt + MS - NS - 2) = the
       // softmax finished that tile: with MS = NS + 2 every consumer has read slot m
       // (and waited on the phase of its mbarrier) by then
       const int gt = gt0 + t, st = gt % NS, round = gt / NS, m = gt % MS;
@@ -547,7 +546,9 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
       const uint32_t sk = sStage + st * STAGE;
 #pragma unroll
       for (int q = 0; q < QT; ++q) {
-        if (gt >= 2) mbar_wait(grp0 + 64 * q + 16 + 8 * sb, ((gt - 2) >> 1) & 1);
+        // S(gt) reuses the S/P buffer of tile gt - 2: this thread already waited for that
+        // tile's p_full (its P.V was issued in an earlier iteration), which each softmax
+        // warp arrives after its last TMEM read of the buffer -- no separate s_free wait
         tc_event(15 + q, gt);
         tc_fence_after();
         static_assert(D == 128 && HALF == 8192 && kTcRows * 128 == 16384, "umma_s8_w operand offsets");
@@ -577,7 +578,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
     const int row = (warp & 3) * 32 + lane;    // row of the group's tile = TMEM lane
     const int grow = row0 + qg * kTcRows + row;
     const bool ok = grow >= 0 && grow < row_end;
-    const uint32_t s_full0 = grp0 + 64 * qg, s_free0 = s_full0 + 16, p_full0 = s_full0 + 32,
+    const uint32_t s_full0 = grp0 + 64 * qg, p_full0 = s_full0 + 32,
                    p_free0 = s_full0 + 48;
     const uint32_t tq = tmem + 256 * qg;       // this group's TMEM columns
     const int tok = ok ? grow / g : 0, jh = ok ? grow - tok * g : 0;
@@ -685,7 +686,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
       // (chunks >= nch hold -inf: p = 0, in P columns no P.V reads); scale-and-shift
       // and the row sums on the packed two-lane FP32 pipe (FFMA2 / FADD2).  Returns
       // the row sum; xmax = the largest exponent.  S(t + 2) reuses the buffer: it is
-      // issued after s_free below and after P.V(t) (one thread's MMAs run in order).
+      // issued after p_full below and after P.V(t) (one thread's MMAs run in order).
       auto exp_store = [&](float base, float &xmax) -> float {
         const float2 sc = make_float2(p.scale_log2, p.scale_log2), nb = make_float2(-base, -base);
         float2 l2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
@@ -716,7 +717,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
 #pragma unroll
         for (int j = 0; j < kTcChunks; ++j) tmem_st8(tq + lane_addr + sb * 64 + 8 * j, z);
         redo = false;
-      } else if (fold) {
+      } else if (fold && ntile > 0) {   // (an item's first tile has no reference yet)
         float xmax;
         const float ls = exp_store(m_ref, xmax);
         redo = __any_sync(FULL, !(m_ref > -INFINITY) || xmax > 8.f);
@@ -784,10 +785,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
       fence_proxy_async_smem();   // (group 0's zeroed V rows: generic writes the MMA reads)
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(s_free0 + 8 * sb);
-        mbar_arrive(p_full0 + 8 * sb);
-      }
+      if (lane == 0) mbar_arrive(p_full0 + 8 * sb);   // (also frees the S buffer for S(t + 2))
       tc_event(23, t);
       prof(6);
       if (kTcProf && threadIdx.x == 0 && blockIdx.x < 148) atomicAdd(&g_tc_prof[(blockIdx.x * 3 + 0) * kProfSlots + 7], 1ull);
