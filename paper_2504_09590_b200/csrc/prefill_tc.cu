@@ -782,7 +782,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
       }
       }   // redo
       tmem_wait_st();
-      fence_proxy_async_smem();   // (group 0's zeroed V rows: generic writes the MMA reads)
+      if (qg == 0 && (tc & kTcPatchFlag)) fence_proxy_async_smem();   // zeroed V rows: generic writes the MMA reads
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full0 + 8 * sb);   // (also frees the S buffer for S(t + 2))
