@@ -814,12 +814,7 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
     }
     uint4 *orow = reinterpret_cast<uint4 *>(p.out + static_cast<int64_t>(q0 + tok) * p.o_st +
                                             static_cast<int64_t>(h * g + jh) * p.o_sh);
-#pragma unroll 1
-    for (int c0 = 0; c0 < D; c0 += 32) {   // 32 columns per TMEM round trip
-      float o[32];
-#pragma unroll
-      for (int c = 0; c < 32; c += 16) tmem_ld16(tq + lane_addr + 128 + c0 + c, o + c);
-      tmem_wait_ld();
+    auto put32 = [&](const float (&o)[32], int c0) {   // 32 columns -> bf16 -> staging / row
 #pragma unroll
       for (int c = 0; c < 32; c += 8) {
         const uint4 w = make_uint4(pack_bf16(o[c] * inv, o[c + 1] * inv), pack_bf16(o[c + 2] * inv, o[c + 3] * inv),
@@ -828,6 +823,24 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
         if (o_tma) st_shared_v4(so + (k >> 3) * (32 * 128) + tswz(lane, k & 7), w);
         else if (ok) orow[k] = w;
       }
+    };
+    // 32 columns per TMEM load, the next batch in flight while this one is packed
+    float oa[32], ob[32];
+    tmem_ld16(tq + lane_addr + 128, oa);
+    tmem_ld16(tq + lane_addr + 144, oa + 16);
+    tmem_wait_ld();
+#pragma unroll
+    for (int c0 = 0; c0 < D; c0 += 64) {
+      tmem_ld16(tq + lane_addr + 128 + c0 + 32, ob);
+      tmem_ld16(tq + lane_addr + 128 + c0 + 48, ob + 16);
+      put32(oa, c0);
+      tmem_wait_ld();
+      if (c0 + 64 < D) {
+        tmem_ld16(tq + lane_addr + 128 + c0 + 64, oa);
+        tmem_ld16(tq + lane_addr + 128 + c0 + 80, oa + 16);
+      }
+      put32(ob, c0 + 32);
+      if (c0 + 64 < D) tmem_wait_ld();
     }
     if (o_tma) {
       fence_proxy_async_smem();
