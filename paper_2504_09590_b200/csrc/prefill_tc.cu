@@ -45,7 +45,8 @@ constexpr int kTcStages = 4;       // key-tile ring (K | V of up to 64 keys per 
 constexpr int kTcChunks = 4;       // chunks (16 keys each) per key tile
 constexpr int kTcKeys = 16 * kTcChunks;
 constexpr int kTcLastFlag = 1 << 8;   // tile metadata: the item's last key tile
-constexpr int kTcPatchFlag = 1 << 9;  // tile metadata: some chunk is partly live (dead V rows to zero)
+constexpr int kTcPatchFlag = 1 << 9;
+constexpr int kLiveCap = 512;         // batches up to this many requests enumerate only the requests with rows  // tile metadata: some chunk is partly live (dead V rows to zero)
 constexpr int kTcRows = 128;       // query rows per CTA = TMEM lanes
 
 __device__ __forceinline__ uint32_t tswz(int row, int c) {
@@ -301,7 +302,12 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
   // tile metadata ring (MS slots; see the producer): [slot][chunk], chunk count | last flag
   int4 *metas = reinterpret_cast<int4 *>(gb + (sO + n_ostage * 2 * kTcRows * 128 - base));
   int2 *tinfo = reinterpret_cast<int2 *>(metas + MS * kTcChunks);   // {chunks | flags, last token}
-  uint64_t *bars = reinterpret_cast<uint64_t *>(tinfo + MS);
+  // live requests (rows > 0) of batches up to kLiveCap, ascending: work items enumerate
+  // these only, so a batch with many zero-row requests costs no empty-item search
+  uint32_t *live_mask = reinterpret_cast<uint32_t *>(tinfo + MS);   // [kLiveCap / 32]
+  uint16_t *live_list = reinterpret_cast<uint16_t *>(live_mask + kLiveCap / 32);
+  int *live_n = reinterpret_cast<int *>(live_list + kLiveCap);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(live_n + 2);
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 4 * NS + 8 * QT + 2 + MS);
   const uint32_t bar0 = smem_u32(bars);
   // K and V stages are handed over separately: a K stage frees as soon as the S
@@ -349,10 +355,33 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
                  "r"(256 * QT));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  const bool compact = p.B <= kLiveCap;
+  constexpr int NW = 4 * QT + 3;
+  if (compact) {   // one ballot mask per 32 requests
+    for (int c = warp; c * 32 < p.B; c += NW) {
+      const int r = c * 32 + lane;
+      const bool live = r < p.B && __ldg(p.cu_q + r + 1) > __ldg(p.cu_q + r);
+      const unsigned m = __ballot_sync(FULL, live);
+      if (lane == 0) live_mask[c] = m;
+    }
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (compact) {   // stable compaction: the same list in every CTA
+    for (int c = warp; c * 32 < p.B; c += NW) {
+      int off = 0;
+      for (int k = 0; k < c; ++k) off += __popc(live_mask[k]);
+      const unsigned m = live_mask[c];
+      if ((m >> lane) & 1u) live_list[off + __popc(m & ((1u << lane) - 1u))] = static_cast<uint16_t>(c * 32 + lane);
+      if (lane == 0 && (c + 1) * 32 >= p.B) *live_n = off + __popc(m);   // the last mask's warp
+    }
+    if (p.B == 0 && threadIdx.x == 0) *live_n = 0;
+    __syncthreads();
+  }
+  const int nreq = compact ? *live_n : p.B;   // requests the work items enumerate
+  auto req_of = [&](int i) -> int { return compact ? static_cast<int>(live_list[i]) : i; };
 
   // Persistent over work items (x, h, r), x = tile counted from the END of the
   // request (its latest, longest rows first): only existing tiles cost a pass;
@@ -363,18 +392,18 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
   const int g = p.g;
   int gt0 = 0;           // key tiles of earlier items (identical in every role)
   int items_done = 0;
-  const int n_items = ((p.tiles_max + QT - 1) / QT) * p.H * p.B;
+  const int n_items = ((p.tiles_max + QT - 1) / QT) * p.H * nreq;
   // First non-empty item >= from in this CTA's progression (from, from + G, ...):
   // the lanes of each warp test 32 candidates at once (warp-uniform result), so
   // the empty items of short or decode-only requests cost ~nothing.
   const int G = static_cast<int>(gridDim.x);
   auto next_item = [&](int from) -> int {
-    const int HB = p.H * p.B;
+    const int HB = p.H * nreq;
     for (; from < n_items; from += 32 * G) {
       const int c = from + lane * G;
       bool live = false;
       if (c < n_items) {
-        const int cx = c / HB, cr = (c - cx * HB) / p.H;
+        const int cx = c / HB, cr = req_of((c - cx * HB) / p.H);
         const int cn = __ldg(p.cu_q + cr + 1) - __ldg(p.cu_q + cr);
         live = (cn * g + kTcRows - 1) / kTcRows - 1 - QT * cx >= 0;
       }
@@ -396,8 +425,9 @@ __global__ void __launch_bounds__(32 * (4 * QT + 3), 1)
   };
   for (int item = next_item(blockIdx.x); item < n_items; item = next_item(item + G)) {
   iprof(4, it_t);
-  const int x = item / (p.H * p.B), hr = item - x * (p.H * p.B);
-  const int r = hr / p.H, h = hr - r * p.H;
+  const int x = item / (p.H * nreq), hr = item - x * (p.H * nreq);
+  const int ri = hr / p.H, h = hr - ri * p.H;
+  const int r = req_of(ri);
   const int q0 = __ldg(p.cu_q + r);
   const int n = __ldg(p.cu_q + r + 1) - q0;
   const int rows = n * g;
@@ -903,7 +933,7 @@ static int tc_smem_bytes(bool o_tma) {
   constexpr int NS = QT == 1 ? kTcStages : 3;
   constexpr int MS = NS + 2;
   return 1024 + QT * 2 * kTcRows * 128 * (o_tma ? 2 : 1) + NS * 4 * kTcKeys * 128 +
-         MS * kTcChunks * 16 + MS * 8 + (4 * NS + 8 * QT + 2 + MS) * 8 + 16;   // + metadata, barriers, TMEM slot
+         MS * kTcChunks * 16 + MS * 8 + kLiveCap / 32 * 4 + kLiveCap * 2 + 8 + (4 * NS + 8 * QT + 2 + MS) * 8 + 16;   // + metadata, barriers, TMEM slot
 }
 
 int prefill_tc_smem_bytes() { return tc_smem_bytes<1>(false); }

@@ -118,6 +118,10 @@ def main():
     ap.add_argument("--tp", type=int, default=1)
     ap.add_argument("--prefill", type=int, default=16, help="BE requests prefilling their whole prompt")
     ap.add_argument("--no-decodes", action="store_true", help="only the prefill rows (n = 0 elsewhere)")
+    ap.add_argument("--prefill-batch", action="store_true",
+                    help="with --no-decodes: the batch holds only the prefill requests (their block tables and "
+                         "lengths), as a prefill-only call would pass them; default keeps the whole batch with "
+                         "n = 0 for the other requests")
     ap.add_argument("--one-kernel", action="store_true",
                     help="serve the whole mixed batch with the prefill kernel (default: P:762-765 dispatch, "
                          "prefill kernel + split-K decode kernel via bkv_paged_mixed_attention)")
@@ -136,9 +140,16 @@ def main():
     pre = rng.choice(be, size=min(a.prefill, be.size), replace=False)
     n = np.zeros(lay.batch, np.int32) if a.no_decodes else np.ones(lay.batch, np.int32)
     n[pre] = lay.lens[pre]
+    prefill_tokens = int(n[pre].sum())
     kv_bytes = float(lay.lens.astype(np.int64).sum()) * 4 * shape.head_dim * (shape.num_kv_heads // a.tp)
     layers = max(4, int(math.ceil(500e6 / kv_bytes)))
     dispatch = not a.one_kernel and not a.no_decodes
+    if a.no_decodes and a.prefill_batch:   # the prefill requests alone (same pool, same block ids)
+        from dataclasses import replace
+        lay = replace(lay, lens=lay.lens[pre], is_be=lay.is_be[pre], block_tables=lay.block_tables[pre],
+                      dirs=lay.dirs[pre])
+        n = n[pre]
+        kv_bytes = float(lay.lens.astype(np.int64).sum()) * 4 * shape.head_dim * (shape.num_kv_heads // a.tp)
     if dispatch:   # reorder the batch: prefill requests first (the paper's batch layout)
         from dataclasses import replace
         perm = np.concatenate([pre, np.setdiff1d(np.arange(lay.batch), pre)])
@@ -157,7 +168,8 @@ def main():
         "config": {"workload": f"{a.config} TP{a.tp} shard: {H} kv / {Hq} q heads x d{d}, bs{shape.block_size}, "
                                f"batch {lay.batch}: {len(pre)} BE requests prefilling their whole prompt "
                                f"(n = L), {int((n == 1).sum())} decodes (n = 1)",
-                   "prefill_tokens": int(n[pre].sum()), "decode_tokens": int((n == 1).sum()),
+                   "prefill_tokens": prefill_tokens, "decode_tokens": int((n == 1).sum()),
+                   "prefill_batch": bool(a.no_decodes and a.prefill_batch),
                    "layers_rotated": layers, "l2": "pools rotated, > L2", "cuda_graphs": True,
                    "dispatch": ("bkv_paged_mixed_attention: prefill kernel + split-K decode kernel"
                                 if dispatch else "bkv_paged_prefill_attention for every row")},
