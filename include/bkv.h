@@ -387,7 +387,12 @@ BKV_API bkv_status bkv_peer_barrier(uint32_t *const *pads, int32_t n, int32_t ra
  *               q[i*q_stride_tok + h*q_stride_head + c] (same for out),
  *               16-byte aligned, strides multiples of 8 elements
  * Dense or general maps (fills).  fp32 accumulation, bf16 RNE output.  No
- * workspace, no split-K (each 128-row query tile runs in one CTA).
+ * workspace, no split-K (each 128-row query tile runs in one CTA).  head_dim
+ * 128 runs on the tcgen05 tensor cores; with g = num_q_heads / num_kv_heads
+ * dividing 128, q rows are read by TMA boxes that may start before a
+ * request's first row (earlier rows of q, or zero-fill before row 0) but never
+ * extend past its last; requests with n = 0 cost no work in batches of up to
+ * 512 requests.
  */
 BKV_API bkv_status bkv_paged_prefill_attention(const bkv_kv_pool *pool, const bkv_block_map *map,
                                                const int32_t *seq_lens, const int32_t *cu_q,
