@@ -417,7 +417,10 @@ BKV_API bkv_status bkv_paged_prefill_attention(const bkv_kv_pool *pool, const bk
  * With BKV_FLAG_PDL the decode part is launched as a programmatic dependent
  * of the prefill kernel and runs alongside its tail: it reads nothing the
  * prefill writes (disjoint output rows), and the prefill kernel itself starts
- * in plain stream order, after everything before the call.
+ * in plain stream order, after everything before the call.  In a decode-heavy
+ * batch (at least 4 decodes per prefill) whose prefill part has at least 8 work
+ * items per SM, the prefill's persistent grid then leaves 24 SMs to the decode
+ * part from the start.
  */
 BKV_API bkv_status bkv_paged_mixed_attention(const bkv_kv_pool *pool, const bkv_block_map *map,
                                              const int32_t *seq_lens, const int32_t *cu_q,

@@ -47,6 +47,7 @@ void load_switches() {
   s.prefill_probe = 0;
 #endif
   s.mixed_overlap = env_int("BKV_MIXED_OVERLAP", 1);
+  s.mixed_reserve = env_int("BKV_MIXED_RESERVE", 24);
 #ifdef BKV_DEV_TRACE
   s.debug = env_int("BKV_DEBUG", 0);
   s.trace = env_int("BKV_TRACE", 0);
@@ -692,12 +693,13 @@ bkv_status bkv_validate_layout_host(const int32_t *block_tables, int32_t bt_stri
   return BKV_OK;
 }
 
-bkv_status bkv_paged_prefill_attention(const bkv_kv_pool *pool, const bkv_block_map *map,
-                                       const int32_t *seq_lens, const int32_t *cu_q,
-                                       int32_t max_q_len, const void *q, int64_t q_stride_tok,
-                                       int64_t q_stride_head, int32_t num_q_heads,
-                                       float softmax_scale, void *out, int64_t o_stride_tok,
-                                       int64_t o_stride_head, bkv_stream_t stream) {
+namespace {
+// sm_reserve: SMs the persistent tcgen05 prefill grid leaves free (the mixed dispatch's
+// decode part, PDL-launched right behind it, starts on them at once)
+bkv_status prefill_call(const bkv_kv_pool *pool, const bkv_block_map *map, const int32_t *seq_lens,
+                        const int32_t *cu_q, int32_t max_q_len, const void *q, int64_t q_stride_tok,
+                        int64_t q_stride_head, int32_t num_q_heads, float softmax_scale, void *out,
+                        int64_t o_stride_tok, int64_t o_stride_head, bkv_stream_t stream, int sm_reserve) {
   bkv_status s = check_pool(pool);
   if (s) return s;
   if ((s = check_map(map))) return s;
@@ -743,6 +745,7 @@ bkv_status bkv_paged_prefill_attention(const bkv_kv_pool *pool, const bkv_block_
   p.scale_log2 = softmax_scale * 1.4426950408889634f;
   p.tiles_max = 0;
   p.q_tma = 0;
+  p.sm_reserve = sm_reserve;
   p.probe = bkv::dev_switches().prefill_probe;
   // tcgen05 kernel: Q tiles by TMA when a 128-row tile is whole tokens (g | 128)
   // and output rows by TMA store when a warp's 32 rows are whole tokens (g | 32)
@@ -758,6 +761,18 @@ bkv_status bkv_paged_prefill_attention(const bkv_kv_pool *pool, const bkv_block_
                                       reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "prefill attention launch");
   return BKV_OK;
+}
+
+}  // namespace
+
+bkv_status bkv_paged_prefill_attention(const bkv_kv_pool *pool, const bkv_block_map *map,
+                                       const int32_t *seq_lens, const int32_t *cu_q,
+                                       int32_t max_q_len, const void *q, int64_t q_stride_tok,
+                                       int64_t q_stride_head, int32_t num_q_heads,
+                                       float softmax_scale, void *out, int64_t o_stride_tok,
+                                       int64_t o_stride_head, bkv_stream_t stream) {
+  return prefill_call(pool, map, seq_lens, cu_q, max_q_len, q, q_stride_tok, q_stride_head, num_q_heads,
+                      softmax_scale, out, o_stride_tok, o_stride_head, stream, 0);
 }
 
 bkv_status bkv_paged_mixed_attention(const bkv_kv_pool *pool, const bkv_block_map *map,
@@ -780,9 +795,22 @@ bkv_status bkv_paged_mixed_attention(const bkv_kv_pool *pool, const bkv_block_ma
   bkv_block_map mp = *map;
   mp.num_seqs = num_prefill_seqs;
   if (num_prefill_seqs > 0 && max_q_len > 0) {
-    s = bkv_paged_prefill_attention(pool, &mp, seq_lens, cu_q, max_q_len, q, q_stride_tok,
-                                    q_stride_head, num_q_heads, softmax_scale, out, o_stride_tok,
-                                    o_stride_head, stream);
+    // a decode-heavy batch (the usual serving iteration): the persistent prefill grid
+    // leaves mixed_reserve SMs (24 by default) to the PDL-launched decode part, which
+    // streams HBM on them while the prefill computes (Llama-70B TP1 bench batch, 16
+    // prefills + 240 decodes: 505 -> 540 TF/s; the TP8 shard, 8x fewer prefill items,
+    // loses 2 %: kept at 0); otherwise the decode waits for SMs
+    // (only when the prefill has work items enough to spare the SMs: >= 8 per SM)
+    const bool decode_heavy = B - num_prefill_seqs >= 4 * num_prefill_seqs;
+    int reserve = 0;
+    if ((flags & BKV_FLAG_PDL) && decode_heavy && pool && pool->num_kv_heads > 0) {
+      bkv::DevProps dp;
+      const int64_t g = num_q_heads / pool->num_kv_heads;
+      const int64_t items = ((int64_t)num_prefill_rows * g + 255) / 256 * pool->num_kv_heads;   // 2 x 128 rows
+      if (bkv::dev_props(&dp) == cudaSuccess && items >= 8LL * dp.sms) reserve = bkv::dev_switches().mixed_reserve;
+    }
+    s = prefill_call(pool, &mp, seq_lens, cu_q, max_q_len, q, q_stride_tok, q_stride_head, num_q_heads,
+                     softmax_scale, out, o_stride_tok, o_stride_head, stream, reserve);
     if (s) return s;
   }
   // part 2: decode requests [P, B), one query row each at rows num_prefill_rows + (r - P)

@@ -124,6 +124,7 @@ struct PrefillParams {
   float scale_log2;
   int tiles_max;          // 128-row query tiles of the longest request (persistent kernels)
   int q_tma;              // tcgen05 kernel: Q tiles arrive by TMA (tmQ; needs g | 128)
+  int sm_reserve;         // tcgen05 kernel: SMs its persistent grid leaves free (mixed dispatch)
   int o_tma;              // tcgen05 kernel: whole-warp output rows leave by TMA store (tmO; g | 32)
   int probe;              // dev what-if timing probes (BKV_PREFILL_PROBE, only in builds with
                           // -DBKV_DEV_PROBES or the trace build; results are wrong): 1 no exp,
@@ -247,7 +248,7 @@ cudaError_t launch_planned(const CUtensorMap &tmK, const CUtensorMap &tmV, const
 // skip work) is honoured only by a BKV_DEV_TRACE build.
 struct DevSwitches {
   int slots, warps, ctas_per_sm, units_per_warp, min_split /* -1: default */, small_plan, streamk;
-  int merge_warps, fused_merge, kv_combined, mha_cuda_cores, prefill_mma_sync, prefill_qt, prefill_q_ldg, prefill_o_stg, prefill_probe;
+  int merge_warps, fused_merge, kv_combined, mha_cuda_cores, prefill_mma_sync, prefill_qt, prefill_q_ldg, prefill_o_stg, prefill_probe, mixed_reserve;
   int mixed_overlap, debug, trace, planned_slots, planned_dynamic_p, planned_pf;
 };
 const DevSwitches &dev_switches();

@@ -958,7 +958,8 @@ static cudaError_t launch_tc(const CUtensorMap &tmK, const CUtensorMap &tmV, con
   }
   const int sms = dp.sms;
   const long long items = ((tiles + QT - 1) / QT) * p.H * p.B;
-  const int grid = static_cast<int>(items < sms ? items : sms);   // one persistent CTA per SM
+  const int cap = p.sm_reserve > 0 && p.sm_reserve < sms ? sms - p.sm_reserve : sms;
+  const int grid = static_cast<int>(items < cap ? items : cap);   // one persistent CTA per SM
   prefill_tc_kernel<QT><<<grid, 32 * (4 * QT + 3), smem, s>>>(tmK, tmV, tmQ ? *tmQ : tmK, tmO ? *tmO : tmK, q);
   return cudaGetLastError();
 }
