@@ -272,3 +272,17 @@ def test_prefill_bench_workload_every_element(hkv, dispatch):
                                         softmax_scale=default_scale(128))
     torch.cuda.synchronize()
     check_close(o, ref, f"bench workload hkv={hkv} dispatch={dispatch}")
+
+
+@pytest.mark.parametrize("batch", [511, 512, 513, 700])
+def test_prefill_many_requests_zero_rows(batch):
+    """Batches around the kernel's live-request compaction limit (512 requests): up to it the
+    work items enumerate only requests with rows, beyond it every request; a third of the
+    requests have no rows, the rest decode or prefill a suffix."""
+    sh = Shape(f"many{batch}", 8, 1, 128, 16, batch, 0.5, "uniform", 160, 1, 8, uniform_max=160)
+    case = make_case(sh, batch, general=bool(batch % 2))
+    rng = np.random.default_rng(batch)
+    n = query_counts(case.layout.lens, rng, decode_frac=0.4)
+    n[rng.random(batch) < 0.33] = 0
+    o, ref = _run(case, bool(batch % 2), n)
+    check_close(o, ref, f"batch {batch}")
